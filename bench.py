@@ -1,0 +1,326 @@
+#!/usr/bin/env python3
+"""bench.py — the driver's benchmark contract for the DARM runtime path on B200.
+
+Default workload (BASELINE.json configs[1], the metric's config that fits one
+GPU): bitonic sort of 2^24 int32 keys per GPU in 64-key buckets, every bucket
+sorted by chaining the corpus compare-exchange step (corpus/bitonic.ir), in the
+MELDED form; the UNMELDED form is timed in the same run and the speed-up
+reported.  One process per GPU (torchrun); the buckets are independent, so each
+rank sorts its own keys with no collective ("scaling": "weak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload bitonic|sb1|...]
+
+Timing: W untimed warm-up steps, then K steps, each timed with CUDA events on
+the launching stream; before every timed step the input is restored from a
+pristine copy and L2 is flushed by writing 256 MiB, both outside the events.
+The max over ranks of the summed step time gives `value`.  `e2e` times the
+public C-ABI call with pinned HOST buffers (H2D + kernel + D2H, library
+events).  `--impl reference` times the reference's own CPU path (oracle/_ref:
+executeWarp chained over bitonic.ir steps) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Melded vs unmelded speedup & SIMT lane efficiency per kernel, 1-8 B200"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profile_summary(name):
+    path = os.path.join(ROOT, "profiles", name)
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ timing
+def time_steps(torch, stream, prepare, step, steps, warmup, flush_buf):
+    """Per-step CUDA-event timing on `stream`; prepare() and the L2 flush run
+    before each step outside the events.  Returns the list of step times (ms)."""
+    for _ in range(warmup):
+        prepare()
+        step()
+    torch.cuda.synchronize()
+    times = []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        prepare()
+        flush_buf.fill_(i & 0xFF)  # write 256 MiB > 126 MB L2
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    for a, b in evs:
+        times.append(a.elapsed_time(b))
+    return times
+
+
+def reduce_max(torch, dist, value):
+    if dist is None:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Reference, Restatement, reference_available
+
+    threads = os.cpu_count() or 1
+    B = args.bucket
+    n_sample = args.ref_sample_buckets * B
+    rng = np.random.default_rng(0)
+    keys0 = rng.integers(-(2 ** 31), 2 ** 31, size=n_sample, dtype=np.int64).astype(np.int32)
+    if reference_available() and B <= 64:
+        kind = "reference"
+        mod = Reference().load("bitonic", 0)
+        run = lambda k: mod.bitonic_sort(k, B, threads=threads)  # noqa: E731
+        what = f"oracle/_ref: reference executeWarp chained over bitonic.ir steps, {threads} threads"
+    else:
+        kind = "port"
+        ora = Restatement()
+        run = lambda k: ora.bitonic_sort(k, B)  # noqa: E731
+        threads = 1
+        what = "oracle restatement (darm_oracle.c), 1 thread"
+    for _ in range(args.warmup):
+        run(keys0.copy())
+    times = []
+    for _ in range(args.steps):
+        k = keys0.copy()
+        t0 = time.perf_counter()
+        run(k)
+        times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    value = n_sample / sec
+    sample = f"{args.ref_sample_buckets} buckets x {B} keys ({n_sample} keys) per step of the {args.keys}-key workload"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": workload_config(args, "unmelded"),
+        "cpu_baseline": {"value": value, "unit": "keys/s", "cores": threads, "kind": kind, "sample": sample,
+                         "what": what},
+        "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def workload_config(args, variant):
+    return {"workload": f"bitonic sort, {args.keys} int32 keys per GPU in {args.bucket}-key buckets "
+                        f"(corpus bitonic.ir compare-exchange step chained over every stage)",
+            "keys_per_gpu": args.keys, "bucket": args.bucket, "variant": variant,
+            "global_batch": args.keys * args.gpus, "parallelism": f"dp{args.gpus} (independent buckets)",
+            "l2": "flushed (256 MiB write) before every timed step; input restored from a pristine copy"}
+
+
+def cpu_baseline(args):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Reference, reference_available
+
+    if not (reference_available() and args.bucket <= 64):
+        return None
+    threads = os.cpu_count() or 1
+    B = args.bucket
+    nb = args.ref_sample_buckets
+    rng = np.random.default_rng(1)
+    keys = rng.integers(-(2 ** 31), 2 ** 31, size=nb * B, dtype=np.int64).astype(np.int32)
+    mod = Reference().load("bitonic", 0)
+    mod.bitonic_sort(keys[: 8 * B].copy(), B, threads=threads)
+    t0 = time.perf_counter()
+    mod.bitonic_sort(keys, B, threads=threads)
+    sec = time.perf_counter() - t0
+    assert (keys.reshape(-1, B)[:, 1:] >= keys.reshape(-1, B)[:, :-1]).all()
+    return {"value": nb * B / sec, "unit": "keys/s", "cores": threads, "kind": "reference",
+            "sample": f"{nb} buckets x {B} keys through oracle/_ref executeWarp chains ({sec:.1f} s)"}
+
+
+# ------------------------------------------------------------------ our arm
+def our_arm(args):
+    import torch
+
+    import paper_2107_05681_b200 as darm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
+    darm.init()
+    stream = torch.cuda.current_stream()
+    n, B = args.keys, args.bucket
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=gen)
+    work = torch.empty_like(pristine)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    want = torch.sort(pristine.view(-1, B), dim=1).values.view(-1)
+
+    results = {}
+    for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
+        prepare = lambda: work.copy_(pristine)  # noqa: E731
+        step = lambda v=variant: darm.bitonic_sort(work, B, v, stream=stream.cuda_stream, want_stats=False)  # noqa: E731
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            times = time_steps(torch, stream, prepare, step, args.steps, args.warmup, flush)
+        torch.cuda.synchronize()
+        if not torch.equal(work, want):
+            raise SystemExit(f"bitonic {vname}: result is not the bucket-sorted input")
+        total_ms = reduce_max(torch, dist, sum(times))
+        results[vname] = {"total_ms": total_ms, "ms_per_step": total_ms / args.steps,
+                          "kernel_ms_mean": sum(times) / len(times), "clocks": clk.summary()}
+    if dist:
+        dist.barrier()
+
+    # e2e: public C-ABI call with pinned host buffers, copies inside the timed region
+    host_pristine = pristine.cpu().numpy()
+    host = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        host[:] = host_pristine
+        st = darm.bitonic_sort(host, B, darm.MELDED, stream=stream.cuda_stream)
+        if i >= args.warmup:
+            e2e_ms.append(st["total_ms"])
+    if not (host.reshape(-1, B) == want.view(-1, B).cpu().numpy()).all():
+        raise SystemExit("bitonic e2e: result is not the bucket-sorted input")
+    e2e_total = reduce_max(torch, dist, sum(e2e_ms))
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    mel, unm = results["melded"], results["unmelded"]
+    value = n * world / (mel["total_ms"] / args.steps / 1e3)
+    peak, peak_src = measured_peaks()
+    alg_bytes = 8 * n
+    achieved = alg_bytes / (mel["kernel_ms_mean"] / 1e3) / 1e9
+    prof = profile_summary("bitonic_sort_r01.json") or {}
+    line = {
+        "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mel["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic (uniform full-range int32, torch.randint)",
+        "config": workload_config(args, "melded"),
+        "melded_vs_unmelded_speedup": unm["total_ms"] / mel["total_ms"],
+        "unmelded": {"value": n * world / (unm["total_ms"] / args.steps / 1e3), "ms_per_step": unm["ms_per_step"]},
+        "lane_efficiency": prof.get("lane_efficiency"),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": prof.get("dram_bytes_per_launch"), "peak_source": peak_src,
+                     "kernel": "bitonic_sort_kernel<true,64,256>",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "note": "issue-bound: 21 compare-exchange steps per 8 B of HBM traffic; see DESIGN.md §Roofline"},
+        "e2e": {"value": n * world / (e2e_total / args.steps / 1e3), "unit": "keys/s",
+                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+                "how": "darm_gpu_bitonic_sort(mem=HOST) on pinned numpy buffers; library CUDA events t0..t3"},
+        "gpu_launches": args.steps,
+        "clocks": mel["clocks"],
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--keys", type=int, default=1 << 24)
+    ap.add_argument("--bucket", type=int, default=64)
+    ap.add_argument("--ref-sample-buckets", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,136 @@
+/*
+ * darm_gpu.h — C-ABI of libdarm_gpu.so, the B200 (sm_100a) runtime path for the
+ * DARM corpus kernels (arXiv 2107.05681).
+ *
+ * This header is the drop-in boundary.  Every entry point replaces one reference
+ * interface on the runtime path; the reference citation is given
+ * per function as /root/reference/proj/<file>:<line>.
+ *
+ * Conventions (SURVEY.md §8b "Errors"):
+ *   - return DARM_OK (0), DARM_USER_ERROR (2: bad kernel name, sizes, arguments,
+ *     device index) or DARM_INTERNAL_ERROR (3: CUDA failure), mirroring the CLI's
+ *     exit codes (tools/darm_cli.cpp:25-27).  No C++ exception crosses the ABI.
+ *   - err/errlen: optional buffer that receives a one-line message on failure.
+ *   - mem: DARM_MEM_HOST -> every data pointer is host memory; the library stages
+ *     it through its own cached device buffers with H2D/D2H copies on `stream`
+ *     (pinned host memory gives full PCIe/C2C speed).  DARM_MEM_DEVICE -> every
+ *     data pointer is device memory on the current device; nothing is copied.
+ *   - stream: a cudaStream_t (NULL = legacy default stream).  HOST calls return
+ *     after the D2H copy completed; DEVICE calls are asynchronous on `stream`.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with DARM_INTERNAL_ERROR.
+ */
+#ifndef DARM_GPU_H
+#define DARM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DARM_GPU_ABI_VERSION 1
+
+#define DARM_OK 0
+#define DARM_USER_ERROR 2
+#define DARM_INTERNAL_ERROR 3
+
+/* Kernel forms (north star: "each kernel ... in two forms"). */
+#define DARM_UNMELDED 0 /* original CFG, IPDOM reconvergence kept            */
+#define DARM_MELDED 1   /* control flow emitted by runDarm   */
+
+#define DARM_MEM_HOST 0
+#define DARM_MEM_DEVICE 1
+
+typedef struct darm_gpu_stats {
+  double kernel_ms;      /* device time of this call's kernel launches        */
+  double h2d_ms;         /* HOST mode: host->device copies                     */
+  double d2h_ms;         /* HOST mode: device->host copies                     */
+  double total_ms;       /* first event to last event on `stream`              */
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  uint64_t algorithmic_bytes; /* minimal HBM bytes the kernels must move      */
+  int32_t launches;      /* kernels launched by this call                      */
+  int32_t reserved;
+} darm_gpu_stats;
+
+/* ---- runtime ------------------------------------------------------------ */
+
+/* Number of visible CUDA devices; fails with DARM_INTERNAL_ERROR when the
+ * driver has no device (there is no CPU fallback). */
+int darm_gpu_init(int *n_devices, char *err, size_t errlen);
+
+int darm_gpu_abi_version(void);
+
+/* Releases cached device buffers on every device. */
+void darm_gpu_shutdown(void);
+
+/* ---- corpus metadata ---------------------------------------------------- */
+
+/* Kernel declaration as written in proj/corpus/<kernel>.ir: parameters
+ * (fn <name>(%p, ...)), globals (global <name>[size]) and shared decls
+ * (shared <name>[size]).  Writes JSON
+ *   {"name":..,"params":[..],"globals":[[name,size],..],"shared":[[name,size],..]}
+ * Returns the length needed including the terminator (0 = unknown kernel). */
+size_t darm_gpu_kernel_info(const char *kernel, char *out, size_t outlen);
+
+/* Comma-separated list of kernels darm_gpu_execute_warps accepts. */
+const char *darm_gpu_kernel_list(void);
+
+/* ---- fixtures: replaces makeRandomInput (include/darm/fixtures.hpp:28-29,
+ *      src/fixtures.cpp:82-108) for n_warps consecutive seeds --------------
+ * Warp w gets exactly makeRandomInput(module, fn, warp, seed0 + w) (mt19937_64,
+ * params named j*|k* -> power of two <= warp, others -> [0, 2*warp), memory
+ * words -> rng() % 257 - 128), laid out for darm_gpu_execute_warps:
+ *   args[p * n_warps + w]               (n_params x n_warps)
+ *   globals[g][w * gstride + i], i < gstride <= declared size (the rest of
+ *                                        the declared words is generated and
+ *                                        dropped, keeping the stream aligned)
+ *   shared[s][w * size_s + i]           (declared size; NULL pointers skip)
+ * Host memory only; multi-threaded over warps. */
+int darm_gpu_make_random_input(const char *kernel, int warp, int64_t n_warps,
+                               uint64_t seed0, int32_t *args,
+                               int32_t *const *globals, int64_t gstride,
+                               int32_t *const *shared, char *err, size_t errlen);
+
+/* ---- replaces executeWarp (include/darm/interp.hpp:57-58,
+ *      src/interp.cpp:332-381) for a batch of independent warps ----------
+ * Runs `n_warps` warps of `warp` lanes (1..64) of corpus kernel `kernel` in
+ * the given form.  Lane t of warp w is global lane g = w*warp + t; `tid`
+ * returns t (interp.cpp:206-208).
+ *   args:    n_params x acount int32; acount = 1 (broadcast, interp.cpp:346-354),
+ *            n_warps (one value per warp) or n_warps*warp (per lane).
+ *   globals: one array per declared global, in declaration order, each
+ *            n_warps*warp words: word g is element t of warp w's array (every
+ *            corpus kernel indexes its globals by %t).  In/out: the final
+ *            contents are written back (WarpResult::globalFinal).
+ *   shared:  one array per shared decl, n_warps*declared-size words (shared
+ *            initialisers, WarpInput::sharedInit); NULL = zero-filled.
+ *            Not written back (compareRuns ignores shared memory,
+ *            interp.cpp:415-424).
+ *   faults:  n_warps int32 (may be NULL): lanes that faulted (out-of-bounds
+ *            shared access; WarpResult::faults.size()).
+ * Corpus kernels return void, so WarpResult::returns is all-nullopt. */
+int darm_gpu_execute_warps(const char *kernel, int variant, int warp,
+                           int64_t n_warps, const int32_t *args, int64_t acount,
+                           int32_t *const *globals, int n_globals,
+                           const int32_t *const *shared, int n_shared,
+                           int32_t *faults, int mem, void *stream,
+                           darm_gpu_stats *stats, char *err, size_t errlen);
+
+/* ---- bitonic sort: the corpus compare-exchange step (corpus/bitonic.ir:6-43)
+ *      chained over every stage dir = 2..bucket and stride k = dir/2..1 -------
+ * Sorts each of the n/bucket consecutive buckets ascending, in place.
+ * bucket: power of two in [2, 1024]; n % bucket == 0.  The chained-step
+ * semantics equal the reference driver's executeWarp chain for bucket <= 64
+ * (oracle: oracle/ref_shim.cpp ref_bitonic_sort). */
+int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket,
+                          int mem, void *stream, darm_gpu_stats *stats,
+                          char *err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DARM_GPU_H */

@@ -1,0 +1,210 @@
+/*
+ * darm_oracle.c — CPU restatement of the reference runtime path (see
+ * darm_oracle.h).  TEST INFRASTRUCTURE ONLY; never part of the product.
+ *
+ * Lane semantics follow /root/reference/proj/src/interp.cpp:
+ *   add/sub/mul/xor wrap as uint32        interp.cpp:118-130
+ *   shl/shr mask the amount with 31       interp.cpp:126-127
+ *   icmp.* signed, 0/1                    interp.cpp:145-164
+ *   out-of-bounds load faults the lane    interp.cpp:172-186
+ *   tid = lane index within the warp      interp.cpp:206-208
+ * and the control flow of /root/reference/proj/corpus/<kernel>.ir (the line
+ * numbers are cited per kernel).  The restatement is closed-form per lane: a
+ * corpus lane only touches element t of each global, so the lockstep order of
+ * the interpreter is unobservable except in bitonic's shared buffer, where
+ * every partner read (bitonic.ir:10) precedes every store (:24, :35) and each
+ * lane writes only its own slot.
+ */
+#include "darm_oracle.h"
+
+#include <string.h>
+
+/* ------------------------------------------------------------ mt19937_64 */
+void oracle_mt64_seed(oracle_mt64 *g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->idx = 312;
+}
+
+uint64_t oracle_mt64_next(oracle_mt64 *g) {
+  if (g->idx >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      uint64_t x = (g->mt[i] & 0xFFFFFFFF80000000ULL) | (g->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+      uint64_t xa = x >> 1;
+      if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+      g->mt[i] = g->mt[(i + 156) % 312] ^ xa;
+    }
+    g->idx = 0;
+  }
+  uint64_t y = g->mt[g->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+/* ------------------------------------------------------ makeRandomInput */
+void oracle_make_random_input(int n_params, const uint8_t *param_kinds, int n_mem,
+                              const int64_t *mem_sizes, int warp, uint64_t seed,
+                              int32_t *args, int32_t *mem_words) {
+  oracle_mt64 g;
+  oracle_mt64_seed(&g, seed);                                   /* fixtures.cpp:87 */
+  for (int p = 0; p < n_params; ++p) {
+    if (param_kinds[p]) {                                       /* 'j'/'k': :91-95 */
+      int maxShift = 0;
+      while ((1 << (maxShift + 1)) <= warp) ++maxShift;
+      args[p] = 1 << (int)(oracle_mt64_next(&g) % (uint64_t)(maxShift + 1));
+    } else {                                                    /* :96 */
+      args[p] = (int32_t)(oracle_mt64_next(&g) % (uint64_t)(2 * warp));
+    }
+  }
+  int64_t off = 0;
+  for (int m = 0; m < n_mem; ++m)                               /* :99-106 */
+    for (int64_t i = 0; i < mem_sizes[m]; ++i)
+      mem_words[off++] = (int32_t)(oracle_mt64_next(&g) % 257) - 128;
+}
+
+/* ------------------------------------------------------------ lanes */
+static inline int32_t wadd(int32_t a, int32_t b) { return (int32_t)((uint32_t)a + (uint32_t)b); }
+static inline int32_t wsub(int32_t a, int32_t b) { return (int32_t)((uint32_t)a - (uint32_t)b); }
+static inline int32_t wmul(int32_t a, int32_t b) { return (int32_t)((uint32_t)a * (uint32_t)b); }
+static inline int32_t wshl(int32_t a, int32_t b) { return (int32_t)((uint32_t)a << ((uint32_t)b & 31u)); }
+
+enum { K_SB1, K_SB1R, K_SB2, K_SB2R, K_SB3, K_SB3R, K_SB4, K_SB4R, K_NESTED, K_BITONIC, K_COUNT };
+static const char *const kNames[K_COUNT] = {"sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r",
+                                            "sb4", "sb4r", "nested", "bitonic"};
+static const int kGlobals[K_COUNT] = {4, 2, 2, 2, 4, 4, 2, 2, 2, 1};
+static const int kParams[K_COUNT] = {1, 1, 1, 1, 1, 1, 2, 2, 1, 2};
+
+static inline int32_t arg_of(const int32_t *args, int64_t acount, int64_t n_warps, int p,
+                             int64_t w, int64_t lane) {
+  const int32_t *a = args + p * acount;
+  if (acount == 1) return a[0];
+  if (acount == n_warps) return a[w];
+  return a[lane];
+}
+
+/* One lane of an sb-family / nested kernel.  G[i] points at element t of the
+ * i-th global of this warp. */
+static void sb_lane(int k, int32_t t, const int32_t *a, int32_t **G) {
+  const int32_t n = a[0];
+  switch (k) {
+    case K_SB1: { /* sb1.ir:7-28 */
+      int32_t e = t < n ? *G[1] : *G[2];
+      *G[3] = wadd(wmul(*G[0], 3), e);
+      break;
+    }
+    case K_SB1R: { /* sb1r.ir:5-26 */
+      int32_t v = *G[0];
+      *G[1] = t < n ? wshl(wadd(wmul(v, 3), n), 1) : wadd(wsub(v ^ n, 7), 2);
+      break;
+    }
+    case K_SB2:
+    case K_SB2R: { /* sb2.ir:5-36, sb2r.ir:5-36 */
+      int32_t v = *G[0];
+      int32_t r = v;
+      if (v > n) r = (k == K_SB2R && !(t < n)) ? wsub(v ^ n, 3) : wadd(wmul(v, 2), 1);
+      *G[1] = r;
+      break;
+    }
+    case K_SB3:
+    case K_SB3R: { /* sb3.ir:7-58, sb3r.ir:7-58 */
+      const int alt = k == K_SB3R && !(t < n);
+      int32_t v1 = *G[0];
+      *G[2] = v1 > n ? (alt ? (v1 ^ 9) : wmul(v1, 2)) : v1;
+      int32_t v2 = *G[1];
+      *G[3] = v2 > n ? (alt ? wsub(v2, 5) : wadd(v2, 7)) : v2;
+      break;
+    }
+    case K_SB4: /* sb4.ir:5-30: every leaf stores in+1 */
+      *G[1] = wadd(*G[0], 1);
+      break;
+    case K_SB4R: { /* sb4r.ir:5-30 */
+      const int32_t h = a[0], q = a[1];
+      int32_t v = *G[0];
+      *G[1] = t < h ? wadd(v, 1) : (t < q ? wmul(v, 3) : (v ^ 7));
+      break;
+    }
+    case K_NESTED: { /* nested.ir:6-41: both sides compute the same diamond */
+      int32_t v = *G[0];
+      *G[1] = v > n ? wmul(v, 2) : wadd(v, 9);
+      break;
+    }
+  }
+}
+
+int oracle_execute_warps(const char *kernel, int warp, int64_t n_warps, const int32_t *args,
+                         int64_t acount, int32_t *globals, int64_t gstride,
+                         const int32_t *shared, int32_t *faults) {
+  int k = -1;
+  for (int i = 0; i < K_COUNT; ++i)
+    if (kernel && strcmp(kernel, kNames[i]) == 0) k = i;
+  if (k < 0 || warp < 1 || warp > 64 || n_warps < 0 || gstride < warp) return 2;
+  if (acount != 1 && acount != n_warps && acount != n_warps * warp) return 2;
+  const int ng = kGlobals[k];
+  if (k == K_BITONIC) {
+    /* bitonic.ir:6-43; shared buf[64] per warp */
+    const int64_t S = 64;
+    for (int64_t w = 0; w < n_warps; ++w) {
+      int32_t buf[64], nbuf[64];
+      for (int i = 0; i < S; ++i) buf[i] = shared ? shared[w * S + i] : 0;
+      memcpy(nbuf, buf, sizeof buf);
+      int32_t nf = 0;
+      int32_t *res = globals + w * gstride;
+      for (int t = 0; t < warp; ++t) {
+        const int64_t lane = w * warp + t;
+        const int32_t kk = arg_of(args, acount, n_warps, 0, w, lane);
+        const int32_t dir = arg_of(args, acount, n_warps, 1, w, lane);
+        const int32_t j = t ^ kk;                               /* :9 */
+        if (j < 0 || j >= S) { ++nf; continue; }                /* :10 faults */
+        const int32_t b0 = buf[j];                              /* :10 */
+        const int keep = t < j;                                 /* :11 */
+        const int up = (t & dir) == 0;                          /* :12-13 */
+        const int32_t cv = buf[t];                              /* :18 / :29 */
+        const int need = up ? (keep ? cv > b0 : cv < b0)        /* :19-21 */
+                            : (keep ? cv < b0 : cv > b0);       /* :30-32 */
+        if (need) nbuf[t] = b0;                                 /* :24 / :35 */
+        res[t] = nbuf[t];                                       /* :40-41 */
+      }
+      if (faults) faults[w] = nf;
+    }
+    return 0;
+  }
+  for (int64_t w = 0; w < n_warps; ++w) {
+    for (int t = 0; t < warp; ++t) {
+      const int64_t lane = w * warp + t;
+      int32_t a[2] = {0, 0};
+      for (int p = 0; p < kParams[k]; ++p) a[p] = arg_of(args, acount, n_warps, p, w, lane);
+      int32_t *G[4];
+      for (int g = 0; g < ng; ++g) G[g] = globals + (int64_t)g * n_warps * gstride + w * gstride + t;
+      sb_lane(k, t, a, G);
+    }
+    if (faults) faults[w] = 0;
+  }
+  return 0;
+}
+
+int oracle_bitonic_sort(int32_t *keys, int64_t n, int bucket) {
+  if (bucket < 2 || (bucket & (bucket - 1)) || n % bucket) return 2;
+  const int B = bucket;
+  for (int64_t b = 0; b < n / B; ++b) {
+    int32_t *v = keys + b * B;
+    for (int dir = 2; dir <= B; dir <<= 1)
+      for (int k = dir >> 1; k >= 1; k >>= 1)
+        for (int t = 0; t < B; ++t) {
+          const int j = t ^ k;
+          if (j < t) continue; /* each pair once, from its lower lane */
+          const int up = (t & dir) == 0;
+          /* lane t (keep) takes b0 if cv > b0 when up; lane j the converse */
+          const int swap = up ? v[t] > v[j] : v[t] < v[j];
+          if (swap) {
+            int32_t x = v[t];
+            v[t] = v[j];
+            v[j] = x;
+          }
+        }
+  }
+  return 0;
+}

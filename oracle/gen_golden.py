@@ -1,0 +1,142 @@
+"""Generate tests/golden/*.json by running the UNMODIFIED reference.
+
+TEST INFRASTRUCTURE.  Requires oracle/_ref/libdarm_ref.so (``make -C oracle ref``,
+built from /root/reference/proj/src).  Every number in the fixtures comes from the
+reference's own code: makeRandomInput (fixtures.cpp:82-108), runDarm
+(melding_driver.cpp:54-100) and executeWarp (interp.cpp:332-381) — see
+DESIGN.md §Oracle.  Re-run with:
+
+    python oracle/gen_golden.py
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from oracle import Reference  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+POSITIVE = ["sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "nested", "bitonic"]
+WARPS = [1, 4, 8, 32, 64]
+SEEDS = [1000, 1001, 3000, 5000]
+
+
+def std_mt19937_64_kat():
+    # C++ [rand.predef]: the 10000th invocation of a default-constructed
+    # std::mt19937_64 (seed 5489) produces 9981545732273789042.
+    return {"seed": 5489, "index": 10000, "value": 9981545732273789042}
+
+
+def stats_rows(stats):
+    keys = ["issuedInstructions", "threadCycles", "usefulThreadCycles", "serializedCycles",
+            "divergentBranchCount", "sharedMemIssues", "globalMemIssues", "flags"]
+    return [dict(zip(keys, map(int, row))) for row in stats]
+
+
+def corpus_fixtures(ref: Reference, name: str) -> dict:
+    orig = ref.load(name, 0)
+    meld = ref.load(name, 1)
+    sizes = [s for _, s in orig.globals]
+    out = {
+        "kernel": name,
+        "params": orig.params,
+        "globals": orig.globals,
+        "shared": orig.shared,
+        "melds": meld.layout["melds"],
+        "cases": [],
+    }
+
+    def run_case(warp, seed, args_override=None, full_range=False):
+        args, gl, sh = orig.make_random_input(warp, seed)
+        if args_override is not None:
+            args = np.array(args_override, dtype=np.int32)
+        if full_range:
+            rng = np.random.Generator(np.random.MT19937(seed))
+            gl = rng.integers(-(2 ** 31), 2 ** 31, size=gl.size, dtype=np.int64).astype(np.int32)
+        S = sizes[0]
+        # one warp, full declared globals (gstride = declared size)
+        gin = gl.copy()
+        res = {}
+        for tag, mod in (("unmelded", orig), ("melded", meld)):
+            g = gin.copy()
+            f, st = mod.execute_warps(warp, 1, args.reshape(-1, 1), g, S,
+                                      shared=sh if orig.shared else None)
+            _, st_unit = mod.execute_warps(warp, 1, args.reshape(-1, 1), gin.copy(), S,
+                                           shared=sh if orig.shared else None, unit_latency=True)
+            res[tag] = {"globals_final": g.tolist(), "faults": int(f[0]),
+                        "stats": stats_rows(st)[0], "stats_unit_latency": stats_rows(st_unit)[0]}
+        assert res["unmelded"]["globals_final"] == res["melded"]["globals_final"], (name, warp, seed)
+        assert res["unmelded"]["faults"] == res["melded"]["faults"]
+        case = {"warp": warp, "seed": seed, "args": args.tolist(), "full_range": full_range,
+                "args_overridden": args_override is not None,
+                "globals_init": gin.tolist(),
+                "shared_init": sh.tolist() if orig.shared else [],
+                "globals_final": res["unmelded"]["globals_final"],
+                "faults": res["unmelded"]["faults"],
+                "stats": {k: {"default": v["stats"], "unit": v["stats_unit_latency"]} for k, v in res.items()}}
+        out["cases"].append(case)
+
+    for warp in WARPS:
+        for seed in SEEDS:
+            run_case(warp, seed)
+    # half-warp split (acceptance.cpp:248-258): n=16, or h=16,q=24
+    if name != "bitonic":
+        half = [16] if len(orig.params) == 1 else [16, 24]
+        for seed in range(3000, 3010):
+            run_case(32, seed, args_override=half)
+        run_case(32, 7, args_override=half, full_range=True)
+        run_case(64, 8, args_override=[40] if len(orig.params) == 1 else [20, 50], full_range=True)
+    else:
+        # every (k, dir) the sort visits at warp 32 and 64, plus k = warp (partner past the lanes)
+        for warp in (32, 64):
+            for dir_ in (2, 4, 8, 16, 32, 64):
+                k = dir_ // 2
+                while k >= 1:
+                    run_case(warp, 6000 + dir_ * 100 + k, args_override=[k, dir_])
+                    k //= 2
+            run_case(warp, 7000, args_override=[warp, 2])      # k == warp: lanes read beyond
+    return out
+
+
+def bitonic_sort_fixtures(ref: Reference) -> dict:
+    mod = ref.load("bitonic", 0)
+    meld = ref.load("bitonic", 1)
+    out = {"kernel": "bitonic", "cases": []}
+    rng = np.random.Generator(np.random.MT19937(11))
+    for B in (2, 4, 8, 16, 32, 64):
+        for dup in (False, True):
+            nb = 4
+            if dup:
+                keys = rng.integers(-128, 129, size=nb * B, dtype=np.int64).astype(np.int32)
+            else:
+                keys = rng.integers(-(2 ** 31), 2 ** 31, size=nb * B, dtype=np.int64).astype(np.int32)
+            a = keys.copy()
+            st_u = mod.bitonic_sort(a, B, unit_latency=True)
+            b = keys.copy()
+            st_m = meld.bitonic_sort(b, B, unit_latency=True)
+            assert (a == b).all()
+            assert (a.reshape(-1, B) == np.sort(keys.reshape(-1, B), axis=1)).all()
+            out["cases"].append({"bucket": B, "keys": keys.tolist(), "sorted": a.tolist(),
+                                 "stats_unit_latency": {"unmelded": st_u.tolist(), "melded": st_m.tolist()}})
+    return out
+
+
+def main():
+    ref = Reference()
+    os.makedirs(OUT, exist_ok=True)
+    for name in POSITIVE:
+        with open(os.path.join(OUT, f"corpus_{name}.json"), "w") as f:
+            json.dump(corpus_fixtures(ref, name), f, separators=(",", ":"))
+    with open(os.path.join(OUT, "bitonic_sort.json"), "w") as f:
+        json.dump(bitonic_sort_fixtures(ref), f, separators=(",", ":"))
+    with open(os.path.join(OUT, "mt19937_64.json"), "w") as f:
+        json.dump(std_mt19937_64_kat(), f)
+    print("wrote", sorted(os.listdir(OUT)))
+
+
+if __name__ == "__main__":
+    main()

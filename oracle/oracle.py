@@ -1,0 +1,216 @@
+"""ctypes access to the oracle libraries.  TEST INFRASTRUCTURE ONLY.
+
+Two checkers live under oracle/ (DESIGN.md §Oracle):
+
+* ``Restatement`` — oracle/build/libdarm_oracle.so, the C restatement of the
+  reference's runtime path (darm_oracle.c).  Always buildable (plain gcc).
+* ``Reference``   — oracle/_ref/libdarm_ref.so, the UNMODIFIED reference sources
+  (/root/reference/proj/src/*.cpp) compiled by oracle/Makefile plus the batching
+  shim oracle/ref_shim.cpp.  Present wherever it was built (it travels to the GPU
+  box inside the repo snapshot; /root/reference itself does not).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs import this module; the product never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import subprocess
+from typing import Dict, List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RESTATEMENT_SO = os.path.join(HERE, "build", "libdarm_oracle.so")
+REFERENCE_SO = os.path.join(HERE, "_ref", "libdarm_ref.so")
+REF_ROOT = "/root/reference/proj"
+
+I32P = ctypes.POINTER(ctypes.c_int32)
+I64P = ctypes.POINTER(ctypes.c_int64)
+U8P = ctypes.POINTER(ctypes.c_uint8)
+
+
+def _p(a: Optional[np.ndarray], t=I32P):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(t)
+
+
+def build(ref: bool = False) -> None:
+    targets = ["all"] + (["ref"] if ref and os.path.isdir(REF_ROOT) else [])
+    subprocess.run(["make", "-C", HERE, "-j8", *targets], check=True, capture_output=True)
+
+
+# ------------------------------------------------------------------ restatement
+class Restatement:
+    def __init__(self, path: str = RESTATEMENT_SO):
+        if not os.path.exists(path):
+            build()
+        L = ctypes.CDLL(path)
+        L.oracle_mt64_seed.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+        L.oracle_mt64_next.argtypes = [ctypes.c_void_p]
+        L.oracle_mt64_next.restype = ctypes.c_uint64
+        L.oracle_make_random_input.argtypes = [ctypes.c_int, U8P, ctypes.c_int, I64P, ctypes.c_int,
+                                               ctypes.c_uint64, I32P, I32P]
+        L.oracle_execute_warps.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int64, I32P,
+                                           ctypes.c_int64, I32P, ctypes.c_int64, I32P, I32P]
+        L.oracle_bitonic_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
+        self.lib = L
+
+    def mt64(self, seed: int, count: int) -> List[int]:
+        state = ctypes.create_string_buffer(312 * 8 + 16)
+        self.lib.oracle_mt64_seed(state, seed)
+        return [self.lib.oracle_mt64_next(state) for _ in range(count)]
+
+    def make_random_input(self, params: List[str], mems: List[int], warp: int, seed: int):
+        kinds = np.array([1 if p[:1] in ("j", "k") else 0 for p in params] or [0], dtype=np.uint8)
+        sizes = np.array(mems or [0], dtype=np.int64)
+        args = np.zeros(max(1, len(params)), dtype=np.int32)
+        words = np.zeros(max(1, int(sum(mems))), dtype=np.int32)
+        self.lib.oracle_make_random_input(len(params), _p(kinds, U8P), len(mems), _p(sizes, I64P), warp,
+                                          seed, _p(args), _p(words))
+        return args[: len(params)], words[: int(sum(mems))]
+
+    def execute_warps(self, kernel: str, warp: int, n_warps: int, args: np.ndarray,
+                      globals_concat: np.ndarray, gstride: int, shared: Optional[np.ndarray] = None):
+        """Mutates ``globals_concat`` in place; returns per-warp fault counts."""
+        args = np.ascontiguousarray(args, dtype=np.int32)
+        faults = np.zeros(max(1, n_warps), dtype=np.int32)
+        rc = self.lib.oracle_execute_warps(kernel.encode(), warp, n_warps, _p(args), args.shape[-1],
+                                           _p(globals_concat), gstride,
+                                           _p(None if shared is None else np.ascontiguousarray(shared, dtype=np.int32)),
+                                           _p(faults))
+        if rc:
+            raise ValueError(f"oracle_execute_warps({kernel}) -> {rc}")
+        return faults[:n_warps]
+
+    def bitonic_sort(self, keys: np.ndarray, bucket: int) -> None:
+        rc = self.lib.oracle_bitonic_sort(_p(keys), keys.size, bucket)
+        if rc:
+            raise ValueError("oracle_bitonic_sort: bad bucket")
+
+
+# ------------------------------------------------------------------ reference
+class RefModule:
+    def __init__(self, ref: "Reference", handle: ctypes.c_void_p):
+        self.ref, self.h = ref, handle
+        buf = ctypes.create_string_buffer(1 << 16)
+        ref.lib.ref_layout(self.h, buf, 1 << 16)
+        self.layout = json.loads(buf.value.decode())
+
+    def __del__(self):
+        try:
+            self.ref.lib.ref_free(self.h)
+        except Exception:
+            pass
+
+    @property
+    def params(self) -> List[str]:
+        return self.layout["params"]
+
+    @property
+    def globals(self) -> List[list]:
+        return self.layout["globals"]
+
+    @property
+    def shared(self) -> List[list]:
+        return self.layout["shared"]
+
+    def text(self) -> str:
+        buf = ctypes.create_string_buffer(1 << 16)
+        self.ref.lib.ref_print(self.h, buf, 1 << 16)
+        return buf.value.decode()
+
+    def make_random_input(self, warp: int, seed: int):
+        args = np.zeros(max(1, len(self.params)), dtype=np.int32)
+        gl = np.zeros(max(1, sum(s for _, s in self.globals)), dtype=np.int32)
+        sh = np.zeros(max(1, sum(s for _, s in self.shared)), dtype=np.int32)
+        self.ref.lib.ref_make_random_input(self.h, warp, seed, _p(args), _p(gl), _p(sh))
+        return args[: len(self.params)], gl, sh
+
+    def execute_warps(self, warp: int, n_warps: int, args: np.ndarray, globals_concat: np.ndarray,
+                      gstride: int, shared: Optional[np.ndarray] = None, unit_latency: bool = False,
+                      threads: int = 1, want_stats: bool = True, max_steps: int = 10_000_000):
+        args = np.ascontiguousarray(args, dtype=np.int32)
+        faults = np.zeros(max(1, n_warps), dtype=np.int32)
+        stats = np.zeros((max(1, n_warps), 8), dtype=np.int64) if want_stats else None
+        err = ctypes.create_string_buffer(512)
+        rc = self.ref.lib.ref_execute_warps(
+            self.h, warp, n_warps, _p(args), args.shape[-1], _p(globals_concat), gstride,
+            _p(None if shared is None else np.ascontiguousarray(shared, dtype=np.int32)),
+            int(unit_latency), max_steps, threads, None, None, _p(faults),
+            _p(stats, I64P) if stats is not None else None, err, 512)
+        if rc:
+            raise RuntimeError(err.value.decode())
+        return faults[:n_warps], (stats[:n_warps] if stats is not None else None)
+
+    def bitonic_sort(self, keys: np.ndarray, bucket: int, threads: int = 1, unit_latency: bool = False):
+        stats = np.zeros(7, dtype=np.int64)
+        err = ctypes.create_string_buffer(512)
+        rc = self.ref.lib.ref_bitonic_sort(self.h, _p(keys), keys.size, bucket, threads, int(unit_latency),
+                                           _p(stats, I64P), err, 512)
+        if rc:
+            raise RuntimeError(err.value.decode())
+        return stats
+
+
+class Reference:
+    def __init__(self, path: str = REFERENCE_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = ctypes.CDLL(path)
+        vp = ctypes.c_void_p
+        L.ref_load.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_double, ctypes.POINTER(vp),
+                               ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_load_corpus.argtypes = L.ref_load.argtypes
+        L.ref_corpus_text.argtypes = [ctypes.c_char_p]
+        L.ref_corpus_text.restype = ctypes.c_char_p
+        L.ref_free.argtypes = [vp]
+        L.ref_print.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_print.restype = ctypes.c_size_t
+        L.ref_layout.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_layout.restype = ctypes.c_size_t
+        L.ref_make_random_input.argtypes = [vp, ctypes.c_int, ctypes.c_uint64, I32P, I32P, I32P]
+        L.ref_execute_warps.argtypes = [vp, ctypes.c_int, ctypes.c_int64, I32P, ctypes.c_int64, I32P,
+                                        ctypes.c_int64, I32P, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+                                        I32P, U8P, I32P, I64P, ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_compare_warps.argtypes = [vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, I32P, I32P, U8P,
+                                        I32P, I32P, I32P, U8P, I32P, ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_compare_warps.restype = ctypes.c_int64
+        L.ref_bitonic_sort.argtypes = [vp, I32P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       I64P, ctypes.c_char_p, ctypes.c_size_t]
+        self.lib = L
+
+    def load(self, name: str, meld: int = 0, threshold: float = 0.2) -> RefModule:
+        h = ctypes.c_void_p()
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_load_corpus(name.encode(), meld, threshold, ctypes.byref(h), err, 512)
+        if rc:
+            raise RuntimeError(err.value.decode())
+        return RefModule(self, h)
+
+    def load_text(self, text: str, meld: int = 0, threshold: float = 0.2) -> RefModule:
+        h = ctypes.c_void_p()
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_load(text.encode(), meld, threshold, ctypes.byref(h), err, 512)
+        if rc:
+            raise RuntimeError(err.value.decode())
+        return RefModule(self, h)
+
+    def compare_warps(self, mod: RefModule, warp: int, n_warps: int, gstride: int,
+                      globals_a: np.ndarray, faults_a: np.ndarray, globals_b: np.ndarray,
+                      faults_b: np.ndarray):
+        """The reference's own compareRuns per warp slice -> (first bad warp or -1, diff)."""
+        diff = ctypes.create_string_buffer(512)
+        w = self.lib.ref_compare_warps(mod.h, warp, n_warps, gstride, _p(globals_a), None, None,
+                                       _p(np.ascontiguousarray(faults_a, dtype=np.int32)), _p(globals_b),
+                                       None, None, _p(np.ascontiguousarray(faults_b, dtype=np.int32)),
+                                       diff, 512)
+        return int(w), diff.value.decode()
+
+
+def reference_available() -> bool:
+    return os.path.exists(REFERENCE_SO)

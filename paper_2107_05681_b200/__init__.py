@@ -1,0 +1,335 @@
+"""paper_2107_05681_b200 — B200-native runtime path for the DARM corpus kernels.
+
+Python host side over the C-ABI in ``include/darm_gpu.h`` (``_lib/libdarm_gpu.so``,
+sm_100a only).  The functions mirror the reference's runtime interface
+(/root/reference/proj/include/darm/interp.hpp, fixtures.hpp):
+
+=====================================  ==============================================
+reference                              here
+=====================================  ==============================================
+``makeRandomInput`` fixtures.hpp:28     :func:`make_random_input` (n consecutive seeds)
+``executeWarp``     interp.hpp:57       :func:`execute_warps` (a batch of warps)
+``WarpResult.globalFinal/faults``       :class:`WarpBatchResult`
+``compareRuns``     interp.hpp:67       :func:`compare_runs` (same verdict order)
+corpus chain of ``bitonic.ir`` steps    :func:`bitonic_sort`
+=====================================  ==============================================
+
+Errors raise :class:`DarmUserError` (C-ABI code 2, the reference's
+``std::runtime_error`` / CLI exit 2) or :class:`DarmInternalError` (code 3,
+``std::logic_error`` / CUDA failures / CLI exit 3).  There is no CPU fallback:
+if the shared library is missing or no sm_100 device is present, every compute
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+UNMELDED = 0
+MELDED = 1
+VARIANTS = {"unmelded": UNMELDED, "melded": MELDED}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libdarm_gpu.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "darm_gpu.h")
+
+# Every symbol include/darm_gpu.h declares.
+ABI_SYMBOLS = (
+    "darm_gpu_init",
+    "darm_gpu_abi_version",
+    "darm_gpu_shutdown",
+    "darm_gpu_kernel_info",
+    "darm_gpu_kernel_list",
+    "darm_gpu_make_random_input",
+    "darm_gpu_execute_warps",
+    "darm_gpu_bitonic_sort",
+)
+
+
+class DarmError(RuntimeError):
+    code = 3
+
+
+class DarmUserError(DarmError):
+    code = 2
+
+
+class DarmInternalError(DarmError):
+    code = 3
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("kernel_ms", ctypes.c_double),
+        ("h2d_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("total_ms", ctypes.c_double),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
+        ("algorithmic_bytes", ctypes.c_uint64),
+        ("launches", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdarm_gpu.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DarmInternalError(
+                f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        c_i32p = ctypes.POINTER(ctypes.c_int32)
+        c_i32pp = ctypes.POINTER(c_i32p)
+        L.darm_gpu_init.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_abi_version.restype = ctypes.c_int
+        L.darm_gpu_shutdown.restype = None
+        L.darm_gpu_kernel_info.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_kernel_info.restype = ctypes.c_size_t
+        L.darm_gpu_kernel_list.restype = ctypes.c_char_p
+        L.darm_gpu_make_random_input.argtypes = [
+            ctypes.c_char_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, c_i32p, c_i32pp,
+            ctypes.c_int64, c_i32pp, ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_execute_warps.argtypes = [
+            ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, c_i32p, ctypes.c_int64,
+            c_i32pp, ctypes.c_int, c_i32pp, ctypes.c_int, c_i32p, ctypes.c_int, ctypes.c_void_p,
+            ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_bitonic_sort.argtypes = [
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+            ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, err: ctypes.Array) -> None:
+    if rc == 0:
+        return
+    msg = err.value.decode(errors="replace")
+    if rc == 2:
+        raise DarmUserError(msg)
+    raise DarmInternalError(msg or f"libdarm_gpu error {rc}")
+
+
+def init() -> int:
+    """Number of CUDA devices (raises DarmInternalError without an sm_100 GPU)."""
+    n = ctypes.c_int(0)
+    err = ctypes.create_string_buffer(512)
+    _check(lib().darm_gpu_init(ctypes.byref(n), err, 512), err)
+    return n.value
+
+
+def kernel_list() -> List[str]:
+    return lib().darm_gpu_kernel_list().decode().split(",")
+
+
+def kernel_info(kernel: str) -> dict:
+    buf = ctypes.create_string_buffer(4096)
+    n = lib().darm_gpu_kernel_info(kernel.encode(), buf, 4096)
+    if n == 0:
+        raise DarmUserError(f"unknown kernel '{kernel}'")
+    return json.loads(buf.value.decode())
+
+
+def _i32p(a: np.ndarray):
+    assert a.dtype == np.int32 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _ptr_array(ptrs: Sequence[int]):
+    arr = (ctypes.POINTER(ctypes.c_int32) * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = ctypes.cast(ctypes.c_void_p(p), ctypes.POINTER(ctypes.c_int32))
+    return arr
+
+
+@dataclass
+class WarpBatchInput:
+    """A batch of ``WarpInput`` (interp.hpp:14-22) in the compact layout."""
+
+    kernel: str
+    warp: int
+    n_warps: int
+    args: np.ndarray                      # (n_params, acount) int32
+    globals: Dict[str, np.ndarray]        # name -> (n_warps*gstride,) int32
+    shared: Dict[str, np.ndarray] = field(default_factory=dict)  # name -> (n_warps*size,)
+    gstride: int = 0
+    seed0: int = 0
+
+
+def make_random_input(kernel: str, warp: int, n_warps: int, seed0: int,
+                      gstride: Optional[int] = None) -> WarpBatchInput:
+    """``makeRandomInput(m, f, warp, seed0 + w)`` for w in [0, n_warps).
+
+    ``gstride`` words of every global are kept per warp (default: ``warp``, the
+    words the corpus kernels can touch); pass the declared size to keep all.
+    """
+    info = kernel_info(kernel)
+    gstride = warp if gstride is None else gstride
+    np_ = len(info["params"])
+    args = np.zeros((max(np_, 1), n_warps), dtype=np.int32)
+    gl = {name: np.zeros(n_warps * gstride, dtype=np.int32) for name, _ in info["globals"]}
+    sh = {name: np.zeros(n_warps * size, dtype=np.int32) for name, size in info["shared"]}
+    err = ctypes.create_string_buffer(512)
+    rc = lib().darm_gpu_make_random_input(
+        kernel.encode(), warp, n_warps, seed0, _i32p(args),
+        _ptr_array([gl[n].ctypes.data for n, _ in info["globals"]]), gstride,
+        _ptr_array([sh[n].ctypes.data for n, _ in info["shared"]]) if sh else None, err, 512)
+    _check(rc, err)
+    return WarpBatchInput(kernel, warp, n_warps, args[:np_], gl, sh, gstride, seed0)
+
+
+@dataclass
+class WarpBatchResult:
+    """``WarpResult`` (interp.hpp:41-53) for a batch: final globals + fault counts."""
+
+    globals: Dict[str, np.ndarray]
+    faults: np.ndarray
+    stats: dict
+
+
+def _is_torch_cuda(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
+
+
+def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, object],
+                  shared: Optional[Dict[str, object]] = None, n_warps: Optional[int] = None,
+                  faults=None, stream=None, want_stats: bool = True) -> WarpBatchResult:
+    """Run a batch of warps of a corpus kernel on the GPU (replaces executeWarp).
+
+    ``globals``/``shared`` are numpy int32 arrays (HOST mode: copied in and the
+    globals copied back in place) or torch int32 CUDA tensors (DEVICE mode:
+    updated in place, asynchronous on ``stream``).  ``args`` is an int32 array of
+    shape (n_params, acount) with acount in {1, n_warps, n_warps*warp}; with
+    acount == 1 it is always host memory.
+    """
+    if isinstance(variant, str):
+        variant = VARIANTS[variant]
+    info = kernel_info(kernel)
+    names = [n for n, _ in info["globals"]]
+    snames = [n for n, _ in info["shared"]]
+    first = globals[names[0]]
+    device = _is_torch_cuda(first)
+    n_lanes = int(first.numel() if device else first.size)
+    if n_warps is None:
+        n_warps = n_lanes // warp
+    if device:
+        import torch
+
+        args_t = args if _is_torch_cuda(args) else None
+        if args_t is None:
+            args_np = np.ascontiguousarray(np.asarray(args, dtype=np.int32).reshape(len(info["params"]), -1))
+            acount = args_np.shape[1]
+            if acount != 1:
+                args_t = torch.from_numpy(args_np).to(first.device)
+        else:
+            acount = args_t.shape[-1]
+        if acount == 1 and args_t is None:
+            aptr = _i32p(args_np)
+        else:
+            aptr = ctypes.cast(ctypes.c_void_p(args_t.data_ptr()), ctypes.POINTER(ctypes.c_int32))
+        gl_ptrs = [globals[n].data_ptr() for n in names]
+        sh_ptrs = [shared[n].data_ptr() for n in snames] if shared else []
+        if faults is None:
+            faults = torch.zeros(n_warps, dtype=torch.int32, device=first.device)
+        fptr = ctypes.cast(ctypes.c_void_p(faults.data_ptr()), ctypes.POINTER(ctypes.c_int32))
+        mem = 1
+        if stream is None:
+            stream = torch.cuda.current_stream(first.device).cuda_stream
+    else:
+        args_np = np.ascontiguousarray(np.asarray(args, dtype=np.int32).reshape(len(info["params"]), -1))
+        acount = args_np.shape[1]
+        aptr = _i32p(args_np)
+        for n in names:
+            g = globals[n]
+            assert g.dtype == np.int32 and g.flags["C_CONTIGUOUS"], n
+        gl_ptrs = [globals[n].ctypes.data for n in names]
+        sh_ptrs = [np.ascontiguousarray(shared[n], dtype=np.int32).ctypes.data for n in snames] if shared else []
+        if faults is None:
+            faults = np.zeros(n_warps, dtype=np.int32)
+        fptr = _i32p(faults)
+        mem = 0
+    st = Stats()
+    err = ctypes.create_string_buffer(512)
+    rc = lib().darm_gpu_execute_warps(
+        kernel.encode(), int(variant), int(warp), int(n_warps), aptr, int(acount),
+        _ptr_array(gl_ptrs), len(gl_ptrs), _ptr_array(sh_ptrs) if sh_ptrs else None, len(sh_ptrs),
+        fptr, mem, ctypes.c_void_p(stream or 0), ctypes.byref(st) if want_stats else None, err, 512)
+    _check(rc, err)
+    return WarpBatchResult({n: globals[n] for n in names}, faults, st.as_dict() if want_stats else {})
+
+
+def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: bool = True) -> dict:
+    """Sort every ``bucket``-key bucket of ``keys`` ascending, in place.
+
+    ``keys``: numpy int32 (HOST mode) or torch int32 CUDA tensor (DEVICE mode).
+    """
+    if isinstance(variant, str):
+        variant = VARIANTS[variant]
+    st = Stats()
+    err = ctypes.create_string_buffer(512)
+    if _is_torch_cuda(keys):
+        import torch
+
+        ptr, n, mem = keys.data_ptr(), keys.numel(), 1
+        if stream is None:
+            stream = torch.cuda.current_stream(keys.device).cuda_stream
+    else:
+        assert keys.dtype == np.int32 and keys.flags["C_CONTIGUOUS"]
+        ptr, n, mem = keys.ctypes.data, keys.size, 0
+    rc = lib().darm_gpu_bitonic_sort(int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), mem,
+                                     ctypes.c_void_p(stream or 0),
+                                     ctypes.byref(st) if want_stats else None, err, 512)
+    _check(rc, err)
+    return st.as_dict() if want_stats else {}
+
+
+@dataclass
+class CompareVerdict:
+    equal: bool = True
+    diff: str = ""
+    warp: int = -1
+
+
+def compare_runs(a: WarpBatchResult, b: WarpBatchResult, warp: int, gstride: Optional[int] = None) -> CompareVerdict:
+    """``compareRuns`` (interp.cpp:383-426) slice by slice: fault counts, then
+    global memories (shared memory is not compared).  Corpus kernels return
+    void, so the per-lane return comparison is vacuous."""
+    def host(x):
+        return x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+
+    fa, fb = host(a.faults), host(b.faults)
+    bad = np.nonzero(fa != fb)[0]
+    first_fault = int(bad[0]) if bad.size else None
+    first_mem, mem_name = None, ""
+    for name in a.globals:
+        ga, gb = host(a.globals[name]), host(b.globals[name])
+        stride = gstride or warp
+        diff = np.nonzero((ga != gb).reshape(-1, stride).any(axis=1))[0]
+        if diff.size and (first_mem is None or diff[0] < first_mem):
+            first_mem, mem_name = int(diff[0]), name
+    cands = [w for w in (first_fault, first_mem) if w is not None]
+    if not cands:
+        return CompareVerdict()
+    w = min(cands)
+    if first_fault is not None and first_fault == w:
+        return CompareVerdict(False, "fault counts differ", w)
+    return CompareVerdict(False, f"global memory '{mem_name}' differs", w)
+
+
+def shutdown() -> None:
+    """Release the library's cached device buffers."""
+    if _lib is not None:
+        _lib.darm_gpu_shutdown()

@@ -1,0 +1,115 @@
+// bitonic_sort.cu — batched bucket sort built from the corpus compare-exchange
+// step (corpus/bitonic.ir:6-43), in its unmelded and melded forms.
+//
+// The reference sorts a bucket by chaining executeWarp over the step kernel:
+// one warp of B lanes, lane t owns buf[t], reads its partner buf[t^k], and keeps
+// the smaller/larger key depending on keep = t < t^k and up = (t & dir) == 0,
+// for dir = 2..B and k = dir/2..1 (oracle/ref_shim.cpp ref_bitonic_sort).
+//
+// On sm_100a each bucket is B consecutive threads and lane t's slot lives in a
+// register for the whole network:
+//   - partner read  k <  32: __shfl_xor_sync (the partner is in the same warp)
+//                   k >= 32: one exchange through double-buffered shared memory
+//                            (one __syncthreads per exchange)
+//   - the divergent `if (up)` of the step (bitonic.ir:16) is a real branch in
+//     the unmelded form and the select chain of SURVEY App. A.2 in the melded
+//     form (bitonic_exchange in corpus.cuh).
+// HBM traffic is one coalesced read and one coalesced write per key (8 B/key);
+// CTAs are persistent and prefetch their next tile while running the network.
+#include <climits>
+
+#include "corpus.cuh"
+#include "kernels.h"
+
+namespace darm_gpu {
+
+template <bool M, int B, int CTA>
+__global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__ keys, uint32_t n) {
+  constexpr bool kNeedSmem = B > 32;
+  __shared__ int32_t xch[kNeedSmem ? 2 : 1][kNeedSmem ? CTA : 1];
+  const uint32_t tiles = (n + CTA - 1) / CTA;
+  const int t = int(threadIdx.x) & (B - 1);
+  uint32_t tile = blockIdx.x;
+  uint32_t idx = tile * CTA + threadIdx.x;
+  int32_t next = (tile < tiles && idx < n) ? keys[idx] : INT_MAX;
+  for (; tile < tiles; tile += gridDim.x) {
+    int32_t v = next;
+    const uint32_t my = idx;
+    idx += gridDim.x * CTA;
+    if (tile + gridDim.x < tiles) next = idx < n ? keys[idx] : INT_MAX;   // prefetch
+    int par = 0;
+#pragma unroll
+    for (int dir = 2; dir <= B; dir <<= 1) {
+#pragma unroll
+      for (int k = dir >> 1; k >= 1; k >>= 1) {
+        int32_t b0;
+        if (k < 32) {
+          b0 = __shfl_xor_sync(0xffffffffu, v, k);        // load.shared buf %j
+        } else {
+          xch[par][threadIdx.x] = v;
+          __syncthreads();
+          b0 = xch[par][threadIdx.x ^ k];
+          par ^= 1;
+        }
+        const bool keep = (t & k) == 0;                   // icmp.lt %t %j, j = t^k
+        const bool up = (t & dir) == 0;                   // icmp.eq (and %t %dir) 0
+        v = bitonic_exchange<M>(v, b0, keep, up);
+      }
+    }
+    if (my < n) keys[my] = v;
+  }
+}
+
+namespace {
+
+int g_sms = 0;
+
+template <bool M, int B>
+cudaError_t launch_b(int32_t *keys, int64_t n, cudaStream_t s) {
+  constexpr int CTA = B > 256 ? B : 256;
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  const int64_t tiles = (n + CTA - 1) / CTA;
+  const int per_sm = 2048 / CTA;
+  int64_t grid = int64_t(g_sms) * per_sm;
+  if (grid > tiles) grid = tiles;
+  if (grid < 1) grid = 1;
+  bitonic_sort_kernel<M, B, CTA><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
+  return cudaGetLastError();
+}
+
+template <bool M>
+cudaError_t launch_m(int32_t *keys, int64_t n, int bucket, cudaStream_t s) {
+  switch (bucket) {
+    case 2: return launch_b<M, 2>(keys, n, s);
+    case 4: return launch_b<M, 4>(keys, n, s);
+    case 8: return launch_b<M, 8>(keys, n, s);
+    case 16: return launch_b<M, 16>(keys, n, s);
+    case 32: return launch_b<M, 32>(keys, n, s);
+    case 64: return launch_b<M, 64>(keys, n, s);
+    case 128: return launch_b<M, 128>(keys, n, s);
+    case 256: return launch_b<M, 256>(keys, n, s);
+    case 512: return launch_b<M, 512>(keys, n, s);
+    case 1024: return launch_b<M, 1024>(keys, n, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+bool bitonic_sort_supported(int bucket) {
+  return bucket >= 2 && bucket <= 1024 && (bucket & (bucket - 1)) == 0;
+}
+
+cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, cudaStream_t s,
+                                int *launches) {
+  if (n == 0) return cudaSuccess;
+  if (launches) *launches += 1;
+  return variant ? launch_m<true>(keys, n, bucket, s) : launch_m<false>(keys, n, bucket, s);
+}
+
+}  // namespace darm_gpu

@@ -1,0 +1,48 @@
+// common.cuh — shared helpers for the sm_100a corpus kernels.
+//
+// IR semantics (from /root/reference/proj/src/interp.cpp):
+//   add/sub/mul/and/or/xor wrap as uint32 (interp.cpp:118-130)
+//   shl/shr mask the amount with 31; shr is logical (interp.cpp:126-127)
+//   icmp.* are signed and produce 0/1 (interp.cpp:145-164)
+//   select takes c != 0 (interp.cpp:165-171)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace darm_gpu {
+
+__device__ __forceinline__ int32_t ir_add(int32_t a, int32_t b) { return int32_t(uint32_t(a) + uint32_t(b)); }
+__device__ __forceinline__ int32_t ir_sub(int32_t a, int32_t b) { return int32_t(uint32_t(a) - uint32_t(b)); }
+__device__ __forceinline__ int32_t ir_mul(int32_t a, int32_t b) { return int32_t(uint32_t(a) * uint32_t(b)); }
+__device__ __forceinline__ int32_t ir_xor(int32_t a, int32_t b) { return a ^ b; }
+__device__ __forceinline__ int32_t ir_and(int32_t a, int32_t b) { return a & b; }
+__device__ __forceinline__ int32_t ir_shl(int32_t a, int32_t b) { return int32_t(uint32_t(a) << (uint32_t(b) & 31u)); }
+__device__ __forceinline__ int32_t ir_shr(int32_t a, int32_t b) { return int32_t(uint32_t(a) >> (uint32_t(b) & 31u)); }
+
+// Arm fence.  The unmelded forms must keep both sides of a divergent branch as
+// separate code: without it LLVM's SimplifyCFG hoists the
+// identical leading instructions of the two arms (`load in; mul 3` in sb1) and
+// sinks the identical tails (`add; store out`), i.e. the compiler would meld
+// the "unmelded" kernel itself.  A volatile asm with a distinct text per arm is
+// never identical across arms and is not speculatable, so neither hoisting,
+// sinking nor if-conversion in NVVM can cross it; it emits no SASS.
+#define DARM_ARM(tag) asm volatile("// arm " tag ::: "memory")
+
+// Lane -> (warp, tid) split for a logical warp of W lanes (1..64).  WT is the
+// compile-time warp size when it is a power of two, 0 for a runtime W.
+template <int WT>
+struct LaneSplit {
+  __device__ __forceinline__ static void split(uint32_t g, uint32_t W, uint32_t &w, int &t) {
+    if constexpr (WT > 0) {
+      constexpr int sh = __builtin_ctz(WT);
+      w = g >> sh;
+      t = int(g & (WT - 1));
+    } else {
+      w = g / W;
+      t = int(g - w * W);
+    }
+  }
+};
+
+}  // namespace darm_gpu

@@ -1,0 +1,426 @@
+// corpus.cuh — lane bodies of the DARM corpus kernels, one struct per
+// /root/reference/proj/corpus/<name>.ir, each in two forms:
+//
+//   MELDED = false : the original CFG.  Every divergent branch of the IR is a
+//                    real branch whose arms are fenced (DARM_ARM) so that NVVM
+//                    cannot hoist/sink/if-convert the common code across them;
+//                    the hardware runs the arms one after the other and
+//                    reconverges at the immediate post-dominator (BSSY/BSYNC).
+//   MELDED = true  : the control flow runDarm emits for the kernel
+//                    (melding_driver.cpp:54-100, threshold 0.2; printed IR in
+//                    SURVEY.md Appendix A and DESIGN.md §Melded forms):
+//                    common instructions hoisted once, select-based operand
+//                    choice, one-sided tails kept as guarded ("unpredicated")
+//                    runs.
+//
+// Every global is indexed by %t in the corpus, so arrays are stored compact:
+// word g = w*warp + t is element t of warp w's copy (see darm_gpu.h).
+// `undef` incomings of the melded phis are materialised as 0; they are never
+// selected (interp.cpp:165-171 propagates only the chosen side).
+#pragma once
+
+#include "common.cuh"
+
+namespace darm_gpu {
+
+struct CorpusParams {
+  int32_t argv[4];           // broadcast argument values
+  const int32_t *argp[4];    // per-warp / per-lane argument arrays
+  int32_t *gl[4];            // globals, declaration order, compact layout
+  const int32_t *sh;         // shared initialiser (n_warps x shared size)
+  int32_t *faults;           // per-warp fault counters (may be null)
+  uint32_t warp;             // logical warp size W (1..64)
+  uint32_t total;            // n_warps * W lanes
+  uint32_t n_warps;
+  uint32_t shared_size;      // declared shared words per warp
+};
+
+// ---------------------------------------------------------------- sb1
+// sb1.ir:7-28  out[t] = in[t]*3 + (t < n ? aux2[t] : aux3[t])
+struct Sb1 {
+  static constexpr int kParams = 1;
+  template <bool M>
+  __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    const int32_t *__restrict__ in = P.gl[0];
+    const int32_t *__restrict__ aux2 = P.gl[1];
+    const int32_t *__restrict__ aux3 = P.gl[2];
+    int32_t *__restrict__ out = P.gl[3];
+    const int32_t n = a[0];
+    const bool c = t < n;                                  // ^a1 sb1.ir:9-10
+    if constexpr (!M) {
+      if (c) {                                             // condbr %c ^a2 ^a3 (:11)
+        DARM_ARM("sb1.a2");                                // ^a2 :12-18
+        int32_t v2 = in[g];
+        int32_t m2 = ir_mul(v2, 3);
+        int32_t e2 = aux2[g];
+        out[g] = ir_add(m2, e2);
+        DARM_ARM("sb1.a2.end");
+      } else {
+        DARM_ARM("sb1.a3");                                // ^a3 :19-25
+        int32_t v3 = in[g];
+        int32_t m3 = ir_mul(v3, 3);
+        int32_t e3 = aux3[g];
+        out[g] = ir_add(m3, e3);
+        DARM_ARM("sb1.a3.end");
+      }
+    } else {
+      int32_t v2 = in[g];                                  // hoisted common
+      int32_t m2 = ir_mul(v2, 3);
+      int32_t e3 = 0, e2 = 0;
+      if (!c) e3 = aux3[g];                                // ^a2.m.g  (false-only run)
+      if (c) e2 = aux2[g];                                 // ^a2.m.g1 (true-only run)
+      int32_t sel = c ? e2 : e3;                           // ^a2.m.u1 select
+      out[g] = ir_add(m2, sel);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- sb1r
+// sb1r.ir:5-26  arms differ except the memory accesses
+struct Sb1r {
+  static constexpr int kParams = 1;
+  template <bool M>
+  __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    const int32_t *__restrict__ in = P.gl[0];
+    int32_t *__restrict__ out = P.gl[1];
+    const int32_t n = a[0];
+    const bool c = t < n;
+    if constexpr (!M) {
+      if (c) {
+        DARM_ARM("sb1r.a2");                               // :10-16
+        int32_t v2 = in[g];
+        int32_t m2 = ir_mul(v2, 3);
+        int32_t y2 = ir_add(m2, n);
+        int32_t z2 = ir_shl(y2, 1);
+        out[g] = z2;
+        DARM_ARM("sb1r.a2.end");
+      } else {
+        DARM_ARM("sb1r.a3");                               // :17-23
+        int32_t v3 = in[g];
+        int32_t x3 = ir_xor(v3, n);
+        int32_t s3 = ir_sub(x3, 7);
+        int32_t y3 = ir_add(s3, 2);
+        out[g] = y3;
+        DARM_ARM("sb1r.a3.end");
+      }
+    } else {                                               // runDarm: block-block, 3 selects, 3 runs
+      int32_t v2 = in[g];
+      int32_t s3 = 0, m2 = 0, z2 = 0;
+      if (!c) {                                            // ^a2.m.g
+        int32_t x3 = ir_xor(v2, n);
+        s3 = ir_sub(x3, 7);
+      }
+      if (c) m2 = ir_mul(v2, 3);                           // ^a2.m.g1
+      int32_t sel = c ? m2 : s3;
+      int32_t sel1 = c ? n : 2;
+      int32_t y2 = ir_add(sel, sel1);
+      if (c) z2 = ir_shl(y2, 1);                           // ^a2.m.g2
+      int32_t sel2 = c ? z2 : y2;
+      out[g] = sel2;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- sb2 / sb2r
+// sb2.ir:5-36 / sb2r.ir:5-36  one if-then region per side
+template <bool R>
+struct Sb2T {
+  static constexpr int kParams = 1;
+  template <bool M>
+  __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    const int32_t *__restrict__ in = P.gl[0];
+    int32_t *__restrict__ out = P.gl[1];
+    const int32_t n = a[0];
+    const bool c = t < n;
+    if constexpr (!M) {
+      if (c) {
+        DARM_ARM("sb2.b2");                                // ^b2 :10-21
+        int32_t v2 = in[g];
+        bool g2 = v2 > n;
+        int32_t p2 = v2;
+        if (g2) {
+          DARM_ARM("sb2.b2a");
+          p2 = ir_add(ir_mul(v2, 2), 1);
+        }
+        DARM_ARM("sb2.b2m");
+        out[g] = p2;
+      } else {
+        DARM_ARM("sb2.b3");                                // ^b3 :22-33
+        int32_t v3 = in[g];
+        bool g3 = v3 > n;
+        int32_t p3 = v3;
+        if (g3) {
+          DARM_ARM("sb2.b3a");
+          p3 = R ? ir_sub(ir_xor(v3, n), 3) : ir_add(ir_mul(v3, 2), 1);
+        }
+        DARM_ARM("sb2.b3m");
+        out[g] = p3;
+      }
+    } else if constexpr (!R) {                             // sb2: region-region, MP 0.5, 1 select
+      int32_t v2 = in[g];
+      bool g2 = v2 > n;
+      int32_t p2 = v2;
+      if (g2) p2 = ir_add(ir_mul(v2, 2), 1);               // ^b2a.m
+      out[g] = c ? p2 : p2;                                // %sel = select %c %p2 %p2
+    } else {                                               // sb2r: region-region, 1 select, 2 runs
+      int32_t v2 = in[g];
+      bool g2 = v2 > n;
+      int32_t u3 = 0, u2 = 0;
+      if (g2) {                                            // ^b2a.m
+        if (!c) u3 = ir_sub(ir_xor(v2, n), 3);             // ^b2a.m.g
+        if (c) u2 = ir_add(ir_mul(v2, 2), 1);              // ^b2a.m.g1
+      }
+      int32_t p2 = g2 ? u2 : v2;                           // ^b2m.m phis
+      int32_t p3 = g2 ? u3 : v2;
+      out[g] = c ? p2 : p3;
+    }
+  }
+};
+using Sb2 = Sb2T<false>;
+using Sb2r = Sb2T<true>;
+
+// ---------------------------------------------------------------- sb3 / sb3r
+// sb3.ir:7-58 / sb3r.ir:7-58  two sequential if-then regions per side
+template <bool R>
+struct Sb3T {
+  static constexpr int kParams = 1;
+  template <bool M>
+  __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    const int32_t *__restrict__ in = P.gl[0];
+    const int32_t *__restrict__ in2 = P.gl[1];
+    int32_t *__restrict__ out = P.gl[2];
+    int32_t *__restrict__ out2 = P.gl[3];
+    const int32_t n = a[0];
+    const bool c = t < n;
+    if constexpr (!M) {
+      if (c) {
+        DARM_ARM("sb3.c2");                                // ^c2..^c3m :12-33
+        int32_t v1 = in[g];
+        int32_t p1 = v1;
+        if (v1 > n) {
+          DARM_ARM("sb3.c2a");
+          p1 = ir_mul(v1, 2);
+        }
+        DARM_ARM("sb3.c2m");
+        out[g] = p1;
+        int32_t v2 = in2[g];
+        int32_t p2 = v2;
+        if (v2 > n) {
+          DARM_ARM("sb3.c3a");
+          p2 = ir_add(v2, 7);
+        }
+        DARM_ARM("sb3.c3m");
+        out2[g] = p2;
+      } else {
+        DARM_ARM("sb3.c5");                                // ^c5..^c6m :34-55
+        int32_t v5 = in[g];
+        int32_t p5 = v5;
+        if (v5 > n) {
+          DARM_ARM("sb3.c5a");
+          p5 = R ? ir_xor(v5, 9) : ir_mul(v5, 2);
+        }
+        DARM_ARM("sb3.c5m");
+        out[g] = p5;
+        int32_t v6 = in2[g];
+        int32_t p6 = v6;
+        if (v6 > n) {
+          DARM_ARM("sb3.c6a");
+          p6 = R ? ir_sub(v6, 5) : ir_add(v6, 7);
+        }
+        DARM_ARM("sb3.c6m");
+        out2[g] = p6;
+      }
+    } else if constexpr (!R) {                             // sb3: 2 region-region melds
+      int32_t v1 = in[g];
+      int32_t p1 = v1;
+      if (v1 > n) p1 = ir_mul(v1, 2);                      // ^c2a.m
+      out[g] = c ? p1 : p1;
+      int32_t v2 = in2[g];
+      int32_t p2 = v2;
+      if (v2 > n) p2 = ir_add(v2, 7);                      // ^c3a.m
+      out2[g] = c ? p2 : p2;
+    } else {                                               // sb3r: 2 melds, 2 runs each
+      int32_t v1 = in[g];
+      bool g1 = v1 > n;
+      int32_t w5 = 0, w1 = 0;
+      if (g1) {                                            // ^c2a.m
+        if (!c) w5 = ir_xor(v1, 9);
+        if (c) w1 = ir_mul(v1, 2);
+      }
+      int32_t p1 = g1 ? w1 : v1, p5 = g1 ? w5 : v1;
+      out[g] = c ? p1 : p5;
+      int32_t v2 = in2[g];
+      bool g2 = v2 > n;
+      int32_t w6 = 0, w2 = 0;
+      if (g2) {                                            // ^c3a.m
+        if (!c) w6 = ir_sub(v2, 5);
+        if (c) w2 = ir_add(v2, 7);
+      }
+      int32_t p2 = g2 ? w2 : v2, p6 = g2 ? w6 : v2;
+      out2[g] = c ? p2 : p6;
+    }
+  }
+};
+using Sb3 = Sb3T<false>;
+using Sb3r = Sb3T<true>;
+
+// ---------------------------------------------------------------- sb4 / sb4r
+// sb4.ir:5-30 / sb4r.ir:5-30  if / else-if / else
+template <bool R>
+struct Sb4T {
+  static constexpr int kParams = 2;
+  template <bool M>
+  __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    const int32_t *__restrict__ in = P.gl[0];
+    int32_t *__restrict__ out = P.gl[1];
+    const int32_t h = a[0], q = a[1];
+    const bool c1 = t < h;                                 // ^d1 :7-8
+    if constexpr (!M) {
+      if (c1) {
+        DARM_ARM("sb4.d2");                                // ^d2 :10-14
+        out[g] = ir_add(in[g], 1);
+        DARM_ARM("sb4.d2.end");
+      } else {
+        DARM_ARM("sb4.d3");                                // ^d3 :15-17
+        const bool c2 = t < q;
+        if (c2) {
+          DARM_ARM("sb4.d4");                              // ^d4 :18-22
+          int32_t v4 = in[g];
+          out[g] = R ? ir_mul(v4, 3) : ir_add(v4, 1);
+          DARM_ARM("sb4.d4.end");
+        } else {
+          DARM_ARM("sb4.d5");                              // ^d5 :23-27
+          int32_t v5 = in[g];
+          out[g] = R ? ir_xor(v5, 7) : ir_add(v5, 1);
+          DARM_ARM("sb4.d5.end");
+        }
+      }
+    } else if constexpr (!R) {                             // sb4: block-region then block-block
+      const bool c2 = t < q;
+      const bool sel = c1 ? true : c2;
+      int32_t w2 = ir_add(in[g], 1);
+      int32_t pred = 0;
+      if (!sel) {                                          // ^d4.r.m.m.g: predicated store
+        int32_t old = out[g];
+        pred = c1 ? old : w2;
+      }
+      out[g] = sel ? w2 : pred;
+    } else {                                               // sb4r: two block-region melds
+      const bool c2 = t < q;
+      const bool sel = c1 ? true : c2;
+      int32_t w4u = 0, v2e = 0;
+      if (sel) {                                           // ^d4.r.m
+        int32_t v2 = in[g];
+        if (!c1) w4u = ir_mul(v2, 3);                      // ^d4.r.m.g
+        v2e = v2;
+      }
+      const bool sel2 = sel ? c1 : true;
+      int32_t w2u = 0;
+      if (sel2) w2u = ir_add(v2e, 1);                      // ^d4.r.m.g1.m
+      int32_t w5u = 0, oldu = 0;
+      if (!sel) {                                          // ^d4.r.m.u1.m.g
+        int32_t v5 = in[g];
+        w5u = ir_xor(v5, 7);
+        oldu = out[g];
+      }
+      int32_t sel3 = sel ? w2u : oldu;
+      int32_t sel4 = sel ? w4u : w5u;
+      out[g] = c1 ? sel3 : sel4;
+    }
+  }
+};
+using Sb4 = Sb4T<false>;
+using Sb4r = Sb4T<true>;
+
+// ---------------------------------------------------------------- nested
+// nested.ir:6-41  divergent diamond whose arms are data-dependent diamonds
+struct Nested {
+  static constexpr int kParams = 1;
+  template <bool M>
+  __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    const int32_t *__restrict__ in = P.gl[0];
+    int32_t *__restrict__ out = P.gl[1];
+    const int32_t n = a[0];
+    const bool c = t < n;
+    if constexpr (!M) {
+      if (c) {
+        DARM_ARM("nested.l");                              // ^l..^lm :11-24
+        int32_t lv = in[g];
+        int32_t lp;
+        if (lv > n) {
+          DARM_ARM("nested.la");
+          lp = ir_mul(lv, 2);
+        } else {
+          DARM_ARM("nested.lb");
+          lp = ir_add(lv, 9);
+        }
+        DARM_ARM("nested.lm");
+        out[g] = lp;
+      } else {
+        DARM_ARM("nested.r");                              // ^r..^rm :25-38
+        int32_t rv = in[g];
+        int32_t rp;
+        if (rv > n) {
+          DARM_ARM("nested.ra");
+          rp = ir_mul(rv, 2);
+        } else {
+          DARM_ARM("nested.rb");
+          rp = ir_add(rv, 9);
+        }
+        DARM_ARM("nested.rm");
+        out[g] = rp;
+      }
+    } else {                                               // region-region then block-block
+      int32_t lv = in[g];
+      bool lc = lv > n;
+      int32_t ly = 0, lx = 0;
+      if (!lc) ly = ir_add(lv, 9);                         // ^la.m.m.g
+      if (lc) lx = ir_mul(lv, 2);                          // ^la.m.m.g1
+      int32_t lp = lc ? lx : ly;                           // ^p phi
+      out[g] = c ? lp : lp;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- bitonic step
+// bitonic.ir:6-43, one compare-exchange step; `cv` is the lane's own slot
+// (buf[t]) and the return value is what the lane leaves in buf[t].
+template <bool M>
+__device__ __forceinline__ int32_t bitonic_exchange(int32_t cv, int32_t b0, bool keep, bool up) {
+  if constexpr (!M) {
+    if (up) {                                              // condbr %up ^c ^d (:16)
+      DARM_ARM("bitonic.c");                               // ^c :17-22
+      bool gt1 = cv > b0;
+      bool lt1 = cv < b0;
+      bool need1 = keep ? gt1 : lt1;
+      if (need1) {
+        DARM_ARM("bitonic.e");                             // ^e store.shared buf %t %b0
+        cv = b0;
+      }
+      DARM_ARM("bitonic.x1");
+    } else {
+      DARM_ARM("bitonic.d");                               // ^d :28-33
+      bool lt2 = cv < b0;
+      bool gt2 = cv > b0;
+      bool need2 = keep ? lt2 : gt2;
+      if (need2) {
+        DARM_ARM("bitonic.f");                             // ^f store.shared buf %t %b0
+        cv = b0;
+      }
+      DARM_ARM("bitonic.x2");
+    }
+    return cv;
+  } else {
+    bool lt2 = false, lt1 = false;
+    if (!up) lt2 = cv < b0;                                // ^c.m.g  (false-only compare)
+    bool gt1 = cv > b0;                                    // melded compare
+    if (up) lt1 = cv < b0;                                 // ^c.m.g1 (true-only compare)
+    bool sel = up ? gt1 : lt2;
+    bool sel1 = up ? lt1 : gt1;
+    bool need1 = keep ? sel : sel1;
+    if (need1) cv = b0;                                    // ^e.m single melded store
+    return cv;
+  }
+}
+
+}  // namespace darm_gpu

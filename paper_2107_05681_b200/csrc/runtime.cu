@@ -1,0 +1,412 @@
+// runtime.cu — the C-ABI of libdarm_gpu.so (include/darm_gpu.h).
+//
+// Replaces the runtime path of the reference: executeWarp's
+// memory initialisation (interp.cpp:342-354) becomes H2D staging into cached
+// device buffers, the per-lane interpreter loop (interp.cpp:254-314) becomes a
+// kernel launch, and the gather of globalFinal (interp.cpp:366-374) becomes a
+// D2H copy.  Errors follow the CLI's exit codes (darm_cli.cpp:25-27).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/darm_gpu.h"
+#include "corpus.cuh"
+#include "kernels.h"
+
+namespace darm_gpu {
+namespace {
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void user_error(const std::string &m) { throw Error{DARM_USER_ERROR, m}; }
+
+#define DARM_CUDA(x)                                                                       \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::darm_gpu::Error{DARM_INTERNAL_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+int report(const Error &e, char *err, size_t errlen) {
+  if (err && errlen) {
+    std::strncpy(err, e.msg.c_str(), errlen - 1);
+    err[errlen - 1] = 0;
+  }
+  return e.code;
+}
+
+template <class F>
+int guarded(char *err, size_t errlen, F &&f) {
+  try {
+    f();
+    return DARM_OK;
+  } catch (const Error &e) {
+    return report(e, err, errlen);
+  } catch (const std::exception &e) {
+    return report(Error{DARM_INTERNAL_ERROR, e.what()}, err, errlen);
+  } catch (...) {
+    return report(Error{DARM_INTERNAL_ERROR, "unknown exception"}, err, errlen);
+  }
+}
+
+// ---------------------------------------------------------------- devices
+struct DeviceState {
+  std::mutex mu;
+  int sms = 0;
+  std::vector<std::pair<void *, size_t>> slots;  // cached staging buffers
+};
+
+std::mutex g_mu;
+std::vector<DeviceState *> g_devices;
+
+DeviceState &device_state(int *dev_out) {
+  int dev = 0;
+  DARM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_devices.empty()) {
+    int n = 0;
+    DARM_CUDA(cudaGetDeviceCount(&n));
+    g_devices.assign(size_t(n), nullptr);
+  }
+  if (dev >= int(g_devices.size())) throw Error{DARM_INTERNAL_ERROR, "device index out of range"};
+  if (!g_devices[dev]) {
+    cudaDeviceProp prop{};
+    DARM_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+      throw Error{DARM_INTERNAL_ERROR, std::string("device ") + prop.name +
+                                           " is not sm_100 (libdarm_gpu is built for sm_100a only)"};
+    auto *st = new DeviceState;
+    st->sms = prop.multiProcessorCount;
+    g_devices[dev] = st;
+  }
+  if (dev_out) *dev_out = dev;
+  return *g_devices[dev];
+}
+
+// Staging buffer `slot` of at least `bytes` on the current device.  Callers hold
+// st.mu for the duration of the call that uses the slots.
+void *slot(DeviceState &st, size_t i, size_t bytes) {
+  if (st.slots.size() <= i) st.slots.resize(i + 1, {nullptr, 0});
+  auto &s = st.slots[i];
+  if (s.second < bytes) {
+    if (s.first) DARM_CUDA(cudaFree(s.first));
+    s.first = nullptr;
+    s.second = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    DARM_CUDA(cudaMalloc(&s.first, want));
+    s.second = want;
+  }
+  return s.first;
+}
+
+// Event bracket for darm_gpu_stats: t0 | H2D | t1 | kernels | t2 | D2H | t3.
+struct Timeline {
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t s;
+  bool on;
+  Timeline(cudaStream_t st, bool enabled) : s(st), on(enabled) {
+    if (on)
+      for (auto &e : ev) DARM_CUDA(cudaEventCreate(&e));
+  }
+  ~Timeline() {
+    for (auto &e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  void mark(int i) {
+    if (on) DARM_CUDA(cudaEventRecord(ev[i], s));
+  }
+  void fill(darm_gpu_stats *st) {
+    if (!on || !st) return;
+    DARM_CUDA(cudaEventSynchronize(ev[3]));
+    float a = 0, b = 0, c = 0, d = 0;
+    DARM_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    DARM_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    DARM_CUDA(cudaEventElapsedTime(&c, ev[2], ev[3]));
+    DARM_CUDA(cudaEventElapsedTime(&d, ev[0], ev[3]));
+    st->h2d_ms = a;
+    st->kernel_ms = b;
+    st->d2h_ms = c;
+    st->total_ms = d;
+  }
+};
+
+const CorpusKernelDesc *find_kernel(const char *name) {
+  if (!name) return nullptr;
+  for (int i = 0; i < kCorpusCount; ++i)
+    if (std::strcmp(kCorpus[i].name, name) == 0) return &kCorpus[i];
+  return nullptr;
+}
+
+}  // namespace
+}  // namespace darm_gpu
+
+using namespace darm_gpu;
+
+extern "C" {
+
+int darm_gpu_abi_version(void) { return DARM_GPU_ABI_VERSION; }
+
+int darm_gpu_init(int *n_devices, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+      throw Error{DARM_INTERNAL_ERROR, std::string("no CUDA device: ") + cudaGetErrorString(e)};
+    if (n_devices) *n_devices = n;
+    device_state(nullptr);
+  });
+}
+
+void darm_gpu_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (size_t d = 0; d < g_devices.size(); ++d) {
+    if (!g_devices[d]) continue;
+    cudaSetDevice(int(d));
+    for (auto &s : g_devices[d]->slots)
+      if (s.first) cudaFree(s.first);
+    delete g_devices[d];
+    g_devices[d] = nullptr;
+  }
+  cudaSetDevice(cur);
+}
+
+const char *darm_gpu_kernel_list(void) {
+  static std::string list = [] {
+    std::string s;
+    for (int i = 0; i < kCorpusCount; ++i) {
+      if (i) s += ",";
+      s += kCorpus[i].name;
+    }
+    return s;
+  }();
+  return list.c_str();
+}
+
+size_t darm_gpu_kernel_info(const char *kernel, char *out, size_t outlen) {
+  const CorpusKernelDesc *d = find_kernel(kernel);
+  if (!d) return 0;
+  std::string j = std::string("{\"name\":\"") + d->name + "\",\"params\":[";
+  for (int p = 0; p < d->n_params; ++p) j += std::string(p ? "," : "") + "\"" + d->params[p] + "\"";
+  j += "],\"globals\":[";
+  for (int g = 0; g < d->n_globals; ++g)
+    j += std::string(g ? "," : "") + "[\"" + d->globals[g].name + "\"," + std::to_string(d->globals[g].size) + "]";
+  j += "],\"shared\":[";
+  for (int s = 0; s < d->n_shared; ++s)
+    j += std::string(s ? "," : "") + "[\"" + d->shared[s].name + "\"," + std::to_string(d->shared[s].size) + "]";
+  j += "],\"lane_bytes\":" + std::to_string(d->lane_bytes) + "}";
+  if (out && outlen) {
+    size_t n = j.size() < outlen - 1 ? j.size() : outlen - 1;
+    std::memcpy(out, j.data(), n);
+    out[n] = 0;
+  }
+  return j.size() + 1;
+}
+
+// makeRandomInput (fixtures.cpp:82-108), one std::mt19937_64 stream per warp.
+int darm_gpu_make_random_input(const char *kernel, int warp, int64_t n_warps, uint64_t seed0,
+                               int32_t *args, int32_t *const *globals, int64_t gstride,
+                               int32_t *const *shared, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const CorpusKernelDesc *d = find_kernel(kernel);
+    if (!d) user_error(std::string("unknown kernel '") + (kernel ? kernel : "") + "'");
+    if (warp < 1 || warp > 64) user_error("warp size must be in [1, 64]");
+    if (n_warps < 0) user_error("n_warps must be >= 0");
+    for (int g = 0; g < d->n_globals; ++g)
+      if (gstride < 0 || gstride > d->globals[g].size) user_error("gstride exceeds a declared global size");
+    auto work = [&](int64_t lo, int64_t hi) {
+      for (int64_t w = lo; w < hi; ++w) {
+        std::mt19937_64 rng(seed0 + uint64_t(w));
+        auto word = [&] { return int32_t(rng() % 257) - 128; };
+        for (int p = 0; p < d->n_params; ++p) {
+          const char c = d->params[p][0];
+          int32_t v;
+          if (c == 'j' || c == 'k') {
+            int maxShift = 0;
+            while ((1 << (maxShift + 1)) <= warp) ++maxShift;
+            v = 1 << int(rng() % uint64_t(maxShift + 1));
+          } else {
+            v = int32_t(rng() % uint64_t(2 * warp));
+          }
+          if (args) args[p * n_warps + w] = v;
+        }
+        for (int g = 0; g < d->n_globals; ++g)
+          for (int i = 0; i < d->globals[g].size; ++i) {
+            int32_t v = word();
+            if (i < gstride && globals && globals[g]) globals[g][w * gstride + i] = v;
+          }
+        for (int s = 0; s < d->n_shared; ++s)
+          for (int i = 0; i < d->shared[s].size; ++i) {
+            int32_t v = word();
+            if (shared && shared[s]) shared[s][w * d->shared[s].size + i] = v;
+          }
+      }
+    };
+    unsigned hw = std::thread::hardware_concurrency();
+    int64_t nt = hw ? hw : 1;
+    if (n_warps < 4096) nt = 1;
+    std::vector<std::thread> pool;
+    int64_t chunk = (n_warps + nt - 1) / (nt ? nt : 1);
+    for (int64_t i = 1; i < nt; ++i) {
+      int64_t lo = i * chunk, hi = std::min<int64_t>(n_warps, lo + chunk);
+      if (lo < hi) pool.emplace_back(work, lo, hi);
+    }
+    work(0, std::min<int64_t>(n_warps, chunk));
+    for (auto &t : pool) t.join();
+  });
+}
+
+int darm_gpu_execute_warps(const char *kernel, int variant, int warp, int64_t n_warps,
+                           const int32_t *args, int64_t acount, int32_t *const *globals,
+                           int n_globals, const int32_t *const *shared, int n_shared,
+                           int32_t *faults, int mem, void *stream, darm_gpu_stats *stats,
+                           char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const CorpusKernelDesc *d = find_kernel(kernel);
+    if (!d) user_error(std::string("unknown kernel '") + (kernel ? kernel : "") + "'");
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if (warp < 1 || warp > 64) user_error("warp size must be in [1, 64]");  // interp.cpp:334-335
+    if (n_warps < 0) user_error("n_warps must be >= 0");
+    if (n_warps * int64_t(warp) >= (int64_t(1) << 31)) user_error("too many lanes (limit 2^31)");
+    if (n_globals != d->n_globals)
+      user_error("expected " + std::to_string(d->n_globals) + " global arrays, got " + std::to_string(n_globals));
+    if (shared && n_shared != d->n_shared)
+      user_error("expected " + std::to_string(d->n_shared) + " shared arrays, got " + std::to_string(n_shared));
+    const int64_t lanes = n_warps * warp;
+    int am;
+    if (acount == 1) am = 0;
+    else if (acount == n_warps) am = 1;
+    else if (acount == lanes) am = 2;
+    else user_error("argument count must be 1, n_warps or n_warps*warp");  // interp.cpp:348-350
+    if (d->n_params && !args) user_error("args is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    for (int g = 0; g < n_globals; ++g)
+      if (!globals || !globals[g]) user_error("global array is NULL");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+
+    DeviceState &st = device_state(nullptr);
+    std::lock_guard<std::mutex> lk(st.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Timeline tl(s, stats != nullptr);
+    tl.mark(0);
+
+    CorpusParams P{};
+    P.warp = uint32_t(warp);
+    P.total = uint32_t(lanes);
+    P.n_warps = uint32_t(n_warps);
+    P.shared_size = d->n_shared ? uint32_t(d->shared[0].size) : 0;
+    const size_t gbytes = size_t(lanes) * 4;
+    const size_t sbytes = size_t(n_warps) * P.shared_size * 4;
+    uint64_t h2d = 0, d2h = 0;
+    size_t si = 0;
+    if (am == 0) {
+      for (int p = 0; p < d->n_params; ++p) P.argv[p] = args[p];  // broadcast: host scalars
+    } else if (mem == DARM_MEM_HOST) {
+      auto *dev = static_cast<int32_t *>(slot(st, si++, size_t(acount) * d->n_params * 4));
+      DARM_CUDA(cudaMemcpyAsync(dev, args, size_t(acount) * d->n_params * 4, cudaMemcpyHostToDevice, s));
+      h2d += size_t(acount) * d->n_params * 4;
+      for (int p = 0; p < d->n_params; ++p) P.argp[p] = dev + size_t(p) * acount;
+    } else {
+      for (int p = 0; p < d->n_params; ++p) P.argp[p] = args + size_t(p) * acount;
+    }
+    for (int g = 0; g < n_globals; ++g) {
+      if (mem == DARM_MEM_HOST) {
+        P.gl[g] = static_cast<int32_t *>(slot(st, si++, gbytes));
+        if (gbytes) DARM_CUDA(cudaMemcpyAsync(P.gl[g], globals[g], gbytes, cudaMemcpyHostToDevice, s));
+        h2d += gbytes;
+      } else {
+        P.gl[g] = globals[g];
+      }
+    }
+    if (d->n_shared && shared && shared[0]) {
+      if (mem == DARM_MEM_HOST) {
+        auto *dev = static_cast<int32_t *>(slot(st, si++, sbytes));
+        if (sbytes) DARM_CUDA(cudaMemcpyAsync(dev, shared[0], sbytes, cudaMemcpyHostToDevice, s));
+        h2d += sbytes;
+        P.sh = dev;
+      } else {
+        P.sh = shared[0];
+      }
+    }
+    int32_t *dfaults = nullptr;
+    if (faults || d->n_shared) {
+      dfaults = (mem == DARM_MEM_DEVICE && faults) ? faults
+                                                   : static_cast<int32_t *>(slot(st, si++, size_t(n_warps) * 4));
+      if (n_warps) DARM_CUDA(cudaMemsetAsync(dfaults, 0, size_t(n_warps) * 4, s));
+    }
+    P.faults = dfaults;
+    tl.mark(1);
+    if (lanes) {
+      DARM_CUDA(d->launch(variant, am, P, st.sms, s));
+      if (stats) stats->launches = 1;
+    }
+    tl.mark(2);
+    if (mem == DARM_MEM_HOST) {
+      for (int g = 0; g < n_globals; ++g) {
+        if (gbytes) DARM_CUDA(cudaMemcpyAsync(globals[g], P.gl[g], gbytes, cudaMemcpyDeviceToHost, s));
+        d2h += gbytes;
+      }
+      if (faults && n_warps) {
+        DARM_CUDA(cudaMemcpyAsync(faults, dfaults, size_t(n_warps) * 4, cudaMemcpyDeviceToHost, s));
+        d2h += size_t(n_warps) * 4;
+      }
+    }
+    tl.mark(3);
+    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+      tl.fill(stats);
+      stats->h2d_bytes = h2d;
+      stats->d2h_bytes = d2h;
+      stats->algorithmic_bytes = uint64_t(lanes) * d->lane_bytes + sbytes;
+    }
+  });
+}
+
+int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int mem, void *stream,
+                          darm_gpu_stats *stats, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if (!bitonic_sort_supported(bucket)) user_error("bucket must be a power of two in [2, 1024]");
+    if (n < 0 || n % bucket) user_error("n must be a non-negative multiple of the bucket size");
+    if (n >= (int64_t(1) << 31)) user_error("too many keys (limit 2^31 - 1)");
+    if (n && !keys) user_error("keys is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    DeviceState &st = device_state(nullptr);
+    std::lock_guard<std::mutex> lk(st.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Timeline tl(s, stats != nullptr);
+    const size_t bytes = size_t(n) * 4;
+    int32_t *dk = keys;
+    tl.mark(0);
+    if (mem == DARM_MEM_HOST) {
+      dk = static_cast<int32_t *>(slot(st, 0, bytes));
+      if (bytes) DARM_CUDA(cudaMemcpyAsync(dk, keys, bytes, cudaMemcpyHostToDevice, s));
+    }
+    tl.mark(1);
+    int launches = 0;
+    DARM_CUDA(launch_bitonic_sort(variant, dk, n, bucket, s, &launches));
+    tl.mark(2);
+    if (mem == DARM_MEM_HOST && bytes) DARM_CUDA(cudaMemcpyAsync(keys, dk, bytes, cudaMemcpyDeviceToHost, s));
+    tl.mark(3);
+    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+      tl.fill(stats);
+      stats->launches = launches;
+      stats->h2d_bytes = mem == DARM_MEM_HOST ? bytes : 0;
+      stats->d2h_bytes = mem == DARM_MEM_HOST ? bytes : 0;
+      stats->algorithmic_bytes = 2 * bytes;
+    }
+  });
+}
+
+}  // extern "C"

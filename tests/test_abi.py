@@ -1,0 +1,157 @@
+"""CPU-side checks of the C-ABI library (no GPU compute calls).
+
+* libdarm_gpu.so loads and exports every function include/darm_gpu.h declares;
+* kernel metadata mirrors the corpus declarations (pinned by the golden files);
+* the host-side fixture generator reproduces makeRandomInput bit-exactly;
+* without a GPU every compute entry point fails loudly (no CPU fallback);
+* the SASS keeps the two forms distinct.
+"""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import CORPUS, ROOT, load_golden
+
+import paper_2107_05681_b200 as darm
+
+HEADER = os.path.join(ROOT, "include", "darm_gpu.h")
+
+
+def header_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(darm_gpu_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(darm.LIB_PATH)
+    names = header_functions()
+    assert set(names) == set(darm.ABI_SYMBOLS)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert darm.lib().darm_gpu_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", darm.LIB_PATH], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+@pytest.mark.parametrize("kernel", CORPUS)
+def test_kernel_info_matches_corpus(kernel):
+    gold = load_golden(f"corpus_{kernel}.json")
+    info = darm.kernel_info(kernel)
+    assert info["params"] == gold["params"]
+    assert info["globals"] == gold["globals"]
+    assert info["shared"] == gold["shared"]
+
+
+def test_kernel_list():
+    assert darm.kernel_list() == CORPUS
+    with pytest.raises(darm.DarmUserError):
+        darm.kernel_info("neg_uniform")
+
+
+@pytest.mark.parametrize("kernel", CORPUS)
+def test_make_random_input_bit_exact(kernel):
+    gold = load_golden(f"corpus_{kernel}.json")
+    S = gold["globals"][0][1]
+    ng = len(gold["globals"])
+    for case in gold["cases"]:
+        if case["full_range"]:
+            continue
+        b = darm.make_random_input(kernel, case["warp"], 1, case["seed"], gstride=S)
+        got = np.concatenate([b.globals[n] for n, _ in gold["globals"]])
+        assert got.tolist() == case["globals_init"]
+        if gold["shared"]:
+            assert b.shared["buf"].tolist() == case["shared_init"]
+        if not case["args_overridden"]:
+            assert b.args[:, 0].tolist() == case["args"]
+    # batched: warp w uses seed0 + w, compact layout keeps the first `warp` words
+    b = darm.make_random_input(kernel, 32, 5, 1000)
+    for w in range(5):
+        one = darm.make_random_input(kernel, 32, 1, 1000 + w, gstride=S)
+        for n, _ in gold["globals"]:
+            assert (b.globals[n][w * 32:(w + 1) * 32] == one.globals[n][:32]).all()
+        assert (b.args[:, w] == one.args[:, 0]).all()
+    assert ng == len(b.globals)
+
+
+def test_make_random_input_multithreaded_matches_restatement(restatement):
+    b = darm.make_random_input("sb1", 32, 5000, 77)       # >= 4096 warps: threaded path
+    for w in (0, 1, 2500, 4999):
+        args, words = restatement.make_random_input(["n"], [64, 64, 64, 64], 32, 77 + w)
+        assert b.args[0, w] == args[0]
+        for i, n in enumerate(["in", "aux2", "aux3", "out"]):
+            assert (b.globals[n][w * 32:(w + 1) * 32] == words[i * 64:i * 64 + 32]).all()
+
+
+def test_user_errors_are_reported_before_device_use():
+    g = {n: np.zeros(32, np.int32) for n in ["in", "aux2", "aux3", "out"]}
+    with pytest.raises(darm.DarmUserError):
+        darm.execute_warps("nope", 0, 32, [[1]], {"in": np.zeros(32, np.int32)})
+    with pytest.raises(darm.DarmUserError):
+        darm.execute_warps("sb1", 0, 65, [[1]], g, n_warps=1)
+    with pytest.raises(darm.DarmUserError):
+        darm.execute_warps("sb1", 0, 32, np.zeros((1, 3), np.int32), g, n_warps=1)
+    with pytest.raises(darm.DarmUserError):
+        darm.bitonic_sort(np.zeros(96, np.int32), 48)
+    with pytest.raises(darm.DarmUserError):
+        darm.bitonic_sort(np.zeros(100, np.int32), 64)
+
+
+def _have_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_have_gpu(), reason="checks the no-GPU failure path")
+def test_no_cpu_fallback_without_gpu():
+    with pytest.raises(darm.DarmInternalError):
+        darm.init()
+    g = {n: np.zeros(32, np.int32) for n in ["in", "aux2", "aux3", "out"]}
+    with pytest.raises(darm.DarmInternalError):
+        darm.execute_warps("sb1", 0, 32, [[16]], g)
+    with pytest.raises(darm.DarmInternalError):
+        darm.bitonic_sort(np.zeros(64, np.int32), 64)
+
+
+def _sass(pattern):
+    from tools.sass_dump import sass_functions
+
+    funcs = sass_functions(darm.LIB_PATH)
+    hits = [(n, b) for n, b in funcs.items() if pattern in n]
+    assert len(hits) == 1, (pattern, [n for n, _ in hits])
+    return [ins for _, ins in hits[0][1]]
+
+
+def test_sass_unmelded_keeps_both_arms():
+    un = _sass("corpus_lanes<darm_gpu::Sb1, false, 32, 0>")
+    me = _sass("corpus_lanes<darm_gpu::Sb1, true, 32, 0>")
+    # unmelded: both arms load `in` and store `out` (two STG, four LDG);
+    # melded: one hoisted load of `in`, two guarded aux loads, one store.
+    assert sum(i.split()[-1].startswith("STG") or " STG" in i or i.startswith("STG") for i in un) == 2
+    assert sum(" STG" in i or i.startswith("STG") for i in me) == 1
+    assert sum("LDG" in i for i in un) == 4
+    assert sum("LDG" in i for i in me) == 3
+
+
+def test_sass_bitonic_sort_forms():
+    un = _sass("bitonic_sort_kernel<false, 64, 256>")
+    me = _sass("bitonic_sort_kernel<true, 64, 256>")
+    # the unmelded network keeps real divergent branches with IPDOM
+    # reconvergence; the melded one is straight-line select code.
+    assert sum("BSSY" in i for i in un) >= 10
+    assert sum("BSYNC" in i for i in un) >= 10
+    assert sum("BSSY" in i for i in me) <= 3
+    assert len(me) < len(un)
+    assert sum("SHFL.BFLY" in i for i in un) == sum("SHFL.BFLY" in i for i in me) == 20
