@@ -143,7 +143,11 @@ cudaError_t launch_lanes(int variant, int am, const CorpusParams &P, int sms, cu
 
 template <bool M, int WT>
 cudaError_t launch_bstep_am(int am, const CorpusParams &P, int sms, cudaStream_t s) {
-  const uint32_t wpc = P.warp >= 256 ? 1 : 256 / P.warp;
+  // IR warps per CTA: up to 256 lanes, and at most 48 KB of shared `buf`
+  // slices (the default dynamic shared-memory limit).
+  uint32_t wpc = P.warp >= 256 ? 1 : 256 / P.warp;
+  const uint32_t cap = (48u << 10) / (4u * (P.shared_size ? P.shared_size : 1));
+  if (wpc > cap) wpc = cap;
   const int block = int(wpc * P.warp);
   const int grid = grid_for(P.n_warps, int(wpc), sms);
   const size_t shm = size_t(wpc) * P.shared_size * sizeof(int32_t);

@@ -1,0 +1,39 @@
+"""Launch the hot kernels once per form for ncu captures (run under gpurun).
+
+    ncu ... python tools/profile_driver.py bitonic   # 2^24 keys, B=64, unmelded then melded
+    ncu ... python tools/profile_driver.py sb1       # 2^20 lanes, n=16, unmelded then melded
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2107_05681_b200 as darm  # noqa: E402
+
+
+def main(which, bucket=64):
+    torch.cuda.set_device(0)
+    darm.init()
+    if which == "bitonic":
+        n = 1 << 24
+        g = torch.Generator(device="cuda").manual_seed(1234)
+        pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+        for v in (darm.UNMELDED, darm.MELDED):
+            k = pristine.clone()
+            darm.bitonic_sort(k, bucket, v, want_stats=False)
+        torch.cuda.synchronize()
+    else:
+        nw = 1 << 15
+        b = darm.make_random_input(which, 32, nw, 1000)
+        args = [[16]] if len(darm.kernel_info(which)["params"]) == 1 else [[16], [24]]
+        for v in (darm.UNMELDED, darm.MELDED):
+            g = {n: torch.from_numpy(a.copy()).cuda() for n, a in b.globals.items()}
+            sh = {n: torch.from_numpy(a).cuda() for n, a in b.shared.items()} or None
+            darm.execute_warps(which, v, 32, args if which != "bitonic" else b.args, g, sh, want_stats=False)
+        torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 64)
