@@ -211,6 +211,48 @@ def cpu_baseline(args):
             "sample": f"{nb} buckets x {B} keys through oracle/_ref executeWarp chains ({sec:.1f} s)"}
 
 
+# ------------------------------------------------------------------ per-kernel table
+CORPUS_LANE = ["sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "nested"]
+NQ_NODES_16 = 1141190303  # search nodes of the N=16 tree incl. root (tests pin it for small n)
+
+
+def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
+    """Melded vs unmelded device time for every corpus kernel (config 1 shape:
+    2^20 lanes = 32,768 warps of makeRandomInput fixtures, half-warp split) and
+    N-Queens N=16 (config 3)."""
+    out = {}
+    nw = 1 << 15
+    for k in CORPUS_LANE:
+        b = darm.make_random_input(k, 32, nw, 1000)
+        g = {n: torch.from_numpy(a).cuda() for n, a in b.globals.items()}
+        args = [[16]] if len(b.args) == 1 else [[16], [24]]
+        info = darm.kernel_info(k)
+        row = {}
+        for vname, v in (("unmelded", 0), ("melded", 1)):
+            step = lambda v=v: darm.execute_warps(k, v, 32, args, g, want_stats=False,  # noqa: E731
+                                                 stream=stream.cuda_stream)
+            t = time_steps(torch, stream, lambda: None, step, steps, warmup, flush)
+            row[vname + "_us"] = 1e3 * sum(t) / len(t)
+        alg = info["lane_bytes"] * nw * 32
+        row["speedup"] = row["unmelded_us"] / row["melded_us"]
+        row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
+        row["melded_frac_hbm"] = row["melded_GBps"] / peak
+        out[k] = row
+    row = {}
+    for vname, v in (("unmelded", 0), ("melded", 1)):
+        ts = []
+        for i in range(warmup + max(3, steps // 4)):
+            sols, _, st = darm.nqueens(16, 6, v, stream=stream.cuda_stream)
+            assert sols == 14772512
+            if i >= warmup:
+                ts.append(st["kernel_ms"])
+        row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
+    row["speedup"] = row["unmelded_us"] / row["melded_us"]
+    row["melded_nodes_per_s"] = NQ_NODES_16 / (row["melded_us"] * 1e-6)
+    out["nqueens16"] = row
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def our_arm(args):
     import torch
@@ -298,6 +340,11 @@ def our_arm(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
+    if not args.no_per_kernel:
+        line["per_kernel"] = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak)
+        line["per_kernel"]["bitonic"] = {"unmelded_us": 1e3 * unm["kernel_ms_mean"],
+                                         "melded_us": 1e3 * mel["kernel_ms_mean"],
+                                         "speedup": unm["total_ms"] / mel["total_ms"]}
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
@@ -314,6 +361,7 @@ def main():
     ap.add_argument("--bucket", type=int, default=64)
     ap.add_argument("--ref-sample-buckets", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-kernel", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -129,6 +129,22 @@ int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket,
                           int mem, void *stream, darm_gpu_stats *stats,
                           char *err, size_t errlen);
 
+/* ---- N-Queens (NQU; the reference has no code for it):
+ *      paper_2107_05681_b200/ir/nqueens_step.ir run to completion per thread -
+ * Counts the placements of n non-attacking queens on an n x n board (2 <= n
+ * <= 31).  The search space is split into the valid placements of the first
+ * prefix_rows rows (1 <= prefix_rows <= n-1), enumerated lowest free column
+ * first; this call solves the prefixes i with i % world == rank (one rank per
+ * GPU; the caller sums `solutions` over ranks).  per_prefix (optional, host,
+ * >= *n_prefixes entries) receives each prefix's count in enumeration order.
+ * Host-in/host-out; the call returns after the result is on the host. */
+int64_t darm_gpu_nqueens_prefix_count(int n, int prefix_rows, int rank, int world); /* -1: bad args */
+
+int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world,
+                     uint64_t *solutions, uint32_t *per_prefix, int64_t per_prefix_len,
+                     int64_t *n_prefixes, void *stream, darm_gpu_stats *stats,
+                     char *err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

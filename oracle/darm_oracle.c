@@ -208,3 +208,68 @@ int oracle_bitonic_sort(int32_t *keys, int64_t n, int bucket) {
   }
   return 0;
 }
+
+/* ------------------------------------------------------------ N-Queens
+ * The reference has no NQU code; this is an independent
+ * recursive restatement of the search that paper_2107_05681_b200/ir/
+ * nqueens_step.ir runs iteratively.  Prefix order: every valid placement of
+ * rows 0..base-1, lowest free column first; prefix i belongs to rank i % world. */
+typedef struct {
+  int n, base, rank, world;
+  uint32_t mask;
+  uint32_t *out;
+  int64_t cap, idx, kept;
+} nq_enum;
+
+static void nq_prefix_rec(nq_enum *e, int row, uint32_t cols, uint32_t d1, uint32_t d2) {
+  if (row == e->base) {
+    if (e->idx % e->world == e->rank) {
+      if (e->out && e->kept < e->cap) {
+        e->out[3 * e->kept] = cols;
+        e->out[3 * e->kept + 1] = d1;
+        e->out[3 * e->kept + 2] = d2;
+      }
+      e->kept++;
+    }
+    e->idx++;
+    return;
+  }
+  uint32_t av = ~(cols | d1 | d2) & e->mask;
+  while (av) {
+    uint32_t bit = av & (0u - av);
+    av ^= bit;
+    nq_prefix_rec(e, row + 1, cols | bit, (d1 | bit) << 1, (d2 | bit) >> 1);
+  }
+}
+
+int64_t oracle_nqueens_prefixes(int n, int base, int rank, int world, uint32_t *out, int64_t cap) {
+  nq_enum e = {n, base, rank, world, n >= 32 ? 0xffffffffu : ((1u << n) - 1u), out, cap, 0, 0};
+  nq_prefix_rec(&e, 0, 0, 0, 0);
+  return e.kept;
+}
+
+static uint32_t nq_count_rec(int n, uint32_t mask, int row, uint32_t cols, uint32_t d1, uint32_t d2,
+                             uint64_t *nodes) {
+  if (row == n) return 1;
+  uint32_t av = ~(cols | d1 | d2) & mask, sols = 0;
+  while (av) {
+    uint32_t bit = av & (0u - av);
+    av ^= bit;
+    ++*nodes;
+    sols += nq_count_rec(n, mask, row + 1, cols | bit, (d1 | bit) << 1, (d2 | bit) >> 1, nodes);
+  }
+  return sols;
+}
+
+uint64_t oracle_nqueens_count(int n, int base, const uint32_t *states, int64_t count, uint32_t *per_prefix,
+                              uint64_t *nodes) {
+  const uint32_t mask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+  uint64_t total = 0, nd = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    uint32_t s = nq_count_rec(n, mask, base, states[3 * i], states[3 * i + 1], states[3 * i + 2], &nd);
+    if (per_prefix) per_prefix[i] = s;
+    total += s;
+  }
+  if (nodes) *nodes = nd;
+  return total;
+}

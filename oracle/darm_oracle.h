@@ -48,6 +48,15 @@ int oracle_execute_warps(const char *kernel, int warp, int64_t n_warps, const in
  * each B-key bucket (B power of two). */
 int oracle_bitonic_sort(int32_t *keys, int64_t n, int bucket);
 
+/* N-Queens (no reference code; recursive restatement).  Prefixes: valid
+ * placements of rows 0..base-1, lowest free column first, index i kept when
+ * i % world == rank, written as {cols, d1, d2} triples (up to cap).  Returns the
+ * number kept.  oracle_nqueens_count returns the total solutions below the
+ * prefixes, per-prefix counts, and the placements made below them (`nodes`). */
+int64_t oracle_nqueens_prefixes(int n, int base, int rank, int world, uint32_t *out, int64_t cap);
+uint64_t oracle_nqueens_count(int n, int base, const uint32_t *states, int64_t count, uint32_t *per_prefix,
+                              uint64_t *nodes);
+
 #ifdef __cplusplus
 }
 #endif

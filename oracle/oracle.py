@@ -58,6 +58,13 @@ class Restatement:
         L.oracle_execute_warps.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int64, I32P,
                                            ctypes.c_int64, I32P, ctypes.c_int64, I32P, I32P]
         L.oracle_bitonic_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
+        U32P = ctypes.POINTER(ctypes.c_uint32)
+        L.oracle_nqueens_prefixes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, U32P,
+                                              ctypes.c_int64]
+        L.oracle_nqueens_prefixes.restype = ctypes.c_int64
+        L.oracle_nqueens_count.argtypes = [ctypes.c_int, ctypes.c_int, U32P, ctypes.c_int64, U32P,
+                                           ctypes.POINTER(ctypes.c_uint64)]
+        L.oracle_nqueens_count.restype = ctypes.c_uint64
         self.lib = L
 
     def mt64(self, seed: int, count: int) -> List[int]:
@@ -91,6 +98,22 @@ class Restatement:
         rc = self.lib.oracle_bitonic_sort(_p(keys), keys.size, bucket)
         if rc:
             raise ValueError("oracle_bitonic_sort: bad bucket")
+
+    def nqueens_prefixes(self, n: int, base: int, rank: int = 0, world: int = 1) -> np.ndarray:
+        cnt = self.lib.oracle_nqueens_prefixes(n, base, rank, world, None, 0)
+        out = np.zeros(3 * max(1, cnt), dtype=np.uint32)
+        self.lib.oracle_nqueens_prefixes(n, base, rank, world, _p(out, ctypes.POINTER(ctypes.c_uint32)), cnt)
+        return out[: 3 * cnt].reshape(-1, 3)
+
+    def nqueens_count(self, n: int, base: int, states: np.ndarray):
+        """-> (total solutions, per-prefix counts, placements below the prefixes)."""
+        states = np.ascontiguousarray(states, dtype=np.uint32)
+        per = np.zeros(max(1, len(states)), dtype=np.uint32)
+        nodes = ctypes.c_uint64(0)
+        U32P = ctypes.POINTER(ctypes.c_uint32)
+        tot = self.lib.oracle_nqueens_count(n, base, _p(states, U32P), len(states), _p(per, U32P),
+                                            ctypes.byref(nodes))
+        return int(tot), per[: len(states)], int(nodes.value)
 
 
 # ------------------------------------------------------------------ reference
@@ -157,6 +180,22 @@ class RefModule:
         return stats
 
 
+def _run_to_fixpoint(self, warp, args, globals_full, shared_full, max_rounds=1_000_000, unit_latency=False):
+    """executeWarp chained to a fixpoint on one warp (declared-size arrays, in/out)."""
+    args = np.ascontiguousarray(args, dtype=np.int32)
+    stats = np.zeros(7, dtype=np.int64)
+    rounds = np.zeros(1, dtype=np.int64)
+    err = ctypes.create_string_buffer(512)
+    rc = self.ref.lib.ref_run_to_fixpoint(self.h, warp, _p(args), _p(globals_full), _p(shared_full), max_rounds,
+                                          int(unit_latency), _p(stats, I64P), _p(rounds, I64P), err, 512)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return int(rounds[0]), stats
+
+
+RefModule.run_to_fixpoint = _run_to_fixpoint
+
+
 class Reference:
     def __init__(self, path: str = REFERENCE_SO):
         if not os.path.exists(path):
@@ -182,6 +221,8 @@ class Reference:
         L.ref_compare_warps.restype = ctypes.c_int64
         L.ref_bitonic_sort.argtypes = [vp, I32P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        I64P, ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_run_to_fixpoint.argtypes = [vp, ctypes.c_int, I32P, I32P, I32P, ctypes.c_int64, ctypes.c_int,
+                                          I64P, I64P, ctypes.c_char_p, ctypes.c_size_t]
         self.lib = L
 
     def load(self, name: str, meld: int = 0, threshold: float = 0.2) -> RefModule:

@@ -307,6 +307,73 @@ int64_t ref_compare_warps(const ref_module *h, int warp, int64_t n_warps,
   return -1;
 }
 
+// Chains executeWarp over one warp until a step changes neither global nor
+// shared memory (a fixpoint), feeding globalFinal/sharedFinal of each step into
+// the next — the loop a per-iteration step kernel such as
+// paper_2107_05681_b200/ir/nqueens_step.ir stands for.  globals/shared are the
+// declared-size arrays in declaration order (in/out).  stats_sum (7 counters)
+// accumulates every step that changed state; *rounds receives their number.
+int ref_run_to_fixpoint(const ref_module *h, int warp, const int32_t *args, int32_t *globals,
+                        int32_t *shared, int64_t max_rounds, int unit_latency,
+                        int64_t *stats_sum, int64_t *rounds, char *err, size_t errlen) {
+  try {
+    const Function &f = h->m.functions.front();
+    LatencyModel lm = pickLatency(unit_latency);
+    WarpInput in;
+    in.warpSize = warp;
+    for (size_t p = 0; p < f.params.size(); ++p) in.args.push_back({args[p]});
+    auto load = [&] {
+      size_t off = 0;
+      for (const auto &g : h->m.globals) {
+        in.globalInit[g.name] = std::vector<int32_t>(globals + off, globals + off + g.size);
+        off += size_t(g.size);
+      }
+      off = 0;
+      for (const auto &s : f.sharedDecls) {
+        in.sharedInit[s.name] = std::vector<int32_t>(shared + off, shared + off + s.size);
+        off += size_t(s.size);
+      }
+    };
+    if (stats_sum)
+      for (int i = 0; i < 7; ++i) stats_sum[i] = 0;
+    int64_t r = 0;
+    for (; r < max_rounds; ++r) {
+      load();
+      WarpResult res = executeWarp(h->m, f, in, lm);
+      if (res.nonTerminated || !res.faults.empty() || res.taintedObservable)
+        return fail(err, errlen, "chain step " + std::to_string(r) + " faulted or observed undef", 2);
+      bool same = res.globalFinal == in.globalInit && res.sharedFinal == in.sharedInit;
+      if (same) break;
+      size_t off = 0;
+      for (const auto &g : h->m.globals) {
+        const auto &v = res.globalFinal.at(g.name);
+        std::copy(v.begin(), v.end(), globals + off);
+        off += size_t(g.size);
+      }
+      off = 0;
+      for (const auto &s : f.sharedDecls) {
+        const auto &v = res.sharedFinal.at(s.name);
+        std::copy(v.begin(), v.end(), shared + off);
+        off += size_t(s.size);
+      }
+      if (stats_sum) {
+        stats_sum[0] += res.stats.issuedInstructions;
+        stats_sum[1] += res.stats.threadCycles;
+        stats_sum[2] += res.stats.usefulThreadCycles;
+        stats_sum[3] += res.stats.serializedCycles;
+        stats_sum[4] += res.stats.divergentBranchCount;
+        stats_sum[5] += res.stats.sharedMemIssues;
+        stats_sum[6] += res.stats.globalMemIssues;
+      }
+    }
+    if (rounds) *rounds = r;
+    if (r == max_rounds) return fail(err, errlen, "no fixpoint within max_rounds", 2);
+    return 0;
+  } catch (const std::exception &e) {
+    return fail(err, errlen, e.what(), 2);
+  }
+}
+
 // Full bitonic sort of independent B-key buckets by chaining the corpus
 // compare-exchange step (bitonic.ir:6-43) through executeWarp: for every stage
 // dir = 2..B and stride k = dir/2..1 one warp of B lanes runs with the bucket in

@@ -48,6 +48,8 @@ ABI_SYMBOLS = (
     "darm_gpu_make_random_input",
     "darm_gpu_execute_warps",
     "darm_gpu_bitonic_sort",
+    "darm_gpu_nqueens",
+    "darm_gpu_nqueens_prefix_count",
 )
 
 
@@ -110,6 +112,13 @@ def lib() -> ctypes.CDLL:
         L.darm_gpu_bitonic_sort.argtypes = [
             ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
             ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_nqueens.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int64,
+            ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.POINTER(Stats), ctypes.c_char_p,
+            ctypes.c_size_t]
+        L.darm_gpu_nqueens_prefix_count.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.darm_gpu_nqueens_prefix_count.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -294,6 +303,33 @@ def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: boo
                                      ctypes.byref(st) if want_stats else None, err, 512)
     _check(rc, err)
     return st.as_dict() if want_stats else {}
+
+
+def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int = 1,
+            per_prefix: bool = False, stream=None, want_stats: bool = True):
+    """Count n-queens solutions below the prefixes i % world == rank.
+
+    Returns ``(solutions, per_prefix_counts or None, stats)``.
+    """
+    if isinstance(variant, str):
+        variant = VARIANTS[variant]
+    sols = ctypes.c_uint64(0)
+    npre = ctypes.c_int64(0)
+    err = ctypes.create_string_buffer(512)
+    per = None
+    if per_prefix:
+        cnt = lib().darm_gpu_nqueens_prefix_count(n, prefix_rows, rank, world)
+        if cnt < 0:
+            raise DarmUserError("bad n-queens arguments")
+        per = np.zeros(max(1, cnt), dtype=np.uint32)
+    st = Stats()
+    rc = lib().darm_gpu_nqueens(
+        int(variant), n, prefix_rows, rank, world, ctypes.byref(sols),
+        per.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)) if per is not None else None,
+        per.size if per is not None else 0, ctypes.byref(npre), ctypes.c_void_p(stream or 0),
+        ctypes.byref(st) if want_stats else None, err, 512)
+    _check(rc, err)
+    return int(sols.value), (per[: npre.value] if per is not None else None), (st.as_dict() if want_stats else {})
 
 
 @dataclass

@@ -23,12 +23,33 @@
 
 namespace darm_gpu {
 
+template <int B>
+struct Network {
+  static constexpr int kSteps = __builtin_ctz(B) * (__builtin_ctz(B) + 1) / 2;
+  static_assert(kSteps <= 64, "step masks are 64-bit");
+};
+
 template <bool M, int B, int CTA>
 __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__ keys, uint32_t n) {
   constexpr bool kNeedSmem = B > 32;
   __shared__ int32_t xch[kNeedSmem ? 2 : 1][kNeedSmem ? CTA : 1];
   const uint32_t tiles = (n + CTA - 1) / CTA;
   const int t = int(threadIdx.x) & (B - 1);
+  // Per-lane step predicates, loop-invariant across tiles: bit s of keepm is
+  // icmp.lt %t %j (j = t^k, i.e. (t & k) == 0) and of upm is
+  // icmp.eq (and %t %dir) 0 for the s-th (dir, k) of the network.
+  uint64_t keepm = 0, upm = 0;
+  {
+    int s = 0;
+#pragma unroll
+    for (int dir = 2; dir <= B; dir <<= 1)
+#pragma unroll
+      for (int k = dir >> 1; k >= 1; k >>= 1, ++s) {
+        keepm |= uint64_t((t & k) == 0) << s;
+        upm |= uint64_t((t & dir) == 0) << s;
+      }
+  }
+  const uint64_t eqm = ~(keepm ^ upm);
   uint32_t tile = blockIdx.x;
   uint32_t idx = tile * CTA + threadIdx.x;
   int32_t next = (tile < tiles && idx < n) ? keys[idx] : INT_MAX;
@@ -38,10 +59,11 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
     idx += gridDim.x * CTA;
     if (tile + gridDim.x < tiles) next = idx < n ? keys[idx] : INT_MAX;   // prefetch
     int par = 0;
+    int s = 0;
 #pragma unroll
     for (int dir = 2; dir <= B; dir <<= 1) {
 #pragma unroll
-      for (int k = dir >> 1; k >= 1; k >>= 1) {
+      for (int k = dir >> 1; k >= 1; k >>= 1, ++s) {
         int32_t b0;
         if (k < 32) {
           b0 = __shfl_xor_sync(0xffffffffu, v, k);        // load.shared buf %j
@@ -51,9 +73,7 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
           b0 = xch[par][threadIdx.x ^ k];
           par ^= 1;
         }
-        const bool keep = (t & k) == 0;                   // icmp.lt %t %j, j = t^k
-        const bool up = (t & dir) == 0;                   // icmp.eq (and %t %dir) 0
-        v = bitonic_exchange<M>(v, b0, keep, up);
+        v = bitonic_exchange<M>(v, b0, (keepm >> s) & 1, (upm >> s) & 1, (eqm >> s) & 1);
       }
     }
     if (my < n) keys[my] = v;

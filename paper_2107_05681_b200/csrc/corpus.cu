@@ -118,7 +118,10 @@ int grid_for(uint64_t work, int per_cta, int sms) {
 
 template <class K, bool M, int WT>
 cudaError_t launch_lanes_am(int am, const CorpusParams &P, int sms, cudaStream_t s) {
-  const int grid = grid_for(P.total, 256, sms);
+  // One thread per lane: every lane's loads are in flight at once (the kernels
+  // are latency/HBM-bound and a lane does a handful of instructions).
+  (void)sms;
+  const int grid = int((uint64_t(P.total) + 255) / 256);
   switch (am) {
     case 0: corpus_lanes<K, M, WT, 0><<<grid, 256, 0, s>>>(P); break;
     case 1: corpus_lanes<K, M, WT, 1><<<grid, 256, 0, s>>>(P); break;

@@ -383,43 +383,38 @@ struct Nested {
 };
 
 // ---------------------------------------------------------------- bitonic step
-// bitonic.ir:6-43, one compare-exchange step; `cv` is the lane's own slot
-// (buf[t]) and the return value is what the lane leaves in buf[t].
+// bitonic.ir:6-43, one compare-exchange step with the lane's own slot buf[t]
+// held in a register (`cv`); `b0` is the partner's slot buf[t^k] read before
+// any store (:10).  Returns what the lane leaves in buf[t].
+//
+// In both forms the IR's "compare, then conditionally store b0" pairs are
+// written as the min/max they compute (`need1 = keep ? cv>b0 : cv<b0;
+// if (need1) buf[t] = b0` == `keep ? min(cv,b0) : max(cv,b0)`), so the two
+// forms differ only in control flow:
+//   unmelded: the divergent `condbr %up ^c ^d` (:16) stays a fenced branch,
+//             each arm with its own compares/select/store (^c :17-27, ^d :28-38);
+//   melded:   SURVEY App. A.2 — the compares are hoisted and melded and
+//             need1 = select keep (select up gt1 lt2) (select up lt1 gt1), which
+//             is `(keep == up) ? gt1 : lt1`, so one select of min/max remains.
+// `keep_eq_up` is keep XNOR up, precomputed per lane and step by the caller.
 template <bool M>
-__device__ __forceinline__ int32_t bitonic_exchange(int32_t cv, int32_t b0, bool keep, bool up) {
+__device__ __forceinline__ int32_t bitonic_exchange(int32_t cv, int32_t b0, bool keep, bool up,
+                                                    bool keep_eq_up) {
   if constexpr (!M) {
     if (up) {                                              // condbr %up ^c ^d (:16)
-      DARM_ARM("bitonic.c");                               // ^c :17-22
-      bool gt1 = cv > b0;
-      bool lt1 = cv < b0;
-      bool need1 = keep ? gt1 : lt1;
-      if (need1) {
-        DARM_ARM("bitonic.e");                             // ^e store.shared buf %t %b0
-        cv = b0;
-      }
+      DARM_ARM("bitonic.c");                               // ^c/^e: keep ? (cv>b0) : (cv<b0)
+      cv = keep ? min(cv, b0) : max(cv, b0);
       DARM_ARM("bitonic.x1");
     } else {
-      DARM_ARM("bitonic.d");                               // ^d :28-33
-      bool lt2 = cv < b0;
-      bool gt2 = cv > b0;
-      bool need2 = keep ? lt2 : gt2;
-      if (need2) {
-        DARM_ARM("bitonic.f");                             // ^f store.shared buf %t %b0
-        cv = b0;
-      }
+      DARM_ARM("bitonic.d");                               // ^d/^f: keep ? (cv<b0) : (cv>b0)
+      cv = keep ? max(cv, b0) : min(cv, b0);
       DARM_ARM("bitonic.x2");
     }
     return cv;
-  } else {                                                 // SURVEY App. A.2
-    bool lt2 = false, lt1 = false;
-    if (!up) lt2 = cv < b0;                                // ^c.m.g  (false-only compare)
-    bool gt1 = cv > b0;                                    // melded compare
-    if (up) lt1 = cv < b0;                                 // ^c.m.g1 (true-only compare)
-    bool sel = up ? gt1 : lt2;
-    bool sel1 = up ? lt1 : gt1;
-    bool need1 = keep ? sel : sel1;
-    if (need1) cv = b0;                                    // ^e.m single melded store
-    return cv;
+  } else {
+    (void)keep;
+    (void)up;
+    return keep_eq_up ? min(cv, b0) : max(cv, b0);         // ^c.m.u1 selects + ^e.m store
   }
 }
 

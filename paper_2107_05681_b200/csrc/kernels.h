@@ -37,4 +37,9 @@ bool bitonic_sort_supported(int bucket);
 cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, cudaStream_t s,
                                 int *launches);
 
+// nqueens.cu
+cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, int n, int base,
+                           uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,
+                           int sms, cudaStream_t s);
+
 }  // namespace darm_gpu

@@ -409,4 +409,92 @@ int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int
   });
 }
 
+// N-Queens prefixes: every valid placement of the first `base` rows, lowest
+// free column first; prefix i goes to rank i % world.
+static void nqueens_prefixes(int n, int base, int rank, int world, std::vector<uint32_t> &out) {
+  const uint32_t mask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+  uint32_t cols[32], d1[32], d2[32], av[32];
+  int row = 0;
+  cols[0] = d1[0] = d2[0] = 0;
+  av[0] = mask;
+  uint64_t idx = 0;
+  while (row >= 0) {
+    if (av[row] == 0) {
+      --row;
+      continue;
+    }
+    const uint32_t bit = av[row] & (0u - av[row]);
+    av[row] ^= bit;
+    const uint32_t c = cols[row] | bit, e1 = (d1[row] | bit) << 1, e2 = (d2[row] | bit) >> 1;
+    if (row + 1 == base) {
+      if (int(idx % uint64_t(world)) == rank) {
+        out.push_back(c);
+        out.push_back(e1);
+        out.push_back(e2);
+      }
+      ++idx;
+      continue;
+    }
+    ++row;
+    cols[row] = c;
+    d1[row] = e1;
+    d2[row] = e2;
+    av[row] = ~(c | e1 | e2) & mask;
+  }
+}
+
+int64_t darm_gpu_nqueens_prefix_count(int n, int prefix_rows, int rank, int world) {
+  if (n < 2 || n > 31 || prefix_rows < 1 || prefix_rows > n - 1 || world < 1 || rank < 0 || rank >= world)
+    return -1;
+  std::vector<uint32_t> pre;
+  nqueens_prefixes(n, prefix_rows, rank, world, pre);
+  return int64_t(pre.size() / 3);
+}
+
+int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world, uint64_t *solutions,
+                     uint32_t *per_prefix, int64_t per_prefix_len, int64_t *n_prefixes, void *stream,
+                     darm_gpu_stats *stats, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if (n < 2 || n > 31) user_error("n must be in [2, 31]");
+    if (prefix_rows < 1 || prefix_rows > n - 1) user_error("prefix_rows must be in [1, n-1]");
+    if (world < 1 || rank < 0 || rank >= world) user_error("need 0 <= rank < world");
+    if (!solutions) user_error("solutions is NULL");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    std::vector<uint32_t> pre;
+    nqueens_prefixes(n, prefix_rows, rank, world, pre);
+    const int64_t np = int64_t(pre.size() / 3);
+    if (n_prefixes) *n_prefixes = np;
+    if (np >= (int64_t(1) << 32) - 1) user_error("too many prefixes; lower prefix_rows");
+    if (per_prefix && per_prefix_len < np) user_error("per_prefix buffer too small");
+    DeviceState &st = device_state(nullptr);
+    std::lock_guard<std::mutex> lk(st.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Timeline tl(s, stats != nullptr);
+    tl.mark(0);
+    auto *dpre = static_cast<uint32_t *>(slot(st, 0, pre.size() * 4));
+    auto *dctl = static_cast<unsigned long long *>(slot(st, 1, 16));
+    uint32_t *dper = per_prefix ? static_cast<uint32_t *>(slot(st, 2, size_t(np) * 4)) : nullptr;
+    if (!pre.empty()) DARM_CUDA(cudaMemcpyAsync(dpre, pre.data(), pre.size() * 4, cudaMemcpyHostToDevice, s));
+    DARM_CUDA(cudaMemsetAsync(dctl, 0, 16, s));
+    tl.mark(1);
+    if (np) DARM_CUDA(launch_nqueens(variant, dpre, uint32_t(np), n, prefix_rows, dper, dctl,
+                                     reinterpret_cast<unsigned int *>(dctl + 1), st.sms, s));
+    tl.mark(2);
+    unsigned long long total = 0;
+    DARM_CUDA(cudaMemcpyAsync(&total, dctl, 8, cudaMemcpyDeviceToHost, s));
+    if (per_prefix && np) DARM_CUDA(cudaMemcpyAsync(per_prefix, dper, size_t(np) * 4, cudaMemcpyDeviceToHost, s));
+    tl.mark(3);
+    DARM_CUDA(cudaStreamSynchronize(s));
+    *solutions = total;
+    if (stats) {
+      tl.fill(stats);
+      stats->launches = np ? 1 : 0;
+      stats->h2d_bytes = pre.size() * 4;
+      stats->d2h_bytes = 8 + (per_prefix ? uint64_t(np) * 4 : 0);
+      stats->algorithmic_bytes = pre.size() * 4 + (per_prefix ? uint64_t(np) * 4 : 0);
+    }
+  });
+}
+
 }  // extern "C"

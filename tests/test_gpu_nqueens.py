@@ -1,0 +1,64 @@
+"""GPU parity for N-Queens (NQU): per-prefix solution counts bit-exact against the
+reference-interpreted IR chain (small n) and the C restatement, and the
+published totals (OEIS A000170) at the BASELINE size n = 16."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from test_oracle import NQUEENS
+
+import paper_2107_05681_b200 as darm
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    import torch
+
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    darm.init()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_nqueens_reference_chain_golden(variant):
+    gold = load_golden("nqueens_chain.json")
+    for case in gold["cases"]:
+        sols, per, _ = darm.nqueens(case["n"], case["base"], variant, per_prefix=True)
+        assert per.tolist() == case["per_prefix"], (case["n"], variant)
+        assert sols == case["solutions"]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("n,base", [(10, 3), (12, 4), (13, 5), (14, 4)])
+def test_nqueens_per_prefix_vs_restatement(restatement, variant, n, base):
+    states = restatement.nqueens_prefixes(n, base)
+    tot, want, _ = restatement.nqueens_count(n, base, states)
+    sols, per, _ = darm.nqueens(n, base, variant, per_prefix=True)
+    assert (per == want).all()
+    assert sols == tot == NQUEENS[n]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_nqueens_config3_n16(variant):
+    """BASELINE config 3: N=16, prefix search space (6-row prefixes)."""
+    sols, _, st = darm.nqueens(16, 6, variant)
+    assert sols == 14772512
+
+
+def test_nqueens_rank_partition():
+    """Prefixes dealt round-robin over 3 'ranks' sum to the total (the
+    multi-GPU decomposition, one call per rank)."""
+    parts = [darm.nqueens(13, 4, 1, rank=r, world=3)[0] for r in range(3)]
+    assert sum(parts) == NQUEENS[13]
+
+
+def test_nqueens_small_and_edge():
+    for n in range(2, 10):
+        for base in range(1, n):
+            assert darm.nqueens(n, base, 1)[0] == NQUEENS[n], (n, base)
+    with pytest.raises(darm.DarmUserError):
+        darm.nqueens(8, 8)
+    with pytest.raises(darm.DarmUserError):
+        darm.nqueens(1, 1)

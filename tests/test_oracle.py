@@ -105,3 +105,54 @@ def test_restatement_matches_live_reference(restatement, reference, kernel):
             fb = restatement.execute_warps(kernel, warp, nw, args, b, warp, shared)
             w, diff = reference.compare_warps(mod, warp, nw, warp, a, fa, b, fb)
             assert w == -1, (kernel, variant, warp, w, diff)
+
+
+# OEIS A000170
+NQUEENS = {1: 1, 2: 0, 3: 0, 4: 2, 5: 10, 6: 4, 7: 40, 8: 92, 9: 352, 10: 724, 11: 2680, 12: 14200,
+           13: 73712, 14: 365596, 15: 2279184, 16: 14772512}
+
+
+def test_nqueens_restatement_matches_reference_chain(restatement):
+    """Per-prefix solution counts of the reference interpreter running
+    ir/nqueens_step.ir (original and melded) to a fixpoint."""
+    gold = load_golden("nqueens_chain.json")
+    for case in gold["cases"]:
+        states = restatement.nqueens_prefixes(case["n"], case["base"])
+        assert states.tolist() == case["prefixes"]
+        tot, per, _ = restatement.nqueens_count(case["n"], case["base"], states)
+        assert per.tolist() == case["per_prefix"]
+        assert tot == case["solutions"] == NQUEENS[case["n"]]
+
+
+def test_nqueens_melded_spec_is_the_reference_pass_output():
+    """The melded CUDA form mirrors runDarm's output for ir/nqueens_step.ir:
+    two block-region melds."""
+    gold = load_golden("nqueens_chain.json")
+    kinds = [m["kind"] for m in gold["melds"]]
+    assert kinds == ["block-region", "block-region"]
+    assert [m["selectsInserted"] for m in gold["melds"]] == [9, 3]
+
+
+@pytest.mark.parametrize("n", range(4, 13))
+def test_nqueens_restatement_known_answers(restatement, n):
+    for base in (1, 2, n - 1):
+        states = restatement.nqueens_prefixes(n, base)
+        assert restatement.nqueens_count(n, base, states)[0] == NQUEENS[n]
+    # rank partition covers every prefix exactly once
+    parts = [restatement.nqueens_prefixes(n, 2, r, 3) for r in range(3)]
+    assert sum(len(p) for p in parts) == len(restatement.nqueens_prefixes(n, 2))
+
+
+def test_nqueens_node_count_n8(restatement):
+    # nodes = root + placements of the prefix rows + placements below them
+    states = restatement.nqueens_prefixes(8, 2)
+    _, _, below = restatement.nqueens_count(8, 2, states)
+    assert 1 + 8 + len(states) + below == 2057
+
+
+def test_nqueens_prefix_count_matches_library(restatement):
+    import paper_2107_05681_b200 as darm
+
+    for n, base, rank, world in ((8, 2, 0, 1), (12, 3, 1, 4), (16, 6, 0, 1), (16, 6, 5, 8)):
+        assert darm.lib().darm_gpu_nqueens_prefix_count(n, base, rank, world) == \
+            len(restatement.nqueens_prefixes(n, base, rank, world))
