@@ -145,6 +145,17 @@ int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world,
                      int64_t *n_prefixes, void *stream, darm_gpu_stats *stats,
                      char *err, size_t errlen);
 
+/* ---- LUD (Rodinia lud, no reference code): blocked LU
+ *      decomposition without pivoting, BLOCK = 16, in place ----------------
+ * a: n x n row-major fp32 (n % 16 == 0, 16 <= n <= 46336); on return the
+ * strictly lower part holds L (unit diagonal implied) and the upper part U.
+ * Diagonal, perimeter (the melded kernel) and internal launches for every
+ * 16-column step are replayed from a cached CUDA graph.  DEVICE pointers must
+ * be 16-byte aligned.  Operation order is fixed, so the
+ * result is identical for both forms and across runs. */
+int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream,
+                 darm_gpu_stats *stats, char *err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

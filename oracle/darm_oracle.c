@@ -17,6 +17,9 @@
  */
 #include "darm_oracle.h"
 
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
 #include <string.h>
 
 /* ------------------------------------------------------------ mt19937_64 */
@@ -272,4 +275,105 @@ uint64_t oracle_nqueens_count(int n, int base, const uint32_t *states, int64_t c
   }
   if (nodes) *nodes = nd;
   return total;
+}
+
+/* ------------------------------------------------------------ LUD
+ * Blocked LU without pivoting, BLOCK = 16 (no reference code; Rodinia's
+ * diagonal / perimeter / internal order).  Every update is
+ * written as the single-rounding fmaf / division / subtraction the CUDA
+ * kernels (paper_2107_05681_b200/csrc/lud.cu) perform, in the same order, so
+ * the results agree bit for bit.  The internal update is split over threads
+ * by rows (rows are independent). */
+#define LUD_BS 16
+
+__attribute__((target("fma"))) static float fma_hw(float a, float b, float c) { return __builtin_fmaf(a, b, c); }
+static float fma_sw(float a, float b, float c) { return fmaf(a, b, c); }
+static float (*lud_fma)(float, float, float) = fma_sw;
+
+typedef struct {
+  float *a;
+  int64_t n, o, r0, r1;
+} lud_job;
+
+/* Per row r: sums[c] = fma(L[r][k], U[k][c], sums[c]) for k = 0..15 (the
+ * per-element order of the GPU kernel, vectorised across c), then
+ * a[r][c] -= sums[c]. */
+#define LUD_ROWS_BODY(FMA)                                                   \
+  lud_job *j = (lud_job *)p;                                                 \
+  float *a = j->a;                                                           \
+  const int64_t n = j->n, o = j->o, w = n - o - LUD_BS;                      \
+  float *sums = (float *)malloc(sizeof(float) * (size_t)(w > 0 ? w : 1));    \
+  for (int64_t r = j->r0; r < j->r1; ++r) {                                  \
+    float *ar = a + r * n + o + LUD_BS;                                      \
+    for (int64_t c = 0; c < w; ++c) sums[c] = 0.f;                           \
+    for (int k = 0; k < LUD_BS; ++k) {                                       \
+      const float l = a[r * n + o + k];                                      \
+      const float *u = a + (o + k) * n + o + LUD_BS;                         \
+      for (int64_t c = 0; c < w; ++c) sums[c] = FMA(l, u[c], sums[c]);       \
+    }                                                                        \
+    for (int64_t c = 0; c < w; ++c) ar[c] = ar[c] - sums[c];                 \
+  }                                                                          \
+  free(sums);                                                                \
+  return NULL;
+
+__attribute__((target("fma"))) static void *lud_internal_rows_fma(void *p) { LUD_ROWS_BODY(__builtin_fmaf) }
+static void *lud_internal_rows_sw(void *p) { LUD_ROWS_BODY(fmaf) }
+
+int oracle_lud(float *a, int64_t n, int threads) {
+  if (n < LUD_BS || n % LUD_BS) return 2;
+  lud_fma = __builtin_cpu_supports("fma") ? fma_hw : fma_sw;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  for (int64_t o = 0; o < n; o += LUD_BS) {
+    float *d = a + o * n + o;
+    /* diagonal: column i of L, then row i+1 of U */
+    for (int i = 0; i < LUD_BS - 1; ++i) {
+      for (int r = i + 1; r < LUD_BS; ++r) {
+        float x = d[r * n + i];
+        for (int j = 0; j < i; ++j) x = lud_fma(-d[r * n + j], d[j * n + i], x);
+        d[r * n + i] = x / d[i * n + i];
+      }
+      for (int c = i + 1; c < LUD_BS; ++c) {
+        float x = d[(i + 1) * n + c];
+        for (int j = 0; j < i + 1; ++j) x = lud_fma(-d[(i + 1) * n + j], d[j * n + c], x);
+        d[(i + 1) * n + c] = x;
+      }
+    }
+    if (o + LUD_BS >= n) break;
+    /* perimeter: U12 = L11^-1 A12 (forward substitution per column) */
+    for (int64_t c = o + LUD_BS; c < n; ++c)
+      for (int i = 1; i < LUD_BS; ++i) {
+        float x = a[(o + i) * n + c];
+        for (int j = 0; j < i; ++j) x = lud_fma(-d[i * n + j], a[(o + j) * n + c], x);
+        a[(o + i) * n + c] = x;
+      }
+    /* perimeter: L21 = A21 U11^-1 (per row) */
+    for (int64_t r = o + LUD_BS; r < n; ++r)
+      for (int i = 0; i < LUD_BS; ++i) {
+        float x = a[r * n + o + i];
+        for (int j = 0; j < i; ++j) x = lud_fma(-a[r * n + o + j], d[j * n + i], x);
+        a[r * n + o + i] = x / d[i * n + i];
+      }
+    /* internal: A22 -= L21 U12, sum over k = 0..15 then one subtraction */
+    const int64_t rows = n - o - LUD_BS;
+    int t = (int)(rows < threads ? rows : threads);
+    if (rows * (n - o) < (1 << 16)) t = 1;
+    pthread_t tid[256];
+    lud_job jobs[256];
+    void *(*rows_fn)(void *) = lud_fma == fma_hw ? lud_internal_rows_fma : lud_internal_rows_sw;
+    for (int q = 0; q < t; ++q) {
+      jobs[q].a = a;
+      jobs[q].n = n;
+      jobs[q].o = o;
+      jobs[q].r0 = o + LUD_BS + rows * q / t;
+      jobs[q].r1 = o + LUD_BS + rows * (q + 1) / t;
+      if (t > 1)
+        pthread_create(&tid[q], NULL, rows_fn, &jobs[q]);
+      else
+        rows_fn(&jobs[q]);
+    }
+    if (t > 1)
+      for (int q = 0; q < t; ++q) pthread_join(tid[q], NULL);
+  }
+  return 0;
 }

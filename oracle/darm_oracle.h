@@ -57,6 +57,11 @@ int64_t oracle_nqueens_prefixes(int n, int base, int rank, int world, uint32_t *
 uint64_t oracle_nqueens_count(int n, int base, const uint32_t *states, int64_t count, uint32_t *per_prefix,
                               uint64_t *nodes);
 
+/* LUD (no reference code): blocked LU without pivoting, BLOCK = 16, in
+ * place, in exactly the floating-point operation order of csrc/lud.cu.
+ * threads > 1 splits the internal update by rows (pthreads). */
+int oracle_lud(float *a, int64_t n, int threads);
+
 #ifdef __cplusplus
 }
 #endif

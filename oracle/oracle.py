@@ -58,6 +58,7 @@ class Restatement:
         L.oracle_execute_warps.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int64, I32P,
                                            ctypes.c_int64, I32P, ctypes.c_int64, I32P, I32P]
         L.oracle_bitonic_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
+        L.oracle_lud.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int]
         U32P = ctypes.POINTER(ctypes.c_uint32)
         L.oracle_nqueens_prefixes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, U32P,
                                               ctypes.c_int64]
@@ -98,6 +99,14 @@ class Restatement:
         rc = self.lib.oracle_bitonic_sort(_p(keys), keys.size, bucket)
         if rc:
             raise ValueError("oracle_bitonic_sort: bad bucket")
+
+    def lud(self, a: np.ndarray, threads: int = 0) -> None:
+        """In-place blocked LU in csrc/lud.cu's operation order."""
+        assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"] and a.shape[0] == a.shape[1]
+        rc = self.lib.oracle_lud(a.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), a.shape[0],
+                                 threads or (os.cpu_count() or 1))
+        if rc:
+            raise ValueError("oracle_lud: n must be a multiple of 16")
 
     def nqueens_prefixes(self, n: int, base: int, rank: int = 0, world: int = 1) -> np.ndarray:
         cnt = self.lib.oracle_nqueens_prefixes(n, base, rank, world, None, 0)

@@ -23,6 +23,7 @@ call raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 import json
 import os
 from dataclasses import dataclass, field
@@ -50,6 +51,7 @@ ABI_SYMBOLS = (
     "darm_gpu_bitonic_sort",
     "darm_gpu_nqueens",
     "darm_gpu_nqueens_prefix_count",
+    "darm_gpu_lud",
 )
 
 
@@ -119,6 +121,8 @@ def lib() -> ctypes.CDLL:
             ctypes.c_size_t]
         L.darm_gpu_nqueens_prefix_count.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.darm_gpu_nqueens_prefix_count.restype = ctypes.c_int64
+        L.darm_gpu_lud.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                   ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
         _lib = L
     return _lib
 
@@ -144,12 +148,17 @@ def kernel_list() -> List[str]:
     return lib().darm_gpu_kernel_list().decode().split(",")
 
 
-def kernel_info(kernel: str) -> dict:
+@functools.lru_cache(maxsize=None)
+def _kernel_info_json(kernel: str) -> str:
     buf = ctypes.create_string_buffer(4096)
     n = lib().darm_gpu_kernel_info(kernel.encode(), buf, 4096)
     if n == 0:
         raise DarmUserError(f"unknown kernel '{kernel}'")
-    return json.loads(buf.value.decode())
+    return buf.value.decode()
+
+
+def kernel_info(kernel: str) -> dict:
+    return json.loads(_kernel_info_json(kernel))
 
 
 def _i32p(a: np.ndarray):
@@ -215,14 +224,15 @@ def _is_torch_cuda(x) -> bool:
 
 def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, object],
                   shared: Optional[Dict[str, object]] = None, n_warps: Optional[int] = None,
-                  faults=None, stream=None, want_stats: bool = True) -> WarpBatchResult:
+                  faults=None, stream=None, want_stats: bool = True, prepare_only: bool = False):
     """Run a batch of warps of a corpus kernel on the GPU (replaces executeWarp).
 
     ``globals``/``shared`` are numpy int32 arrays (HOST mode: copied in and the
     globals copied back in place) or torch int32 CUDA tensors (DEVICE mode:
     updated in place, asynchronous on ``stream``).  ``args`` is an int32 array of
     shape (n_params, acount) with acount in {1, n_warps, n_warps*warp}; with
-    acount == 1 it is always host memory.
+    acount == 1 it is always host memory.  ``prepare_only`` returns a
+    :class:`PreparedCall` instead of running.
     """
     if isinstance(variant, str):
         variant = VARIANTS[variant]
@@ -270,25 +280,41 @@ def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, obje
             faults = np.zeros(n_warps, dtype=np.int32)
         fptr = _i32p(faults)
         mem = 0
-    st = Stats()
-    err = ctypes.create_string_buffer(512)
-    rc = lib().darm_gpu_execute_warps(
+    call = PreparedCall(lib().darm_gpu_execute_warps, (
         kernel.encode(), int(variant), int(warp), int(n_warps), aptr, int(acount),
         _ptr_array(gl_ptrs), len(gl_ptrs), _ptr_array(sh_ptrs) if sh_ptrs else None, len(sh_ptrs),
-        fptr, mem, ctypes.c_void_p(stream or 0), ctypes.byref(st) if want_stats else None, err, 512)
-    _check(rc, err)
-    return WarpBatchResult({n: globals[n] for n in names}, faults, st.as_dict() if want_stats else {})
+        fptr, mem, ctypes.c_void_p(stream or 0)), want_stats,
+        keepalive=(args_np if not device or acount == 1 else args_t, globals, shared, faults))
+    if prepare_only:
+        return call
+    st = call()
+    return WarpBatchResult({n: globals[n] for n in names}, faults, st)
 
 
-def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: bool = True) -> dict:
+class PreparedCall:
+    """One C-ABI call with its ctypes arguments built once; calling it costs a
+    single foreign call (used by bench.py so host overhead stays off the GPU
+    timeline).  Holds references to every buffer the pointers refer to."""
+
+    def __init__(self, fn, args, want_stats, keepalive=()):
+        self.fn, self.args, self.keepalive = fn, args, keepalive
+        self.stats = Stats() if want_stats else None
+        self.err = ctypes.create_string_buffer(512)
+        self.full = args + ((ctypes.byref(self.stats) if want_stats else None), self.err, 512)
+
+    def __call__(self) -> dict:
+        _check(self.fn(*self.full), self.err)
+        return self.stats.as_dict() if self.stats is not None else {}
+
+
+def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: bool = True,
+                 prepare_only: bool = False):
     """Sort every ``bucket``-key bucket of ``keys`` ascending, in place.
 
     ``keys``: numpy int32 (HOST mode) or torch int32 CUDA tensor (DEVICE mode).
     """
     if isinstance(variant, str):
         variant = VARIANTS[variant]
-    st = Stats()
-    err = ctypes.create_string_buffer(512)
     if _is_torch_cuda(keys):
         import torch
 
@@ -298,11 +324,9 @@ def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: boo
     else:
         assert keys.dtype == np.int32 and keys.flags["C_CONTIGUOUS"]
         ptr, n, mem = keys.ctypes.data, keys.size, 0
-    rc = lib().darm_gpu_bitonic_sort(int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), mem,
-                                     ctypes.c_void_p(stream or 0),
-                                     ctypes.byref(st) if want_stats else None, err, 512)
-    _check(rc, err)
-    return st.as_dict() if want_stats else {}
+    call = PreparedCall(lib().darm_gpu_bitonic_sort, (int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), mem,
+                                                      ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
+    return call if prepare_only else call()
 
 
 def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int = 1,
@@ -330,6 +354,29 @@ def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int 
         ctypes.byref(st) if want_stats else None, err, 512)
     _check(rc, err)
     return int(sols.value), (per[: npre.value] if per is not None else None), (st.as_dict() if want_stats else {})
+
+
+def lud(a, variant=MELDED, stream=None, want_stats: bool = True, prepare_only: bool = False):
+    """In-place blocked LU (no pivoting) of a square fp32 matrix.
+
+    ``a``: numpy float32 (HOST mode) or torch float32 CUDA tensor (DEVICE mode),
+    row-major n x n with n % 16 == 0.
+    """
+    if isinstance(variant, str):
+        variant = VARIANTS[variant]
+    if _is_torch_cuda(a):
+        import torch
+
+        assert a.dtype == torch.float32 and a.is_contiguous() and a.dim() == 2 and a.shape[0] == a.shape[1]
+        ptr, n, mem = a.data_ptr(), a.shape[0], 1
+        if stream is None:
+            stream = torch.cuda.current_stream(a.device).cuda_stream
+    else:
+        assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"] and a.ndim == 2 and a.shape[0] == a.shape[1]
+        ptr, n, mem = a.ctypes.data, a.shape[0], 0
+    call = PreparedCall(lib().darm_gpu_lud, (int(variant), ctypes.c_void_p(ptr), int(n), mem,
+                                             ctypes.c_void_p(stream or 0)), want_stats, keepalive=(a,))
+    return call if prepare_only else call()
 
 
 @dataclass

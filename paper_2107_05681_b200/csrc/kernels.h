@@ -42,4 +42,7 @@ cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefi
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,
                            int sms, cudaStream_t s);
 
+// lud.cu: records the 3 x n/16 launches of one decomposition on `s`
+cudaError_t record_lud(int variant, float *a, int n, cudaStream_t s, int *launches);
+
 }  // namespace darm_gpu

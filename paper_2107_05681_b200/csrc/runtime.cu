@@ -58,10 +58,20 @@ int guarded(char *err, size_t errlen, F &&f) {
 }
 
 // ---------------------------------------------------------------- devices
+struct GraphEntry {
+  int kind, variant;
+  const void *ptr;
+  int64_t n;
+  cudaGraphExec_t exec;
+  int launches;
+};
+
 struct DeviceState {
   std::mutex mu;
   int sms = 0;
   std::vector<std::pair<void *, size_t>> slots;  // cached staging buffers
+  std::vector<GraphEntry> graphs;                // instantiated launch sequences
+  cudaStream_t capture = nullptr;                // private stream for graph capture
 };
 
 std::mutex g_mu;
@@ -138,6 +148,28 @@ struct Timeline {
   }
 };
 
+// Returns the cached executable graph for (kind, variant, ptr, n), recording
+// it with `record` on the device's private capture stream the first time.
+template <class Rec>
+GraphEntry &cached_graph(DeviceState &st, int kind, int variant, const void *ptr, int64_t n, Rec &&record) {
+  for (auto &g : st.graphs)
+    if (g.kind == kind && g.variant == variant && g.ptr == ptr && g.n == n) return g;
+  if (!st.capture) DARM_CUDA(cudaStreamCreateWithFlags(&st.capture, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  int launches = 0;
+  DARM_CUDA(cudaStreamBeginCapture(st.capture, cudaStreamCaptureModeThreadLocal));
+  cudaError_t rec = record(st.capture, &launches);
+  cudaError_t end = cudaStreamEndCapture(st.capture, &graph);
+  DARM_CUDA(rec);
+  DARM_CUDA(end);
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t inst = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  DARM_CUDA(inst);
+  st.graphs.push_back({kind, variant, ptr, n, exec, launches});
+  return st.graphs.back();
+}
+
 const CorpusKernelDesc *find_kernel(const char *name) {
   if (!name) return nullptr;
   for (int i = 0; i < kCorpusCount; ++i)
@@ -174,6 +206,8 @@ void darm_gpu_shutdown(void) {
     cudaSetDevice(int(d));
     for (auto &s : g_devices[d]->slots)
       if (s.first) cudaFree(s.first);
+    for (auto &g : g_devices[d]->graphs) cudaGraphExecDestroy(g.exec);
+    if (g_devices[d]->capture) cudaStreamDestroy(g_devices[d]->capture);
     delete g_devices[d];
     g_devices[d] = nullptr;
   }
@@ -493,6 +527,48 @@ int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world, u
       stats->h2d_bytes = pre.size() * 4;
       stats->d2h_bytes = 8 + (per_prefix ? uint64_t(np) * 4 : 0);
       stats->algorithmic_bytes = pre.size() * 4 + (per_prefix ? uint64_t(np) * 4 : 0);
+    }
+  });
+}
+
+int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream, darm_gpu_stats *stats, char *err,
+                 size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if (n < 16 || n % 16 || n > 46336) user_error("n must be a multiple of 16 in [16, 46336]");
+    if (!a) user_error("matrix is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    if (mem == DARM_MEM_DEVICE && (reinterpret_cast<uintptr_t>(a) & 15)) user_error("device matrix must be 16-byte aligned");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    DeviceState &st = device_state(nullptr);
+    std::lock_guard<std::mutex> lk(st.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t bytes = size_t(n) * size_t(n) * 4;
+    Timeline tl(s, stats != nullptr);
+    tl.mark(0);
+    float *d = a;
+    if (mem == DARM_MEM_HOST) {
+      d = static_cast<float *>(slot(st, 0, bytes));
+      DARM_CUDA(cudaMemcpyAsync(d, a, bytes, cudaMemcpyHostToDevice, s));
+    }
+    GraphEntry &g = cached_graph(st, 1, variant, d, n, [&](cudaStream_t cs, int *launches) {
+      return record_lud(variant, d, int(n), cs, launches);
+    });
+    tl.mark(1);
+    DARM_CUDA(cudaGraphLaunch(g.exec, s));
+    tl.mark(2);
+    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaMemcpyAsync(a, d, bytes, cudaMemcpyDeviceToHost, s));
+    tl.mark(3);
+    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+      tl.fill(stats);
+      stats->launches = g.launches;
+      stats->h2d_bytes = mem == DARM_MEM_HOST ? bytes : 0;
+      stats->d2h_bytes = mem == DARM_MEM_HOST ? bytes : 0;
+      // internal update reads + writes the trailing matrix once per step
+      double nb = double(n) / 16.0, tb = 0;
+      for (double m = nb - 1; m > 0; m -= 1) tb += m * m;
+      stats->algorithmic_bytes = uint64_t(tb * 16.0 * 16.0 * 8.0);
     }
   });
 }

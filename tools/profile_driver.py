@@ -16,6 +16,15 @@ import paper_2107_05681_b200 as darm  # noqa: E402
 def main(which, bucket=64):
     torch.cuda.set_device(0)
     darm.init()
+    if which == "lud":
+        n = bucket if bucket > 64 else 8192
+        g = torch.Generator(device="cuda").manual_seed(4)
+        a0 = torch.rand((n, n), generator=g, device="cuda") + n * torch.eye(n, device="cuda")
+        for v in (darm.UNMELDED, darm.MELDED):
+            a = a0.clone()
+            darm.lud(a, v, want_stats=False)
+        torch.cuda.synchronize()
+        return
     if which == "nqueens":
         for v in (darm.UNMELDED, darm.MELDED):
             assert darm.nqueens(16, 6, v, want_stats=False)[0] == 14772512
