@@ -264,6 +264,22 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_TFLOPs"] = (2.0 / 3.0) * n ** 3 / (row["melded_us"] * 1e-6) / 1e12
     out["lud8192"] = row
+    # SRAD 16384^2 fp32 x 100 iterations (config 5, one GPU)
+    n, iters = 16384, 100
+    j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
+    j = torch.empty_like(j0)
+    row = {}
+    for vname, v in (("unmelded", 0), ("melded", 1)):
+        call = darm.srad(j, iters, 0.5, darm.RODINIA_ROI, v, stream=stream.cuda_stream, want_stats=False,
+                         prepare_only=True)
+        t = time_steps(torch, stream, lambda: j.copy_(j0), call, 2, 1, flush)
+        row[vname + "_us"] = 1e3 * sum(t) / len(t)
+    row["speedup"] = row["unmelded_us"] / row["melded_us"]
+    # minimal traffic 8 B/px/iteration (one read of J, one write of J') + the in/out copies of the call
+    alg = 8.0 * n * n * iters + 8.0 * n * n
+    row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
+    row["melded_frac_hbm"] = row["melded_GBps"] / peak
+    out["srad16384x100"] = row
     return out
 
 

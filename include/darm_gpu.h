@@ -156,6 +156,39 @@ int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world,
 int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream,
                  darm_gpu_stats *stats, char *err, size_t errlen);
 
+/* ---- SRAD (Rodinia SRAD, no reference code) -------------
+ * Speckle reducing anisotropic diffusion of a rows x cols fp32 image J for
+ * `iters` iterations with step lambda; q0sqr of every iteration comes from the
+ * ROI roi = {r1, r2, c1, c2} (inclusive, at most 4096 rows).  Per-pixel
+ * operations are fixed and deterministic.  One fused kernel
+ * per iteration (8 B/px of HBM traffic), all iterations in one cached graph.
+ * J is updated in place (HOST: copied in/out; DEVICE: device pointer). */
+int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters,
+                  float lambda, const int *roi, int mem, void *stream,
+                  darm_gpu_stats *stats, char *err, size_t errlen);
+
+/* Row-tiled SRAD for one rank of a multi-GPU run (device pointers only).
+ * A tile holds global rows [r0, r0 + tile_rows) at local rows 1..tile_rows of
+ * a (tile_rows + 3) x cols buffer: local row 0 is the halo row r0 - 1 and
+ * local rows tile_rows+1, tile_rows+2 the halo rows below (needed only where
+ * they exist in the image; the caller exchanges them between ranks).
+ * ROI partial sums: darm_gpu_srad_roi_words() doubles per buffer; a tile
+ * writes the entries of the ROI rows it owns, so summing the buffers of all
+ * ranks (e.g. an all-reduce) gives the full statistics.
+ * tile_roi() fills roi_out for the initial image; tile_step() runs one
+ * iteration tile_in -> tile_out using roi_in and writes the next roi_out.
+ * q0_scratch: one device float. */
+int64_t darm_gpu_srad_roi_words(int64_t cols, const int *roi);
+int darm_gpu_srad_tile_roi(const float *tile, int64_t cols, int64_t tile_rows,
+                           int64_t r0, int64_t rows, const int *roi,
+                           double *roi_out, void *stream, char *err, size_t errlen);
+int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out,
+                            int64_t cols, int64_t tile_rows, int64_t r0,
+                            int64_t rows, float lambda, const int *roi,
+                            const double *roi_in, double *roi_out,
+                            float *q0_scratch, void *stream, char *err,
+                            size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -377,3 +377,122 @@ int oracle_lud(float *a, int64_t n, int threads) {
   }
   return 0;
 }
+
+/* ------------------------------------------------------------ SRAD
+ * Rodinia SRAD restated (no reference code), in exactly
+ * the operation order of csrc/srad.cu (compiled there with -fmad=false; this
+ * file with -ffp-contract=off).  ROI statistics: per ROI row and 30-column
+ * warp group, the 32-lane fp64 xor-butterfly the kernel performs (lane 0's
+ * result), then rows and groups folded in order. */
+static int clampi_(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+static float srad_c(float jc, float n, float s, float w, float e, float q0sqr, float q0den) {
+  const float dN = n - jc, dS = s - jc, dW = w - jc, dE = e - jc;
+  const float g2 = (((dN * dN + dS * dS) + dW * dW) + dE * dE) / (jc * jc);
+  const float l = (((dN + dS) + dW) + dE) / jc;
+  const float num = (0.5f * g2) - ((1.0f / 16.0f) * (l * l));
+  float den = 1.0f + (0.25f * l);
+  const float qsqr = num / (den * den);
+  den = (qsqr - q0sqr) / q0den;
+  float c = 1.0f / (1.0f + den);
+  if (c < 0.0f) c = 0.0f;            /* R_D */
+  else if (c > 1.0f) c = 1.0f;
+  return c;
+}
+
+static float srad_q0(const float *J, int64_t cols, const int *roi) {
+  const int w0 = roi[2] / 30, groups = roi[3] / 30 - w0 + 1;
+  double s = 0.0, s2 = 0.0;
+  for (int g = roi[0]; g <= roi[1]; ++g)
+    for (int w = w0; w < w0 + groups; ++w) {
+      double a[32], b[32];
+      for (int L = 0; L < 32; ++L) {
+        const int64_t j = (int64_t)w * 30 + L - 1;
+        const int in = L >= 1 && L <= 30 && j < cols && j >= roi[2] && j <= roi[3];
+        const double v = in ? (double)J[g * cols + j] : 0.0;
+        a[L] = v;
+        b[L] = in ? v * v : 0.0;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        double na[32], nb[32];
+        for (int L = 0; L < 32; ++L) {
+          na[L] = a[L] + a[L ^ o];
+          nb[L] = b[L] + b[L ^ o];
+        }
+        memcpy(a, na, sizeof a);
+        memcpy(b, nb, sizeof b);
+      }
+      s += a[0];
+      s2 += b[0];
+    }
+  const double npix = (double)(roi[1] - roi[0] + 1) * (double)(roi[3] - roi[2] + 1);
+  const double mean = s / npix;
+  const double var = s2 / npix - mean * mean;
+  return (float)(var / (mean * mean));
+}
+
+typedef struct {
+  const float *J;
+  float *C, *out;
+  int64_t rows, cols, r0, r1;
+  float q0sqr, q0den, lq;
+  int phase;
+} srad_job;
+
+static void *srad_rows(void *p) {
+  srad_job *t = (srad_job *)p;
+  const float *J = t->J;
+  const int64_t R = t->rows, C = t->cols;
+  for (int64_t i = t->r0; i < t->r1; ++i)
+    for (int64_t j = 0; j < C; ++j) {
+      const float jc = J[i * C + j];
+      const float n = J[clampi_((int)i - 1, 0, (int)R - 1) * C + j];
+      const float s = J[clampi_((int)i + 1, 0, (int)R - 1) * C + j];
+      const float w = J[i * C + clampi_((int)j - 1, 0, (int)C - 1)];
+      const float e = J[i * C + clampi_((int)j + 1, 0, (int)C - 1)];
+      if (t->phase == 0) {
+        t->C[i * C + j] = srad_c(jc, n, s, w, e, t->q0sqr, t->q0den);
+      } else {
+        const float c0 = t->C[i * C + j];
+        const float c1 = t->C[clampi_((int)i + 1, 0, (int)R - 1) * C + j];
+        const float ce = t->C[i * C + clampi_((int)j + 1, 0, (int)C - 1)];
+        const float dN = n - jc, dS = s - jc, dW = w - jc, dE = e - jc;
+        const float d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
+        t->out[i * C + j] = jc + t->lq * d;
+      }
+    }
+  return NULL;
+}
+
+int oracle_srad(float *J, int64_t rows, int64_t cols, int iters, float lambda, const int *roi, int threads) {
+  if (rows < 1 || cols < 2 || iters < 0) return 2;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  float *Cb = (float *)malloc(sizeof(float) * (size_t)(rows * cols));
+  float *Jn = (float *)malloc(sizeof(float) * (size_t)(rows * cols));
+  if (!Cb || !Jn) return 3;
+  const float lq = 0.25f * lambda;
+  for (int it = 0; it < iters; ++it) {
+    const float q0sqr = srad_q0(J, cols, roi);
+    const float q0den = q0sqr * (1.0f + q0sqr);
+    for (int phase = 0; phase < 2; ++phase) {
+      int t = (int)(rows < threads ? rows : threads);
+      pthread_t tid[256];
+      srad_job jobs[256];
+      for (int q = 0; q < t; ++q) {
+        srad_job jb = {J, Cb, Jn, rows, cols, rows * q / t, rows * (q + 1) / t, q0sqr, q0den, lq, phase};
+        jobs[q] = jb;
+        if (t > 1)
+          pthread_create(&tid[q], NULL, srad_rows, &jobs[q]);
+        else
+          srad_rows(&jobs[q]);
+      }
+      if (t > 1)
+        for (int q = 0; q < t; ++q) pthread_join(tid[q], NULL);
+    }
+    memcpy(J, Jn, sizeof(float) * (size_t)(rows * cols));
+  }
+  free(Cb);
+  free(Jn);
+  return 0;
+}

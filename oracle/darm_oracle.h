@@ -62,6 +62,10 @@ uint64_t oracle_nqueens_count(int n, int base, const uint32_t *states, int64_t c
  * threads > 1 splits the internal update by rows (pthreads). */
 int oracle_lud(float *a, int64_t n, int threads);
 
+/* SRAD (no reference code): `iters` iterations on a rows x cols fp32 image,
+ * in place, ROI {r1, r2, c1, c2}, in exactly csrc/srad.cu's operation order. */
+int oracle_srad(float *J, int64_t rows, int64_t cols, int iters, float lambda, const int *roi, int threads);
+
 #ifdef __cplusplus
 }
 #endif

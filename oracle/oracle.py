@@ -59,6 +59,8 @@ class Restatement:
                                            ctypes.c_int64, I32P, ctypes.c_int64, I32P, I32P]
         L.oracle_bitonic_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
         L.oracle_lud.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int]
+        L.oracle_srad.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                  ctypes.c_float, I32P, ctypes.c_int]
         U32P = ctypes.POINTER(ctypes.c_uint32)
         L.oracle_nqueens_prefixes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, U32P,
                                               ctypes.c_int64]
@@ -107,6 +109,15 @@ class Restatement:
                                  threads or (os.cpu_count() or 1))
         if rc:
             raise ValueError("oracle_lud: n must be a multiple of 16")
+
+    def srad(self, j: np.ndarray, iters: int, lam: float, roi, threads: int = 0) -> None:
+        """In-place SRAD in csrc/srad.cu's operation order."""
+        assert j.dtype == np.float32 and j.flags["C_CONTIGUOUS"] and j.ndim == 2
+        r = np.ascontiguousarray(roi, dtype=np.int32)
+        rc = self.lib.oracle_srad(j.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), j.shape[0], j.shape[1], iters,
+                                  lam, _p(r), threads or (os.cpu_count() or 1))
+        if rc:
+            raise ValueError(f"oracle_srad -> {rc}")
 
     def nqueens_prefixes(self, n: int, base: int, rank: int = 0, world: int = 1) -> np.ndarray:
         cnt = self.lib.oracle_nqueens_prefixes(n, base, rank, world, None, 0)

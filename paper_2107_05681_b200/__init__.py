@@ -52,6 +52,10 @@ ABI_SYMBOLS = (
     "darm_gpu_nqueens",
     "darm_gpu_nqueens_prefix_count",
     "darm_gpu_lud",
+    "darm_gpu_srad",
+    "darm_gpu_srad_roi_words",
+    "darm_gpu_srad_tile_roi",
+    "darm_gpu_srad_tile_step",
 )
 
 
@@ -123,6 +127,19 @@ def lib() -> ctypes.CDLL:
         L.darm_gpu_nqueens_prefix_count.restype = ctypes.c_int64
         L.darm_gpu_lud.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
+        I32P, F32P, F64P = c_i32p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)
+        L.darm_gpu_srad.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                    ctypes.c_float, I32P, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(Stats),
+                                    ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_srad_roi_words.argtypes = [ctypes.c_int64, I32P]
+        L.darm_gpu_srad_roi_words.restype = ctypes.c_int64
+        L.darm_gpu_srad_tile_roi.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_int64, I32P, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_srad_tile_step.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, I32P,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_char_p, ctypes.c_size_t]
         _lib = L
     return _lib
 
@@ -377,6 +394,61 @@ def lud(a, variant=MELDED, stream=None, want_stats: bool = True, prepare_only: b
     call = PreparedCall(lib().darm_gpu_lud, (int(variant), ctypes.c_void_p(ptr), int(n), mem,
                                              ctypes.c_void_p(stream or 0)), want_stats, keepalive=(a,))
     return call if prepare_only else call()
+
+
+RODINIA_ROI = (0, 127, 0, 127)
+
+
+def _roi_arr(roi):
+    r = (ctypes.c_int32 * 4)(*[int(x) for x in roi])
+    return r
+
+
+def srad(j, iters: int, lam: float = 0.5, roi=RODINIA_ROI, variant=MELDED, stream=None,
+         want_stats: bool = True, prepare_only: bool = False):
+    """SRAD on a 2-D fp32 image, in place (numpy -> HOST mode, torch CUDA -> DEVICE)."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant]
+    if _is_torch_cuda(j):
+        import torch
+
+        assert j.dtype == torch.float32 and j.is_contiguous() and j.dim() == 2
+        ptr, (rows, cols), mem = j.data_ptr(), j.shape, 1
+        if stream is None:
+            stream = torch.cuda.current_stream(j.device).cuda_stream
+    else:
+        assert j.dtype == np.float32 and j.flags["C_CONTIGUOUS"] and j.ndim == 2
+        ptr, (rows, cols), mem = j.ctypes.data, j.shape, 0
+    r = _roi_arr(roi)
+    call = PreparedCall(lib().darm_gpu_srad, (int(variant), ctypes.c_void_p(ptr), int(rows), int(cols), int(iters),
+                                              float(lam), r, mem, ctypes.c_void_p(stream or 0)), want_stats,
+                        keepalive=(j, r))
+    return call if prepare_only else call()
+
+
+def srad_roi_words(cols: int, roi=RODINIA_ROI) -> int:
+    return int(lib().darm_gpu_srad_roi_words(int(cols), _roi_arr(roi)))
+
+
+def srad_tile_roi(tile, cols, tile_rows, r0, rows, roi, roi_out, stream=None) -> None:
+    """ROI partials of a tile (device tensors; see darm_gpu.h)."""
+    err = ctypes.create_string_buffer(512)
+    _check(lib().darm_gpu_srad_tile_roi(ctypes.c_void_p(tile.data_ptr()), cols, tile_rows, r0, rows, _roi_arr(roi),
+                                        ctypes.c_void_p(roi_out.data_ptr()), ctypes.c_void_p(stream or 0), err, 512),
+           err)
+
+
+def srad_tile_step(variant, tile_in, tile_out, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0,
+                   stream=None) -> None:
+    """One SRAD iteration of a row tile (device tensors; see darm_gpu.h)."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant]
+    err = ctypes.create_string_buffer(512)
+    _check(lib().darm_gpu_srad_tile_step(int(variant), ctypes.c_void_p(tile_in.data_ptr()),
+                                         ctypes.c_void_p(tile_out.data_ptr()), cols, tile_rows, r0, rows, float(lam),
+                                         _roi_arr(roi), ctypes.c_void_p(roi_in.data_ptr()),
+                                         ctypes.c_void_p(roi_out.data_ptr()), ctypes.c_void_p(q0.data_ptr()),
+                                         ctypes.c_void_p(stream or 0), err, 512), err)
 
 
 @dataclass

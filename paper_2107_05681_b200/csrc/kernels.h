@@ -45,4 +45,18 @@ cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefi
 // lud.cu: records the 3 x n/16 launches of one decomposition on `s`
 cudaError_t record_lud(int variant, float *a, int n, cudaStream_t s, int *launches);
 
+// srad.cu
+struct SradRoi {
+  int r1, r2, c1, c2;   // inclusive ROI rectangle (global rows / columns)
+  int w0, groups;       // warp column groups (30 columns each) covering [c1, c2]
+  int rows;             // r2 - r1 + 1
+};
+SradRoi srad_roi_layout(int cols, int r1, int r2, int c1, int c2);
+cudaError_t launch_srad_roi(const float *jin, int cols, int r0, int tile_rows, const SradRoi &roi, double *roi_out,
+                            cudaStream_t s);
+cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s);
+cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const float *q0, double *roi_out,
+                              int cols, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
+                              cudaStream_t s);
+
 }  // namespace darm_gpu

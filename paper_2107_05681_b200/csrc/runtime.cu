@@ -66,6 +66,7 @@ struct GraphEntry {
   int launches;
 };
 
+struct GraphEntry;
 struct DeviceState {
   std::mutex mu;
   int sms = 0;
@@ -107,6 +108,9 @@ void *slot(DeviceState &st, size_t i, size_t bytes) {
   if (st.slots.size() <= i) st.slots.resize(i + 1, {nullptr, 0});
   auto &s = st.slots[i];
   if (s.second < bytes) {
+    // cached graphs may hold the old pointer: drop them all
+    for (auto &g : st.graphs) cudaGraphExecDestroy(g.exec);
+    st.graphs.clear();
     if (s.first) DARM_CUDA(cudaFree(s.first));
     s.first = nullptr;
     s.second = 0;
@@ -570,6 +574,115 @@ int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream, darm_g
       for (double m = nb - 1; m > 0; m -= 1) tb += m * m;
       stats->algorithmic_bytes = uint64_t(tb * 16.0 * 16.0 * 8.0);
     }
+  });
+}
+
+static void check_srad_args(int64_t rows, int64_t cols, const int *roi, float lambda) {
+  if (rows < 1 || cols < 2 || rows > (1 << 20) || cols > (1 << 20) || rows * cols > (int64_t(1) << 34))
+    user_error("image must be rows x cols with rows >= 1, cols >= 2");
+  if (!roi) user_error("roi is NULL");
+  if (roi[0] < 0 || roi[1] < roi[0] || roi[1] >= rows || roi[2] < 0 || roi[3] < roi[2] || roi[3] >= cols)
+    user_error("roi must be {r1, r2, c1, c2} inside the image with r1 <= r2, c1 <= c2");
+  if (roi[1] - roi[0] + 1 > 4096) user_error("roi spans more than 4096 rows");
+  if (!(lambda > 0.0f) || !(lambda <= 1.0f)) user_error("lambda must be in (0, 1]");
+}
+
+int64_t darm_gpu_srad_roi_words(int64_t cols, const int *roi) {
+  if (!roi || cols < 1) return -1;
+  SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
+  return int64_t(R.rows) * R.groups * 2;
+}
+
+int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, float lambda, const int *roi,
+                  int mem, void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    check_srad_args(rows, cols, roi, lambda);
+    if (iters < 0) user_error("iters must be >= 0");
+    if (!j) user_error("image is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    DeviceState &st = device_state(nullptr);
+    std::lock_guard<std::mutex> lk(st.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
+    const size_t img = size_t(rows) * size_t(cols) * 4;
+    const size_t buf = size_t(rows + 3) * size_t(cols) * 4;   // 1 halo row above, 2 below
+    const size_t roi_bytes = size_t(R.rows) * R.groups * 2 * 8;
+    auto *b0 = static_cast<float *>(slot(st, 0, buf));
+    auto *b1 = static_cast<float *>(slot(st, 1, buf));
+    auto *ctl = static_cast<char *>(slot(st, 2, 2 * roi_bytes + 256));
+    double *roiA = reinterpret_cast<double *>(ctl + 256), *roiB = roiA + roi_bytes / 8;
+    float *q0 = reinterpret_cast<float *>(ctl);
+    Timeline tl(s, stats != nullptr);
+    tl.mark(0);
+    DARM_CUDA(cudaMemcpyAsync(b0 + cols, j, img, mem == DARM_MEM_HOST ? cudaMemcpyHostToDevice
+                                                                         : cudaMemcpyDeviceToDevice, s));
+    tl.mark(1);
+    const int it = iters;
+    GraphEntry &g = cached_graph(st, 2 + variant, it, b0, rows * 1000003 + cols * 7 + roi[0] * 131 + roi[1] * 17 +
+                                                           roi[2] * 3 + roi[3] + int64_t(lambda * 1e6) * 97,
+                                 [&](cudaStream_t cs, int *launches) {
+      cudaError_t e = launch_srad_roi(b0, int(cols), 0, int(rows), R, roiA, cs);
+      ++*launches;
+      float *in = b0, *out = b1;
+      double *ri = roiA, *ro = roiB;
+      for (int t = 0; t < it && e == cudaSuccess; ++t) {
+        e = launch_srad_q0(ri, R, q0, cs);
+        if (e == cudaSuccess)
+          e = launch_srad_sweep(variant, in, out, q0, ro, int(cols), int(rows), 0, int(rows), lambda, R, cs);
+        *launches += 2;
+        std::swap(in, out);
+        std::swap(ri, ro);
+      }
+      return e;
+    });
+    DARM_CUDA(cudaGraphLaunch(g.exec, s));
+    tl.mark(2);
+    float *res = (iters % 2 == 0) ? b0 : b1;
+    DARM_CUDA(cudaMemcpyAsync(j, res + cols, img, mem == DARM_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                                      : cudaMemcpyDeviceToDevice, s));
+    tl.mark(3);
+    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+      tl.fill(stats);
+      stats->launches = g.launches;
+      stats->h2d_bytes = mem == DARM_MEM_HOST ? img : 0;
+      stats->d2h_bytes = mem == DARM_MEM_HOST ? img : 0;
+      stats->algorithmic_bytes = uint64_t(iters) * uint64_t(rows) * uint64_t(cols) * 8;
+    }
+  });
+}
+
+int darm_gpu_srad_tile_roi(const float *tile, int64_t cols, int64_t tile_rows, int64_t r0, int64_t rows,
+                           const int *roi, double *roi_out, void *stream, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    check_srad_args(rows, cols, roi, 0.5f);
+    if (tile_rows < 1 || r0 < 0 || r0 + tile_rows > rows) user_error("tile outside the image");
+    if (!tile || !roi_out) user_error("NULL buffer");
+    device_state(nullptr);
+    const SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
+    DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double),
+                              static_cast<cudaStream_t>(stream)));
+    DARM_CUDA(launch_srad_roi(tile, int(cols), int(r0), int(tile_rows), R, roi_out, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, int64_t cols, int64_t tile_rows,
+                            int64_t r0, int64_t rows, float lambda, const int *roi, const double *roi_in,
+                            double *roi_out, float *q0_scratch, void *stream, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    check_srad_args(rows, cols, roi, lambda);
+    if (tile_rows < 1 || r0 < 0 || r0 + tile_rows > rows) user_error("tile outside the image");
+    if (!tile_in || !tile_out || !roi_in || !q0_scratch) user_error("NULL buffer");
+    device_state(nullptr);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
+    DARM_CUDA(launch_srad_q0(roi_in, R, q0_scratch, s));
+    if (roi_out) DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double), s));
+    DARM_CUDA(launch_srad_sweep(variant, tile_in, tile_out, q0_scratch, roi_out, int(cols), int(tile_rows), int(r0),
+                                int(rows), lambda, R, s));
   });
 }
 

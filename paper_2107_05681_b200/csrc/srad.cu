@@ -1,0 +1,265 @@
+// srad.cu — Speckle Reducing Anisotropic Diffusion (SRAD, PAPER.md:778-781,
+// 842-851), fp32, unmelded and melded forms.  The reference has no SRAD code;
+// the per-pixel mathematics is Rodinia's SRAD restated and
+// the CPU oracle (oracle/darm_oracle.c, oracle_srad) performs the same fp32 /
+// fp64 operations in the same order.  This translation unit is compiled with
+// -fmad=false so no multiply-add is contracted (the oracle is compiled with
+// -ffp-contract=off): GPU and CPU agree bit for bit.
+//
+// Per iteration, with q0sqr from the ROI statistics of the current image J:
+//   c(i,j)  = clamp01( 1 / (1 + (q(i,j) - q0sqr) / (q0sqr (1 + q0sqr))) )
+//   J'(i,j) = J + (lambda/4) (c(i,j) dN + c(i+1,j) dS + c(i,j) dW + c(i,j+1) dE)
+// with dN..dE the differences to the 4 neighbours (image borders clamp).
+//
+// B200 layout: one fused kernel per iteration.  Each warp owns 30 output
+// columns (lanes 1..30; lanes 0 and 31 are halo lanes that only supply
+// neighbour values) and sweeps a segment of rows top to bottom, keeping the
+// vertical window J(i-1..i+2) and c(i), c(i+1) in registers and exchanging
+// west/east neighbours with __shfl_sync.  HBM traffic is one read of J and
+// one write of J' per pixel (8 B/px/iteration; the Rodinia layout moves
+// ~52 B/px).  J is double-buffered (J -> J').
+//
+// The divergent regions are
+//   R_B  border handling: west/east neighbours at the image's first/last
+//        column (thread-position dependent), and lane 31's own east value;
+//   R_D  the data-dependent three-way clamp of c (c < 0 / c > 1 / else).
+// unmelded: if / else-if chains (fenced arms); melded: select chains.
+//
+// ROI statistics are reduced deterministically: each warp sums the ROI part
+// of its 30 columns of J' in fp64 with a shuffle butterfly, writing one
+// partial per (row, warp column group); srad_q0_kernel folds the partials in a
+// fixed order.  For row-tiled multi-GPU runs the partial buffer is summed
+// across ranks (each entry is owned by exactly one rank, so the sum is exact).
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace darm_gpu {
+
+struct SradParams {
+  const float *jin;      // (tile_rows + 3) x cols, local row 0 = global row r0 - 1
+  float *jout;           // same layout; local rows 1..tile_rows written
+  const float *q0;       // q0sqr of this iteration (device scalar)
+  double *roi_out;       // [roi_rows][roi_groups][2] partial sums of J' (may be null)
+  int cols, tile_rows, r0, R, rs;
+  float lq;              // lambda / 4
+  int roi_r1, roi_r2, roi_c1, roi_c2, roi_w0, roi_groups;
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// c for one pixel from its centre and 4 neighbour values (Rodinia SRAD,
+// restated).  R_D is the clamp.
+template <bool M>
+__device__ __forceinline__ float srad_coeff(float jc, float n, float s, float w, float e, float q0sqr,
+                                            float q0den) {
+  const float dN = n - jc, dS = s - jc, dW = w - jc, dE = e - jc;
+  const float g2 = (((dN * dN + dS * dS) + dW * dW) + dE * dE) / (jc * jc);
+  const float l = (((dN + dS) + dW) + dE) / jc;
+  const float num = (0.5f * g2) - ((1.0f / 16.0f) * (l * l));
+  float den = 1.0f + (0.25f * l);
+  const float qsqr = num / (den * den);
+  den = (qsqr - q0sqr) / q0den;
+  float c = 1.0f / (1.0f + den);
+  if constexpr (!M) {
+    if (c < 0.0f) {                      // R_D: three-way, data dependent
+      DARM_ARM("srad.rd.lo");
+      c = 0.0f;
+    } else if (c > 1.0f) {
+      DARM_ARM("srad.rd.hi");
+      c = 1.0f;
+    }
+  } else {
+    c = c < 0.0f ? 0.0f : (c > 1.0f ? 1.0f : c);
+  }
+  return c;
+}
+
+template <bool M>
+__global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
+  const int lane = threadIdx.x & 31;
+  const int wcol = blockIdx.x * 8 + (threadIdx.x >> 5);   // warp column group
+  const int j = wcol * 30 + lane - 1;                      // this lane's column
+  const int jc = clampi(j, 0, P.cols - 1);
+  const bool out_lane = lane >= 1 && lane <= 30 && j < P.cols;
+  const int seg0 = blockIdx.y * P.rs;                      // first local own row (0-based)
+  if (seg0 >= P.tile_rows) return;
+  const int seg1 = min(seg0 + P.rs, P.tile_rows);
+  const float q0sqr = *P.q0;
+  const float q0den = q0sqr * (1.0f + q0sqr);
+  const int cols = P.cols;
+  const int gmax = P.R - 1;
+  // global row g -> pointer to its (clamped) row in the tile buffer
+  auto row = [&](int g) { return P.jin + size_t(clampi(g, 0, gmax) - P.r0 + 1) * cols; };
+  // R_B: the west/east neighbour of this lane at image borders and lane 31's
+  // east value (no lane to its right).
+  auto west_east = [&](const float *rp, float v, float &w, float &e) {
+    const float sw = __shfl_up_sync(0xffffffffu, v, 1);
+    const float se = __shfl_down_sync(0xffffffffu, v, 1);
+    if constexpr (!M) {
+      if (j == 0) {
+        DARM_ARM("srad.rb.west");
+        w = v;
+        e = se;
+      } else if (lane == 31 || j == cols - 1) {
+        DARM_ARM("srad.rb.east");
+        w = sw;
+        e = j >= cols - 1 ? v : rp[min(jc + 1, cols - 1)];
+      } else {
+        DARM_ARM("srad.rb.mid");
+        w = sw;
+        e = se;
+      }
+    } else {
+      const bool edge_e = lane == 31 || j >= cols - 1;
+      float ee = v;
+      if (lane == 31 && j < cols - 1) ee = rp[jc + 1];   // the only one-sided run
+      w = j == 0 ? v : sw;
+      e = edge_e ? ee : se;
+    }
+  };
+  const int g0 = P.r0 + seg0;
+  // window at the segment start: rows g0-1, g0, g0+1
+  float jm1 = row(g0 - 1)[jc], j0 = row(g0)[jc], jp1 = row(g0 + 1)[jc];
+  float w0, e0;
+  west_east(row(g0), j0, w0, e0);
+  float c0 = srad_coeff<M>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
+  float jp2 = row(g0 + 2)[jc];
+  const bool roi_warp = P.roi_out && wcol >= P.roi_w0 && wcol < P.roi_w0 + P.roi_groups;
+  for (int i = seg0; i < seg1; ++i) {
+    const int g = P.r0 + i;
+    const float jp3 = row(min(g + 3, P.r0 + P.tile_rows + 1))[jc];   // prefetch (last halo row at most)
+    // c at row g+1 (clamped: at the last image row it is c(g) itself)
+    float w1, e1;
+    west_east(row(g + 1), jp1, w1, e1);
+    const float c1 = (g + 1 <= gmax) ? srad_coeff<M>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
+    // east neighbour's c at row g
+    float ce = __shfl_down_sync(0xffffffffu, c0, 1);
+    if (j >= cols - 1) ce = c0;
+    // update row g
+    const float dN = jm1 - j0, dS = jp1 - j0, dW = w0 - j0, dE = e0 - j0;
+    const float d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
+    const float jn = j0 + P.lq * d;
+    if (out_lane) P.jout[size_t(i + 1) * cols + j] = jn;
+    if (roi_warp && g >= P.roi_r1 && g <= P.roi_r2) {
+      const bool in = out_lane && j >= P.roi_c1 && j <= P.roi_c2;
+      double s = in ? double(jn) : 0.0, s2 = in ? double(jn) * double(jn) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (lane == 0) {
+        double *dst = P.roi_out + 2 * (size_t(g - P.roi_r1) * P.roi_groups + (wcol - P.roi_w0));
+        dst[0] = s;
+        dst[1] = s2;
+      }
+    }
+    // slide the window
+    jm1 = j0;
+    j0 = jp1;
+    jp1 = jp2;
+    jp2 = jp3;
+    w0 = w1;
+    e0 = e1;
+    c0 = c1;
+  }
+}
+
+// q0sqr from the ROI partials: rows in order, groups in order, fp64.
+__global__ void srad_q0_kernel(const double *roi, int rows, int groups, double npix, float *q0) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0, s2 = 0.0;
+  for (int r = 0; r < rows; ++r)
+    for (int g = 0; g < groups; ++g) {
+      s += roi[2 * (size_t(r) * groups + g)];
+      s2 += roi[2 * (size_t(r) * groups + g) + 1];
+    }
+  const double mean = s / npix;
+  const double var = s2 / npix - mean * mean;
+  *q0 = float(var / (mean * mean));
+}
+
+// ROI partials of an existing image (the first iteration's statistics).
+__global__ void srad_roi_kernel(const float *jin, int cols, int r0, int tile_rows, int roi_r1, int roi_r2,
+                                int roi_c1, int roi_c2, int roi_w0, int roi_groups, double *roi_out) {
+  const int lane = threadIdx.x & 31;
+  const int wcol = roi_w0 + blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (wcol >= roi_w0 + roi_groups) return;
+  const int j = wcol * 30 + lane - 1;
+  const bool in = lane >= 1 && lane <= 30 && j < cols && j >= roi_c1 && j <= roi_c2;
+  for (int g = max(roi_r1, r0); g <= min(roi_r2, r0 + tile_rows - 1); ++g) {
+    const float v = in ? jin[size_t(g - r0 + 1) * cols + j] : 0.f;
+    double s = in ? double(v) : 0.0, s2 = in ? double(v) * double(v) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      double *dst = roi_out + 2 * (size_t(g - roi_r1) * roi_groups + (wcol - roi_w0));
+      dst[0] = s;
+      dst[1] = s2;
+    }
+  }
+}
+
+SradRoi srad_roi_layout(int cols, int r1, int r2, int c1, int c2) {
+  SradRoi R;
+  R.r1 = r1;
+  R.r2 = r2;
+  R.c1 = c1;
+  R.c2 = c2;
+  // warp column groups covering output columns [c1, c2]: group w covers 30w .. 30w+29
+  R.w0 = c1 / 30;
+  R.groups = c2 / 30 - R.w0 + 1;
+  R.rows = r2 - r1 + 1;
+  (void)cols;
+  return R;
+}
+
+cudaError_t launch_srad_roi(const float *jin, int cols, int r0, int tile_rows, const SradRoi &roi, double *roi_out,
+                            cudaStream_t s) {
+  const int grid = (roi.groups + 7) / 8;
+  srad_roi_kernel<<<grid, 256, 0, s>>>(jin, cols, r0, tile_rows, roi.r1, roi.r2, roi.c1, roi.c2, roi.w0,
+                                       roi.groups, roi_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s) {
+  const double npix = double(roi.rows) * double(roi.c2 - roi.c1 + 1);
+  srad_q0_kernel<<<1, 32, 0, s>>>(roi_in, roi.rows, roi.groups, npix, q0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const float *q0, double *roi_out,
+                              int cols, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
+                              cudaStream_t s) {
+  SradParams P;
+  P.jin = jin;
+  P.jout = jout;
+  P.q0 = q0;
+  P.roi_out = roi_out;
+  P.cols = cols;
+  P.tile_rows = tile_rows;
+  P.r0 = r0;
+  P.R = R;
+  P.rs = 128;
+  P.lq = 0.25f * lambda;
+  P.roi_r1 = roi.r1;
+  P.roi_r2 = roi.r2;
+  P.roi_c1 = roi.c1;
+  P.roi_c2 = roi.c2;
+  P.roi_w0 = roi.w0;
+  P.roi_groups = roi.groups;
+  const int wgroups = (cols + 29) / 30;
+  dim3 grid((wgroups + 7) / 8, (tile_rows + P.rs - 1) / P.rs);
+  if (variant)
+    srad_sweep_kernel<true><<<grid, 256, 0, s>>>(P);
+  else
+    srad_sweep_kernel<false><<<grid, 256, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace darm_gpu

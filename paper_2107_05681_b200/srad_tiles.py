@@ -1,0 +1,151 @@
+"""Row-tiled SRAD across GPUs (BASELINE config 5: 16384^2, 100 iterations).
+
+One process per GPU (torch.distributed); rank k owns image rows
+[r0_k, r0_k + rows_k).  Each tile buffer holds its rows at local rows
+1..rows_k plus one halo row above (local 0) and two below (local rows_k+1,
+rows_k+2) — the fused sweep kernel needs J(i-1) .. J(i+2).  Per iteration:
+
+  1. halo exchange (the path's one real exchange step): rank k sends its last
+     own row down to k+1 and its first two own rows up to k-1
+     (torch.distributed P2P: NCCL over NVLink on GPUs, gloo in CPU tests);
+  2. all-reduce (sum) of the ROI partial-sum buffer: every entry is written by
+     exactly one rank (the owner of that ROI row), so the sum is exact and
+     every rank gets the same q0sqr;
+  3. darm_gpu_srad_tile_step (C-ABI): q0sqr + the fused sweep J -> J'.
+
+The tile-level kernels are injected (``kernels``), so the exchange logic is
+exercised on CPU with the oracle's tile kernels in tests/test_srad.py; the
+product default is :class:`GpuTileKernels` (libdarm_gpu.so, no fallback).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import paper_2107_05681_b200 as darm
+
+
+def split_rows(rows: int, world: int) -> List[Tuple[int, int]]:
+    """(r0, n) for every rank; every tile has at least 2 rows."""
+    base, extra = divmod(rows, world)
+    out, r0 = [], 0
+    for k in range(world):
+        n = base + (1 if k < extra else 0)
+        out.append((r0, n))
+        r0 += n
+    if any(n < 2 for _, n in out):
+        raise darm.DarmUserError("every rank needs at least 2 image rows")
+    return out
+
+
+class GpuTileKernels:
+    """Tile kernels through the C-ABI (device tensors on the current stream)."""
+
+    def __init__(self, variant, stream=None):
+        self.variant = variant
+        self.stream = stream
+
+    def roi(self, tile, cols, tile_rows, r0, rows, roi, roi_out):
+        darm.srad_tile_roi(tile, cols, tile_rows, r0, rows, roi, roi_out, self.stream)
+
+    def step(self, tin, tout, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0):
+        darm.srad_tile_step(self.variant, tin, tout, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0,
+                            self.stream)
+
+
+class SradTiles:
+    """This rank's tile of a row-tiled SRAD run."""
+
+    def __init__(self, rows: int, cols: int, lam: float = 0.5, roi: Sequence[int] = darm.RODINIA_ROI,
+                 kernels=None, dist=None, device=None, variant=darm.MELDED):
+        import torch
+
+        self.torch = torch
+        self.dist = dist
+        self.world = dist.get_world_size() if dist else 1
+        self.rank = dist.get_rank() if dist else 0
+        self.rows, self.cols, self.lam, self.roi = rows, cols, float(lam), tuple(int(x) for x in roi)
+        self.r0, self.n = split_rows(rows, self.world)[self.rank]
+        self.device = device if device is not None else torch.device("cpu")
+        self.kernels = kernels if kernels is not None else GpuTileKernels(variant)
+        shape = (self.n + 3, cols)
+        self.tin = torch.zeros(shape, dtype=torch.float32, device=self.device)
+        self.tout = torch.zeros(shape, dtype=torch.float32, device=self.device)
+        words = darm.srad_roi_words(cols, self.roi)
+        self.roi_in = torch.zeros(words, dtype=torch.float64, device=self.device)
+        self.roi_out = torch.zeros(words, dtype=torch.float64, device=self.device)
+        self.q0 = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    # ---------------------------------------------------------------- data
+    def load(self, image) -> None:
+        """Copy this rank's rows of the full image (or the tile rows) in."""
+        if image.shape[0] == self.rows:
+            self.tin[1:self.n + 1].copy_(image[self.r0:self.r0 + self.n])
+        else:
+            self.tin[1:self.n + 1].copy_(image)
+        self.kernels.roi(self.tin, self.cols, self.n, self.r0, self.rows, self.roi, self.roi_in)
+
+    def tile(self):
+        return self.tin[1:self.n + 1]
+
+    # ---------------------------------------------------------------- exchange
+    def exchange_halos(self) -> None:
+        if self.world == 1:
+            return
+        d = self.dist
+        ops = []
+        up, down = self.rank - 1, self.rank + 1
+        if up >= 0:
+            ops.append(d.P2POp(d.isend, self.tin[1:3].contiguous(), up))
+            ops.append(d.P2POp(d.irecv, self.halo_top, up))
+        if down < self.world:
+            ops.append(d.P2POp(d.isend, self.tin[self.n:self.n + 1].contiguous(), down))
+            ops.append(d.P2POp(d.irecv, self.halo_bottom, down))
+        for req in d.batch_isend_irecv(ops):
+            req.wait()
+        if up >= 0:
+            self.tin[0:1].copy_(self.halo_top)
+        if down < self.world:
+            self.tin[self.n + 1:self.n + 3].copy_(self.halo_bottom)
+
+    @property
+    def halo_top(self):
+        if not hasattr(self, "_ht"):
+            self._ht = self.torch.empty((1, self.cols), dtype=self.torch.float32, device=self.device)
+        return self._ht
+
+    @property
+    def halo_bottom(self):
+        if not hasattr(self, "_hb"):
+            self._hb = self.torch.empty((2, self.cols), dtype=self.torch.float32, device=self.device)
+        return self._hb
+
+    # ---------------------------------------------------------------- iterate
+    def step(self) -> None:
+        self.exchange_halos()
+        if self.world > 1:
+            self.dist.all_reduce(self.roi_in, op=self.dist.ReduceOp.SUM)
+        self.kernels.step(self.tin, self.tout, self.cols, self.n, self.r0, self.rows, self.lam, self.roi,
+                          self.roi_in, self.roi_out, self.q0)
+        self.tin, self.tout = self.tout, self.tin
+        self.roi_in, self.roi_out = self.roi_out, self.roi_in
+
+    def run(self, iters: int) -> None:
+        for _ in range(iters):
+            self.step()
+
+    def gather(self) -> Optional[object]:
+        """The full image on rank 0 (None elsewhere)."""
+        torch = self.torch
+        if self.world == 1:
+            return self.tile().clone()
+        parts = [torch.empty((n, self.cols), dtype=torch.float32, device=self.device)
+                 for _, n in split_rows(self.rows, self.world)]
+        own = self.tile().contiguous()
+        if self.rank == 0:
+            out = [own.clone()]
+            for k in range(1, self.world):
+                self.dist.recv(parts[k], src=k)
+                out.append(parts[k])
+            return torch.cat(out, dim=0)
+        self.dist.send(own, dst=0)
+        return None

@@ -100,7 +100,7 @@ def test_gpu_config4_8192(restatement):
     L = torch.tril(a, -1) + torch.eye(n, device="cuda", dtype=torch.float64)
     U = torch.triu(a)
     r = torch.linalg.norm(L @ U - a0.double()) / torch.linalg.norm(a0.double())
-    assert float(r) < 1e-6
+    assert float(r) < 1e-4  # fp32 LU of an 8192 matrix: ~n * eps_fp32 bound
 
 
 @pytest.mark.gpu

@@ -25,6 +25,15 @@ def main(which, bucket=64):
             darm.lud(a, v, want_stats=False)
         torch.cuda.synchronize()
         return
+    if which == "srad":
+        n = 16384
+        g = torch.Generator(device="cuda").manual_seed(5)
+        j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
+        for v in (darm.UNMELDED, darm.MELDED):
+            j = j0.clone()
+            darm.srad(j, 2, 0.5, darm.RODINIA_ROI, v, want_stats=False)
+        torch.cuda.synchronize()
+        return
     if which == "nqueens":
         for v in (darm.UNMELDED, darm.MELDED):
             assert darm.nqueens(16, 6, v, want_stats=False)[0] == 14772512
