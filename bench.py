@@ -48,12 +48,20 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def profile_summary(name):
-    path = os.path.join(ROOT, "profiles", name)
-    if os.path.exists(path):
-        with open(path) as f:
-            return json.load(f)
-    return None
+def ncu_kernel_summary(stem, pattern):
+    """Latest committed ncu summary profiles/r<NN>_ncu_<stem>.json -> entry whose
+    kernel name contains `pattern` (None when absent)."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r[0-9][0-9]_ncu_{stem}.json")))
+    if not paths:
+        return None, None
+    with open(paths[-1]) as f:
+        d = json.load(f)
+    for k in d.get("kernels", []):
+        if pattern in k.get("kernel", ""):
+            return k, os.path.relpath(paths[-1], ROOT)
+    return None, os.path.relpath(paths[-1], ROOT)
 
 
 # ------------------------------------------------------------------ clocks
@@ -348,7 +356,17 @@ def our_arm(args):
     peak, peak_src = measured_peaks()
     alg_bytes = 8 * n
     achieved = alg_bytes / (mel["kernel_ms_mean"] / 1e3) / 1e9
-    prof = profile_summary("bitonic_sort_r01.json") or {}
+    prof_m, prof_src = ncu_kernel_summary("bitonic", "bitonic_sort_kernel<1, 64")
+    prof_u, _ = ncu_kernel_summary("bitonic", "bitonic_sort_kernel<0, 64")
+    lane_eff = None
+    if prof_m and prof_u:
+        lane_eff = {"source": prof_src + " (ncu --set full, one launch per form)",
+                    "unmelded": {"thread_inst_per_inst_div32": prof_u.get("lane_efficiency"),
+                                 "pred_on_div32": prof_u.get("lane_efficiency_pred_on"),
+                                 "branch_uniform_pct": prof_u.get("branch_uniform_pct")},
+                    "melded": {"thread_inst_per_inst_div32": prof_m.get("lane_efficiency"),
+                               "pred_on_div32": prof_m.get("lane_efficiency_pred_on"),
+                               "branch_uniform_pct": prof_m.get("branch_uniform_pct")}}
     line = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mel["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -356,9 +374,11 @@ def our_arm(args):
         "config": workload_config(args, "melded"),
         "melded_vs_unmelded_speedup": unm["total_ms"] / mel["total_ms"],
         "unmelded": {"value": n * world / (unm["total_ms"] / args.steps / 1e3), "ms_per_step": unm["ms_per_step"]},
-        "lane_efficiency": prof.get("lane_efficiency"),
+        "lane_efficiency": lane_eff,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": prof.get("dram_bytes_per_launch"), "peak_source": peak_src,
+                     "traffic": (prof_m or {}).get("dram_bytes"), "peak_source": peak_src,
+                     "traffic_note": "ncu dram__bytes read+write of one launch; below the algorithmic bytes "
+                                     "because the written keys stay in the 126 MB L2 at kernel end",
                      "kernel": "bitonic_sort_kernel<true,64,256>",
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "note": "issue-bound: 21 compare-exchange steps per 8 B of HBM traffic; see DESIGN.md §Roofline"},
