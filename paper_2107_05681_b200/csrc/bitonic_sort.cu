@@ -31,25 +31,17 @@ struct Network {
 
 template <bool M, int B, int CTA>
 __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__ keys, uint32_t n) {
+  constexpr int LB = __builtin_ctz(B);
   constexpr bool kNeedSmem = B > 32;
   __shared__ int32_t xch[kNeedSmem ? 2 : 1][kNeedSmem ? CTA : 1];
   const uint32_t tiles = (n + CTA - 1) / CTA;
   const int t = int(threadIdx.x) & (B - 1);
-  // Per-lane step predicates, loop-invariant across tiles: bit s of keepm is
-  // icmp.lt %t %j (j = t^k, i.e. (t & k) == 0) and of upm is
-  // icmp.eq (and %t %dir) 0 for the s-th (dir, k) of the network.
-  uint64_t keepm = 0, upm = 0;
-  {
-    int s = 0;
+  // Lane-invariant bits of t (loop-invariant across tiles, kept in predicate
+  // registers): keep = icmp.lt %t %j <=> !bit[log k], up = icmp.eq (and %t
+  // %dir) 0 <=> !bit[log dir].
+  bool bit[LB > 0 ? LB : 1];
 #pragma unroll
-    for (int dir = 2; dir <= B; dir <<= 1)
-#pragma unroll
-      for (int k = dir >> 1; k >= 1; k >>= 1, ++s) {
-        keepm |= uint64_t((t & k) == 0) << s;
-        upm |= uint64_t((t & dir) == 0) << s;
-      }
-  }
-  const uint64_t eqm = ~(keepm ^ upm);
+  for (int i = 0; i < LB; ++i) bit[i] = (t >> i) & 1;
   uint32_t tile = blockIdx.x;
   uint32_t idx = tile * CTA + threadIdx.x;
   int32_t next = (tile < tiles && idx < n) ? keys[idx] : INT_MAX;
@@ -59,11 +51,19 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
     idx += gridDim.x * CTA;
     if (tile + gridDim.x < tiles) next = idx < n ? keys[idx] : INT_MAX;   // prefetch
     int par = 0;
-    int s = 0;
+    int32_t neg = 0;   // melded: lanes of a descending half work on ~v (order reversal)
 #pragma unroll
-    for (int dir = 2; dir <= B; dir <<= 1) {
+    for (int d = 1; d <= LB; ++d) {
+      if constexpr (M) {
+        // melded `select %up`: within stage dir = 2^d the !up lanes flip their
+        // keys' order once (bitwise not), so every lane's exchange is the up-form
+        const int32_t m = (d < LB && bit[d]) ? -1 : 0;
+        v ^= m ^ neg;
+        neg = m;
+      }
 #pragma unroll
-      for (int k = dir >> 1; k >= 1; k >>= 1, ++s) {
+      for (int kb = d - 1; kb >= 0; --kb) {
+        const int k = 1 << kb;
         int32_t b0;
         if (k < 32) {
           b0 = __shfl_xor_sync(0xffffffffu, v, k);        // load.shared buf %j
@@ -73,9 +73,17 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
           b0 = xch[par][threadIdx.x ^ k];
           par ^= 1;
         }
-        v = bitonic_exchange<M>(v, b0, (keepm >> s) & 1, (upm >> s) & 1, (eqm >> s) & 1);
+        if constexpr (!M) {
+          v = bitonic_exchange<false>(v, b0, !bit[kb], d >= LB ? true : !bit[d], false);
+        } else {
+          // need1 = (keep == up) ? cv > b0 : cv < b0 with up folded into the data:
+          // take the partner's key iff (b0 < cv) xor !keep   (equal keys: either)
+          const bool take = (b0 < v) ^ bit[kb];
+          v = take ? b0 : v;                               // ^e.m: the single melded store
+        }
       }
     }
+    if constexpr (M) v ^= neg;
     if (my < n) keys[my] = v;
   }
 }

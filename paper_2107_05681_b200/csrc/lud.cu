@@ -5,9 +5,9 @@
 // (oracle/darm_oracle.c, oracle_lud) performs the same floating-point
 // operations in the same order, so GPU and CPU results agree bit for bit.
 //
-// Per 16-column step at offset o:
-//   diagonal   factor A[o:o+16, o:o+16]                          (1 CTA)
-//   perimeter  U12 = L11^-1 A12 for every block right of the diagonal and
+// Per 16-column step at offset o (two launches):
+//   panel      factor A[o:o+16, o:o+16] (every CTA, in shared memory), then
+//              U12 = L11^-1 A12 for every block right of the diagonal and
 //              L21 = A21 U11^-1 for every block below it          (melded kernel)
 //   internal   A22 -= L21 U12, 16-term fp32 FMA chains             (64x64 tiles)
 // The perimeter kernel is the paper's melding target: each warp owns one
@@ -18,7 +18,7 @@
 //   melded:   hand-melded as the paper did for LUD: one load,
 //             one solve and one store sequence whose addresses, shared-memory
 //             operands and the role-only division are chosen per lane.
-// The 3 x (n/16) launches are recorded once into a CUDA graph per (n, form,
+// The 2 x (n/16) launches are recorded once into a CUDA graph per (n, form,
 // buffer) and replayed.
 #include <cstdint>
 
@@ -32,131 +32,113 @@ constexpr int BS = 16;
 constexpr int LD = BS + 1;  // padded shared row: conflict-free column walks
 }  // namespace
 
-// ------------------------------------------------------------------ diagonal
-// Doolittle on the 16x16 diagonal block; column i of L then row i+1 of U.
-__global__ void __launch_bounds__(BS) lud_diagonal_kernel(float *__restrict__ a, int n, int o) {
-  __shared__ float s[BS][LD];
-  const int tx = threadIdx.x;
-  const float *blk = a + size_t(o) * n + o;
-  for (int i = 0; i < BS; ++i) s[i][tx] = blk[size_t(i) * n + tx];
-  __syncthreads();
-  for (int i = 0; i < BS - 1; ++i) {
-    if (tx > i) {
-      float x = s[tx][i];
-      for (int j = 0; j < i; ++j) x = fmaf(-s[tx][j], s[j][i], x);
-      s[tx][i] = x / s[i][i];
-    }
-    __syncthreads();
-    if (tx > i) {
-      float x = s[i + 1][tx];
-      for (int j = 0; j < i + 1; ++j) x = fmaf(-s[i + 1][j], s[j][tx], x);
-      s[i + 1][tx] = x;
-    }
-    __syncthreads();
-  }
-  float *out = a + size_t(o) * n + o;
-  for (int i = 1; i < BS; ++i) out[size_t(i) * n + tx] = s[i][tx];
-}
-
-// ------------------------------------------------------------------ perimeter
-// One warp per block pair p (row block right of the diagonal, column block
-// below it); kPairs warps per CTA share the diagonal block.
+// ------------------------------------------------------------------ panel
+// One launch per 16-column step: every CTA factors the 16x16 diagonal block
+// (Doolittle: column i of L, then row i+1 of U — warp 0, lanes 0..15) into
+// shared memory, CTA 0 writes it back, and each warp then solves one
+// perimeter block pair p (row block right of the diagonal, column block below
+// it) with the pair's 16 values per lane in registers.  Redundant diagonal
+// factorisations replace a separate launch and a global round trip.
 constexpr int kPairs = 4;
 
 template <bool M>
-__global__ void __launch_bounds__(32 * kPairs) lud_perimeter_kernel(float *__restrict__ a, int n, int o,
-                                                                   int npairs) {
+__global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs) {
   __shared__ float dia[BS][LD];
-  __shared__ float peri_row[kPairs][BS][LD];   // [pair][i][idx]  = A[o+i][cb+idx]
-  __shared__ float peri_col[kPairs][BS][LD];   // [pair][i][idx]  = A[rb+i][o+idx]
+  __shared__ float diaT[BS][LD];   // diaT[i][j] = dia[j][i]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * kPairs + warp;   // pair index; block column/row (p+1)
-  const bool live = p < npairs;
-  const size_t cb = size_t(o) + size_t(BS) * (p + 1);   // column of the row block
-  const size_t rb = cb;                                   // row of the column block
-  // diagonal block, shared by the CTA's warps
   for (int e = threadIdx.x; e < BS * BS; e += blockDim.x)
     dia[e / BS][e % BS] = a[(size_t(o) + e / BS) * n + o + e % BS];
-  float(*prow)[LD] = peri_row[warp];
-  float(*pcol)[LD] = peri_col[warp];
+  __syncthreads();
+  if (warp == 0) {
+    const int tx = lane;
+    for (int i = 0; i < BS - 1; ++i) {
+      if (tx > i && tx < BS) {
+        float x = dia[tx][i];
+        for (int j = 0; j < i; ++j) x = fmaf(-dia[tx][j], dia[j][i], x);
+        dia[tx][i] = x / dia[i][i];
+      }
+      __syncwarp();
+      if (tx > i && tx < BS) {
+        float x = dia[i + 1][tx];
+        for (int j = 0; j < i + 1; ++j) x = fmaf(-dia[i + 1][j], dia[j][tx], x);
+        dia[i + 1][tx] = x;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < BS * BS; e += blockDim.x) {
+    diaT[e % BS][e / BS] = dia[e / BS][e % BS];
+    if (blockIdx.x == 0 && e >= BS) a[(size_t(o) + e / BS) * n + o + e % BS] = dia[e / BS][e % BS];
+  }
+  __syncthreads();
+  const int p = blockIdx.x * kPairs + warp;
+  if (p >= npairs) return;                                 // warp-uniform
+  const size_t cb = size_t(o) + size_t(BS) * (p + 1);      // column of the row block
+  const size_t rb = cb;                                    // row of the column block
   if constexpr (!M) {
-    if (live) {
-      if (lane < BS) {                                   // row role
-        DARM_ARM("lud.row.load");
-        const int idx = lane;
-        for (int i = 0; i < BS; ++i) prow[i][idx] = a[(size_t(o) + i) * n + cb + idx];
-        DARM_ARM("lud.row.load.end");
-      } else {                                           // column role
-        DARM_ARM("lud.col.load");
-        const int idx = lane - BS;
-        for (int i = 0; i < BS; ++i) pcol[i][idx] = a[(rb + i) * n + o + idx];
-        DARM_ARM("lud.col.load.end");
+    if (lane < BS) {                                       // U12 = L11^-1 A12, column idx
+      DARM_ARM("lud.row");
+      const int idx = lane;
+      float x[BS];
+#pragma unroll
+      for (int i = 0; i < BS; ++i) x[i] = a[(size_t(o) + i) * n + cb + idx];
+#pragma unroll
+      for (int i = 1; i < BS; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j) x[i] = fmaf(-dia[i][j], x[j], x[i]);
+#pragma unroll
+      for (int i = 1; i < BS; ++i) a[(size_t(o) + i) * n + cb + idx] = x[i];
+      DARM_ARM("lud.row.end");
+    } else {                                               // L21 = A21 U11^-1, row idx
+      DARM_ARM("lud.col");
+      const int idx = lane - BS;
+      float y[BS];
+      const float4 *src = reinterpret_cast<const float4 *>(a + (rb + idx) * n + o);
+#pragma unroll
+      for (int q = 0; q < BS / 4; ++q) {
+        const float4 v = src[q];
+        y[4 * q] = v.x;
+        y[4 * q + 1] = v.y;
+        y[4 * q + 2] = v.z;
+        y[4 * q + 3] = v.w;
       }
-    }
-    __syncthreads();
-    if (live) {
-      if (lane < BS) {                                   // U12 = L11^-1 A12
-        DARM_ARM("lud.row.solve");
-        const int idx = lane;
-        for (int i = 1; i < BS; ++i) {
-          float x = prow[i][idx];
-          for (int j = 0; j < i; ++j) x = fmaf(-dia[i][j], prow[j][idx], x);
-          prow[i][idx] = x;
-        }
-        DARM_ARM("lud.row.solve.end");
-      } else {                                           // L21 = A21 U11^-1
-        DARM_ARM("lud.col.solve");
-        const int idx = lane - BS;
-        for (int i = 0; i < BS; ++i) {
-          float x = pcol[idx][i];
-          for (int j = 0; j < i; ++j) x = fmaf(-pcol[idx][j], dia[j][i], x);
-          pcol[idx][i] = x / dia[i][i];
-        }
-        DARM_ARM("lud.col.solve.end");
+#pragma unroll
+      for (int i = 0; i < BS; ++i) {
+#pragma unroll
+        for (int j = 0; j < i; ++j) y[i] = fmaf(-y[j], dia[j][i], y[i]);
+        y[i] = y[i] / dia[i][i];
       }
-    }
-    __syncwarp();
-    if (live) {
-      if (lane < BS) {
-        DARM_ARM("lud.row.store");
-        const int idx = lane;
-        for (int i = 1; i < BS; ++i) a[(size_t(o) + i) * n + cb + idx] = prow[i][idx];
-        DARM_ARM("lud.row.store.end");
-      } else {
-        DARM_ARM("lud.col.store");
-        const int idx = lane - BS;
-        for (int i = 0; i < BS; ++i) a[(rb + i) * n + o + idx] = pcol[i][idx];
-        DARM_ARM("lud.col.store.end");
-      }
+      float4 *dst = reinterpret_cast<float4 *>(a + (rb + idx) * n + o);
+#pragma unroll
+      for (int q = 0; q < BS / 4; ++q) dst[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+      DARM_ARM("lud.col.end");
     }
   } else {
-    // Melded: lane role r = lane >= 16 selects addresses; the loops, loads,
-    // FMAs and stores are shared.  The row solve runs i = 0..15 with an empty
-    // i = 0 step (j < 0); fmaf(a,b,c) == fmaf(b,a,c), so the column role's
-    // pcol[idx][j] * dia[j][i] is the same operation as -X(j) * D(i,j) with
-    // D the role-transposed diagonal access.
+    // Melded (by hand, as the paper did for LUD): one load / solve / store
+    // sequence.  The role picks the global addresses (row role: column idx of
+    // the row block, stride n; column role: row idx of the column block,
+    // stride 1) and the diagonal operand (dia or its transpose, so both read
+    // D[i][j]); fmaf(a,b,c) == fmaf(b,a,c), so -x[j] * D[i][j] is the same
+    // operation as either arm's.  The column role's division is the only
+    // one-sided run.
     const bool col = lane >= BS;
     const int idx = lane & (BS - 1);
-    float *X = col ? &pcol[idx][0] : &prow[0][idx];       // X(i) = X[i * xs]
-    const int xs = col ? 1 : LD;
-    float *L = col ? &pcol[0][idx] : &prow[0][idx];       // load/store slots [i*LD]
-    const size_t g0 = col ? rb * n + o + idx : size_t(o) * n + cb + idx;
-    const int di = col ? 1 : LD, dj = col ? LD : 1;       // D(i,j) = dia[i*di + j*dj]
-    const float *D = &dia[0][0];
-    if (live)
-      for (int i = 0; i < BS; ++i) L[i * LD] = a[g0 + size_t(i) * n];
-    __syncthreads();
-    if (live) {
-      for (int i = 0; i < BS; ++i) {
-        float x = X[i * xs];
-        for (int j = 0; j < i; ++j) x = fmaf(-X[j * xs], D[i * di + j * dj], x);
-        if (col) x = x / D[i * LD + i];                  // column-role-only run
-        X[i * xs] = x;
-      }
+    const float(*D)[LD] = col ? diaT : dia;
+    const size_t g0 = col ? (rb + idx) * n + o : size_t(o) * n + cb + idx;
+    const size_t gs = col ? 1 : size_t(n);
+    float x[BS];
+#pragma unroll
+    for (int i = 0; i < BS; ++i) x[i] = a[g0 + i * gs];
+#pragma unroll
+    for (int i = 0; i < BS; ++i) {
+#pragma unroll
+      for (int j = 0; j < i; ++j) x[i] = fmaf(-x[j], D[i][j], x[i]);
+      if (col) x[i] = x[i] / D[i][i];
     }
-    __syncwarp();
-    if (live)
-      for (int i = col ? 0 : 1; i < BS; ++i) a[g0 + size_t(i) * n] = L[i * LD];
+#pragma unroll
+    for (int i = 0; i < BS; ++i)
+      if (i > 0 || col) a[g0 + i * gs] = x[i];
   }
 }
 
@@ -217,18 +199,17 @@ cudaError_t record_lud(int variant, float *a, int n, cudaStream_t s, int *launch
   const int nb = n / BS;
   for (int step = 0; step < nb; ++step) {
     const int o = step * BS;
-    lud_diagonal_kernel<<<1, BS, 0, s>>>(a, n, o);
-    ++*launches;
     const int m = nb - step - 1;   // trailing blocks
-    if (m == 0) break;
-    const int grid = (m + kPairs - 1) / kPairs;
+    const int grid = m > 0 ? (m + kPairs - 1) / kPairs : 1;
     if (variant)
-      lud_perimeter_kernel<true><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m);
+      lud_panel_kernel<true><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m);
     else
-      lud_perimeter_kernel<false><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m);
+      lud_panel_kernel<false><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m);
+    ++*launches;
+    if (m == 0) break;
     const int t = (m + 3) / 4;
     lud_internal_kernel<<<dim3(t, t), 256, 0, s>>>(a, n, o, m);
-    *launches += 2;
+    ++*launches;
   }
   return cudaGetLastError();
 }
