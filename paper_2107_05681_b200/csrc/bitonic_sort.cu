@@ -29,11 +29,11 @@ struct Network {
   static_assert(kSteps <= 64, "step masks are 64-bit");
 };
 
-template <bool M, int B, int CTA>
+template <bool M, int B, int CTA, int U>
 __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__ keys, uint32_t n) {
   constexpr int LB = __builtin_ctz(B);
   constexpr bool kNeedSmem = B > 32;
-  __shared__ int32_t xch[kNeedSmem ? 2 : 1][kNeedSmem ? CTA : 1];
+  __shared__ int32_t xch[kNeedSmem ? 2 : 1][U][kNeedSmem ? CTA : 1];
   const uint32_t tiles = (n + CTA - 1) / CTA;
   const int t = int(threadIdx.x) & (B - 1);
   // Lane-invariant bits of t (loop-invariant across tiles, kept in predicate
@@ -42,14 +42,26 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
   bool bit[LB > 0 ? LB : 1];
 #pragma unroll
   for (int i = 0; i < LB; ++i) bit[i] = (t >> i) & 1;
+  // U independent tiles per iteration (tile, tile + G, ...): their
+  // shuffle -> compare -> select chains interleave and hide each other's latency.
+  const uint32_t G = gridDim.x;
   uint32_t tile = blockIdx.x;
-  uint32_t idx = tile * CTA + threadIdx.x;
-  int32_t next = (tile < tiles && idx < n) ? keys[idx] : INT_MAX;
-  for (; tile < tiles; tile += gridDim.x) {
-    int32_t v = next;
-    const uint32_t my = idx;
-    idx += gridDim.x * CTA;
-    if (tile + gridDim.x < tiles) next = idx < n ? keys[idx] : INT_MAX;   // prefetch
+  int32_t next[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t tt = tile + u * G, id = tt * CTA + threadIdx.x;
+    next[u] = (tt < tiles && id < n) ? keys[id] : INT_MAX;
+  }
+  for (; tile < tiles; tile += U * G) {
+    int32_t v[U];
+    uint32_t my[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = next[u];
+      my[u] = (tile + u * G) * CTA + threadIdx.x;
+      const uint32_t tn = tile + (U + u) * G, id = tn * CTA + threadIdx.x;
+      if (tn < tiles) next[u] = id < n ? keys[id] : INT_MAX;   // prefetch
+    }
     int par = 0;
     int32_t neg = 0;   // melded: lanes of a descending half work on ~v (order reversal)
 #pragma unroll
@@ -58,33 +70,43 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
         // melded `select %up`: within stage dir = 2^d the !up lanes flip their
         // keys' order once (bitwise not), so every lane's exchange is the up-form
         const int32_t m = (d < LB && bit[d]) ? -1 : 0;
-        v ^= m ^ neg;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] ^= m ^ neg;
         neg = m;
       }
 #pragma unroll
       for (int kb = d - 1; kb >= 0; --kb) {
         const int k = 1 << kb;
-        int32_t b0;
+        int32_t b0[U];
         if (k < 32) {
-          b0 = __shfl_xor_sync(0xffffffffu, v, k);        // load.shared buf %j
+#pragma unroll
+          for (int u = 0; u < U; ++u) b0[u] = __shfl_xor_sync(0xffffffffu, v[u], k);   // load.shared buf %j
         } else {
-          xch[par][threadIdx.x] = v;
+#pragma unroll
+          for (int u = 0; u < U; ++u) xch[par][u][threadIdx.x] = v[u];
           __syncthreads();
-          b0 = xch[par][threadIdx.x ^ k];
+#pragma unroll
+          for (int u = 0; u < U; ++u) b0[u] = xch[par][u][threadIdx.x ^ k];
           par ^= 1;
         }
-        if constexpr (!M) {
-          v = bitonic_exchange<false>(v, b0, !bit[kb], d >= LB ? true : !bit[d], false);
-        } else {
-          // need1 = (keep == up) ? cv > b0 : cv < b0 with up folded into the data:
-          // take the partner's key iff (b0 < cv) xor !keep   (equal keys: either)
-          const bool take = (b0 < v) ^ bit[kb];
-          v = take ? b0 : v;                               // ^e.m: the single melded store
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if constexpr (!M) {
+            v[u] = bitonic_exchange<false>(v[u], b0[u], !bit[kb], d >= LB ? true : !bit[d], false);
+          } else {
+            // need1 = (keep == up) ? cv > b0 : cv < b0 with up folded into the data:
+            // take the partner's key iff (b0 < cv) xor !keep   (equal keys: either)
+            const bool take = (b0[u] < v[u]) ^ bit[kb];
+            v[u] = take ? b0[u] : v[u];                       // ^e.m: the single melded store
+          }
         }
       }
     }
-    if constexpr (M) v ^= neg;
-    if (my < n) keys[my] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if constexpr (M) v[u] ^= neg;
+      if (tile + u * G < tiles && my[u] < n) keys[my[u]] = v[u];
+    }
   }
 }
 
@@ -101,12 +123,13 @@ cudaError_t launch_b(int32_t *keys, int64_t n, cudaStream_t s) {
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_sms <= 0) g_sms = 148;
   }
+  constexpr int U = B <= 256 ? 2 : 1;
   const int64_t tiles = (n + CTA - 1) / CTA;
   const int per_sm = 2048 / CTA;
   int64_t grid = int64_t(g_sms) * per_sm;
-  if (grid > tiles) grid = tiles;
+  if (grid > (tiles + U - 1) / U) grid = (tiles + U - 1) / U;
   if (grid < 1) grid = 1;
-  bitonic_sort_kernel<M, B, CTA><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
+  bitonic_sort_kernel<M, B, CTA, U><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
 }
 

@@ -126,13 +126,21 @@ __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
   west_east(row(g0), j0, w0, e0);
   float c0 = srad_coeff<M>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
   float jp2 = row(g0 + 2)[jc];
+  // sliding row pointers: p1 -> row g+1 (lane 31's east value), pn -> the
+  // next row to prefetch (g+3, held at the last row the buffer/image has)
+  const int glim = min(gmax, P.r0 + P.tile_rows + 1);
+  const float *p1 = row(g0 + 1);
+  int g1 = min(g0 + 1, gmax);
+  int gn = min(g0 + 3, glim);
+  const float *pn = row(gn);
   const bool roi_warp = P.roi_out && wcol >= P.roi_w0 && wcol < P.roi_w0 + P.roi_groups;
+  float *outp = P.jout + size_t(seg0 + 1) * cols + j;
   for (int i = seg0; i < seg1; ++i) {
     const int g = P.r0 + i;
-    const float jp3 = row(min(g + 3, P.r0 + P.tile_rows + 1))[jc];   // prefetch (last halo row at most)
+    const float jp3 = pn[jc];                              // prefetch
     // c at row g+1 (clamped: at the last image row it is c(g) itself)
     float w1, e1;
-    west_east(row(g + 1), jp1, w1, e1);
+    west_east(p1, jp1, w1, e1);
     const float c1 = (g + 1 <= gmax) ? srad_coeff<M>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
     // east neighbour's c at row g
     float ce = __shfl_down_sync(0xffffffffu, c0, 1);
@@ -141,7 +149,8 @@ __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
     const float dN = jm1 - j0, dS = jp1 - j0, dW = w0 - j0, dE = e0 - j0;
     const float d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
     const float jn = j0 + P.lq * d;
-    if (out_lane) P.jout[size_t(i + 1) * cols + j] = jn;
+    if (out_lane) *outp = jn;
+    outp += cols;
     if (roi_warp && g >= P.roi_r1 && g <= P.roi_r2) {
       const bool in = out_lane && j >= P.roi_c1 && j <= P.roi_c2;
       double s = in ? double(jn) : 0.0, s2 = in ? double(jn) * double(jn) : 0.0;
@@ -164,6 +173,14 @@ __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
     w0 = w1;
     e0 = e1;
     c0 = c1;
+    if (g1 < gmax) {
+      ++g1;
+      p1 += cols;
+    }
+    if (gn < glim) {
+      ++gn;
+      pn += cols;
+    }
   }
 }
 

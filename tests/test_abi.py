@@ -146,17 +146,18 @@ def test_sass_unmelded_keeps_both_arms():
 
 
 def test_sass_bitonic_sort_forms():
-    un = _sass("bitonic_sort_kernel<false, 64, 256>")
-    me = _sass("bitonic_sort_kernel<true, 64, 256>")
+    un = _sass("bitonic_sort_kernel<false, 64, 256, 2>")
+    me = _sass("bitonic_sort_kernel<true, 64, 256, 2>")
     # Same partner reads in both forms (20 shuffles + 1 shared exchange for
     # B=64); the unmelded network issues both arms of every `up` branch
     # (ptxas if-converts them into complementary predicated min/max), the
     # melded one a single predicated min/max per step.
-    assert sum("SHFL.BFLY" in i for i in un) == sum("SHFL.BFLY" in i for i in me) == 20
+    # (two tiles per iteration, U = 2)
+    assert sum("SHFL.BFLY" in i for i in un) == sum("SHFL.BFLY" in i for i in me) == 2 * 20
     assert sum("BAR.SYNC" in i for i in un) == sum("BAR.SYNC" in i for i in me) == 1
     assert len(un) > 1.4 * len(me)
     # unmelded: both arms' min/max per step (predicated VIMNMX pairs); melded:
     # one compare folded with keep (ISETP.*.XOR) and one select per step
-    assert sum("IMNMX" in i for i in un) >= 60
-    assert sum("ISETP" in i and ".XOR" in i for i in me) >= 20
-    assert sum(i.startswith("SEL") for i in me) >= 20
+    assert sum("IMNMX" in i for i in un) >= 2 * 60
+    assert sum("ISETP" in i and ".XOR" in i for i in me) >= 2 * 20
+    assert sum(i.startswith("SEL") for i in me) >= 2 * 20
