@@ -215,7 +215,7 @@ int oracle_bitonic_sort(int32_t *keys, int64_t n, int bucket) {
 /* ------------------------------------------------------------ N-Queens
  * The reference has no NQU code; this is an independent
  * recursive restatement of the search that paper_2107_05681_b200/ir/
- * nqueens_step.ir runs iteratively.  Prefix order: every valid placement of
+ * nqueens_sym.ir runs iteratively.  Prefix order: every valid placement of
  * rows 0..base-1, lowest free column first; prefix i belongs to rank i % world. */
 typedef struct {
   int n, base, rank, world;

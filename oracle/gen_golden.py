@@ -126,7 +126,7 @@ def bitonic_sort_fixtures(ref: Reference) -> dict:
 
 
 NQ_IR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                     "paper_2107_05681_b200", "ir", "nqueens_step.ir")
+                     "paper_2107_05681_b200", "ir", "nqueens_sym.ir")
 
 
 def nq_prefixes(n, base):
@@ -147,13 +147,15 @@ def nq_prefixes(n, base):
 
 
 def nqueens_chain_fixtures(ref: Reference) -> dict:
-    """The reference interpreter runs ir/nqueens_step.ir (original and as melded
+    """The reference interpreter runs ir/nqueens_sym.ir (original and as melded
     by runDarm) to a fixpoint per warp of prefixes: per-prefix solution counts
-    and unit-latency utilisation."""
+    and unit-latency utilisation.  The IR keeps the diagonals in board
+    coordinates: st_d1 = d2_rel << base (bit r + c), st_d2 = (d1_rel & mask) <<
+    (n - 1 - base) (bit c - r + n - 1)."""
     text = open(NQ_IR).read()
     orig = ref.load_text(text, 0)
     meld = ref.load_text(text, 1)
-    out = {"ir": "paper_2107_05681_b200/ir/nqueens_step.ir", "melds": meld.layout["melds"], "cases": []}
+    out = {"ir": "paper_2107_05681_b200/ir/nqueens_sym.ir", "melds": meld.layout["melds"], "cases": []}
     W = 32
     for n, base in ((4, 1), (5, 1), (6, 2), (7, 2), (8, 2), (9, 2), (10, 3)):
         pre = nq_prefixes(n, base)
@@ -168,11 +170,14 @@ def nqueens_chain_fixtures(ref: Reference) -> dict:
                 for t in range(W):
                     if t < len(chunk):
                         c, d1, d2 = chunk[t]
-                        g[t], g[64 + t], g[128 + t], g[192 + t] = base, c, np.int64(d1).astype(np.int32), d2
+                        a1 = (d2 << base) & 0xFFFFFFFF
+                        a2 = ((d1 & mask) << (n - 1 - base)) & 0xFFFFFFFF
+                        g[t], g[64 + t] = base, c
+                        g[128 + t], g[192 + t] = np.int64(a1).astype(np.int32), np.int64(a2).astype(np.int32)
                         g[256 + t] = ~(c | d1 | d2) & mask
                     else:
                         g[t] = base - 1
-                sh = np.zeros(4 * 1024, np.int32)
+                sh = np.zeros(1024, np.int32)
                 rounds, st = mod.run_to_fixpoint(W, np.array([n, mask, base], np.int32), g, sh, unit_latency=True)
                 res[tag] = g[320:320 + len(chunk)].tolist()
                 case["rounds"][tag] += rounds

@@ -310,7 +310,7 @@ int64_t ref_compare_warps(const ref_module *h, int warp, int64_t n_warps,
 // Chains executeWarp over one warp until a step changes neither global nor
 // shared memory (a fixpoint), feeding globalFinal/sharedFinal of each step into
 // the next — the loop a per-iteration step kernel such as
-// paper_2107_05681_b200/ir/nqueens_step.ir stands for.  globals/shared are the
+// paper_2107_05681_b200/ir/nqueens_sym.ir stands for.  globals/shared are the
 // declared-size arrays in declaration order (in/out).  stats_sum (7 counters)
 // accumulates every step that changed state; *rounds receives their number.
 int ref_run_to_fixpoint(const ref_module *h, int warp, const int32_t *args, int32_t *globals,

@@ -1,21 +1,31 @@
 // nqueens.cu — N-Queens solution count (NQU) in
-// the unmelded and melded forms of paper_2107_05681_b200/ir/nqueens_step.ir.
+// the unmelded and melded forms of paper_2107_05681_b200/ir/nqueens_sym.ir.
 //
 // The reference has no NQU code; the search loop is written in the reference's
-// mini-IR (ir/nqueens_step.ir: one iteration = pop / count a solution / push,
-// the paper's "if-then-elseif-then") and the melded form below mirrors what the
-// reference pass emits for it (runDarm, threshold 0.2: two block-region melds,
-// 12 selects, 7 unpredicated runs — DESIGN.md §NQU).  The reference interpreter
-// runs the same IR as the oracle (tests/golden/nqueens_chain.json).
+// mini-IR (ir/nqueens_sym.ir: one iteration = push a queen or pop one, the
+// paper's divergent search-loop branch) and the melded form below mirrors what
+// the reference pass emits for it (runDarm, threshold 0.2: one block-block
+// meld of ^pop and ^push, MP 0.435, 7 selects, 6 unpredicated runs —
+// DESIGN.md §NQU).  The reference interpreter runs the same IR as the oracle
+// (tests/golden/nqueens_chain.json).
+//
+// Formulation (ir/nqueens_sym.ir header): the diagonals are kept in board
+// coordinates (d1 bit r + c, d2 bit c - r + n - 1), the per-row stack holds
+// only the column bit placed at that row, and a pop takes that bit back.  Push
+// and pop then toggle the same three words with b shifted by the same row, so
+// the two arms are one chain in mirror image.  A solution is a push that
+// reaches row n.  The words are 32-bit for n <= 16 and 64-bit up to n = 31.
 //
 // Work decomposition: the host enumerates every valid placement of the first
 // `base` rows (lowest free column first, so prefix i is deterministic) and
 // deals prefix i to rank i % world.  On the GPU every thread runs the IR loop
-// on one prefix at a time, fetching the next from a global counter when its
-// subtree is exhausted (row < base, the IR's ^s %done test).  Thread state
-// (row, cols, d1, d2, av, sol) lives in registers — the IR's st_* globals —
-// and the per-row stack (the IR's sk_* shared arrays) in shared memory at
-// [array][row - base + 1][thread], conflict-free.
+// on one prefix at a time; a lane whose subtree is exhausted (row < base, the
+// IR's ^s %done test) takes the next prefix, the lanes of a warp that need one
+// in the same iteration claiming consecutive prefixes with one atomic
+// (__activemask / __popc / __shfl_sync).  Thread state (row, cols, d1, d2, av,
+// sol) lives in registers — the IR's st_* globals — and the one-word-per-row
+// stack (the IR's sk_b) in shared memory at [row - base + 1][thread],
+// conflict-free.
 #include <cstdint>
 
 #include "common.cuh"
@@ -24,7 +34,7 @@
 namespace darm_gpu {
 
 struct NqParams {
-  const uint32_t *prefix;          // n_prefix x {cols, d1, d2}
+  const uint32_t *prefix;          // n_prefix x {cols, d1, d2} (row-relative, as enumerated)
   uint32_t n_prefix;
   uint32_t *per_prefix;            // solutions per prefix (may be null)
   unsigned long long *total;       // sum of solutions
@@ -33,16 +43,18 @@ struct NqParams {
   uint32_t mask;
 };
 
-template <bool M>
+template <bool M, typename W>
 __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
-  extern __shared__ uint32_t sk[];
+  extern __shared__ uint32_t sk_b[];
+  constexpr int kShift = 8 * sizeof(W) - 1;   // shift amounts wrap like the IR's (interp.cpp:126-127)
   const int T = blockDim.x;
-  const int L = P.levels;
-  uint32_t *sk_cols = sk, *sk_d1 = sk + L * T, *sk_d2 = sk + 2 * L * T, *sk_av = sk + 3 * L * T;
-  const int lane_off = int(threadIdx.x) - (P.base - 1) * T;  // slot(row) = row*T + lane_off
-  const int n1 = P.n - 1;
+  const int lane = int(threadIdx.x) & 31;
+  uint32_t *const stk = sk_b + (int(threadIdx.x) - (P.base - 1) * T);  // row r's slot: stk[r * T]
+  const int n = P.n, nm1 = P.n - 1;
+  const uint32_t mask = P.mask;
   int row = P.base - 1;
-  uint32_t cols = 0, d1 = 0, d2 = 0, av = 0, sol = 0;
+  uint32_t cols = 0, av = 0, sol = 0;
+  W d1 = 0, d2 = 0;
   uint32_t pidx = 0xffffffffu;
   unsigned long long acc = 0;
   for (;;) {
@@ -51,107 +63,111 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
         if (P.per_prefix) P.per_prefix[pidx] = sol;
         acc += sol;
       }
-      pidx = atomicAdd(P.next, 1u);
+      // the lanes refilling in this iteration take consecutive prefixes
+      const unsigned act = __activemask();
+      const int leader = __ffs(act) - 1;
+      unsigned first = 0;
+      if (lane == leader) first = atomicAdd(P.next, unsigned(__popc(act)));
+      first = __shfl_sync(act, first, leader);
+      pidx = first + __popc(act & ((1u << lane) - 1u));
       if (pidx >= P.n_prefix) break;
-      cols = __ldg(P.prefix + 3 * pidx);
-      d1 = __ldg(P.prefix + 3 * pidx + 1);
-      d2 = __ldg(P.prefix + 3 * pidx + 2);
-      av = ~(cols | d1 | d2) & P.mask;
+      const uint32_t pc = __ldg(P.prefix + 3 * pidx);
+      const uint32_t p1 = __ldg(P.prefix + 3 * pidx + 1);
+      const uint32_t p2 = __ldg(P.prefix + 3 * pidx + 2);
+      // row-relative prefix diagonals -> board coordinates at row `base`
+      cols = pc;
+      d1 = W(p2) << P.base;                                // anti-diagonals r + c
+      d2 = W(p1 & mask) << (nm1 - P.base);                 // diagonals c - r + n - 1
+      av = ~(pc | p1 | p2) & mask;
       row = P.base;
       sol = 0;
     }
     if constexpr (!M) {
-      // ^e: condbr %z ^pop ^nz ; ^nz: condbr %last ^leaf ^push
+      // ^e: condbr %z ^pop ^push
       if (av == 0) {
         DARM_ARM("nq.pop");                                // ^pop
         const int r1 = row - 1;
-        const int ix1 = r1 * T + lane_off;
-        cols = sk_cols[ix1];
-        d1 = sk_d1[ix1];
-        d2 = sk_d2[ix1];
-        av = sk_av[ix1];
+        const uint32_t b1 = stk[r1 * T];
+        cols ^= b1;
+        d1 ^= W(b1) << r1;
+        const int k1 = nm1 - r1;
+        d2 ^= W(b1) << k1;
+        const uint32_t a1 = ~(cols | uint32_t(d1 >> r1) | uint32_t(d2 >> k1)) & mask;
+        av = a1 & (0u - (b1 << 1));                        // the free columns above b1
         row = r1;
         DARM_ARM("nq.pop.end");
-      } else if (row == n1) {
-        DARM_ARM("nq.leaf");                               // ^leaf
-        const uint32_t b1 = av & (0u - av);
-        av = av ^ b1;
-        sol += 1;
-        DARM_ARM("nq.leaf.end");
       } else {
         DARM_ARM("nq.push");                               // ^push
         const uint32_t b2 = av & (0u - av);
-        const uint32_t rem2 = av ^ b2;
-        const int ix2 = row * T + lane_off;
-        sk_av[ix2] = rem2;
-        sk_cols[ix2] = cols;
-        sk_d1[ix2] = d1;
-        sk_d2[ix2] = d2;
-        cols = cols | b2;
-        d1 = (d1 | b2) << 1;
-        d2 = (d2 | b2) >> 1;
-        av = ~(cols | d1 | d2) & P.mask;
-        row = row + 1;
+        stk[row * T] = b2;
+        cols ^= b2;
+        d1 ^= W(b2) << row;
+        const int k2 = nm1 - row;
+        d2 ^= W(b2) << k2;
+        const int r2 = row + 1;
+        const int k3 = (k2 - 1) & kShift;
+        av = ~(cols | uint32_t(d1 >> r2) | uint32_t(d2 >> k3)) & mask;
+        sol += r2 == n;
+        row = r2;
         DARM_ARM("nq.push.end");
       }
     } else {
-      // runDarm output: block-region melds of ^pop and ^leaf
-      // into the ^push region.
+      // runDarm output: ^pop and ^push melded block-block.
       const bool z = av == 0;
-      const bool last = row == n1;
-      const bool sel = z ? false : last;                   // the ^leaf lanes
-      const int r1 = (z ? row : 0) - (z ? 1 : int(av));    // melded sub: row-1 | 0-av
-      uint32_t b2 = 0, rem2 = 0;
-      if (!sel && !z) {                                    // ^push.r.m.g
-        b2 = av & uint32_t(r1);
-        rem2 = av ^ b2;
+      const int r1 = (z ? row : 0) - (z ? 1 : int(av));   // melded sub: row - 1 | 0 - av
+      uint32_t b2 = 0;
+      if (!z) b2 = av & uint32_t(r1);                      // ^pop.m.g
+      const int rr = z ? r1 : row;                         // the stack row both arms touch
+      uint32_t *const slot = stk + rr * T;
+      if (!z) *slot = b2;                                  // ^pop.m.g1
+      uint32_t b1 = 0;
+      if (z) b1 = *slot;                                   // ^pop.m.g2
+      const uint32_t b = z ? b1 : b2;                      // %sel3
+      cols ^= b;
+      d1 ^= W(b) << rr;
+      const int k1 = nm1 - rr;
+      d2 ^= W(b) << k1;
+      int r2 = 0, k3 = 0;
+      if (!z) {                                            // ^pop.m.g3
+        r2 = row + 1;
+        k3 = (nm1 - r2) & kShift;
       }
-      const int sel3 = z ? r1 : row;                       // stack row: pop row-1 | push row
-      const int ix1 = sel3 * T + lane_off;
-      const bool sel9 = sel ? false : z;                   // the ^pop lanes
-      uint32_t c2 = 0, f1 = 0, f2 = 0, b1 = 0;
-      if (!sel9) {
-        uint32_t u3 = 0, ng1 = 0;
-        if (!sel) {                                        // ^push.r.m.g1.r.m.g
-          sk_av[ix1] = rem2;
-          sk_cols[ix1] = cols;
-          sk_d1[ix1] = d1;
-          sk_d2[ix1] = d2;
-          c2 = cols | b2;
-          f1 = (d1 | b2) << 1;
-          f2 = (d2 | b2) >> 1;
-          u3 = ~(c2 | f1 | f2);
-        }
-        if (sel) ng1 = 0u - av;                            // ^push.r.m.g1.r.m.g1
-        b1 = (sel ? av : u3) & (sel ? ng1 : P.mask);       // melded and: bit | new av
-        if (sel) {                                         // ^push.r.m.g1.r.m.g2
-          av = av ^ b1;
-          sol += 1;
-        }
-      }
-      if (!sel) {                                          // ^push.r.m.u1
-        uint32_t pc = 0, pd1 = 0, pd2 = 0, pav = 0;
-        if (z) {                                           // ^push.r.m.g2
-          pc = sk_cols[ix1];
-          pd1 = sk_d1[ix1];
-          pd2 = sk_d2[ix1];
-          pav = sk_av[ix1];
-        }
-        cols = z ? pc : c2;
-        d1 = z ? pd1 : f1;
-        d2 = z ? pd2 : f2;
-        av = z ? pav : b1;
-        int r2 = 0;
-        if (!z) r2 = row + 1;                              // ^push.r.m.g3
-        row = z ? r1 : r2;
-      }
+      const int rn = z ? r1 : r2;                          // %sel4
+      const int kn = z ? k1 : k3;                          // %sel5
+      const uint32_t a1 = ~(cols | uint32_t(d1 >> rn) | uint32_t(d2 >> kn)) & mask;
+      if (!z) sol += r2 == n;                              // ^pop.m.g4
+      uint32_t na1 = 0;
+      if (z) na1 = a1 & (0u - (b1 << 1));                  // ^pop.m.g5
+      av = z ? na1 : a1;                                   // %sel6
+      row = rn;
     }
   }
   // every lane has left the loop: reduce the warp's solution counts
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(P.total, acc);
+  if (lane == 0 && acc) atomicAdd(P.total, acc);
 }
+
+namespace {
+template <bool M, typename W>
+cudaError_t launch_form(const NqParams &P, int sms, cudaStream_t s) {
+  const int T = 256;
+  const size_t shm = size_t(P.levels) * T * sizeof(uint32_t);
+  auto kern = nqueens_kernel<M, W>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, shm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  uint64_t grid = uint64_t(sms) * per_sm;
+  const uint64_t need = (uint64_t(P.n_prefix) + T - 1) / T;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<unsigned(grid), T, shm, s>>>(P);
+  return cudaGetLastError();
+}
+}  // namespace
 
 cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, int n, int base,
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,
@@ -166,21 +182,9 @@ cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefi
   P.base = base;
   P.levels = n - base + 1;
   P.mask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
-  const int T = 256;
-  const size_t shm = size_t(4) * P.levels * T * sizeof(uint32_t);
-  auto kern = variant ? nqueens_kernel<true> : nqueens_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, shm);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  uint64_t grid = uint64_t(sms) * per_sm;
-  const uint64_t need = (uint64_t(n_prefix) + T - 1) / T;
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
-  kern<<<unsigned(grid), T, shm, s>>>(P);
-  return cudaGetLastError();
+  if (n <= 16)
+    return variant ? launch_form<true, uint32_t>(P, sms, s) : launch_form<false, uint32_t>(P, sms, s);
+  return variant ? launch_form<true, uint64_t>(P, sms, s) : launch_form<false, uint64_t>(P, sms, s);
 }
 
 }  // namespace darm_gpu

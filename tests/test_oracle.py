@@ -114,7 +114,7 @@ NQUEENS = {1: 1, 2: 0, 3: 0, 4: 2, 5: 10, 6: 4, 7: 40, 8: 92, 9: 352, 10: 724, 1
 
 def test_nqueens_restatement_matches_reference_chain(restatement):
     """Per-prefix solution counts of the reference interpreter running
-    ir/nqueens_step.ir (original and melded) to a fixpoint."""
+    ir/nqueens_sym.ir (original and melded) to a fixpoint."""
     gold = load_golden("nqueens_chain.json")
     for case in gold["cases"]:
         states = restatement.nqueens_prefixes(case["n"], case["base"])
@@ -125,12 +125,17 @@ def test_nqueens_restatement_matches_reference_chain(restatement):
 
 
 def test_nqueens_melded_spec_is_the_reference_pass_output():
-    """The melded CUDA form mirrors runDarm's output for ir/nqueens_step.ir:
-    two block-region melds."""
+    """The melded CUDA form mirrors runDarm's output for ir/nqueens_sym.ir: one
+    block-block meld of ^pop and ^push, and the reference's
+    own simulator sees fewer serialized cycles after it (the paper's
+    direction, PAPER.md:840-841)."""
     gold = load_golden("nqueens_chain.json")
-    kinds = [m["kind"] for m in gold["melds"]]
-    assert kinds == ["block-region", "block-region"]
-    assert [m["selectsInserted"] for m in gold["melds"]] == [9, 3]
+    assert [(m["kind"], m["selectsInserted"], m["unpredicatedRuns"]) for m in gold["melds"]] == \
+        [("block-block", 7, 6)]
+    big = gold["cases"][-1]["stats_unit_latency"]
+    # stats: issued, threadCycles, usefulThreadCycles, serializedCycles, divergentBranches, shared, global
+    assert big["melded"][3] < big["unmelded"][3]
+    assert big["melded"][2] / big["melded"][1] > big["unmelded"][2] / big["unmelded"][1]
 
 
 @pytest.mark.parametrize("n", range(4, 13))
