@@ -42,8 +42,9 @@ cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefi
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,
                            int sms, cudaStream_t s);
 
-// lud.cu: records the 3 x n/16 launches of one decomposition on `s`
-cudaError_t record_lud(int variant, float *a, int n, cudaStream_t s, int *launches);
+// lud.cu: records the launches of one decomposition on `s`; dscr: 256-float
+// device scratch for the factored diagonal block
+cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches);
 
 // srad.cu
 struct SradRoi {

@@ -35,103 +35,148 @@ constexpr int LD = BS + 1;  // padded shared row: conflict-free column walks
 }  // namespace
 
 // ------------------------------------------------------------------ panel
-// One launch per 16-column step: every CTA factors the 16x16 diagonal block
-// (Doolittle: column i of L, then row i+1 of U — warp 0, lanes 0..15) into
-// shared memory, CTA 0 writes it back, and each warp then solves one
-// perimeter block pair p (row block right of the diagonal, column block below
-// it) with the pair's 16 values per lane in registers.  Redundant diagonal
-// factorisations replace a separate launch and a global round trip.
+// One launch per 16-column step: every warp solves one perimeter block pair p
+// (row block right of the diagonal, column block below it).  Latency first:
+//   1. the pair's two 16x16 blocks are requested from HBM at kernel entry
+//      (coalesced float4 loads into registers), and so is the diagonal block;
+//   2. while they are in flight every warp factors the diagonal block in
+//      registers (lane r holds row r; right-looking, U row k broadcast by
+//      __shfl_sync) — per element the same fmaf(-L, U, x) sequence in
+//      ascending k and the same division as the restatement's left-looking
+//      Doolittle (oracle_lud), so the bits agree — and keeps a private
+//      shared copy of it (no block barrier anywhere);
+//   3. the blocks are staged in shared memory (the column block transposed),
+//      so lane t of either role reads its 16 values at [i][t];
+//   4. the divergent solve: lanes 0-15 U12 = L11^-1 A12 (one column each),
+//      lanes 16-31 L21 = A21 U11^-1 (one row each) — the thread-ID split
+//      `lane < 16` of the paper's perimeter kernel (divergent on a 32-wide
+//      warp only at BLOCK = 16);
+//   5. results go back through shared memory as coalesced float4 stores.
+// The factored diagonal block goes to `dst` (CTA 0, row stride `dstride`):
+// a scratch block while CTAs of this launch may still be reading the
+// unfactored block from `a` (the next launch, lud_update_kernel, moves it
+// into place), or straight into `a` for the last block (one CTA).
 constexpr int kPairs = 4;
 
 template <bool M>
-__global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs) {
-  __shared__ float dia[BS][LD];
-  __shared__ float diaT[BS][LD];   // diaT[i][j] = dia[j][i]
+__global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs,
+                                                               float *__restrict__ dst, int dstride) {
+  __shared__ float dia[kPairs][BS][LD];
+  __shared__ float diaT[kPairs][BS][LD];      // diaT[i][j] = dia[j][i]
+  __shared__ float blk[kPairs][2][BS][LD];    // [0] row block R[i][c]; [1] column block transposed C[i][r]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < BS * BS; e += blockDim.x)
-    dia[e / BS][e % BS] = a[(size_t(o) + e / BS) * n + o + e % BS];
-  __syncthreads();
-  if (warp == 0) {
-    const int tx = lane;
-    for (int i = 0; i < BS - 1; ++i) {
-      if (tx > i && tx < BS) {
-        float x = dia[tx][i];
-        for (int j = 0; j < i; ++j) x = fmaf(-dia[tx][j], dia[j][i], x);
-        dia[tx][i] = x / dia[i][i];
-      }
-      __syncwarp();
-      if (tx > i && tx < BS) {
-        float x = dia[i + 1][tx];
-        for (int j = 0; j < i + 1; ++j) x = fmaf(-dia[i + 1][j], dia[j][tx], x);
-        dia[i + 1][tx] = x;
-      }
-      __syncwarp();
+  const int p = blockIdx.x * kPairs + warp;
+  const bool have = p < npairs;                             // warp-uniform
+  const size_t cb = size_t(o) + size_t(BS) * (p + 1);       // column of the row block = row of the column block
+  // 1. requests in flight: the pair (2 float4 per lane per block) and the diagonal row of lane r
+  float4 rv[2], cv[2];
+  if (have) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h, i = q >> 2, c4 = q & 3;
+      rv[h] = *reinterpret_cast<const float4 *>(a + (size_t(o) + i) * n + cb + 4 * c4);
+      cv[h] = *reinterpret_cast<const float4 *>(a + (cb + i) * n + o + 4 * c4);
     }
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < BS * BS; e += blockDim.x) {
-    diaT[e % BS][e / BS] = dia[e / BS][e % BS];
-    if (blockIdx.x == 0 && e >= BS) a[(size_t(o) + e / BS) * n + o + e % BS] = dia[e / BS][e % BS];
+  const int r = lane & (BS - 1);
+  float v[BS];
+  {
+    const float4 *src = reinterpret_cast<const float4 *>(a + (size_t(o) + r) * n + o);
+#pragma unroll
+    for (int q = 0; q < BS / 4; ++q) {
+      const float4 t = src[q];
+      v[4 * q] = t.x;
+      v[4 * q + 1] = t.y;
+      v[4 * q + 2] = t.z;
+      v[4 * q + 3] = t.w;
+    }
   }
-  __syncthreads();
-  const int p = blockIdx.x * kPairs + warp;
-  if (p >= npairs) return;                                 // warp-uniform
-  const size_t cb = size_t(o) + size_t(BS) * (p + 1);      // column of the row block
-  const size_t rb = cb;                                    // row of the column block
+  // 2. diagonal factorisation in registers
+#pragma unroll
+  for (int k = 0; k < BS - 1; ++k) {
+    const float ukk = __shfl_sync(0xffffffffu, v[k], k);
+    if (r > k) v[k] = v[k] / ukk;                           // L[r][k]
+#pragma unroll
+    for (int c = k + 1; c < BS; ++c) {
+      const float ukc = __shfl_sync(0xffffffffu, v[c], k);  // U[k][c]
+      if (r > k) v[c] = fmaf(-v[k], ukc, v[c]);
+    }
+  }
+  if (lane < BS) {
+#pragma unroll
+    for (int c = 0; c < BS; ++c) {
+      dia[warp][r][c] = v[c];
+      diaT[warp][c][r] = v[c];
+    }
+    if (blockIdx.x == 0 && warp == 0) {
+      float4 *d4 = reinterpret_cast<float4 *>(dst + size_t(r) * dstride);
+#pragma unroll
+      for (int q = 0; q < BS / 4; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
+  if (!have) return;                                        // warp-uniform
+  // 3. stage the pair
+  float(*R)[LD] = blk[warp][0];
+  float(*C)[LD] = blk[warp][1];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = lane + 32 * h, i = q >> 2, c = 4 * (q & 3);
+    R[i][c] = rv[h].x;
+    R[i][c + 1] = rv[h].y;
+    R[i][c + 2] = rv[h].z;
+    R[i][c + 3] = rv[h].w;
+    C[c][i] = cv[h].x;
+    C[c + 1][i] = cv[h].y;
+    C[c + 2][i] = cv[h].z;
+    C[c + 3][i] = cv[h].w;
+  }
+  __syncwarp();
+  const float(*Dg)[LD] = dia[warp];
+  // 4. the perimeter solve
   if constexpr (!M) {
-    if (lane < BS) {                                       // U12 = L11^-1 A12, column idx
+    if (lane < BS) {                                        // U12 = L11^-1 A12, column idx
       DARM_ARM("lud.row");
       const int idx = lane;
       float x[BS];
 #pragma unroll
-      for (int i = 0; i < BS; ++i) x[i] = a[(size_t(o) + i) * n + cb + idx];
+      for (int i = 0; i < BS; ++i) x[i] = R[i][idx];
 #pragma unroll
       for (int i = 1; i < BS; ++i)
 #pragma unroll
-        for (int j = 0; j < i; ++j) x[i] = fmaf(-dia[i][j], x[j], x[i]);
+        for (int j = 0; j < i; ++j) x[i] = fmaf(-Dg[i][j], x[j], x[i]);
 #pragma unroll
-      for (int i = 1; i < BS; ++i) a[(size_t(o) + i) * n + cb + idx] = x[i];
+      for (int i = 1; i < BS; ++i) R[i][idx] = x[i];
       DARM_ARM("lud.row.end");
-    } else {                                               // L21 = A21 U11^-1, row idx
+    } else {                                                // L21 = A21 U11^-1, row idx
       DARM_ARM("lud.col");
       const int idx = lane - BS;
       float y[BS];
-      const float4 *src = reinterpret_cast<const float4 *>(a + (rb + idx) * n + o);
 #pragma unroll
-      for (int q = 0; q < BS / 4; ++q) {
-        const float4 v = src[q];
-        y[4 * q] = v.x;
-        y[4 * q + 1] = v.y;
-        y[4 * q + 2] = v.z;
-        y[4 * q + 3] = v.w;
-      }
+      for (int i = 0; i < BS; ++i) y[i] = C[i][idx];
 #pragma unroll
       for (int i = 0; i < BS; ++i) {
 #pragma unroll
-        for (int j = 0; j < i; ++j) y[i] = fmaf(-y[j], dia[j][i], y[i]);
-        y[i] = y[i] / dia[i][i];
+        for (int j = 0; j < i; ++j) y[i] = fmaf(-y[j], Dg[j][i], y[i]);
+        y[i] = y[i] / Dg[i][i];
       }
-      float4 *dst = reinterpret_cast<float4 *>(a + (rb + idx) * n + o);
 #pragma unroll
-      for (int q = 0; q < BS / 4; ++q) dst[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+      for (int i = 0; i < BS; ++i) C[i][idx] = y[i];
       DARM_ARM("lud.col.end");
     }
   } else {
-    // Melded (by hand, as the paper did for LUD): one load / solve / store
-    // sequence.  The role picks the global addresses (row role: column idx of
-    // the row block, stride n; column role: row idx of the column block,
-    // stride 1) and the diagonal operand (dia or its transpose, so both read
-    // D[i][j]); fmaf(a,b,c) == fmaf(b,a,c), so -x[j] * D[i][j] is the same
+    // Melded (by hand, as the paper did for LUD): one
+    // load / solve / store sequence.  The role picks the staged block (both
+    // read [i][idx]) and the diagonal operand (dia or its transpose, so both
+    // read D[i][j]); fmaf(a,b,c) == fmaf(b,a,c), so -x[j] * D[i][j] is the same
     // operation as either arm's.  The column role's division is the only
     // one-sided run.
     const bool col = lane >= BS;
     const int idx = lane & (BS - 1);
-    const float(*D)[LD] = col ? diaT : dia;
-    const size_t g0 = col ? (rb + idx) * n + o : size_t(o) * n + cb + idx;
-    const size_t gs = col ? 1 : size_t(n);
+    float(*S)[LD] = col ? C : R;
+    const float(*D)[LD] = col ? diaT[warp] : dia[warp];
     float x[BS];
 #pragma unroll
-    for (int i = 0; i < BS; ++i) x[i] = a[g0 + i * gs];
+    for (int i = 0; i < BS; ++i) x[i] = S[i][idx];
 #pragma unroll
     for (int i = 0; i < BS; ++i) {
 #pragma unroll
@@ -139,8 +184,15 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
       if (col) x[i] = x[i] / D[i][i];
     }
 #pragma unroll
-    for (int i = 0; i < BS; ++i)
-      if (i > 0 || col) a[g0 + i * gs] = x[i];
+    for (int i = 0; i < BS; ++i) S[i][idx] = x[i];
+  }
+  __syncwarp();
+  // 5. coalesced write-back of both blocks
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = lane + 32 * h, i = q >> 2, c = 4 * (q & 3);
+    if (i > 0) *reinterpret_cast<float4 *>(a + (size_t(o) + i) * n + cb + c) = make_float4(R[i][c], R[i][c + 1], R[i][c + 2], R[i][c + 3]);
+    *reinterpret_cast<float4 *>(a + (cb + i) * n + o + c) = make_float4(C[c][i], C[c + 1][i], C[c + 2][i], C[c + 3][i]);
   }
 }
 
@@ -153,8 +205,11 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
 // 16-column step after another, so deferring the far trailing block's T
 // updates into one pass over it (look-ahead) leaves every bit unchanged while
 // the trailing matrix crosses HBM once per 64 columns instead of once per 16.
-// 64x64 tile per CTA; thread (tx, ty) owns rows ty + 16r (r < 4) and the 4
-// consecutive columns 4tx..4tx+3; the element stays in registers across t.
+// 64x64 tile per CTA, L (transposed) and U panels staged in shared memory;
+// thread (tx, ty) owns the 4x4 micro-tile rows 4ty.., columns 4tx.., so each
+// k costs two 16-byte shared loads for 16 FMAs; the element stays in registers
+// across t.  CTA (0,0,0) also moves the previous panel launch's factored
+// diagonal block from `dsrc` into place (nothing this launch touches reads it).
 constexpr int kLook = 4;   // steps per look-ahead super-step
 
 struct Rect {
@@ -162,67 +217,88 @@ struct Rect {
 };
 
 __global__ void __launch_bounds__(256) lud_update_kernel(float *__restrict__ a, int n, int o, int T, Rect R0,
-                                                         Rect R1) {
-  __shared__ float colp[64][kLook * BS + 1];                   // L rows of the tile, (t,k)
-  __shared__ __align__(16) float rowp[kLook * BS][64 + 4];     // U (t,k), columns of the tile
+                                                         Rect R1, const float *__restrict__ dsrc, int dofs) {
+  __shared__ __align__(16) float lt[kLook * BS][64 + 4];      // lt[(t,k)][r] = L_t[r][k]
+  __shared__ __align__(16) float up[kLook * BS][64 + 4];      // up[(t,k)][c] = U_t[k][c]
+  if (dsrc && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    const int e = threadIdx.x;                                  // 256 = 16 x 16
+    a[size_t(dofs + e / BS) * n + dofs + e % BS] = dsrc[e];
+  }
   const Rect R = blockIdx.z ? R1 : R0;
   const int r0 = R.r_lo + 64 * int(blockIdx.y), c0 = R.c_lo + 64 * int(blockIdx.x);
   if (r0 >= R.r_hi || c0 >= R.c_hi) return;                    // CTA-uniform
   const int nr = min(64, R.r_hi - r0), nc = min(64, R.c_hi - c0);
-  const int K = T * BS;
-  for (int e = threadIdx.x; e < 64 * K; e += 256) {
-    const int r = e / K, k = e % K;
-    colp[r][k] = r < nr ? a[size_t(r0 + r) * n + o + k] : 0.f;
-    const int kk = e >> 6, c = e & 63;
-    rowp[kk][c] = c < nc ? a[size_t(o + kk) * n + c0 + c] : 0.f;
+  const int K = T * BS, K4 = K / 4;
+  // L: float4 along k from row r (lanes walk rows: conflict-free transposed stores)
+  for (int e = threadIdx.x; e < 64 * K4; e += 256) {
+    const int rr = e & 63, k4 = e >> 6;
+    float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rr < nr) l = *reinterpret_cast<const float4 *>(a + size_t(r0 + rr) * n + o + 4 * k4);
+    lt[4 * k4][rr] = l.x;
+    lt[4 * k4 + 1][rr] = l.y;
+    lt[4 * k4 + 2][rr] = l.z;
+    lt[4 * k4 + 3][rr] = l.w;
+  }
+  // U: float4 along c
+  for (int e = threadIdx.x; e < K * 16; e += 256) {
+    const int kk = e >> 4, c4 = e & 15;
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * c4 < nc) u = *reinterpret_cast<const float4 *>(a + size_t(o + kk) * n + c0 + 4 * c4);
+    *reinterpret_cast<float4 *>(&up[kk][4 * c4]) = u;
+  }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int c = 4 * tx, rb = 4 * ty;
+  const bool live = c < nc && rb < nr;
+  float4 v[4];
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = *reinterpret_cast<const float4 *>(a + size_t(r0 + rb + i) * n + c0 + c);
   }
   __syncthreads();
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int c = 4 * tx;
-  if (c >= nc) return;
-  float4 v[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-    if (ty + 16 * r < nr) v[r] = *reinterpret_cast<const float4 *>(a + size_t(r0 + ty + 16 * r) * n + c0 + c);
+  if (!live) return;
   for (int t = 0; t < T; ++t) {
     float acc[4][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[r][q] = 0.f;
+      for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
 #pragma unroll
     for (int k = 0; k < BS; ++k) {
-      const float4 u = *reinterpret_cast<const float4 *>(&rowp[t * BS + k][c]);
+      const float4 u = *reinterpret_cast<const float4 *>(&up[t * BS + k][c]);
+      const float4 l = *reinterpret_cast<const float4 *>(&lt[t * BS + k][rb]);
+      const float lv[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float l = colp[ty + 16 * r][t * BS + k];
-        acc[r][0] = fmaf(l, u.x, acc[r][0]);
-        acc[r][1] = fmaf(l, u.y, acc[r][1]);
-        acc[r][2] = fmaf(l, u.z, acc[r][2]);
-        acc[r][3] = fmaf(l, u.w, acc[r][3]);
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] = fmaf(lv[i], u.x, acc[i][0]);
+        acc[i][1] = fmaf(lv[i], u.y, acc[i][1]);
+        acc[i][2] = fmaf(lv[i], u.z, acc[i][2]);
+        acc[i][3] = fmaf(lv[i], u.w, acc[i][3]);
       }
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      v[r].x -= acc[r][0];
-      v[r].y -= acc[r][1];
-      v[r].z -= acc[r][2];
-      v[r].w -= acc[r][3];
+    for (int i = 0; i < 4; ++i) {
+      v[i].x -= acc[i][0];
+      v[i].y -= acc[i][1];
+      v[i].z -= acc[i][2];
+      v[i].w -= acc[i][3];
     }
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
-    if (ty + 16 * r < nr) *reinterpret_cast<float4 *>(a + size_t(r0 + ty + 16 * r) * n + c0 + c) = v[r];
+  for (int i = 0; i < 4; ++i) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
 }
 
 namespace {
-cudaError_t launch_update(float *a, int n, int o, int T, Rect R0, Rect R1, cudaStream_t s) {
+cudaError_t launch_update(float *a, int n, int o, int T, Rect R0, Rect R1, const float *dsrc, int dofs,
+                          cudaStream_t s) {
   auto tiles = [](int lo, int hi) { return hi > lo ? (hi - lo + 63) / 64 : 0; };
-  const int gx = max(tiles(R0.c_lo, R0.c_hi), tiles(R1.c_lo, R1.c_hi));
-  const int gy = max(tiles(R0.r_lo, R0.r_hi), tiles(R1.r_lo, R1.r_hi));
+  int gx = max(tiles(R0.c_lo, R0.c_hi), tiles(R1.c_lo, R1.c_hi));
+  int gy = max(tiles(R0.r_lo, R0.r_hi), tiles(R1.r_lo, R1.r_hi));
   const int gz = (R1.r_hi > R1.r_lo && R1.c_hi > R1.c_lo) ? 2 : 1;
-  if (gx == 0 || gy == 0) return cudaSuccess;
-  lud_update_kernel<<<dim3(gx, gy, gz), 256, 0, s>>>(a, n, o, T, R0, R1);
+  if (gx == 0 || gy == 0) {
+    if (!dsrc) return cudaSuccess;
+    gx = gy = 1;                                   // still move the diagonal block
+  }
+  lud_update_kernel<<<dim3(gx, gy, gz), 256, 0, s>>>(a, n, o, T, R0, R1, dsrc, dofs);
   return cudaGetLastError();
 }
 }  // namespace
@@ -235,7 +311,7 @@ cudaError_t launch_update(float *a, int n, int o, int T, Rect R0, Rect R1, cudaS
 // all rows below, and the super-row rows [o_t+16, O+64) for all columns to
 // the right.  The far trailing block [O+64, n)^2 then takes the super-step's
 // kLook updates in one pass (lud_update_kernel with T = kLook).
-cudaError_t record_lud(int variant, float *a, int n, cudaStream_t s, int *launches) {
+cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches) {
   const int nb = n / BS;
   for (int O = 0; O < n; O += kLook * BS) {
     const int T = min(kLook, (n - O) / BS);
@@ -244,21 +320,24 @@ cudaError_t record_lud(int variant, float *a, int n, cudaStream_t s, int *launch
       const int o = O + t * BS;
       const int m = nb - o / BS - 1;   // blocks right of / below the diagonal
       const int grid = m > 0 ? (m + kPairs - 1) / kPairs : 1;
+      // the last diagonal block has no other reader: factor it in place
+      float *dst = m > 0 ? dscr : a + size_t(o) * n + o;
+      const int dstride = m > 0 ? BS : n;
       if (variant)
-        lud_panel_kernel<true><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m);
+        lud_panel_kernel<true><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m, dst, dstride);
       else
-        lud_panel_kernel<false><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m);
+        lud_panel_kernel<false><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m, dst, dstride);
       ++*launches;
       if (m == 0) break;
       const Rect panel_cols{o + BS, n, o + BS, E};   // rows below, panel columns
       const Rect super_row{o + BS, E, E, n};         // super-row rows, columns right
-      cudaError_t e = launch_update(a, n, o, 1, panel_cols, super_row, s);
+      cudaError_t e = launch_update(a, n, o, 1, panel_cols, super_row, dscr, o, s);
       if (e != cudaSuccess) return e;
       ++*launches;
     }
     if (E < n) {
       const Rect far{E, n, E, n};
-      cudaError_t e = launch_update(a, n, O, T, far, Rect{0, 0, 0, 0}, s);
+      cudaError_t e = launch_update(a, n, O, T, far, Rect{0, 0, 0, 0}, nullptr, 0, s);
       if (e != cudaSuccess) return e;
       ++*launches;
     }
