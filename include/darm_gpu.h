@@ -52,7 +52,7 @@ typedef struct darm_gpu_stats {
   uint64_t d2h_bytes;
   uint64_t algorithmic_bytes; /* minimal HBM bytes the kernels must move      */
   int32_t launches;      /* kernels launched by this call                      */
-  int32_t reserved;
+  int32_t reserved;      /* call-specific (bitonic: keys per thread used)      */
 } darm_gpu_stats;
 
 /* ---- runtime ------------------------------------------------------------ */
@@ -128,6 +128,18 @@ int darm_gpu_execute_warps(const char *kernel, int variant, int warp,
 int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket,
                           int mem, void *stream, darm_gpu_stats *stats,
                           char *err, size_t errlen);
+
+/* Same, choosing how many IR lanes (keys) one hardware thread carries:
+ *   1        one key per thread: an IR warp of `bucket` lanes is `bucket`
+ *            threads (the shape the reference interpreter runs);
+ *   4, 8, 16 register-blocked: a thread holds that many consecutive keys of a
+ *            bucket, strides below it are exchanged inside the thread
+ *            (needs bucket / keys_per_thread <= 32, 16-byte aligned keys);
+ *   0        the fastest supported (what darm_gpu_bitonic_sort uses).
+ * stats->reserved receives the keys per thread used. */
+int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket,
+                             int keys_per_thread, int mem, void *stream,
+                             darm_gpu_stats *stats, char *err, size_t errlen);
 
 /* ---- N-Queens (NQU; the reference has no code for it):
  *      paper_2107_05681_b200/ir/nqueens_step.ir run to completion per thread -

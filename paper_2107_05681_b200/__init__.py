@@ -49,6 +49,7 @@ ABI_SYMBOLS = (
     "darm_gpu_make_random_input",
     "darm_gpu_execute_warps",
     "darm_gpu_bitonic_sort",
+    "darm_gpu_bitonic_sort_ex",
     "darm_gpu_nqueens",
     "darm_gpu_nqueens_prefix_count",
     "darm_gpu_lud",
@@ -85,7 +86,9 @@ class Stats(ctypes.Structure):
     ]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        d["keys_per_thread"] = self.reserved  # call-specific; bitonic sort only
+        return d
 
 
 _lib = None
@@ -118,6 +121,9 @@ def lib() -> ctypes.CDLL:
         L.darm_gpu_bitonic_sort.argtypes = [
             ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
             ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_bitonic_sort_ex.argtypes = [
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.c_void_p, ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
         L.darm_gpu_nqueens.argtypes = [
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int64,
@@ -325,10 +331,13 @@ class PreparedCall:
 
 
 def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: bool = True,
-                 prepare_only: bool = False):
+                 prepare_only: bool = False, keys_per_thread: int = 0):
     """Sort every ``bucket``-key bucket of ``keys`` ascending, in place.
 
     ``keys``: numpy int32 (HOST mode) or torch int32 CUDA tensor (DEVICE mode).
+    ``keys_per_thread``: 1 = one key per thread (the IR warp shape), 4/8/16 =
+    register-blocked, 0 = fastest (``darm_gpu_bitonic_sort_ex``).  The stats
+    dict reports the choice as ``keys_per_thread``.
     """
     if isinstance(variant, str):
         variant = VARIANTS[variant]
@@ -341,8 +350,9 @@ def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: boo
     else:
         assert keys.dtype == np.int32 and keys.flags["C_CONTIGUOUS"]
         ptr, n, mem = keys.ctypes.data, keys.size, 0
-    call = PreparedCall(lib().darm_gpu_bitonic_sort, (int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), mem,
-                                                      ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
+    call = PreparedCall(lib().darm_gpu_bitonic_sort_ex,
+                        (int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), int(keys_per_thread), mem,
+                         ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
     return call if prepare_only else call()
 
 

@@ -23,6 +23,13 @@
 
 namespace darm_gpu {
 
+// Order flip x ^ m for m in {0, -1} written as x * (1 + 2m) + m: one IMAD on
+// the FMA pipe instead of a LOP3 on the ALU pipe, which the compare-exchanges
+// (VIMNMX) saturate.
+__device__ __forceinline__ int32_t flip_fma(int32_t x, int32_t m) {
+  return int32_t(uint32_t(x) * uint32_t(1 + 2 * m) + uint32_t(m));
+}
+
 template <int B>
 struct Network {
   static constexpr int kSteps = __builtin_ctz(B) * (__builtin_ctz(B) + 1) / 2;
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
         // keys' order once (bitwise not), so every lane's exchange is the up-form
         const int32_t m = (d < LB && bit[d]) ? -1 : 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] ^= m ^ neg;
+        for (int u = 0; u < U; ++u) v[u] = flip_fma(v[u], m ^ neg);
         neg = m;
       }
 #pragma unroll
@@ -95,17 +102,165 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
             v[u] = bitonic_exchange<false>(v[u], b0[u], !bit[kb], d >= LB ? true : !bit[d], false);
           } else {
             // need1 = (keep == up) ? cv > b0 : cv < b0 with up folded into the data:
-            // take the partner's key iff (b0 < cv) xor !keep   (equal keys: either)
-            const bool take = (b0[u] < v[u]) ^ bit[kb];
-            v[u] = take ? b0[u] : v[u];                       // ^e.m: the single melded store
+            // need1 = (keep == up) ? gt : lt with up folded into the data: the
+            // lower slot keeps the smaller key — one predicated min/max
+            v[u] = bit[kb] ? max(v[u], b0[u]) : min(v[u], b0[u]);   // ^e.m: the single melded store
           }
         }
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if constexpr (M) v[u] ^= neg;
+      if constexpr (M) v[u] = flip_fma(v[u], neg);
       if (tile + u * G < tiles && my[u] < n) keys[my[u]] = v[u];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Register-blocked form: each thread carries R consecutive keys of a bucket
+// (R lanes of the IR warp; B/R <= 32 threads per bucket, so a bucket never
+// leaves its warp).  Steps with stride k < R compare-exchange two registers of
+// the same thread (min + max); steps with k >= R exchange with the thread
+// lane ^ k/R (__shfl_xor_sync) and keep min or max, as the one-key form does.
+// The divergent `if (up)` of the step (bitonic.ir:16) exists where up depends
+// on the thread: stages dir >= R below the last one.  There the unmelded
+// form branches once per step (both arms of the R-key step under the branch)
+// and the melded form folds up into the data as in the one-key form (the !up
+// threads flip their keys' order once per stage, so every exchange is the
+// up-form).  Stages dir < R have a compile-time up per register pair: no
+// branch in either form.  Loads and stores are 16-byte vectors; each warp
+// sorts 32*R keys per iteration and walks the array with a grid stride, the
+// next tile's keys in flight (PF) while the network runs on the current one.
+// The network is bound by the ALU pipe (VIMNMX, half a warp-instruction per
+// cycle per SMSP), so the melded form's order flips are IMADs (flip_fma).
+template <int R>
+__device__ __forceinline__ void load_keys(int32_t (&v)[R], const int32_t *__restrict__ keys, uint32_t base, uint32_t n) {
+  if (base < n) {                                         // whole bucket in or out (n % B == 0)
+    const int4 *src = reinterpret_cast<const int4 *>(keys + base);
+#pragma unroll
+    for (int q = 0; q < R / 4; ++q) {
+      const int4 x = src[q];
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = INT_MAX;
+  }
+}
+
+template <bool M, int B, int R, bool PF>
+__global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
+  constexpr int LB = __builtin_ctz(B), LR = __builtin_ctz(R), P = B / R;
+  static_assert(R >= 4 && R <= B && P <= 32, "R keys per thread, at most 32 threads per bucket");
+  constexpr uint32_t kTile = 32u * R;
+  const int lane = int(threadIdx.x) & 31;
+  const int tib = lane & (P - 1);                       // thread index within the bucket
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t tiles = (n + kTile - 1) / kTile;
+  uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int32_t nxt[R];
+  if (PF && tile < tiles) load_keys<R>(nxt, keys, tile * kTile + uint32_t(lane) * R, n);
+  for (; tile < tiles; tile += warps) {
+    const uint32_t base = tile * kTile + uint32_t(lane) * R;
+    const bool live = base < n;
+    int32_t v[R];
+    if constexpr (PF) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) v[j] = nxt[j];
+      if (tile + warps < tiles) load_keys<R>(nxt, keys, base + warps * kTile, n);   // next tile in flight
+    } else {
+      load_keys<R>(v, keys, base, n);
+    }
+    int32_t neg = 0;                                      // melded: current order flip of this thread
+#pragma unroll
+    for (int d = 1; d <= LB; ++d) {
+      const bool thread_up = d >= LR && d < LB;           // up depends on the thread (runtime)
+      const bool upT = d >= LB ? true : !((tib >> (d > LR ? d - LR : 0)) & 1);
+      if constexpr (M) {
+        const int32_t m = (thread_up && !upT) ? -1 : 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) v[j] = flip_fma(v[j], m ^ neg);
+        neg = m;
+      }
+#pragma unroll
+      for (int kb = d - 1; kb >= 0; --kb) {
+        const int k = 1 << kb;
+        if (k < R) {
+          // in-register compare-exchange of the pairs (j, j | k)
+          if (!thread_up || M) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              if (j & k) continue;
+              const bool up = d < LR ? !((j >> d) & 1) : true;   // compile-time (or folded) direction
+              const int32_t lo = min(v[j], v[j | k]), hi = max(v[j], v[j | k]);
+              v[j] = up ? lo : hi;
+              v[j | k] = up ? hi : lo;
+            }
+          } else {
+            if (upT) {                                    // condbr %up ^c ^d
+              DARM_ARM("bitonic.reg.up");
+#pragma unroll
+              for (int j = 0; j < R; ++j) {
+                if (j & k) continue;
+                const int32_t lo = min(v[j], v[j | k]), hi = max(v[j], v[j | k]);
+                v[j] = lo;
+                v[j | k] = hi;
+              }
+              DARM_ARM("bitonic.reg.up.end");
+            } else {
+              DARM_ARM("bitonic.reg.down");
+#pragma unroll
+              for (int j = 0; j < R; ++j) {
+                if (j & k) continue;
+                const int32_t lo = min(v[j], v[j | k]), hi = max(v[j], v[j | k]);
+                v[j] = hi;
+                v[j | k] = lo;
+              }
+              DARM_ARM("bitonic.reg.down.end");
+            }
+          }
+        } else {
+          // partner thread lane ^ k/R holds the partner keys in the same registers
+          const int pk = k / R;
+          const bool keep = !(tib & pk);                  // icmp.lt %t %j
+          int32_t b0[R];
+#pragma unroll
+          for (int j = 0; j < R; ++j) b0[j] = __shfl_xor_sync(0xffffffffu, v[j], pk);   // load.shared buf %j
+          if constexpr (M) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              // need1 with up folded into the data: one predicated min/max
+              v[j] = keep ? min(v[j], b0[j]) : max(v[j], b0[j]);   // ^e.m: the single melded store
+            }
+          } else if (!thread_up) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) v[j] = keep ? min(v[j], b0[j]) : max(v[j], b0[j]);
+          } else {
+            if (upT) {                                    // condbr %up ^c ^d
+              DARM_ARM("bitonic.xr.up");
+#pragma unroll
+              for (int j = 0; j < R; ++j) v[j] = keep ? min(v[j], b0[j]) : max(v[j], b0[j]);
+              DARM_ARM("bitonic.xr.up.end");
+            } else {
+              DARM_ARM("bitonic.xr.down");
+#pragma unroll
+              for (int j = 0; j < R; ++j) v[j] = keep ? max(v[j], b0[j]) : min(v[j], b0[j]);
+              DARM_ARM("bitonic.xr.down.end");
+            }
+          }
+        }
+      }
+    }
+    if (live) {
+      int4 *dst = reinterpret_cast<int4 *>(keys + base);
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q)
+        dst[q] = make_int4(flip_fma(v[4 * q], neg), flip_fma(v[4 * q + 1], neg), flip_fma(v[4 * q + 2], neg),
+                           flip_fma(v[4 * q + 3], neg));
     }
   }
 }
@@ -113,16 +268,12 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
 namespace {
 
 int g_sms = 0;
+int sm_count();
 
 template <bool M, int B>
 cudaError_t launch_b(int32_t *keys, int64_t n, cudaStream_t s) {
   constexpr int CTA = B > 256 ? B : 256;
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
-  }
+  sm_count();
   constexpr int U = B <= 256 ? 2 : 1;
   const int64_t tiles = (n + CTA - 1) / CTA;
   const int per_sm = 2048 / CTA;
@@ -133,19 +284,75 @@ cudaError_t launch_b(int32_t *keys, int64_t n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+int sm_count() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+// Register-blocked launch: warps walk 32*R-key tiles with a grid stride.  The
+// grid is sized so every warp gets the same number of tiles (up to one): with
+// I = ceil(tiles / max resident warps) iterations, only ceil(tiles / I) warps
+// are launched, spread evenly over the SMs.
+template <bool M, int B, int R, bool PF>
+cudaError_t launch_reg_pf(int32_t *keys, int64_t n, cudaStream_t s) {
+  constexpr int CTA = 256, WPC = CTA / 32;
+  static int per_sm = 0;                          // resident CTAs per SM (registers bound it)
+  if (!per_sm) {
+    cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bitonic_sort_reg_kernel<M, B, R, PF>, CTA, 0);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+  }
+  const int sms = sm_count();
+  const int64_t tiles = (n + 32 * R - 1) / (32 * R);
+  const int64_t max_warps = int64_t(sms) * per_sm * WPC;
+  const int64_t iters = (tiles + max_warps - 1) / max_warps;
+  const int64_t warps_per_sm = (tiles + int64_t(sms) * iters - 1) / (int64_t(sms) * iters);
+  int64_t grid = int64_t(sms) * ((warps_per_sm + WPC - 1) / WPC);
+  const int64_t need = (tiles + WPC - 1) / WPC;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  bitonic_sort_reg_kernel<M, B, R, PF><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
+  return cudaGetLastError();
+}
+
+template <bool M, int B, int R>
+cudaError_t launch_reg(int32_t *keys, int64_t n, cudaStream_t s) {
+  return launch_reg_pf<M, B, R, true>(keys, n, s);
+}
+
+template <bool M, int B>
+cudaError_t launch_r(int32_t *keys, int64_t n, int r, cudaStream_t s) {
+  if constexpr (B >= 4 && B / 4 <= 32) {
+    if (r == 4) return launch_reg<M, B, 4>(keys, n, s);
+  }
+  if constexpr (B >= 8 && B / 8 <= 32) {
+    if (r == 8) return launch_reg<M, B, 8>(keys, n, s);
+  }
+  if constexpr (B >= 16 && B / 16 <= 32) {
+    if (r == 16) return launch_reg<M, B, 16>(keys, n, s);
+  }
+  if (r == 1) return launch_b<M, B>(keys, n, s);
+  return cudaErrorInvalidValue;
+}
+
 template <bool M>
-cudaError_t launch_m(int32_t *keys, int64_t n, int bucket, cudaStream_t s) {
+cudaError_t launch_m(int32_t *keys, int64_t n, int bucket, int r, cudaStream_t s) {
   switch (bucket) {
-    case 2: return launch_b<M, 2>(keys, n, s);
-    case 4: return launch_b<M, 4>(keys, n, s);
-    case 8: return launch_b<M, 8>(keys, n, s);
-    case 16: return launch_b<M, 16>(keys, n, s);
-    case 32: return launch_b<M, 32>(keys, n, s);
-    case 64: return launch_b<M, 64>(keys, n, s);
-    case 128: return launch_b<M, 128>(keys, n, s);
-    case 256: return launch_b<M, 256>(keys, n, s);
-    case 512: return launch_b<M, 512>(keys, n, s);
-    case 1024: return launch_b<M, 1024>(keys, n, s);
+    case 2: return launch_r<M, 2>(keys, n, r, s);
+    case 4: return launch_r<M, 4>(keys, n, r, s);
+    case 8: return launch_r<M, 8>(keys, n, r, s);
+    case 16: return launch_r<M, 16>(keys, n, r, s);
+    case 32: return launch_r<M, 32>(keys, n, r, s);
+    case 64: return launch_r<M, 64>(keys, n, r, s);
+    case 128: return launch_r<M, 128>(keys, n, r, s);
+    case 256: return launch_r<M, 256>(keys, n, r, s);
+    case 512: return launch_r<M, 512>(keys, n, r, s);
+    case 1024: return launch_r<M, 1024>(keys, n, r, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -156,11 +363,29 @@ bool bitonic_sort_supported(int bucket) {
   return bucket >= 2 && bucket <= 1024 && (bucket & (bucket - 1)) == 0;
 }
 
-cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, cudaStream_t s,
-                                int *launches) {
+// keys_per_thread: 1 = one key per thread (the IR warp shape), 4 / 8 / 16 =
+// register-blocked (needs 16-byte aligned keys and bucket / r <= 32), 0 = the
+// fastest supported: 16 for buckets 32..512, the bucket itself for 4..16.
+int bitonic_keys_per_thread(int bucket, int keys_per_thread, const void *keys) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+  if (keys_per_thread == 0) {
+    if (!aligned) return 1;
+    if (bucket >= 32 && bucket <= 512) return 16;
+    if (bucket >= 4 && bucket <= 16) return bucket;
+    return 1;
+  }
+  if (keys_per_thread == 1) return 1;
+  if (keys_per_thread != 4 && keys_per_thread != 8 && keys_per_thread != 16) return -1;
+  if (!aligned || keys_per_thread > bucket || bucket / keys_per_thread > 32) return -1;
+  return keys_per_thread;
+}
+
+cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread,
+                                cudaStream_t s, int *launches) {
   if (n == 0) return cudaSuccess;
   if (launches) *launches += 1;
-  return variant ? launch_m<true>(keys, n, bucket, s) : launch_m<false>(keys, n, bucket, s);
+  return variant ? launch_m<true>(keys, n, bucket, keys_per_thread, s)
+                 : launch_m<false>(keys, n, bucket, keys_per_thread, s);
 }
 
 }  // namespace darm_gpu

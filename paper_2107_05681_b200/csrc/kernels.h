@@ -34,8 +34,10 @@ extern const int kCorpusCount;
 
 // bitonic_sort.cu
 bool bitonic_sort_supported(int bucket);
-cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, cudaStream_t s,
-                                int *launches);
+// resolves keys_per_thread (0 = auto) for this bucket / pointer; -1 = unsupported
+int bitonic_keys_per_thread(int bucket, int keys_per_thread, const void *keys);
+cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread,
+                                cudaStream_t s, int *launches);
 
 // nqueens.cu
 cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, int n, int base,

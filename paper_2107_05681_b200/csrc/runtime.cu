@@ -411,6 +411,11 @@ int darm_gpu_execute_warps(const char *kernel, int variant, int warp, int64_t n_
 
 int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int mem, void *stream,
                           darm_gpu_stats *stats, char *err, size_t errlen) {
+  return darm_gpu_bitonic_sort_ex(variant, keys, n, bucket, 0, mem, stream, stats, err, errlen);
+}
+
+int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
+                             void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
     if (!bitonic_sort_supported(bucket)) user_error("bucket must be a power of two in [2, 1024]");
@@ -418,6 +423,11 @@ int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int
     if (n >= (int64_t(1) << 31)) user_error("too many keys (limit 2^31 - 1)");
     if (n && !keys) user_error("keys is NULL");
     if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    // HOST mode stages through a cudaMalloc'd (aligned) buffer
+    const int kpt = bitonic_keys_per_thread(bucket, keys_per_thread, mem == DARM_MEM_DEVICE ? keys : nullptr);
+    if (kpt < 0)
+      user_error("keys_per_thread must be 0, 1, 4, 8 or 16, with bucket / keys_per_thread <= 32 and "
+                 "16-byte aligned keys");
     if (stats) std::memset(stats, 0, sizeof(*stats));
     DeviceState &st = device_state(nullptr);
     std::lock_guard<std::mutex> lk(st.mu);
@@ -432,7 +442,7 @@ int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int
     }
     tl.mark(1);
     int launches = 0;
-    DARM_CUDA(launch_bitonic_sort(variant, dk, n, bucket, s, &launches));
+    DARM_CUDA(launch_bitonic_sort(variant, dk, n, bucket, kpt, s, &launches));
     tl.mark(2);
     if (mem == DARM_MEM_HOST && bytes) DARM_CUDA(cudaMemcpyAsync(keys, dk, bytes, cudaMemcpyDeviceToHost, s));
     tl.mark(3);
@@ -443,6 +453,7 @@ int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int
       stats->h2d_bytes = mem == DARM_MEM_HOST ? bytes : 0;
       stats->d2h_bytes = mem == DARM_MEM_HOST ? bytes : 0;
       stats->algorithmic_bytes = 2 * bytes;
+      stats->reserved = kpt;
     }
   });
 }

@@ -135,13 +135,57 @@ def test_device_mode_matches_host_mode(kernel):
         assert (rd.faults.cpu().numpy() == rh.faults).all()
 
 
-def test_bitonic_sort_golden():
+@pytest.mark.parametrize("kpt", [0, 1, 4, 8, 16])
+def test_bitonic_sort_golden(kpt):
     gold = load_golden("bitonic_sort.json")
     for case in gold["cases"]:
+        B = case["bucket"]
+        if kpt > 1 and (kpt > B or B // kpt > 32):
+            continue
         for variant in (0, 1):
             keys = np.array(case["keys"], dtype=np.int32)
-            darm.bitonic_sort(keys, case["bucket"], variant)
-            assert keys.tolist() == case["sorted"], (case["bucket"], variant)
+            st = darm.bitonic_sort(keys, B, variant, keys_per_thread=kpt)
+            assert keys.tolist() == case["sorted"], (B, variant, kpt)
+            if kpt:
+                assert st["keys_per_thread"] == kpt
+
+
+BUCKET_KPT = [(B, r) for B in (4, 8, 16, 32, 64, 128, 256, 512) for r in (4, 8, 16) if r <= B and B // r <= 32]
+
+
+@pytest.mark.parametrize("bucket,kpt", BUCKET_KPT)
+def test_bitonic_sort_register_blocked(bucket, kpt):
+    """Register-blocked forms (kpt keys per thread) against np.sort: full-range
+    and duplicate-heavy keys, a ragged tail (n not a multiple of the 32*kpt
+    warp tile) and a size that leaves most warps idle."""
+    import torch
+
+    rng = np.random.default_rng(bucket * 100 + kpt)
+    for n in (1 << 18, bucket * 37, bucket):
+        for dup in (False, True):
+            lo, hi = (-128, 129) if dup else (-(2 ** 31), 2 ** 31)
+            keys = rng.integers(lo, hi, size=n, dtype=np.int64).astype(np.int32)
+            want = np.sort(keys.reshape(-1, bucket), axis=1).reshape(-1)
+            for variant in (0, 1):
+                k = torch.from_numpy(keys.copy()).cuda()
+                st = darm.bitonic_sort(k, bucket, variant, keys_per_thread=kpt)
+                assert st["keys_per_thread"] == kpt
+                assert (k.cpu().numpy() == want).all(), (bucket, kpt, n, dup, variant)
+
+
+def test_bitonic_sort_keys_per_thread_contract():
+    import torch
+
+    buf = torch.zeros(64 * 4 + 1, dtype=torch.int32, device="cuda")
+    mis = buf[1:]                      # 4-byte aligned only
+    with pytest.raises(darm.DarmError):
+        darm.bitonic_sort(mis, 64, 1, keys_per_thread=16)
+    assert darm.bitonic_sort(mis, 64, 1)["keys_per_thread"] == 1   # auto falls back
+    with pytest.raises(darm.DarmError):
+        darm.bitonic_sort(buf[:64 * 4], 64, 1, keys_per_thread=2)
+    with pytest.raises(darm.DarmError):
+        darm.bitonic_sort(buf[:64 * 4], 1024, 1, keys_per_thread=16)
+    assert darm.bitonic_sort(buf[:64 * 4], 64, 1)["keys_per_thread"] == 16
 
 
 @pytest.mark.parametrize("bucket", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024])

@@ -1,0 +1,52 @@
+"""Time the bitonic bucket sort (both forms, every keys-per-thread shape) on cuda:0.
+
+    python tools/time_bitonic.py [bucket ...]      (run under gpurun)
+L2 is flushed (256 MiB write) before every timed launch; min and mean of 10.
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2107_05681_b200 as darm  # noqa: E402
+
+
+def main(*buckets):
+    darm.init()
+    s = torch.cuda.current_stream()
+    n = 1 << 24
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+    work = torch.empty_like(pristine)
+    flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
+    for B in buckets or (64,):
+        want = torch.sort(pristine.view(-1, B), dim=1).values.view(-1)
+        for kpt in (1, 4, 8, 16):
+            if kpt > 1 and (kpt > B or B // kpt > 32):
+                continue
+            res = {}
+            for v in (darm.UNMELDED, darm.MELDED):
+                call = darm.bitonic_sort(work, B, v, stream=s.cuda_stream, want_stats=False, prepare_only=True,
+                                         keys_per_thread=kpt)
+                ts = []
+                for i in range(13):
+                    work.copy_(pristine)
+                    flush.fill_(i)
+                    torch.cuda._sleep(100_000)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(s)
+                    call()
+                    e1.record(s)
+                    torch.cuda.synchronize()
+                    if i >= 3:
+                        ts.append(e0.elapsed_time(e1) * 1e3)
+                assert torch.equal(work, want), (B, kpt, v)
+                res[v] = (min(ts), sum(ts) / len(ts))
+            gbs = 8 * n / (res[1][1] * 1e-6) / 1e9
+            print(f"B={B} kpt={kpt:2d} unmelded {res[0][1]:7.1f} us (min {res[0][0]:6.1f}) melded {res[1][1]:7.1f} us "
+                  f"(min {res[1][0]:6.1f}) speedup {res[0][1] / res[1][1]:.3f} melded {gbs:6.0f} GB/s", flush=True)
+
+
+if __name__ == "__main__":
+    main(*(int(x) for x in sys.argv[1:]))
