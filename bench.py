@@ -195,11 +195,15 @@ def workload_config(args, variant):
     return {"workload": f"bitonic sort, {args.keys} int32 keys per GPU in {args.bucket}-key buckets "
                         f"(corpus bitonic.ir compare-exchange step chained over every stage)",
             "keys_per_gpu": args.keys, "bucket": args.bucket, "variant": variant,
+            "keys_per_thread": args.keys_per_thread or "auto (16)",
             "global_batch": args.keys * args.gpus, "parallelism": f"dp{args.gpus} (independent buckets)",
             "l2": "flushed (256 MiB write) before every timed step; input restored from a pristine copy"}
 
 
 def cpu_baseline(args):
+    """The reference itself (oracle/_ref: executeWarp chained over bitonic.ir
+    steps) on all host cores, on a bounded sample of the workload: batches of
+    4096 buckets until about args.cpu_seconds of CPU work."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import Reference, reference_available
 
@@ -209,15 +213,20 @@ def cpu_baseline(args):
     B = args.bucket
     nb = args.ref_sample_buckets
     rng = np.random.default_rng(1)
-    keys = rng.integers(-(2 ** 31), 2 ** 31, size=nb * B, dtype=np.int64).astype(np.int32)
     mod = Reference().load("bitonic", 0)
-    mod.bitonic_sort(keys[: 8 * B].copy(), B, threads=threads)
-    t0 = time.perf_counter()
-    mod.bitonic_sort(keys, B, threads=threads)
-    sec = time.perf_counter() - t0
-    assert (keys.reshape(-1, B)[:, 1:] >= keys.reshape(-1, B)[:, :-1]).all()
-    return {"value": nb * B / sec, "unit": "keys/s", "cores": threads, "kind": "reference",
-            "sample": f"{nb} buckets x {B} keys through oracle/_ref executeWarp chains ({sec:.1f} s)"}
+    mod.bitonic_sort(rng.integers(-(2 ** 31), 2 ** 31, size=8 * B, dtype=np.int64).astype(np.int32), B,
+                     threads=threads)
+    done, sec = 0, 0.0
+    while sec < args.cpu_seconds:
+        keys = rng.integers(-(2 ** 31), 2 ** 31, size=nb * B, dtype=np.int64).astype(np.int32)
+        t0 = time.perf_counter()
+        mod.bitonic_sort(keys, B, threads=threads)
+        sec += time.perf_counter() - t0
+        done += nb
+        assert (keys.reshape(-1, B)[:, 1:] >= keys.reshape(-1, B)[:, :-1]).all()
+    return {"value": done * B / sec, "unit": "keys/s", "cores": threads, "kind": "reference",
+            "sample": f"{done} buckets x {B} keys ({done * B} keys) through oracle/_ref executeWarp chains, "
+                      f"{sec:.1f} s on {threads} threads"}
 
 
 # ------------------------------------------------------------------ per-kernel table
@@ -251,13 +260,14 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
     for vname, v in (("unmelded", 0), ("melded", 1)):
         ts = []
         for i in range(warmup + max(3, steps // 4)):
-            sols, _, st = darm.nqueens(16, 6, v, stream=stream.cuda_stream)
+            sols, _, st = darm.nqueens(16, 7, v, stream=stream.cuda_stream)
             assert sols == 14772512
             if i >= warmup:
                 ts.append(st["kernel_ms"])
         row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_nodes_per_s"] = NQ_NODES_16 / (row["melded_us"] * 1e-6)
+    row["prefix_rows"] = 7
     out["nqueens16"] = row
     # LUD 8192^2 fp32 (config 4): the whole decomposition (3 x 512 launches in one graph)
     n = 8192
@@ -319,7 +329,8 @@ def our_arm(args):
     results = {}
     for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
         prepare = lambda: work.copy_(pristine)  # noqa: E731
-        step = darm.bitonic_sort(work, B, variant, stream=stream.cuda_stream, want_stats=False, prepare_only=True)
+        step = darm.bitonic_sort(work, B, variant, stream=stream.cuda_stream, want_stats=False, prepare_only=True,
+                                 keys_per_thread=args.keys_per_thread)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -340,7 +351,7 @@ def our_arm(args):
     e2e_ms = []
     for i in range(args.warmup + args.steps):
         host[:] = host_pristine
-        st = darm.bitonic_sort(host, B, darm.MELDED, stream=stream.cuda_stream)
+        st = darm.bitonic_sort(host, B, darm.MELDED, stream=stream.cuda_stream, keys_per_thread=args.keys_per_thread)
         if i >= args.warmup:
             e2e_ms.append(st["total_ms"])
     if not (host.reshape(-1, B) == want.view(-1, B).cpu().numpy()).all():
@@ -356,8 +367,10 @@ def our_arm(args):
     peak, peak_src = measured_peaks()
     alg_bytes = 8 * n
     achieved = alg_bytes / (mel["kernel_ms_mean"] / 1e3) / 1e9
-    prof_m, prof_src = ncu_kernel_summary("bitonic", "bitonic_sort_kernel<1, 64")
-    prof_u, _ = ncu_kernel_summary("bitonic", "bitonic_sort_kernel<0, 64")
+    kpt = args.keys_per_thread or 16
+    kname = "bitonic_sort_reg_kernel<{}, %d, %d" % (B, kpt) if kpt > 1 else "bitonic_sort_kernel<{}, %d" % B
+    prof_m, prof_src = ncu_kernel_summary("bitonic", kname.format(1))
+    prof_u, _ = ncu_kernel_summary("bitonic", kname.format(0))
     lane_eff = None
     if prof_m and prof_u:
         lane_eff = {"source": prof_src + " (ncu --set full, one launch per form)",
@@ -379,9 +392,11 @@ def our_arm(args):
                      "traffic": (prof_m or {}).get("dram_bytes"), "peak_source": peak_src,
                      "traffic_note": "ncu dram__bytes read+write of one launch; below the algorithmic bytes "
                                      "because the written keys stay in the 126 MB L2 at kernel end",
-                     "kernel": "bitonic_sort_kernel<true,64,256>",
+                     "kernel": kname.format("true"),
                      "algorithmic_bytes_per_launch": alg_bytes,
-                     "note": "issue-bound: 21 compare-exchange steps per 8 B of HBM traffic; see DESIGN.md §Roofline"},
+                     "alu_pipe_pct": (prof_m or {}).get("alu_pipe_pct"),
+                     "note": "ALU-pipe-bound (VIMNMX compare-exchanges, 21 steps per key) at about the HBM "
+                             "time; see DESIGN.md §5"},
         "e2e": {"value": n * world / (e2e_total / args.steps / 1e3), "unit": "keys/s",
                 "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                 "how": "darm_gpu_bitonic_sort(mem=HOST) on pinned numpy buffers; library CUDA events t0..t3"},
@@ -394,7 +409,20 @@ def our_arm(args):
         line["per_kernel"] = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak)
         line["per_kernel"]["bitonic"] = {"unmelded_us": 1e3 * unm["kernel_ms_mean"],
                                          "melded_us": 1e3 * mel["kernel_ms_mean"],
-                                         "speedup": unm["total_ms"] / mel["total_ms"]}
+                                         "speedup": unm["total_ms"] / mel["total_ms"],
+                                         "keys_per_thread": kpt}
+        # the IR warp shape: one key (one IR lane) per hardware thread
+        row = {}
+        for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
+            step = darm.bitonic_sort(work, B, variant, stream=stream.cuda_stream, want_stats=False,
+                                     prepare_only=True, keys_per_thread=1)
+            t = time_steps(torch, stream, lambda: work.copy_(pristine), step, args.steps, args.warmup, flush)
+            if not torch.equal(work, want):
+                raise SystemExit(f"bitonic one-key {vname}: result is not the bucket-sorted input")
+            row[vname + "_us"] = 1e3 * sum(t) / len(t)
+        row["speedup"] = row["unmelded_us"] / row["melded_us"]
+        row["keys_per_thread"] = 1
+        line["per_kernel"]["bitonic_1key"] = row
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
@@ -410,6 +438,8 @@ def main():
     ap.add_argument("--keys", type=int, default=1 << 24)
     ap.add_argument("--bucket", type=int, default=64)
     ap.add_argument("--ref-sample-buckets", type=int, default=4096)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--keys-per-thread", type=int, default=0, help="0 = auto (16), 1 = one key per thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-kernel", action="store_true")
     args = ap.parse_args()

@@ -136,7 +136,10 @@ int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket,
  *            bucket, strides below it are exchanged inside the thread
  *            (needs bucket / keys_per_thread <= 32, 16-byte aligned keys);
  *   0        the fastest supported (what darm_gpu_bitonic_sort uses).
- * stats->reserved receives the keys per thread used. */
+ * stats->reserved receives the keys per thread used.
+ * HOST mode with n >= 2^22 keys pipelines 2^21-key chunks over three internal
+ * streams (copy in / sort / copy out overlap); then h2d_ms is the time to the
+ * first chunk's sort, kernel_ms the span of the sorts, d2h_ms the rest. */
 int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket,
                              int keys_per_thread, int mem, void *stream,
                              darm_gpu_stats *stats, char *err, size_t errlen);

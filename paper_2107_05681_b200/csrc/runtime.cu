@@ -5,6 +5,7 @@
 // device buffers, the per-lane interpreter loop (interp.cpp:254-314) becomes a
 // kernel launch, and the gather of globalFinal (interp.cpp:366-374) becomes a
 // D2H copy.  Errors follow the CLI's exit codes (darm_cli.cpp:25-27).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -73,7 +74,20 @@ struct DeviceState {
   std::vector<std::pair<void *, size_t>> slots;  // cached staging buffers
   std::vector<GraphEntry> graphs;                // instantiated launch sequences
   cudaStream_t capture = nullptr;                // private stream for graph capture
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // HOST-mode pipeline: copy in, compute, copy out
+  std::vector<cudaEvent_t> events;               // pipeline events (timing disabled)
 };
+
+// HOST-mode pipeline streams and >= count sync events of a device.
+void pipeline_resources(DeviceState &st, size_t count) {
+  for (auto &p : st.pipe)
+    if (!p) DARM_CUDA(cudaStreamCreateWithFlags(&p, cudaStreamNonBlocking));
+  while (st.events.size() < count) {
+    cudaEvent_t e = nullptr;
+    DARM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    st.events.push_back(e);
+  }
+}
 
 std::mutex g_mu;
 std::vector<DeviceState *> g_devices;
@@ -136,6 +150,9 @@ struct Timeline {
   }
   void mark(int i) {
     if (on) DARM_CUDA(cudaEventRecord(ev[i], s));
+  }
+  void mark_on(int i, cudaStream_t other) {
+    if (on) DARM_CUDA(cudaEventRecord(ev[i], other));
   }
   void fill(darm_gpu_stats *st) {
     if (!on || !st) return;
@@ -435,18 +452,52 @@ int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, 
     Timeline tl(s, stats != nullptr);
     const size_t bytes = size_t(n) * 4;
     int32_t *dk = keys;
-    tl.mark(0);
-    if (mem == DARM_MEM_HOST) {
-      dk = static_cast<int32_t *>(slot(st, 0, bytes));
-      if (bytes) DARM_CUDA(cudaMemcpyAsync(dk, keys, bytes, cudaMemcpyHostToDevice, s));
-    }
-    tl.mark(1);
     int launches = 0;
-    DARM_CUDA(launch_bitonic_sort(variant, dk, n, bucket, kpt, s, &launches));
-    tl.mark(2);
-    if (mem == DARM_MEM_HOST && bytes) DARM_CUDA(cudaMemcpyAsync(keys, dk, bytes, cudaMemcpyDeviceToHost, s));
-    tl.mark(3);
-    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+    // HOST mode, large inputs: chunks pipelined over three streams so the
+    // host->device copy of chunk i+1, the sort of chunk i and the
+    // device->host copy of chunk i-1 overlap (the buckets are independent).
+    const int64_t chunk = int64_t(1) << 21;   // keys (8 MiB), a multiple of every bucket and warp tile
+    if (mem == DARM_MEM_HOST && n >= 2 * chunk) {
+      dk = static_cast<int32_t *>(slot(st, 0, bytes));
+      const int64_t nc = (n + chunk - 1) / chunk;
+      pipeline_resources(st, size_t(2 * nc + 2));
+      cudaStream_t in = st.pipe[0], comp = st.pipe[1], out = st.pipe[2];
+      cudaEvent_t start = st.events[0], done = st.events[1];
+      tl.mark(0);
+      DARM_CUDA(cudaEventRecord(start, s));                 // after the caller's prior work on s
+      DARM_CUDA(cudaStreamWaitEvent(in, start, 0));
+      DARM_CUDA(cudaStreamWaitEvent(comp, start, 0));
+      DARM_CUDA(cudaStreamWaitEvent(out, start, 0));
+      for (int64_t c = 0; c < nc; ++c) {
+        const int64_t off = c * chunk, len = std::min(chunk, n - off);
+        cudaEvent_t copied = st.events[2 + 2 * c], sorted = st.events[3 + 2 * c];
+        DARM_CUDA(cudaMemcpyAsync(dk + off, keys + off, size_t(len) * 4, cudaMemcpyHostToDevice, in));
+        DARM_CUDA(cudaEventRecord(copied, in));
+        DARM_CUDA(cudaStreamWaitEvent(comp, copied, 0));
+        if (c == 0) tl.mark_on(1, comp);
+        DARM_CUDA(launch_bitonic_sort(variant, dk + off, len, bucket, kpt, comp, &launches));
+        DARM_CUDA(cudaEventRecord(sorted, comp));
+        if (c == nc - 1) tl.mark_on(2, comp);
+        DARM_CUDA(cudaStreamWaitEvent(out, sorted, 0));
+        DARM_CUDA(cudaMemcpyAsync(keys + off, dk + off, size_t(len) * 4, cudaMemcpyDeviceToHost, out));
+      }
+      DARM_CUDA(cudaEventRecord(done, out));
+      DARM_CUDA(cudaStreamWaitEvent(s, done, 0));
+      tl.mark(3);
+      DARM_CUDA(cudaStreamSynchronize(s));
+    } else {
+      tl.mark(0);
+      if (mem == DARM_MEM_HOST) {
+        dk = static_cast<int32_t *>(slot(st, 0, bytes));
+        if (bytes) DARM_CUDA(cudaMemcpyAsync(dk, keys, bytes, cudaMemcpyHostToDevice, s));
+      }
+      tl.mark(1);
+      DARM_CUDA(launch_bitonic_sort(variant, dk, n, bucket, kpt, s, &launches));
+      tl.mark(2);
+      if (mem == DARM_MEM_HOST && bytes) DARM_CUDA(cudaMemcpyAsync(keys, dk, bytes, cudaMemcpyDeviceToHost, s));
+      tl.mark(3);
+      if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+    }
     if (stats) {
       tl.fill(stats);
       stats->launches = launches;

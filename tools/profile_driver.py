@@ -42,9 +42,10 @@ def main(which, bucket=64):
         n = 1 << 24
         g = torch.Generator(device="cuda").manual_seed(1234)
         pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
-        for v in (darm.UNMELDED, darm.MELDED):
-            k = pristine.clone()
-            darm.bitonic_sort(k, bucket, v, want_stats=False)
+        for kpt in (0, 1):       # register-blocked (auto: 16 keys per thread), then one key per thread
+            for v in (darm.UNMELDED, darm.MELDED):
+                k = pristine.clone()
+                darm.bitonic_sort(k, bucket, v, want_stats=False, keys_per_thread=kpt)
         torch.cuda.synchronize()
     else:
         nw = 1 << 15
