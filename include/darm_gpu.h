@@ -144,6 +144,18 @@ int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket,
                              int keys_per_thread, int mem, void *stream,
                              darm_gpu_stats *stats, char *err, size_t errlen);
 
+/* ---- PCM: Batcher odd-even merge sort of buckets (the
+ *      reference has no PCM code) — paper_2107_05681_b200/ir/oddeven_step.ir
+ *      chained over p = 1..bucket/2, k = p..1 ----------------------------------
+ * Sorts each of the n/bucket consecutive buckets ascending, in place; the
+ * arguments, shapes (keys_per_thread), HOST-mode pipelining and stats are those
+ * of darm_gpu_bitonic_sort_ex.  The chained-step semantics equal the
+ * reference interpreter's executeWarp chain of the IR step for bucket <= 64
+ * (oracle: oracle/ref_shim.cpp ref_chain_sort). */
+int darm_gpu_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket,
+                          int keys_per_thread, int mem, void *stream,
+                          darm_gpu_stats *stats, char *err, size_t errlen);
+
 /* ---- N-Queens (NQU; the reference has no code for it):
  *      paper_2107_05681_b200/ir/nqueens_step.ir run to completion per thread -
  * Counts the placements of n non-attacking queens on an n x n board (2 <= n

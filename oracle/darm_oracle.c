@@ -212,6 +212,31 @@ int oracle_bitonic_sort(int32_t *keys, int64_t n, int bucket) {
   return 0;
 }
 
+/* Batcher odd-even merge sort of each B-key bucket (PCM; no
+ * reference code): the chain of ir/oddeven_step.ir steps, p = 1..B/2,
+ * k = p..1; comparator (x, x + k) for x >= k % p, (x - k % p) mod 2k < k,
+ * x + k < B, x and x + k in the same 2p block. */
+int oracle_oddeven_sort(int32_t *keys, int64_t n, int bucket) {
+  if (bucket < 2 || (bucket & (bucket - 1)) || n % bucket) return 2;
+  const int B = bucket;
+  for (int64_t b = 0; b < n / B; ++b) {
+    int32_t *v = keys + b * B;
+    for (int p = 1; p < B; p <<= 1)
+      for (int k = p; k >= 1; k >>= 1) {
+        const int kp = k % p;
+        for (int x = kp; x + k < B; ++x) {
+          if ((x - kp) % (2 * k) >= k || x / (2 * p) != (x + k) / (2 * p)) continue;
+          if (v[x] > v[x + k]) {
+            int32_t t = v[x];
+            v[x] = v[x + k];
+            v[x + k] = t;
+          }
+        }
+      }
+  }
+  return 0;
+}
+
 /* ------------------------------------------------------------ N-Queens
  * The reference has no NQU code; this is an independent
  * recursive restatement of the search that paper_2107_05681_b200/ir/

@@ -48,6 +48,10 @@ int oracle_execute_warps(const char *kernel, int warp, int64_t n_warps, const in
  * each B-key bucket (B power of two). */
 int oracle_bitonic_sort(int32_t *keys, int64_t n, int bucket);
 
+/* Batcher odd-even merge sort of each B-key bucket (PCM; the chain of
+ * ir/oddeven_step.ir steps p = 1..B/2, k = p..1). */
+int oracle_oddeven_sort(int32_t *keys, int64_t n, int bucket);
+
 /* N-Queens (no reference code; recursive restatement).  Prefixes: valid
  * placements of rows 0..base-1, lowest free column first, index i kept when
  * i % world == rank, written as {cols, d1, d2} triples (up to cap).  Returns the

@@ -125,6 +125,37 @@ def bitonic_sort_fixtures(ref: Reference) -> dict:
     return out
 
 
+OE_IR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                     "paper_2107_05681_b200", "ir", "oddeven_step.ir")
+
+
+def oddeven_sort_fixtures(ref: Reference) -> dict:
+    """PCM: the reference interpreter chains ir/oddeven_step.ir (original and
+    as melded by runDarm) over every Batcher odd-even merge step of B-key
+    buckets: sorted outputs and unit-latency simulator statistics."""
+    from oracle import oddeven_schedule
+
+    text = open(OE_IR).read()
+    mod = ref.load_text(text, 0)
+    meld = ref.load_text(text, 1)
+    out = {"ir": "paper_2107_05681_b200/ir/oddeven_step.ir", "melds": meld.layout["melds"], "cases": []}
+    rng = np.random.Generator(np.random.MT19937(13))
+    for B in (2, 4, 8, 16, 32, 64):
+        for dup in (False, True):
+            nb = 4
+            lo, hi = (-128, 129) if dup else (-(2 ** 31), 2 ** 31)
+            keys = rng.integers(lo, hi, size=nb * B, dtype=np.int64).astype(np.int32)
+            a = keys.copy()
+            st_u = mod.chain_sort(a, B, oddeven_schedule(B), unit_latency=True)
+            b = keys.copy()
+            st_m = meld.chain_sort(b, B, oddeven_schedule(B), unit_latency=True)
+            assert (a == b).all()
+            assert (a.reshape(-1, B) == np.sort(keys.reshape(-1, B), axis=1)).all()
+            out["cases"].append({"bucket": B, "keys": keys.tolist(), "sorted": a.tolist(),
+                                 "stats_unit_latency": {"unmelded": st_u.tolist(), "melded": st_m.tolist()}})
+    return out
+
+
 NQ_IR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                      "paper_2107_05681_b200", "ir", "nqueens_sym.ir")
 
@@ -197,6 +228,8 @@ def main():
             json.dump(corpus_fixtures(ref, name), f, separators=(",", ":"))
     with open(os.path.join(OUT, "bitonic_sort.json"), "w") as f:
         json.dump(bitonic_sort_fixtures(ref), f, separators=(",", ":"))
+    with open(os.path.join(OUT, "oddeven_sort.json"), "w") as f:
+        json.dump(oddeven_sort_fixtures(ref), f, separators=(",", ":"))
     with open(os.path.join(OUT, "nqueens_chain.json"), "w") as f:
         json.dump(nqueens_chain_fixtures(ref), f, separators=(",", ":"))
     with open(os.path.join(OUT, "mt19937_64.json"), "w") as f:

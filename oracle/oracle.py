@@ -58,6 +58,7 @@ class Restatement:
         L.oracle_execute_warps.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int64, I32P,
                                            ctypes.c_int64, I32P, ctypes.c_int64, I32P, I32P]
         L.oracle_bitonic_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
+        L.oracle_oddeven_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
         L.oracle_lud.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int]
         L.oracle_srad.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                   ctypes.c_float, I32P, ctypes.c_int]
@@ -101,6 +102,11 @@ class Restatement:
         rc = self.lib.oracle_bitonic_sort(_p(keys), keys.size, bucket)
         if rc:
             raise ValueError("oracle_bitonic_sort: bad bucket")
+
+    def oddeven_sort(self, keys: np.ndarray, bucket: int) -> None:
+        rc = self.lib.oracle_oddeven_sort(_p(keys), keys.size, bucket)
+        if rc:
+            raise ValueError("oracle_oddeven_sort: bad bucket")
 
     def lud(self, a: np.ndarray, threads: int = 0) -> None:
         """In-place blocked LU in csrc/lud.cu's operation order."""
@@ -200,6 +206,36 @@ class RefModule:
         return stats
 
 
+def oddeven_schedule(bucket: int) -> np.ndarray:
+    """(p, k, n) params of every Batcher odd-even merge step of a bucket, in
+    order: p = 1, 2, .., B/2 and k = p, p/2, .., 1 (ir/oddeven_step.ir)."""
+    steps = []
+    p = 1
+    while p < bucket:
+        k = p
+        while k >= 1:
+            steps.append((p, k, bucket))
+            k //= 2
+        p *= 2
+    return np.array(steps, dtype=np.int32).reshape(-1, 3)
+
+
+def _chain_sort(self, keys: np.ndarray, bucket: int, schedule: np.ndarray, threads: int = 1,
+                unit_latency: bool = False):
+    """executeWarp chained over a network step kernel's schedule, per bucket (in place)."""
+    stats = np.zeros(7, dtype=np.int64)
+    err = ctypes.create_string_buffer(512)
+    sched = np.ascontiguousarray(schedule, dtype=np.int32)
+    rc = self.ref.lib.ref_chain_sort(self.h, _p(keys), keys.size, bucket, _p(sched), sched.shape[0],
+                                     sched.shape[1], threads, int(unit_latency), _p(stats, I64P), err, 512)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return stats
+
+
+RefModule.chain_sort = _chain_sort
+
+
 def _run_to_fixpoint(self, warp, args, globals_full, shared_full, max_rounds=1_000_000, unit_latency=False):
     """executeWarp chained to a fixpoint on one warp (declared-size arrays, in/out)."""
     args = np.ascontiguousarray(args, dtype=np.int32)
@@ -243,6 +279,8 @@ class Reference:
                                        I64P, ctypes.c_char_p, ctypes.c_size_t]
         L.ref_run_to_fixpoint.argtypes = [vp, ctypes.c_int, I32P, I32P, I32P, ctypes.c_int64, ctypes.c_int,
                                           I64P, I64P, ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_chain_sort.argtypes = [vp, I32P, ctypes.c_int64, ctypes.c_int, I32P, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, I64P, ctypes.c_char_p, ctypes.c_size_t]
         self.lib = L
 
     def load(self, name: str, meld: int = 0, threshold: float = 0.2) -> RefModule:

@@ -437,4 +437,63 @@ int ref_bitonic_sort(const ref_module *h, int32_t *keys, int64_t n, int B,
   return 0;
 }
 
+// Generic chain of a one-warp sorting-network step kernel over B-key buckets:
+// step s runs with the params step_args[s*arity .. s*arity+arity-1], the
+// bucket in the step's shared array and its global `res` as the next step's
+// input (the loop a network driver runs; used for ir/oddeven_step.ir, PCM).
+// B <= 64 (warp limit, interp.cpp:334-335).  stats_sum as ref_bitonic_sort.
+int ref_chain_sort(const ref_module *h, int32_t *keys, int64_t n, int B, const int32_t *step_args,
+                   int nsteps, int arity, int threads, int unit_latency, int64_t *stats_sum,
+                   char *err, size_t errlen) {
+  if (B < 2 || B > 64 || n % B) return fail(err, errlen, "bucket must be in [2,64] and divide n", 2);
+  const Function &f = h->m.functions.front();
+  if (int(f.params.size()) != arity || f.sharedDecls.size() != 1 || h->m.globals.size() != 1)
+    return fail(err, errlen, "module is not a one-buffer network step kernel of this arity", 2);
+  const std::string bufName = f.sharedDecls[0].name;
+  const int64_t bufSize = f.sharedDecls[0].size;
+  const std::string resName = h->m.globals[0].name;
+  LatencyModel lm = pickLatency(unit_latency);
+  const int64_t nb = n / B;
+  std::vector<std::array<int64_t, 7>> per(size_t(stats_sum ? nb : 0));
+  std::vector<std::string> errors(1);
+  std::atomic<bool> bad{false};
+  parallelFor(nb, threads, [&](int64_t b) {
+    if (bad.load()) return;
+    try {
+      std::vector<int32_t> cur(keys + b * B, keys + (b + 1) * B);
+      std::array<int64_t, 7> acc{};
+      for (int st = 0; st < nsteps; ++st) {
+        WarpInput in;
+        in.warpSize = B;
+        for (int a = 0; a < arity; ++a) in.args.push_back({step_args[st * arity + a]});
+        std::vector<int32_t> buf(size_t(bufSize), 0);
+        std::copy(cur.begin(), cur.end(), buf.begin());
+        in.sharedInit[bufName] = buf;
+        WarpResult r = executeWarp(h->m, f, in, lm);
+        if (r.nonTerminated || !r.faults.empty()) throw std::runtime_error("network step faulted");
+        const auto &res = r.globalFinal.at(resName);
+        std::copy(res.begin(), res.begin() + B, cur.begin());
+        acc[0] += r.stats.issuedInstructions;
+        acc[1] += r.stats.threadCycles;
+        acc[2] += r.stats.usefulThreadCycles;
+        acc[3] += r.stats.serializedCycles;
+        acc[4] += r.stats.divergentBranchCount;
+        acc[5] += r.stats.sharedMemIssues;
+        acc[6] += r.stats.globalMemIssues;
+      }
+      std::copy(cur.begin(), cur.end(), keys + b * B);
+      if (stats_sum) per[size_t(b)] = acc;
+    } catch (const std::exception &e) {
+      if (!bad.exchange(true)) errors[0] = e.what();
+    }
+  });
+  if (bad) return fail(err, errlen, errors[0], 2);
+  if (stats_sum) {
+    for (int i = 0; i < 7; ++i) stats_sum[i] = 0;
+    for (const auto &a : per)
+      for (int i = 0; i < 7; ++i) stats_sum[i] += a[size_t(i)];
+  }
+  return 0;
+}
+
 }  // extern "C"

@@ -50,6 +50,7 @@ ABI_SYMBOLS = (
     "darm_gpu_execute_warps",
     "darm_gpu_bitonic_sort",
     "darm_gpu_bitonic_sort_ex",
+    "darm_gpu_oddeven_sort",
     "darm_gpu_nqueens",
     "darm_gpu_nqueens_prefix_count",
     "darm_gpu_lud",
@@ -124,6 +125,7 @@ def lib() -> ctypes.CDLL:
         L.darm_gpu_bitonic_sort_ex.argtypes = [
             ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.c_void_p, ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_oddeven_sort.argtypes = L.darm_gpu_bitonic_sort_ex.argtypes
         L.darm_gpu_nqueens.argtypes = [
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int64,
@@ -330,15 +332,7 @@ class PreparedCall:
         return self.stats.as_dict() if self.stats is not None else {}
 
 
-def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: bool = True,
-                 prepare_only: bool = False, keys_per_thread: int = 0):
-    """Sort every ``bucket``-key bucket of ``keys`` ascending, in place.
-
-    ``keys``: numpy int32 (HOST mode) or torch int32 CUDA tensor (DEVICE mode).
-    ``keys_per_thread``: 1 = one key per thread (the IR warp shape), 4/8/16 =
-    register-blocked, 0 = fastest (``darm_gpu_bitonic_sort_ex``).  The stats
-    dict reports the choice as ``keys_per_thread``.
-    """
+def _network_sort(fn, keys, bucket, variant, stream, want_stats, prepare_only, keys_per_thread):
     if isinstance(variant, str):
         variant = VARIANTS[variant]
     if _is_torch_cuda(keys):
@@ -350,10 +344,32 @@ def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: boo
     else:
         assert keys.dtype == np.int32 and keys.flags["C_CONTIGUOUS"]
         ptr, n, mem = keys.ctypes.data, keys.size, 0
-    call = PreparedCall(lib().darm_gpu_bitonic_sort_ex,
-                        (int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), int(keys_per_thread), mem,
-                         ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
+    call = PreparedCall(fn, (int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), int(keys_per_thread), mem,
+                             ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
     return call if prepare_only else call()
+
+
+def bitonic_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: bool = True,
+                 prepare_only: bool = False, keys_per_thread: int = 0):
+    """Sort every ``bucket``-key bucket of ``keys`` ascending, in place, by the
+    chain of corpus bitonic.ir steps.
+
+    ``keys``: numpy int32 (HOST mode) or torch int32 CUDA tensor (DEVICE mode).
+    ``keys_per_thread``: 1 = one key per thread (the IR warp shape), 4/8/16 =
+    register-blocked, 0 = fastest (``darm_gpu_bitonic_sort_ex``).  The stats
+    dict reports the choice as ``keys_per_thread``.
+    """
+    return _network_sort(lib().darm_gpu_bitonic_sort_ex, keys, bucket, variant, stream, want_stats, prepare_only,
+                         keys_per_thread)
+
+
+def oddeven_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: bool = True,
+                 prepare_only: bool = False, keys_per_thread: int = 0):
+    """PCM: Batcher odd-even merge sort of every ``bucket``-key bucket, in place,
+    by the chain of ir/oddeven_step.ir steps (``darm_gpu_oddeven_sort``);
+    arguments as :func:`bitonic_sort`."""
+    return _network_sort(lib().darm_gpu_oddeven_sort, keys, bucket, variant, stream, want_stats, prepare_only,
+                         keys_per_thread)
 
 
 def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int = 1,

@@ -39,6 +39,10 @@ int bitonic_keys_per_thread(int bucket, int keys_per_thread, const void *keys);
 cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread,
                                 cudaStream_t s, int *launches);
 
+// oddeven_sort.cu (PCM): keys_per_thread already resolved by bitonic_keys_per_thread
+cudaError_t launch_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread,
+                                cudaStream_t s, int *launches);
+
 // nqueens.cu
 cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, int n, int base,
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,

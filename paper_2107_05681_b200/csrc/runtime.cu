@@ -431,8 +431,13 @@ int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int
   return darm_gpu_bitonic_sort_ex(variant, keys, n, bucket, 0, mem, stream, stats, err, errlen);
 }
 
-int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
-                             void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
+using NetworkLaunch = cudaError_t (*)(int, int32_t *, int64_t, int, int, cudaStream_t, int *);
+
+// Bucket sorts built from a one-warp network step (bitonic.ir, oddeven_step.ir):
+// argument checks, HOST-mode staging (pipelined for large inputs), stats.
+static int network_sort(NetworkLaunch launch, int variant, int32_t *keys, int64_t n, int bucket,
+                        int keys_per_thread, int mem, void *stream, darm_gpu_stats *stats, char *err,
+                        size_t errlen) {
   return guarded(err, errlen, [&] {
     if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
     if (!bitonic_sort_supported(bucket)) user_error("bucket must be a power of two in [2, 1024]");
@@ -475,7 +480,7 @@ int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, 
         DARM_CUDA(cudaEventRecord(copied, in));
         DARM_CUDA(cudaStreamWaitEvent(comp, copied, 0));
         if (c == 0) tl.mark_on(1, comp);
-        DARM_CUDA(launch_bitonic_sort(variant, dk + off, len, bucket, kpt, comp, &launches));
+        DARM_CUDA(launch(variant, dk + off, len, bucket, kpt, comp, &launches));
         DARM_CUDA(cudaEventRecord(sorted, comp));
         if (c == nc - 1) tl.mark_on(2, comp);
         DARM_CUDA(cudaStreamWaitEvent(out, sorted, 0));
@@ -492,7 +497,7 @@ int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, 
         if (bytes) DARM_CUDA(cudaMemcpyAsync(dk, keys, bytes, cudaMemcpyHostToDevice, s));
       }
       tl.mark(1);
-      DARM_CUDA(launch_bitonic_sort(variant, dk, n, bucket, kpt, s, &launches));
+      DARM_CUDA(launch(variant, dk, n, bucket, kpt, s, &launches));
       tl.mark(2);
       if (mem == DARM_MEM_HOST && bytes) DARM_CUDA(cudaMemcpyAsync(keys, dk, bytes, cudaMemcpyDeviceToHost, s));
       tl.mark(3);
@@ -507,6 +512,18 @@ int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, 
       stats->reserved = kpt;
     }
   });
+}
+
+int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
+                             void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
+  return network_sort(launch_bitonic_sort, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
+                      errlen);
+}
+
+int darm_gpu_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
+                          void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
+  return network_sort(launch_oddeven_sort, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
+                      errlen);
 }
 
 // N-Queens prefixes: every valid placement of the first `base` rows, lowest

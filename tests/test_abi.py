@@ -6,6 +6,7 @@
 * without a GPU every compute entry point fails loudly (no CPU fallback);
 * the SASS keeps the two forms distinct.
 """
+import functools
 import ctypes
 import os
 import re
@@ -125,10 +126,15 @@ def test_no_cpu_fallback_without_gpu():
         darm.bitonic_sort(np.zeros(64, np.int32), 64)
 
 
-def _sass(pattern):
+@functools.lru_cache(maxsize=1)
+def _all_sass():
     from tools.sass_dump import sass_functions
 
-    funcs = sass_functions(darm.LIB_PATH)
+    return sass_functions(darm.LIB_PATH)
+
+
+def _sass(pattern):
+    funcs = _all_sass()
     hits = [(n, b) for n, b in funcs.items() if pattern in n]
     assert len(hits) == 1, (pattern, [n for n, _ in hits])
     return [ins for _, ins in hits[0][1]]
@@ -151,13 +157,24 @@ def test_sass_bitonic_sort_forms():
     # Same partner reads in both forms (20 shuffles + 1 shared exchange for
     # B=64); the unmelded network issues both arms of every `up` branch
     # (ptxas if-converts them into complementary predicated min/max), the
-    # melded one a single predicated min/max per step.
+    # melded one a single keep-predicated min/max per step.
     # (two tiles per iteration, U = 2)
     assert sum("SHFL.BFLY" in i for i in un) == sum("SHFL.BFLY" in i for i in me) == 2 * 20
     assert sum("BAR.SYNC" in i for i in un) == sum("BAR.SYNC" in i for i in me) == 1
     assert len(un) > 1.4 * len(me)
-    # unmelded: both arms' min/max per step (predicated VIMNMX pairs); melded:
-    # one compare folded with keep (ISETP.*.XOR) and one select per step
     assert sum("IMNMX" in i for i in un) >= 2 * 60
-    assert sum("ISETP" in i and ".XOR" in i for i in me) >= 2 * 20
-    assert sum(i.startswith("SEL") for i in me) >= 2 * 20
+    assert sum("IMNMX" in i for i in me) < 0.75 * sum("IMNMX" in i for i in un)
+    # melded order flips run on the FMA pipe (IMAD), not as LOP3
+    assert sum(i.startswith("IMAD") and "MOV" not in i for i in me) >= 2 * 5
+
+
+def test_sass_register_blocked_forms():
+    """16 keys per thread, B = 64: the unmelded form keeps a divergent branch
+    (BSSY/BSYNC pair) around the up/down arms of every thread-dependent step;
+    the melded form has none in the network and more straight-line code."""
+    for kern in ("bitonic_sort_reg_kernel<{}, 64, 16, true>", "oddeven_sort_reg_kernel<{}, 64, 16>"):
+        un = _sass(kern.format("false"))
+        me = _sass(kern.format("true"))
+        assert sum("SHFL" in i for i in un) > 0 and sum("SHFL" in i for i in me) > 0
+        assert sum(i.startswith("BSSY") for i in un) > sum(i.startswith("BSSY") for i in me)
+        assert sum("IMNMX" in i for i in un) > sum("IMNMX" in i for i in me)

@@ -1,0 +1,90 @@
+"""PCM — Batcher odd-even merge sort of buckets (no reference
+code): ir/oddeven_step.ir run by the reference interpreter pins the oracle
+restatement (golden fixtures, oracle/gen_golden.py), and — on the GPU — both
+forms and every keys-per-thread shape of csrc/oddeven_sort.cu against it."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+import paper_2107_05681_b200 as darm
+
+
+def test_oddeven_restatement_matches_reference_golden(restatement):
+    gold = load_golden("oddeven_sort.json")
+    for case in gold["cases"]:
+        keys = np.array(case["keys"], dtype=np.int32)
+        restatement.oddeven_sort(keys, case["bucket"])
+        assert keys.tolist() == case["sorted"], case["bucket"]
+
+
+def test_oddeven_melded_spec_is_the_reference_pass_output():
+    """The melded forms mirror runDarm's output for ir/oddeven_step.ir: one
+    region-region meld with one select (the role picks gt / lt), and the
+    reference simulator sees fewer serialized cycles after it."""
+    gold = load_golden("oddeven_sort.json")
+    assert [(m["kind"], m["selectsInserted"]) for m in gold["melds"]] == [("region-region", 1)]
+    for case in gold["cases"]:
+        u, m = case["stats_unit_latency"]["unmelded"], case["stats_unit_latency"]["melded"]
+        assert m[3] < u[3]                      # serialized cycles
+        assert m[2] / m[1] > u[2] / u[1]        # utilisation
+
+
+@pytest.mark.parametrize("B", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024])
+def test_oddeven_restatement_sorts(restatement, B):
+    rng = np.random.default_rng(B)
+    keys = rng.integers(-(2 ** 31), 2 ** 31, size=B * 16, dtype=np.int64).astype(np.int32)
+    want = np.sort(keys.reshape(-1, B), axis=1).reshape(-1)
+    restatement.oddeven_sort(keys, B)
+    assert (keys == want).all()
+
+
+SHAPES = [(B, 1) for B in (2, 4, 8, 16, 32, 64, 128, 256, 512, 1024)] + \
+         [(B, r) for B in (4, 8, 16, 32, 64, 128, 256, 512) for r in (4, 8, 16) if r <= B and B // r <= 32]
+
+
+@pytest.mark.gpu
+def test_oddeven_gpu_golden():
+    gold = load_golden("oddeven_sort.json")
+    for case in gold["cases"]:
+        B = case["bucket"]
+        for kpt in (0, 1, 4, 8, 16):
+            if kpt > 1 and (kpt > B or B // kpt > 32):
+                continue
+            for variant in (0, 1):
+                keys = np.array(case["keys"], dtype=np.int32)
+                darm.oddeven_sort(keys, B, variant, keys_per_thread=kpt)
+                assert keys.tolist() == case["sorted"], (B, kpt, variant)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bucket,kpt", SHAPES)
+def test_oddeven_gpu_vs_restatement(restatement, bucket, kpt):
+    import torch
+
+    rng = np.random.default_rng(bucket * 31 + kpt)
+    for n in (1 << 17, bucket * 37, bucket):
+        for dup in (False, True):
+            lo, hi = (-128, 129) if dup else (-(2 ** 31), 2 ** 31)
+            keys = rng.integers(lo, hi, size=n, dtype=np.int64).astype(np.int32)
+            want = keys.copy()
+            restatement.oddeven_sort(want, bucket)
+            for variant in (0, 1):
+                k = torch.from_numpy(keys.copy()).cuda()
+                st = darm.oddeven_sort(k, bucket, variant, keys_per_thread=kpt)
+                assert st["keys_per_thread"] == kpt
+                assert (k.cpu().numpy() == want).all(), (bucket, kpt, n, dup, variant)
+
+
+@pytest.mark.gpu
+def test_oddeven_gpu_full_size_host_pipeline():
+    """2^24 keys, 64-key buckets through the HOST path (pipelined chunks):
+    every bucket sorted and a permutation of its input."""
+    rng = np.random.default_rng(7)
+    keys = rng.integers(-(2 ** 31), 2 ** 31, size=1 << 24, dtype=np.int64).astype(np.int32)
+    want = np.sort(keys.reshape(-1, 64), axis=1).reshape(-1)
+    for variant in (0, 1):
+        k = keys.copy()
+        st = darm.oddeven_sort(k, 64, variant)
+        assert st["launches"] == 8
+        assert (k == want).all()

@@ -38,6 +38,16 @@ def main(which, bucket=64):
         for v in (darm.UNMELDED, darm.MELDED):
             assert darm.nqueens(16, 6, v, want_stats=False)[0] == 14772512
         return
+    if which == "oddeven":
+        n = 1 << 24
+        g = torch.Generator(device="cuda").manual_seed(1234)
+        pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+        for kpt in (0, 1):
+            for v in (darm.UNMELDED, darm.MELDED):
+                k = pristine.clone()
+                darm.oddeven_sort(k, bucket, v, want_stats=False, keys_per_thread=kpt)
+        torch.cuda.synchronize()
+        return
     if which == "bitonic":
         n = 1 << 24
         g = torch.Generator(device="cuda").manual_seed(1234)

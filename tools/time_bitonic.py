@@ -1,6 +1,7 @@
-"""Time the bitonic bucket sort (both forms, every keys-per-thread shape) on cuda:0.
+"""Time the bitonic (or, with --oddeven, the PCM odd-even) bucket sort, both
+forms and every keys-per-thread shape, on cuda:0.
 
-    python tools/time_bitonic.py [bucket ...]      (run under gpurun)
+    python tools/time_bitonic.py [--oddeven] [bucket ...]      (run under gpurun)
 L2 is flushed (256 MiB write) before every timed launch; min and mean of 10.
 """
 import os
@@ -12,7 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2107_05681_b200 as darm  # noqa: E402
 
 
-def main(*buckets):
+def main(*buckets, sort=None):
+    sort = sort or darm.bitonic_sort
     darm.init()
     s = torch.cuda.current_stream()
     n = 1 << 24
@@ -27,7 +29,7 @@ def main(*buckets):
                 continue
             res = {}
             for v in (darm.UNMELDED, darm.MELDED):
-                call = darm.bitonic_sort(work, B, v, stream=s.cuda_stream, want_stats=False, prepare_only=True,
+                call = sort(work, B, v, stream=s.cuda_stream, want_stats=False, prepare_only=True,
                                          keys_per_thread=kpt)
                 ts = []
                 for i in range(13):
@@ -44,9 +46,11 @@ def main(*buckets):
                 assert torch.equal(work, want), (B, kpt, v)
                 res[v] = (min(ts), sum(ts) / len(ts))
             gbs = 8 * n / (res[1][1] * 1e-6) / 1e9
-            print(f"B={B} kpt={kpt:2d} unmelded {res[0][1]:7.1f} us (min {res[0][0]:6.1f}) melded {res[1][1]:7.1f} us "
+            print(f"{sort.__name__} B={B} kpt={kpt:2d} unmelded {res[0][1]:7.1f} us (min {res[0][0]:6.1f}) melded {res[1][1]:7.1f} us "
                   f"(min {res[1][0]:6.1f}) speedup {res[0][1] / res[1][1]:.3f} melded {gbs:6.0f} GB/s", flush=True)
 
 
 if __name__ == "__main__":
-    main(*(int(x) for x in sys.argv[1:]))
+    args = sys.argv[1:]
+    fn = darm.oddeven_sort if "--oddeven" in args else darm.bitonic_sort
+    main(*(int(x) for x in args if x != "--oddeven"), sort=fn)
