@@ -156,6 +156,17 @@ int darm_gpu_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket,
                           int keys_per_thread, int mem, void *stream,
                           darm_gpu_stats *stats, char *err, size_t errlen);
 
+/* ---- MS: bottom-up merge sort of the whole array (the
+ *      reference has no MS code) — the merge loop of
+ *      paper_2107_05681_b200/ir/merge_step.ir, passes w = 1, 2, 4, .. < n ----
+ * Sorts keys[0..n) ascending in place (0 <= n < 2^30).  The chained-step
+ * semantics equal the reference interpreter running the IR loop to a fixpoint
+ * per pass for n <= 1024 (oracle: tests/golden/merge_sort.json).  The pass
+ * sequence is recorded once per (keys, n, variant) as a CUDA graph. */
+int darm_gpu_merge_sort(int variant, int32_t *keys, int64_t n, int mem,
+                        void *stream, darm_gpu_stats *stats, char *err,
+                        size_t errlen);
+
 /* ---- N-Queens (NQU; the reference has no code for it):
  *      paper_2107_05681_b200/ir/nqueens_step.ir run to completion per thread -
  * Counts the placements of n non-attacking queens on an n x n board (2 <= n

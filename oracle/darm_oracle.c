@@ -237,6 +237,33 @@ int oracle_oddeven_sort(int32_t *keys, int64_t n, int bucket) {
   return 0;
 }
 
+/* Bottom-up merge sort of keys[0..n) (MS; no reference
+ * code): passes w = 1, 2, 4, .. < n merge runs [a, a+w) and [a+w, a+2w),
+ * clipped to n, taking the left head on ties (the loop of
+ * paper_2107_05681_b200/ir/merge_step.ir). */
+int oracle_merge_sort(int32_t *keys, int64_t n) {
+  if (n < 0) return 2;
+  if (n < 2) return 0;
+  int32_t *tmp = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  if (!tmp) return 3;
+  int32_t *src = keys, *dst = tmp;
+  for (int64_t w = 1; w < n; w <<= 1) {
+    for (int64_t a = 0; a < n; a += 2 * w) {
+      int64_t i = a, iend = a + w < n ? a + w : n, j = iend, jend = a + 2 * w < n ? a + 2 * w : n, k = a;
+      while (k < jend) {
+        const int take = j >= jend || (i < iend && src[i] <= src[j]);
+        dst[k++] = take ? src[i++] : src[j++];
+      }
+    }
+    int32_t *t = src;
+    src = dst;
+    dst = t;
+  }
+  if (src != keys) memcpy(keys, src, sizeof(int32_t) * (size_t)n);
+  free(tmp);
+  return 0;
+}
+
 /* ------------------------------------------------------------ N-Queens
  * The reference has no NQU code; this is an independent
  * recursive restatement of the search that paper_2107_05681_b200/ir/

@@ -52,6 +52,9 @@ int oracle_bitonic_sort(int32_t *keys, int64_t n, int bucket);
  * ir/oddeven_step.ir steps p = 1..B/2, k = p..1). */
 int oracle_oddeven_sort(int32_t *keys, int64_t n, int bucket);
 
+/* Bottom-up merge sort of keys[0..n) (MS; the loop of ir/merge_step.ir). */
+int oracle_merge_sort(int32_t *keys, int64_t n);
+
 /* N-Queens (no reference code; recursive restatement).  Prefixes: valid
  * placements of rows 0..base-1, lowest free column first, index i kept when
  * i % world == rank, written as {cols, d1, d2} triples (up to cap).  Returns the

@@ -156,6 +156,75 @@ def oddeven_sort_fixtures(ref: Reference) -> dict:
     return out
 
 
+MS_IR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                     "paper_2107_05681_b200", "ir", "merge_step.ir")
+
+
+def _merge_path(a, na, b, nb, d):
+    lo, hi = max(0, d - nb), min(d, na)
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if a[mid] <= b[d - 1 - mid]:
+            lo = mid + 1
+        else:
+            hi = mid
+    return lo
+
+
+def merge_chain(mod, keys, warp=32, chunk=16):
+    """Bottom-up merge sort of keys (n <= 1024) by the reference interpreter:
+    per pass, every merge is cut into `chunk`-output jobs (the host finds each
+    job's start on the merge path, as the GPU does), jobs are dealt to the
+    lanes of a warp, and ir/merge_step.ir runs to a fixpoint per batch."""
+    n = len(keys)
+    cur = np.zeros(1024, np.int32)
+    cur[:n] = keys
+    stats = np.zeros(7, np.int64)
+    rounds = 0
+    w = 1
+    while w < n:
+        jobs = []
+        for a in range(0, n, 2 * w):
+            iend, jend = min(a + w, n), min(a + 2 * w, n)
+            A, B = cur[a:iend], cur[iend:jend]
+            for s in range(0, jend - a, chunk):
+                x = _merge_path(A, len(A), B, len(B), s)
+                jobs.append((a + x, iend, iend + s - x, jend, a + s, min(a + s + chunk, jend)))
+        dst = cur.copy()
+        for b0 in range(0, len(jobs), warp):
+            g = np.zeros(2 * 1024 + 6 * 64, np.int32)
+            g[:1024] = cur
+            g[1024:2048] = dst
+            for t, (i, ie, j, je, k, ke) in enumerate(jobs[b0:b0 + warp]):
+                for f, v in enumerate((i, j, k, ie, je, ke)):
+                    g[2048 + 64 * f + t] = v
+            r, st = mod.run_to_fixpoint(warp, np.zeros(0, np.int32), g, np.zeros(0, np.int32), unit_latency=True)
+            rounds += r
+            stats += st
+            dst = g[1024:2048].copy()
+        cur = dst
+        w *= 2
+    return cur[:n].copy(), stats, rounds
+
+
+def merge_sort_fixtures(ref: Reference) -> dict:
+    text = open(MS_IR).read()
+    mod = ref.load_text(text, 0)
+    meld = ref.load_text(text, 1)
+    out = {"ir": "paper_2107_05681_b200/ir/merge_step.ir", "melds": meld.layout["melds"], "cases": []}
+    rng = np.random.Generator(np.random.MT19937(17))
+    for n in (1, 2, 3, 17, 64, 100, 256, 777, 1024):
+        for dup in (False, True):
+            lo, hi = (-8, 9) if dup else (-(2 ** 31), 2 ** 31)
+            keys = rng.integers(lo, hi, size=n, dtype=np.int64).astype(np.int32)
+            a, st_u, _ = merge_chain(mod, keys)
+            b, st_m, _ = merge_chain(meld, keys)
+            assert (a == b).all() and (a == np.sort(keys)).all(), (n, dup)
+            out["cases"].append({"n": n, "keys": keys.tolist(), "sorted": a.tolist(),
+                                 "stats_unit_latency": {"unmelded": st_u.tolist(), "melded": st_m.tolist()}})
+    return out
+
+
 NQ_IR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                      "paper_2107_05681_b200", "ir", "nqueens_sym.ir")
 
@@ -228,6 +297,8 @@ def main():
             json.dump(corpus_fixtures(ref, name), f, separators=(",", ":"))
     with open(os.path.join(OUT, "bitonic_sort.json"), "w") as f:
         json.dump(bitonic_sort_fixtures(ref), f, separators=(",", ":"))
+    with open(os.path.join(OUT, "merge_sort.json"), "w") as f:
+        json.dump(merge_sort_fixtures(ref), f, separators=(",", ":"))
     with open(os.path.join(OUT, "oddeven_sort.json"), "w") as f:
         json.dump(oddeven_sort_fixtures(ref), f, separators=(",", ":"))
     with open(os.path.join(OUT, "nqueens_chain.json"), "w") as f:

@@ -59,6 +59,7 @@ class Restatement:
                                            ctypes.c_int64, I32P, ctypes.c_int64, I32P, I32P]
         L.oracle_bitonic_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
         L.oracle_oddeven_sort.argtypes = [I32P, ctypes.c_int64, ctypes.c_int]
+        L.oracle_merge_sort.argtypes = [I32P, ctypes.c_int64]
         L.oracle_lud.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int]
         L.oracle_srad.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                   ctypes.c_float, I32P, ctypes.c_int]
@@ -102,6 +103,11 @@ class Restatement:
         rc = self.lib.oracle_bitonic_sort(_p(keys), keys.size, bucket)
         if rc:
             raise ValueError("oracle_bitonic_sort: bad bucket")
+
+    def merge_sort(self, keys: np.ndarray) -> None:
+        rc = self.lib.oracle_merge_sort(_p(keys), keys.size)
+        if rc:
+            raise ValueError("oracle_merge_sort failed")
 
     def oddeven_sort(self, keys: np.ndarray, bucket: int) -> None:
         rc = self.lib.oracle_oddeven_sort(_p(keys), keys.size, bucket)

@@ -51,6 +51,7 @@ ABI_SYMBOLS = (
     "darm_gpu_bitonic_sort",
     "darm_gpu_bitonic_sort_ex",
     "darm_gpu_oddeven_sort",
+    "darm_gpu_merge_sort",
     "darm_gpu_nqueens",
     "darm_gpu_nqueens_prefix_count",
     "darm_gpu_lud",
@@ -126,6 +127,9 @@ def lib() -> ctypes.CDLL:
             ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.c_void_p, ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
         L.darm_gpu_oddeven_sort.argtypes = L.darm_gpu_bitonic_sort_ex.argtypes
+        L.darm_gpu_merge_sort.argtypes = [
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(Stats),
+            ctypes.c_char_p, ctypes.c_size_t]
         L.darm_gpu_nqueens.argtypes = [
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int64,
@@ -370,6 +374,26 @@ def oddeven_sort(keys, bucket: int, variant=MELDED, stream=None, want_stats: boo
     arguments as :func:`bitonic_sort`."""
     return _network_sort(lib().darm_gpu_oddeven_sort, keys, bucket, variant, stream, want_stats, prepare_only,
                          keys_per_thread)
+
+
+def merge_sort(keys, variant=MELDED, stream=None, want_stats: bool = True, prepare_only: bool = False):
+    """MS: bottom-up merge sort of the whole of ``keys`` (int32, numpy HOST or
+    torch CUDA), in place, by the merge loop of ir/merge_step.ir
+    (``darm_gpu_merge_sort``)."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant]
+    if _is_torch_cuda(keys):
+        import torch
+
+        ptr, n, mem = keys.data_ptr(), keys.numel(), 1
+        if stream is None:
+            stream = torch.cuda.current_stream(keys.device).cuda_stream
+    else:
+        assert keys.dtype == np.int32 and keys.flags["C_CONTIGUOUS"]
+        ptr, n, mem = keys.ctypes.data, keys.size, 0
+    call = PreparedCall(lib().darm_gpu_merge_sort, (int(variant), ctypes.c_void_p(ptr), int(n), mem,
+                                                    ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
+    return call if prepare_only else call()
 
 
 def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int = 1,

@@ -43,6 +43,10 @@ cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucke
 cudaError_t launch_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread,
                                 cudaStream_t s, int *launches);
 
+// merge_sort.cu (MS): bottom-up merge sort of keys[0..n) (tmp: n-key scratch)
+cudaError_t record_merge_sort(int variant, int32_t *keys, int32_t *tmp, int64_t n, cudaStream_t s, int *launches);
+int merge_sort_passes(int64_t n);   // global passes over the array, incl. the tile pass
+
 // nqueens.cu
 cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, int n, int base,
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,

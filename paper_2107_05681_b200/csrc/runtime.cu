@@ -526,6 +526,49 @@ int darm_gpu_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket, int
                       errlen);
 }
 
+int darm_gpu_merge_sort(int variant, int32_t *keys, int64_t n, int mem, void *stream, darm_gpu_stats *stats,
+                        char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if (n < 0 || n >= (int64_t(1) << 30)) user_error("n must be in [0, 2^30)");
+    if (n && !keys) user_error("keys is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    DeviceState &st = device_state(nullptr);
+    std::lock_guard<std::mutex> lk(st.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t bytes = size_t(n) * 4;
+    Timeline tl(s, stats != nullptr);
+    tl.mark(0);
+    int32_t *dk = keys;
+    if (mem == DARM_MEM_HOST) {
+      dk = static_cast<int32_t *>(slot(st, 0, bytes));
+      if (bytes) DARM_CUDA(cudaMemcpyAsync(dk, keys, bytes, cudaMemcpyHostToDevice, s));
+    }
+    auto *tmp = static_cast<int32_t *>(slot(st, 8, bytes));
+    int launches = 0;
+    tl.mark(1);
+    if (n > 1) {
+      GraphEntry &g = cached_graph(st, 2, variant, dk, n, [&](cudaStream_t cs, int *l) {
+        return record_merge_sort(variant, dk, tmp, n, cs, l);
+      });
+      DARM_CUDA(cudaGraphLaunch(g.exec, s));
+      launches = g.launches;
+    }
+    tl.mark(2);
+    if (mem == DARM_MEM_HOST && bytes) DARM_CUDA(cudaMemcpyAsync(keys, dk, bytes, cudaMemcpyDeviceToHost, s));
+    tl.mark(3);
+    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+      tl.fill(stats);
+      stats->launches = launches;
+      stats->h2d_bytes = mem == DARM_MEM_HOST ? bytes : 0;
+      stats->d2h_bytes = mem == DARM_MEM_HOST ? bytes : 0;
+      stats->algorithmic_bytes = uint64_t(merge_sort_passes(n)) * 2 * bytes;
+    }
+  });
+}
+
 // N-Queens prefixes: every valid placement of the first `base` rows, lowest
 // free column first; prefix i goes to rank i % world.
 static void nqueens_prefixes(int n, int base, int rank, int world, std::vector<uint32_t> &out) {

@@ -38,6 +38,15 @@ def main(which, bucket=64):
         for v in (darm.UNMELDED, darm.MELDED):
             assert darm.nqueens(16, 6, v, want_stats=False)[0] == 14772512
         return
+    if which == "merge":
+        n = bucket if bucket > 64 else 1 << 24
+        g = torch.Generator(device="cuda").manual_seed(9)
+        pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+        for v in (darm.UNMELDED, darm.MELDED):
+            k = pristine.clone()
+            darm.merge_sort(k, v, want_stats=False)
+        torch.cuda.synchronize()
+        return
     if which == "oddeven":
         n = 1 << 24
         g = torch.Generator(device="cuda").manual_seed(1234)
