@@ -66,33 +66,69 @@ def ncu_kernel_summary(stem, pattern):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region.
+
+    NVML (nvidia-ml-py) is polled every 0.5 ms from a thread, so even a
+    few-millisecond timed region yields samples; nvidia-smi (100 ms) is the
+    fallback when NVML is unavailable."""
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.samples = []
+        self.samples = []          # (sm_mhz, max_mhz, set of reason names)
+        self.stop = threading.Event()
+        self.thread = None
         self.proc = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(sm), float(mx), {n for n, b in bits.items() if r & b}))
+                    except Exception:
+                        pass
+                    time.sleep(0.0005)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            pass
+        try:
+            fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={fields}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+            def read():
+                for line in self.proc.stdout:
+                    p = [x.strip() for x in line.split(",")]
+                    if len(p) == 6 and p[0].replace(".", "").isdigit():
+                        self.samples.append((float(p[0]), float(p[1]),
+                                             {n for n, v in zip(self.NAMES, p[2:]) if v.lower() == "active"}))
+
+            self.thread = threading.Thread(target=read, daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.samples.append(parts)
-
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
@@ -100,16 +136,16 @@ class ClockSampler:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(set().union(*(s[2] for s in self.samples))),
+                "samples": len(self.samples)}
 
 
 # ------------------------------------------------------------------ timing
@@ -269,6 +305,41 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
     row["melded_nodes_per_s"] = NQ_NODES_16 / (row["melded_us"] * 1e-6)
     row["prefix_rows"] = 7
     out["nqueens16"] = row
+    # PCM (Batcher odd-even merge sort of 64-key buckets, 2^24 keys) and MS (bottom-up
+    # merge sort of 2^20 keys, the paper's input size)
+    n = 1 << 24
+    g = torch.Generator(device="cuda").manual_seed(6)
+    pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+    work = torch.empty_like(pristine)
+    want = torch.sort(pristine.view(-1, 64), dim=1).values.view(-1)
+    for name, kpt in (("pcm", 0), ("pcm_1key", 1)):
+        row = {}
+        for vname, v in (("unmelded", 0), ("melded", 1)):
+            call = darm.oddeven_sort(work, 64, v, stream=stream.cuda_stream, want_stats=False, prepare_only=True,
+                                     keys_per_thread=kpt)
+            t = time_steps(torch, stream, lambda: work.copy_(pristine), call, steps, warmup, flush)
+            if not torch.equal(work, want):
+                raise SystemExit(f"{name} {vname}: result is not the bucket-sorted input")
+            row[vname + "_us"] = 1e3 * sum(t) / len(t)
+        row["speedup"] = row["unmelded_us"] / row["melded_us"]
+        row["keys_per_thread"] = kpt or 16
+        row["melded_GBps"] = 8.0 * n / (row["melded_us"] * 1e-6) / 1e9
+        row["melded_frac_hbm"] = row["melded_GBps"] / peak
+        out[name] = row
+    n = 1 << 20
+    keys = pristine[:n].clone()
+    ms = torch.empty_like(keys)
+    want = torch.sort(keys).values
+    row = {}
+    for vname, v in (("unmelded", 0), ("melded", 1)):
+        call = darm.merge_sort(ms, v, stream=stream.cuda_stream, want_stats=False, prepare_only=True)
+        t = time_steps(torch, stream, lambda: ms.copy_(keys), call, steps, warmup, flush)
+        if not torch.equal(ms, want):
+            raise SystemExit(f"ms {vname}: result is not sorted")
+        row[vname + "_us"] = 1e3 * sum(t) / len(t)
+    row["speedup"] = row["unmelded_us"] / row["melded_us"]
+    row["melded_keys_per_s"] = n / (row["melded_us"] * 1e-6)
+    out["ms1m"] = row
     # LUD 8192^2 fp32 (config 4): the whole decomposition (3 x 512 launches in one graph)
     n = 8192
     g = torch.Generator(device="cuda").manual_seed(4)
