@@ -270,11 +270,21 @@ CORPUS_LANE = ["sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "nest
 NQ_NODES_16 = 1141190303  # search nodes of the N=16 tree incl. root (tests pin it for small n)
 
 
-def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
+def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None, rank=0, world=1):
     """Melded vs unmelded device time for every corpus kernel (config 1 shape:
-    2^20 lanes = 32,768 warps of makeRandomInput fixtures, half-warp split) and
-    N-Queens N=16 (config 3)."""
+    2^20 lanes = 32,768 warps of makeRandomInput fixtures, half-warp split),
+    N-Queens N=16 (config 3), PCM, MS, LUD 8192^2 (config 4) and SRAD
+    16384^2 x 100 (config 5).  Every rank runs it: NQU (prefix i on rank
+    i % world) and SRAD (row tiles with halo exchange) are sharded over the
+    ranks (strong scaling); the other kernels run as replicas.  Times are the
+    max over ranks."""
     out = {}
+
+    def tmax(row):
+        for key in [k for k in row if k.endswith("_us")]:
+            row[key] = reduce_max(torch, dist, row[key])
+        return row
+
     nw = 1 << 15
     for k in CORPUS_LANE:
         b = darm.make_random_input(k, 32, nw, 1000)
@@ -288,22 +298,32 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
             t = time_steps(torch, stream, lambda: None, step, steps, warmup, flush)
             row[vname + "_us"] = 1e3 * sum(t) / len(t)
         alg = info["lane_bytes"] * nw * 32
+        tmax(row)
         row["speedup"] = row["unmelded_us"] / row["melded_us"]
         row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
         row["melded_frac_hbm"] = row["melded_GBps"] / peak
         out[k] = row
+    # N-Queens N=16: the 7-row prefixes dealt round-robin over the ranks
     row = {}
     for vname, v in (("unmelded", 0), ("melded", 1)):
         ts = []
         for i in range(warmup + max(3, steps // 4)):
-            sols, _, st = darm.nqueens(16, 7, v, stream=stream.cuda_stream)
-            assert sols == 14772512
+            if dist:
+                dist.barrier()
+            sols, _, st = darm.nqueens(16, 7, v, rank=rank, world=world, stream=stream.cuda_stream)
+            if dist:
+                t = torch.tensor([sols], dtype=torch.int64, device="cuda")
+                dist.all_reduce(t)
+                sols = int(t.item())
+            assert sols == 14772512, sols
             if i >= warmup:
                 ts.append(st["kernel_ms"])
         row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
+    tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_nodes_per_s"] = NQ_NODES_16 / (row["melded_us"] * 1e-6)
     row["prefix_rows"] = 7
+    row["n_gpus"], row["scaling"] = world, "strong (prefixes sharded over the ranks)"
     out["nqueens16"] = row
     # PCM (Batcher odd-even merge sort of 64-key buckets, 2^24 keys) and MS (bottom-up
     # merge sort of 2^20 keys, the paper's input size)
@@ -321,6 +341,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
             if not torch.equal(work, want):
                 raise SystemExit(f"{name} {vname}: result is not the bucket-sorted input")
             row[vname + "_us"] = 1e3 * sum(t) / len(t)
+        tmax(row)
         row["speedup"] = row["unmelded_us"] / row["melded_us"]
         row["keys_per_thread"] = kpt or 16
         row["melded_GBps"] = 8.0 * n / (row["melded_us"] * 1e-6) / 1e9
@@ -337,6 +358,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
         if not torch.equal(ms, want):
             raise SystemExit(f"ms {vname}: result is not sorted")
         row[vname + "_us"] = 1e3 * sum(t) / len(t)
+    tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_keys_per_s"] = n / (row["melded_us"] * 1e-6)
     out["ms1m"] = row
@@ -350,24 +372,48 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak):
         call = darm.lud(a, v, stream=stream.cuda_stream, want_stats=False, prepare_only=True)
         t = time_steps(torch, stream, lambda: a.copy_(a0), call, max(2, steps // 4), min(warmup, 3), flush)
         row[vname + "_us"] = 1e3 * sum(t) / len(t)
+    tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_TFLOPs"] = (2.0 / 3.0) * n ** 3 / (row["melded_us"] * 1e-6) / 1e12
     out["lud8192"] = row
-    # SRAD 16384^2 fp32 x 100 iterations (config 5, one GPU)
+    # SRAD 16384^2 fp32 x 100 iterations (config 5): one GPU, or row tiles with a
+    # halo exchange and the ROI all-reduce every iteration over NCCL
     n, iters = 16384, 100
     j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
-    j = torch.empty_like(j0)
     row = {}
-    for vname, v in (("unmelded", 0), ("melded", 1)):
-        call = darm.srad(j, iters, 0.5, darm.RODINIA_ROI, v, stream=stream.cuda_stream, want_stats=False,
-                         prepare_only=True)
-        t = time_steps(torch, stream, lambda: j.copy_(j0), call, 2, 1, flush)
-        row[vname + "_us"] = 1e3 * sum(t) / len(t)
+    if world == 1:
+        j = torch.empty_like(j0)
+        for vname, v in (("unmelded", 0), ("melded", 1)):
+            call = darm.srad(j, iters, 0.5, darm.RODINIA_ROI, v, stream=stream.cuda_stream, want_stats=False,
+                             prepare_only=True)
+            t = time_steps(torch, stream, lambda: j.copy_(j0), call, 2, 1, flush)
+            row[vname + "_us"] = 1e3 * sum(t) / len(t)
+    else:
+        from paper_2107_05681_b200.srad_tiles import SradTiles
+
+        for vname, v in (("unmelded", 0), ("melded", 1)):
+            tiles = SradTiles(n, n, 0.5, darm.RODINIA_ROI, dist=dist, device=torch.device("cuda"), variant=v)
+            ts = []
+            for rep in range(2):
+                tiles.load(j0)
+                torch.cuda.synchronize()
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                tiles.run(iters)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if rep:
+                    ts.append(e0.elapsed_time(e1))
+            row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
+            del tiles
+    tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     # minimal traffic 8 B/px/iteration (one read of J, one write of J') + the in/out copies of the call
     alg = 8.0 * n * n * iters + 8.0 * n * n
     row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
-    row["melded_frac_hbm"] = row["melded_GBps"] / peak
+    row["melded_frac_hbm"] = row["melded_GBps"] / (peak * world)
+    row["n_gpus"], row["scaling"] = world, "strong (row tiles, NCCL halo exchange)" if world > 1 else "single GPU"
     out["srad16384x100"] = row
     return out
 
@@ -429,6 +475,28 @@ def our_arm(args):
         raise SystemExit("bitonic e2e: result is not the bucket-sorted input")
     e2e_total = reduce_max(torch, dist, sum(e2e_ms))
 
+    kpt = args.keys_per_thread or 16
+    per_kernel = None
+    if not args.no_per_kernel:
+        peak0, _ = measured_peaks()
+        per_kernel = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak0, dist, rank, world)
+        per_kernel["bitonic"] = {"unmelded_us": 1e3 * results["unmelded"]["kernel_ms_mean"],
+                                 "melded_us": 1e3 * results["melded"]["kernel_ms_mean"],
+                                 "speedup": results["unmelded"]["total_ms"] / results["melded"]["total_ms"],
+                                 "keys_per_thread": kpt}
+        # the IR warp shape: one key (one IR lane) per hardware thread
+        row = {}
+        for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
+            step = darm.bitonic_sort(work, B, variant, stream=stream.cuda_stream, want_stats=False,
+                                     prepare_only=True, keys_per_thread=1)
+            t = time_steps(torch, stream, lambda: work.copy_(pristine), step, args.steps, args.warmup, flush)
+            if not torch.equal(work, want):
+                raise SystemExit(f"bitonic one-key {vname}: result is not the bucket-sorted input")
+            row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(t) / len(t))
+        row["speedup"] = row["unmelded_us"] / row["melded_us"]
+        row["keys_per_thread"] = 1
+        per_kernel["bitonic_1key"] = row
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -438,7 +506,6 @@ def our_arm(args):
     peak, peak_src = measured_peaks()
     alg_bytes = 8 * n
     achieved = alg_bytes / (mel["kernel_ms_mean"] / 1e3) / 1e9
-    kpt = args.keys_per_thread or 16
     kname = "bitonic_sort_reg_kernel<{}, %d, %d" % (B, kpt) if kpt > 1 else "bitonic_sort_kernel<{}, %d" % B
     prof_m, prof_src = ncu_kernel_summary("bitonic", kname.format(1))
     prof_u, _ = ncu_kernel_summary("bitonic", kname.format(0))
@@ -476,24 +543,8 @@ def our_arm(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
-    if not args.no_per_kernel:
-        line["per_kernel"] = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak)
-        line["per_kernel"]["bitonic"] = {"unmelded_us": 1e3 * unm["kernel_ms_mean"],
-                                         "melded_us": 1e3 * mel["kernel_ms_mean"],
-                                         "speedup": unm["total_ms"] / mel["total_ms"],
-                                         "keys_per_thread": kpt}
-        # the IR warp shape: one key (one IR lane) per hardware thread
-        row = {}
-        for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
-            step = darm.bitonic_sort(work, B, variant, stream=stream.cuda_stream, want_stats=False,
-                                     prepare_only=True, keys_per_thread=1)
-            t = time_steps(torch, stream, lambda: work.copy_(pristine), step, args.steps, args.warmup, flush)
-            if not torch.equal(work, want):
-                raise SystemExit(f"bitonic one-key {vname}: result is not the bucket-sorted input")
-            row[vname + "_us"] = 1e3 * sum(t) / len(t)
-        row["speedup"] = row["unmelded_us"] / row["melded_us"]
-        row["keys_per_thread"] = 1
-        line["per_kernel"]["bitonic_1key"] = row
+    if per_kernel is not None:
+        line["per_kernel"] = per_kernel
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
