@@ -227,6 +227,53 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out,
                             float *q0_scratch, void *stream, char *err,
                             size_t errlen);
 
+/* ---- GPU executeWarp for arbitrary mini-IR -------
+ * executeWarp (include/darm/interp.hpp:57-58, src/interp.cpp:332-381) for a
+ * batch of warps of ANY function in the reference's textual IR (SPEC.md:
+ * 111-121): the library parses and lowers the first function of `ir_text`
+ * (its own reader; the reference's pass output prints in the same grammar),
+ * one CUDA warp interprets one IR warp, and every result field equals the
+ * reference interpreter's: per-lane returns, final global / shared memory,
+ * fault counts, and the WarpExecStats counters (latencies: the reference's
+ * defaults, ir.cpp:235-244, or `latency`, 28 entries in the opcode order of
+ * ir.hpp:17-46).  Limits: 160 values per function, 16 phis per block, SIMT
+ * stack depth 48.
+ *
+ * Buffers (HOST or DEVICE per `mem`):
+ *   args     n_params x acount, acount = 1 (broadcast), n_warps or n_warps*warp
+ *   globals  n_warps x global_words (in/out): warp w's globals in declaration
+ *            order (darm_gpu_program_memory gives each array's offset / size)
+ *   shared   n_warps x shared_words (in/out; NULL: zero-initialised scratch)
+ *   returns / ret_valid  n_warps x warp (may be NULL): a lane's return value
+ *            and whether it returned one (WarpResult::returns)
+ *   faults   n_warps (may be NULL): faulted lanes (WarpResult::faults.size())
+ *   stats    n_warps x 8 int64 (may be NULL): issuedInstructions, threadCycles,
+ *            usefulThreadCycles, serializedCycles, divergentBranchCount,
+ *            sharedMemIssues, globalMemIssues, flags (bit 0 nonTerminated,
+ *            bit 1 taintedObservable)
+ * max_steps <= 0 means executeWarp's default budget (10^7 issues).
+ * Returns 2 for malformed IR and for the reference's execution errors (a phi
+ * without an incoming for the lane's predecessor, a divergent branch without
+ * a reconvergence point). */
+typedef struct darm_gpu_program darm_gpu_program;
+int darm_gpu_program_load(const char *ir_text, const int64_t *latency,
+                          darm_gpu_program **out, char *err, size_t errlen);
+void darm_gpu_program_free(darm_gpu_program *program);
+int darm_gpu_program_shape(const darm_gpu_program *program, int *n_params,
+                           int *n_globals, int *n_shared, int64_t *global_words,
+                           int64_t *shared_words);
+/* memory `index` (globals, then shared arrays): name, or NULL past the end */
+const char *darm_gpu_program_memory(const darm_gpu_program *program, int index,
+                                    int64_t *size, int64_t *offset, int *is_shared);
+const char *darm_gpu_program_param(const darm_gpu_program *program, int index);
+int darm_gpu_program_execute(darm_gpu_program *program, int warp, int64_t n_warps,
+                             const int32_t *args, int64_t acount,
+                             int32_t *globals, int32_t *shared,
+                             int32_t *returns, uint8_t *ret_valid,
+                             int32_t *faults, int64_t *stats_out,
+                             int64_t max_steps, int mem, void *stream,
+                             darm_gpu_stats *stats, char *err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

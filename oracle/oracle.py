@@ -242,6 +242,30 @@ def _chain_sort(self, keys: np.ndarray, bucket: int, schedule: np.ndarray, threa
 RefModule.chain_sort = _chain_sort
 
 
+def _execute_program(self, warp, n_warps, args, globals_, shared=None, latency=None, max_steps=10_000_000,
+                     threads=1):
+    """executeWarp per warp in the GPU program layout (globals / shared in/out,
+    n_warps x words); -> (returns, has_ret, faults, stats[n_warps, 8])."""
+    args = np.ascontiguousarray(args, dtype=np.int32)
+    acount = args.shape[-1] if args.size else 1
+    rets = np.zeros(max(1, n_warps * warp), np.int32)
+    has = np.zeros(max(1, n_warps * warp), np.uint8)
+    faults = np.zeros(max(1, n_warps), np.int32)
+    stats = np.zeros((max(1, n_warps), 8), np.int64)
+    lat = None if latency is None else np.ascontiguousarray(latency, dtype=np.int64)
+    err = ctypes.create_string_buffer(512)
+    rc = self.ref.lib.ref_execute_program(self.h, warp, n_warps, _p(args), acount, _p(globals_), _p(shared),
+                                          _p(lat, I64P), max_steps, threads, _p(rets), _p(has, U8P), _p(faults),
+                                          _p(stats, I64P), err, 512)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return (rets[:n_warps * warp].reshape(n_warps, warp), has[:n_warps * warp].reshape(n_warps, warp),
+            faults[:n_warps], stats[:n_warps])
+
+
+RefModule.execute_program = _execute_program
+
+
 def _run_to_fixpoint(self, warp, args, globals_full, shared_full, max_rounds=1_000_000, unit_latency=False):
     """executeWarp chained to a fixpoint on one warp (declared-size arrays, in/out)."""
     args = np.ascontiguousarray(args, dtype=np.int32)
@@ -285,6 +309,9 @@ class Reference:
                                        I64P, ctypes.c_char_p, ctypes.c_size_t]
         L.ref_run_to_fixpoint.argtypes = [vp, ctypes.c_int, I32P, I32P, I32P, ctypes.c_int64, ctypes.c_int,
                                           I64P, I64P, ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_execute_program.argtypes = [vp, ctypes.c_int, ctypes.c_int64, I32P, ctypes.c_int64, I32P, I32P, I64P,
+                                          ctypes.c_int64, ctypes.c_int, I32P, U8P, I32P, I64P, ctypes.c_char_p,
+                                          ctypes.c_size_t]
         L.ref_chain_sort.argtypes = [vp, I32P, ctypes.c_int64, ctypes.c_int, I32P, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, I64P, ctypes.c_char_p, ctypes.c_size_t]
         self.lib = L

@@ -496,4 +496,93 @@ int ref_chain_sort(const ref_module *h, int32_t *keys, int64_t n, int B, const i
   return 0;
 }
 
+// executeWarp over a batch in the GPU program layout (darm_gpu_program_execute):
+// globals n_warps x (all globals, declaration order), shared n_warps x (all
+// shared arrays) in/out (NULL: zero init, not returned), returns / has_ret
+// n_warps x warp, faults n_warps, stats n_warps x 8 (ref_execute_warps' slots).
+// latency: 28 entries in opcode order, or NULL for the defaults.
+int ref_execute_program(const ref_module *h, int warp, int64_t n_warps, const int32_t *args, int64_t acount,
+                        int32_t *globals, int32_t *shared, const int64_t *latency, int64_t max_steps,
+                        int threads, int32_t *returns, uint8_t *has_ret, int32_t *faults, int64_t *stats,
+                        char *err, size_t errlen) {
+  const Function &f = h->m.functions.front();
+  const size_t np = f.params.size();
+  if (np && acount != 1 && acount != n_warps && acount != n_warps * warp)
+    return fail(err, errlen, "bad argument count", 2);
+  LatencyModel lm = LatencyModel::defaults();
+  if (latency)
+    for (int k = 0; k <= int(Opcode::Barrier); ++k) lm.set(Opcode(k), latency[k]);
+  int64_t gw = 0, sw = 0;
+  for (const auto &g : h->m.globals) gw += g.size;
+  for (const auto &s : f.sharedDecls) sw += s.size;
+  std::vector<std::string> errors(1);
+  std::atomic<bool> bad{false};
+  parallelFor(n_warps, threads, [&](int64_t w) {
+    if (bad.load()) return;
+    try {
+      WarpInput in;
+      in.warpSize = warp;
+      for (size_t p = 0; p < np; ++p) {
+        const int32_t *a = args + p * acount;
+        if (acount == 1)
+          in.args.push_back({a[0]});
+        else if (acount == n_warps)
+          in.args.push_back({a[w]});
+        else
+          in.args.push_back(std::vector<int32_t>(a + w * warp, a + (w + 1) * warp));
+      }
+      int64_t off = 0;
+      for (const auto &g : h->m.globals) {
+        const int32_t *src = globals + w * gw + off;
+        in.globalInit[g.name] = std::vector<int32_t>(src, src + g.size);
+        off += g.size;
+      }
+      off = 0;
+      for (const auto &s : f.sharedDecls) {
+        if (shared) {
+          const int32_t *src = shared + w * sw + off;
+          in.sharedInit[s.name] = std::vector<int32_t>(src, src + s.size);
+        }
+        off += s.size;
+      }
+      WarpResult r = executeWarp(h->m, f, in, lm, max_steps);
+      off = 0;
+      for (const auto &g : h->m.globals) {
+        const auto &v = r.globalFinal.at(g.name);
+        std::memcpy(globals + w * gw + off, v.data(), size_t(g.size) * 4);
+        off += g.size;
+      }
+      off = 0;
+      for (const auto &s : f.sharedDecls) {
+        if (shared) {
+          const auto &v = r.sharedFinal.at(s.name);
+          std::memcpy(shared + w * sw + off, v.data(), size_t(s.size) * 4);
+        }
+        off += s.size;
+      }
+      if (returns)
+        for (int l = 0; l < warp; ++l) {
+          returns[w * warp + l] = r.returns[l].value_or(0);
+          if (has_ret) has_ret[w * warp + l] = r.returns[l].has_value();
+        }
+      if (faults) faults[w] = int32_t(r.faults.size());
+      if (stats) {
+        int64_t *o = stats + w * 8;
+        o[0] = r.stats.issuedInstructions;
+        o[1] = r.stats.threadCycles;
+        o[2] = r.stats.usefulThreadCycles;
+        o[3] = r.stats.serializedCycles;
+        o[4] = r.stats.divergentBranchCount;
+        o[5] = r.stats.sharedMemIssues;
+        o[6] = r.stats.globalMemIssues;
+        o[7] = (r.nonTerminated ? 1 : 0) | (r.taintedObservable ? 2 : 0);
+      }
+    } catch (const std::exception &e) {
+      if (!bad.exchange(true)) errors[0] = e.what();
+    }
+  });
+  if (bad) return fail(err, errlen, errors[0], 2);
+  return 0;
+}
+
 }  // extern "C"

@@ -59,6 +59,12 @@ ABI_SYMBOLS = (
     "darm_gpu_srad_roi_words",
     "darm_gpu_srad_tile_roi",
     "darm_gpu_srad_tile_step",
+    "darm_gpu_program_load",
+    "darm_gpu_program_free",
+    "darm_gpu_program_shape",
+    "darm_gpu_program_memory",
+    "darm_gpu_program_param",
+    "darm_gpu_program_execute",
 )
 
 
@@ -127,6 +133,21 @@ def lib() -> ctypes.CDLL:
             ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.c_void_p, ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
         L.darm_gpu_oddeven_sort.argtypes = L.darm_gpu_bitonic_sort_ex.argtypes
+        vp = ctypes.c_void_p
+        L.darm_gpu_program_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(vp),
+                                            ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_program_free.argtypes = [vp]
+        L.darm_gpu_program_free.restype = None
+        L.darm_gpu_program_shape.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 3 + \
+            [ctypes.POINTER(ctypes.c_int64)] * 2
+        L.darm_gpu_program_memory.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]
+        L.darm_gpu_program_memory.restype = ctypes.c_char_p
+        L.darm_gpu_program_param.argtypes = [vp, ctypes.c_int]
+        L.darm_gpu_program_param.restype = ctypes.c_char_p
+        L.darm_gpu_program_execute.argtypes = [vp, ctypes.c_int, ctypes.c_int64, vp, ctypes.c_int64, vp, vp, vp, vp,
+                                               vp, vp, ctypes.c_int64, ctypes.c_int, vp, ctypes.POINTER(Stats),
+                                               ctypes.c_char_p, ctypes.c_size_t]
         L.darm_gpu_merge_sort.argtypes = [
             ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(Stats),
             ctypes.c_char_p, ctypes.c_size_t]
@@ -394,6 +415,108 @@ def merge_sort(keys, variant=MELDED, stream=None, want_stats: bool = True, prepa
     call = PreparedCall(lib().darm_gpu_merge_sort, (int(variant), ctypes.c_void_p(ptr), int(n), mem,
                                                     ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
     return call if prepare_only else call()
+
+
+@dataclass
+class ProgramResult:
+    """WarpResult fields for a batch (interp.hpp:41-53): ``returns`` /
+    ``ret_valid`` [n_warps, warp], ``globals`` / ``shared`` [n_warps, words]
+    (final memories), ``faults`` [n_warps], ``stats`` [n_warps, 8] in the
+    order issuedInstructions, threadCycles, usefulThreadCycles,
+    serializedCycles, divergentBranchCount, sharedMemIssues, globalMemIssues,
+    flags (bit 0 nonTerminated, bit 1 taintedObservable)."""
+    returns: object
+    ret_valid: object
+    globals: object
+    shared: object
+    faults: object
+    stats: object
+    call_stats: dict = field(default_factory=dict)
+
+    @property
+    def utilization(self):
+        thread, useful = self.stats[:, 1], self.stats[:, 2]
+        return np.where(thread == 0, 1.0, useful / np.maximum(thread, 1))
+
+
+class Program:
+    """A mini-IR function (the reference's textual IR) loaded
+    into the GPU warp interpreter: :meth:`execute_warps` is executeWarp
+    (interp.hpp:57-58) for a batch of warps of ANY function, results equal to
+    the reference interpreter's (``darm_gpu_program_*``)."""
+
+    def __init__(self, ir_text: str, latency: Optional[Sequence[int]] = None):
+        err = ctypes.create_string_buffer(512)
+        h = ctypes.c_void_p()
+        lat = None
+        if latency is not None:
+            lat = (ctypes.c_int64 * 28)(*[int(x) for x in latency])
+        _check(lib().darm_gpu_program_load(ir_text.encode(), lat, ctypes.byref(h), err, 512), err)
+        self.h = h
+        np_, ng, ns = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        gw, sw = ctypes.c_int64(), ctypes.c_int64()
+        lib().darm_gpu_program_shape(h, ctypes.byref(np_), ctypes.byref(ng), ctypes.byref(ns), ctypes.byref(gw),
+                                     ctypes.byref(sw))
+        self.params = [lib().darm_gpu_program_param(h, i).decode() for i in range(np_.value)]
+        self.memories = []   # (name, size, offset, is_shared) — globals, then shared arrays
+        for i in range(ng.value + ns.value):
+            size, off, sh = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+            name = lib().darm_gpu_program_memory(h, i, ctypes.byref(size), ctypes.byref(off), ctypes.byref(sh))
+            self.memories.append((name.decode(), size.value, off.value, bool(sh.value)))
+        self.global_words, self.shared_words = gw.value, sw.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().darm_gpu_program_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def execute_warps(self, warp: int, args, globals_, shared=None, max_steps: int = 0, stream=None,
+                      want_stats: bool = True, n_warps: Optional[int] = None) -> ProgramResult:
+        """``args``: [n_params, acount] (acount 1, n_warps or n_warps*warp);
+        ``globals_``: [n_warps, global_words] int32, updated in place;
+        ``shared``: [n_warps, shared_words] or None (zeros); ``n_warps``
+        defaults to ``globals_.shape[0]``.  numpy arrays run through HOST
+        buffers, torch CUDA tensors in place (DEVICE)."""
+        dev = _is_torch_cuda(globals_)
+        if n_warps is None:
+            n_warps = int(globals_.shape[0])
+        if dev:
+            import torch
+
+            ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+            args_t = torch.as_tensor(np.asarray(args, np.int32) if not _is_torch_cuda(args) else args,
+                                     device=globals_.device).to(torch.int32).contiguous()
+            rets = torch.zeros((n_warps, warp), dtype=torch.int32, device=globals_.device)
+            valid = torch.zeros((n_warps, warp), dtype=torch.uint8, device=globals_.device)
+            faults = torch.zeros(n_warps, dtype=torch.int32, device=globals_.device)
+            stats = torch.zeros((n_warps, 8), dtype=torch.int64, device=globals_.device)
+            if stream is None:
+                stream = torch.cuda.current_stream(globals_.device).cuda_stream
+            mem, keep = 1, (args_t,)
+            a_ptr = ptr(args_t)
+            acount = args_t.shape[-1] if args_t.numel() else 1
+        else:
+            args_n = np.ascontiguousarray(args, dtype=np.int32)
+            rets = np.zeros((n_warps, warp), np.int32)
+            valid = np.zeros((n_warps, warp), np.uint8)
+            faults = np.zeros(n_warps, np.int32)
+            stats = np.zeros((n_warps, 8), np.int64)
+            ptr = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else None  # noqa: E731
+            mem, keep = 0, (args_n,)
+            a_ptr = ptr(args_n) if args_n.size else None
+            acount = args_n.shape[-1] if args_n.size else 1
+        st = Stats()
+        err = ctypes.create_string_buffer(512)
+        rc = lib().darm_gpu_program_execute(self.h, warp, n_warps, a_ptr, acount, ptr(globals_), ptr(shared),
+                                            ptr(rets), ptr(valid), ptr(faults), ptr(stats), int(max_steps), mem,
+                                            ctypes.c_void_p(stream or 0), ctypes.byref(st) if want_stats else None,
+                                            err, 512)
+        del keep
+        _check(rc, err)
+        return ProgramResult(rets, valid, globals_, shared, faults, stats, st.as_dict() if want_stats else {})
 
 
 def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int = 1,

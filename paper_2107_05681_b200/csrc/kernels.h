@@ -47,6 +47,33 @@ cudaError_t launch_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucke
 cudaError_t record_merge_sort(int variant, int32_t *keys, int32_t *tmp, int64_t n, cudaStream_t s, int *launches);
 int merge_sort_passes(int64_t n);   // global passes over the array, incl. the tile pass
 
+// interp.cu: the GPU executeWarp over a lowered mini-IR program (ir_program.h)
+struct InterpLaunch {
+  const void *blocks, *insts, *phis, *phi_ins;   // device copies of the IrProgram arrays
+  const int64_t *mem_off, *mem_size;
+  const uint8_t *mem_shared;
+  int64_t latency[28];
+  int n_params, n_regs, entry, ret_block;
+  int64_t gwords, swords;
+  int W;
+  int64_t n_warps;
+  int am;
+  const int32_t *args;
+  int64_t acount;
+  int32_t *globals, *shared;
+  uint8_t *taint;
+  int32_t *returns;
+  uint8_t *ret_valid;
+  int32_t *faults;
+  int64_t *stats;
+  int32_t *errors;
+  int64_t max_steps;
+  int sms;
+};
+cudaError_t launch_ir_interp(const InterpLaunch &L, cudaStream_t s);
+int ir_interp_max_regs();
+int ir_interp_max_phis();
+
 // nqueens.cu
 cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, int n, int base,
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,

@@ -17,6 +17,7 @@
 
 #include "../../include/darm_gpu.h"
 #include "corpus.cuh"
+#include "ir_program.h"
 #include "kernels.h"
 
 namespace darm_gpu {
@@ -806,6 +807,248 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, 
     if (roi_out) DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double), s));
     DARM_CUDA(launch_srad_sweep(variant, tile_in, tile_out, q0_scratch, roi_out, int(cols), int(tile_rows), int(r0),
                                 int(rows), lambda, R, s));
+  });
+}
+
+
+// ---------------------------------------------------------------- mini-IR programs
+struct darm_gpu_program {
+  darm_gpu::IrProgram prog;
+  int device = -1;
+  void *dev = nullptr;            // one allocation: blocks, insts, phis, phi_ins, mem tables
+  size_t off_insts = 0, off_phis = 0, off_phi_ins = 0, off_mem_off = 0, off_mem_size = 0, off_mem_sh = 0;
+};
+
+int darm_gpu_program_load(const char *ir_text, const int64_t *latency, darm_gpu_program **out, char *err,
+                          size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ir_text || !out) user_error("ir_text / out is NULL");
+    *out = nullptr;
+    auto *p = new darm_gpu_program;
+    try {
+      p->prog = compile_ir(ir_text);
+    } catch (const std::runtime_error &e) {
+      delete p;
+      user_error(e.what());
+    }
+    if (int(p->prog.reg_names.size()) > ir_interp_max_regs()) {
+      delete p;
+      user_error("the GPU interpreter supports at most " + std::to_string(ir_interp_max_regs()) + " values");
+    }
+    for (const auto &b : p->prog.blocks)
+      if (b.n_phi > ir_interp_max_phis()) {
+        delete p;
+        user_error("the GPU interpreter supports at most " + std::to_string(ir_interp_max_phis()) +
+                   " phis per block");
+      }
+    if (latency)
+      for (int k = 0; k < kNumOps; ++k) {
+        if (latency[k] <= 0) {
+          delete p;
+          user_error("latencies must be positive");
+        }
+        p->prog.latency[k] = latency[k];
+      }
+    *out = p;
+  });
+}
+
+void darm_gpu_program_free(darm_gpu_program *p) {
+  if (!p) return;
+  if (p->dev) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    cudaFree(p->dev);
+    cudaSetDevice(cur);
+  }
+  delete p;
+}
+
+int darm_gpu_program_shape(const darm_gpu_program *p, int *n_params, int *n_globals, int *n_shared,
+                           int64_t *global_words, int64_t *shared_words) {
+  if (!p) return DARM_USER_ERROR;
+  if (n_params) *n_params = int(p->prog.params.size());
+  if (n_globals) *n_globals = p->prog.n_globals;
+  if (n_shared) *n_shared = p->prog.n_shared;
+  if (global_words) *global_words = p->prog.global_words;
+  if (shared_words) *shared_words = p->prog.shared_words;
+  return DARM_OK;
+}
+
+const char *darm_gpu_program_memory(const darm_gpu_program *p, int index, int64_t *size, int64_t *offset,
+                                    int *is_shared) {
+  if (!p || index < 0 || index >= int(p->prog.mems.size())) return nullptr;
+  const auto &m = p->prog.mems[size_t(index)];
+  if (size) *size = m.size;
+  if (offset) *offset = m.offset;
+  if (is_shared) *is_shared = m.shared ? 1 : 0;
+  return m.name.c_str();
+}
+
+const char *darm_gpu_program_param(const darm_gpu_program *p, int index) {
+  if (!p || index < 0 || index >= int(p->prog.params.size())) return nullptr;
+  return p->prog.params[size_t(index)].c_str();
+}
+
+int darm_gpu_program_execute(darm_gpu_program *p, int warp, int64_t n_warps, const int32_t *args, int64_t acount,
+                             int32_t *globals, int32_t *shared, int32_t *returns, uint8_t *ret_valid,
+                             int32_t *faults, int64_t *stats_out, int64_t max_steps, int mem, void *stream,
+                             darm_gpu_stats *stats, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!p) user_error("program is NULL");
+    const IrProgram &P = p->prog;
+    if (warp < 1 || warp > 64) user_error("warp size must be in [1, 64]");  // interp.cpp:334-335
+    if (n_warps < 0) user_error("n_warps must be >= 0");
+    const int np = int(P.params.size());
+    int am = 0;
+    if (np) {
+      if (acount == 1) am = 0;
+      else if (acount == n_warps) am = 1;
+      else if (acount == n_warps * warp) am = 2;
+      else user_error("argument count must be 1, n_warps or n_warps*warp");  // interp.cpp:348-350
+      if (!args) user_error("args is NULL");
+    }
+    if (P.global_words && n_warps && !globals) user_error("globals is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    if (max_steps <= 0) max_steps = 10000000;   // executeWarp's default (interp.hpp:57-58)
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    int dev = 0;
+    DARM_CUDA(cudaGetDevice(&dev));
+    DeviceState &st = device_state(nullptr);
+    std::lock_guard<std::mutex> lk(st.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // program arrays on this device (uploaded once)
+    if (!p->dev || p->device != dev) {
+      if (p->dev) {
+        cudaSetDevice(p->device);
+        cudaFree(p->dev);
+        cudaSetDevice(dev);
+      }
+      auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+      size_t o = 0;
+      const size_t ob = o; o = al(o + P.blocks.size() * sizeof(IrBlock));
+      p->off_insts = o; o = al(o + P.insts.size() * sizeof(IrInst));
+      p->off_phis = o; o = al(o + P.phis.size() * sizeof(IrPhi));
+      p->off_phi_ins = o; o = al(o + P.phi_ins.size() * sizeof(IrPhiIn));
+      p->off_mem_off = o; o = al(o + P.mems.size() * 8);
+      p->off_mem_size = o; o = al(o + P.mems.size() * 8);
+      p->off_mem_sh = o; o = al(o + P.mems.size() + 1);
+      std::vector<char> host(o, 0);
+      std::memcpy(host.data() + ob, P.blocks.data(), P.blocks.size() * sizeof(IrBlock));
+      if (!P.insts.empty()) std::memcpy(host.data() + p->off_insts, P.insts.data(), P.insts.size() * sizeof(IrInst));
+      if (!P.phis.empty()) std::memcpy(host.data() + p->off_phis, P.phis.data(), P.phis.size() * sizeof(IrPhi));
+      if (!P.phi_ins.empty())
+        std::memcpy(host.data() + p->off_phi_ins, P.phi_ins.data(), P.phi_ins.size() * sizeof(IrPhiIn));
+      for (size_t m = 0; m < P.mems.size(); ++m) {
+        reinterpret_cast<int64_t *>(host.data() + p->off_mem_off)[m] = P.mems[m].offset;
+        reinterpret_cast<int64_t *>(host.data() + p->off_mem_size)[m] = P.mems[m].size;
+        reinterpret_cast<uint8_t *>(host.data() + p->off_mem_sh)[m] = P.mems[m].shared;
+      }
+      DARM_CUDA(cudaMalloc(&p->dev, o));
+      DARM_CUDA(cudaMemcpy(p->dev, host.data(), o, cudaMemcpyHostToDevice));
+      p->device = dev;
+    }
+    Timeline tl(s, stats != nullptr);
+    tl.mark(0);
+    const int64_t gbytes = n_warps * P.global_words * 4, sbytes = n_warps * P.shared_words * 4;
+    const int64_t acnt = np ? acount : 0;
+    size_t si = 16;   // slots 16.. (the other entry points use the low ones)
+    InterpLaunch L{};
+    char *base = static_cast<char *>(p->dev);
+    L.blocks = base;
+    L.insts = base + p->off_insts;
+    L.phis = base + p->off_phis;
+    L.phi_ins = base + p->off_phi_ins;
+    L.mem_off = reinterpret_cast<const int64_t *>(base + p->off_mem_off);
+    L.mem_size = reinterpret_cast<const int64_t *>(base + p->off_mem_size);
+    L.mem_shared = reinterpret_cast<const uint8_t *>(base + p->off_mem_sh);
+    for (int k = 0; k < kNumOps; ++k) L.latency[k] = P.latency[k];
+    L.n_params = np;
+    L.n_regs = int(P.reg_names.size());
+    L.entry = P.entry;
+    L.ret_block = P.ret_block;
+    L.gwords = P.global_words;
+    L.swords = P.shared_words;
+    L.W = warp;
+    L.n_warps = n_warps;
+    L.am = am;
+    L.acount = acnt;
+    L.max_steps = max_steps;
+    L.sms = st.sms;
+    uint64_t h2d = 0, d2h = 0;
+    auto stage_in = [&](const void *src, size_t bytes) -> void * {
+      void *d = slot(st, si++, bytes ? bytes : 4);
+      if (bytes) DARM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
+      h2d += bytes;
+      return d;
+    };
+    if (mem == DARM_MEM_HOST) {
+      L.args = np ? static_cast<const int32_t *>(stage_in(args, size_t(np) * acnt * 4)) : nullptr;
+      L.globals = static_cast<int32_t *>(stage_in(globals, size_t(gbytes)));
+      if (shared) {
+        L.shared = static_cast<int32_t *>(stage_in(shared, size_t(sbytes)));
+      } else {
+        L.shared = static_cast<int32_t *>(slot(st, si++, sbytes ? size_t(sbytes) : 4));
+        if (sbytes) DARM_CUDA(cudaMemsetAsync(L.shared, 0, size_t(sbytes), s));
+      }
+      L.returns = returns ? static_cast<int32_t *>(slot(st, si++, size_t(n_warps * warp) * 4 + 4)) : nullptr;
+      L.ret_valid = ret_valid ? static_cast<uint8_t *>(slot(st, si++, size_t(n_warps * warp) + 4)) : nullptr;
+      L.faults = faults ? static_cast<int32_t *>(slot(st, si++, size_t(n_warps) * 4 + 4)) : nullptr;
+      L.stats = stats_out ? static_cast<int64_t *>(slot(st, si++, size_t(n_warps) * 64 + 8)) : nullptr;
+    } else {
+      L.args = args;
+      L.globals = globals;
+      if (shared) {
+        L.shared = shared;
+      } else {
+        L.shared = static_cast<int32_t *>(slot(st, si++, sbytes ? size_t(sbytes) : 4));
+        if (sbytes) DARM_CUDA(cudaMemsetAsync(L.shared, 0, size_t(sbytes), s));
+      }
+      L.returns = returns;
+      L.ret_valid = ret_valid;
+      L.faults = faults;
+      L.stats = stats_out;
+    }
+    const size_t tbytes = size_t(n_warps) * size_t(P.global_words + P.shared_words);
+    L.taint = static_cast<uint8_t *>(slot(st, si++, tbytes ? tbytes : 4));
+    if (tbytes) DARM_CUDA(cudaMemsetAsync(L.taint, 0, tbytes, s));   // initial cells are untainted
+    auto *derr = static_cast<int32_t *>(slot(st, si++, size_t(n_warps) * 4 + 4));
+    L.errors = derr;
+    tl.mark(1);
+    DARM_CUDA(launch_ir_interp(L, s));
+    tl.mark(2);
+    std::vector<int32_t> herr(static_cast<size_t>(n_warps));
+    if (n_warps) DARM_CUDA(cudaMemcpyAsync(herr.data(), derr, size_t(n_warps) * 4, cudaMemcpyDeviceToHost, s));
+    if (mem == DARM_MEM_HOST) {
+      auto back = [&](void *dst, const void *src, size_t bytes) {
+        if (dst && bytes) DARM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        if (dst) d2h += bytes;
+      };
+      back(globals, L.globals, size_t(gbytes));
+      back(shared, L.shared, size_t(sbytes));
+      back(returns, L.returns, size_t(n_warps * warp) * 4);
+      back(ret_valid, L.ret_valid, size_t(n_warps * warp));
+      back(faults, L.faults, size_t(n_warps) * 4);
+      back(stats_out, L.stats, size_t(n_warps) * 64);
+    }
+    tl.mark(3);
+    DARM_CUDA(cudaStreamSynchronize(s));
+    for (int64_t w = 0; w < n_warps; ++w)
+      if (herr[size_t(w)]) {
+        static const char *const what[] = {"", "a phi has no incoming for the lane's predecessor",
+                                           "divergent branch without a reconvergence point",
+                                           "SIMT stack deeper than the interpreter supports"};
+        const int e = herr[size_t(w)];
+        user_error("warp " + std::to_string(w) + ": " + (e >= 1 && e <= 3 ? what[e] : "execution error"));
+      }
+    if (stats) {
+      tl.fill(stats);
+      stats->launches = n_warps ? 1 : 0;
+      stats->h2d_bytes = h2d;
+      stats->d2h_bytes = d2h;
+      stats->algorithmic_bytes = uint64_t(2 * (gbytes + sbytes));
+    }
   });
 }
 

@@ -1,0 +1,236 @@
+"""GPU executeWarp for arbitrary mini-IR (csrc/interp.cu)
+against the reference interpreter itself (oracle/_ref, ref_execute_program):
+for every corpus kernel (positives and negatives), every corpus kernel as
+melded by the reference pass, and this repo's IR kernels (N-Queens, PCM, MS
+steps), on makeRandomInput fixtures at warp sizes 1..64 and both latency
+models, every WarpResult field must be equal — returns, final global and
+shared memory, fault counts, the taint / non-termination flags and all seven
+WarpExecStats counters.  Plus the reference's interpreter known-answer cases
+(test_interp.cpp:21-160) written as IR."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+import paper_2107_05681_b200 as darm
+
+CORPUS_DIR = "/root/reference/proj/corpus"
+OWN_IR = sorted(glob.glob(os.path.join(ROOT, "paper_2107_05681_b200", "ir", "*.ir")))
+CORPUS_NAMES = ["sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "nested", "bitonic",
+                "neg_barrier", "neg_emptyarm", "neg_ifthen", "neg_looparms", "neg_multiret", "neg_uniform"]
+UNIT = [1] * 28
+
+
+def _texts(reference):
+    """(tag, ir text) for every corpus kernel, its runDarm output, and our IR."""
+    out = []
+    for name in CORPUS_NAMES:
+        mod = reference.load(name, 0)
+        out.append((name, mod.text()))
+        if name != "neg_multiret":      # the pass (and executeWarp) need a unique ret block
+            out.append((name + ".melded", reference.load(name, 1).text()))
+    for path in OWN_IR:
+        text = open(path).read()
+        tag = os.path.basename(path)[:-3]
+        out.append((tag, text))
+        out.append((tag + ".melded", reference.load_text(text, 1).text()))
+    return out
+
+
+def test_loader_layout_matches_reference(reference):
+    """The GPU program's params and memories are the reference module's (names,
+    sizes, declaration order) for every kernel the GPU tests run."""
+    for tag, text in _texts(reference):
+        if "neg_multiret" in tag:
+            with pytest.raises(darm.DarmUserError):
+                darm.Program(text)          # uniqueRetBlock (dominators.cpp:110-123)
+            continue
+        p = darm.Program(text)
+        mod = reference.load_text(text, 0)
+        assert p.params == mod.params, tag
+        assert [(n, s) for n, s, _, sh in p.memories if not sh] == [tuple(g) for g in mod.globals], tag
+        assert [(n, s) for n, s, _, sh in p.memories if sh] == [tuple(x) for x in mod.shared], tag
+
+
+def _run_both(reference, text, warp, n_warps, seed, latency=None, max_steps=0):
+    mod = reference.load_text(text, 0)
+    prog = darm.Program(text, latency)
+    args = np.zeros((len(mod.params), n_warps), np.int32)
+    gl = np.zeros((n_warps, prog.global_words), np.int32)
+    sh = np.zeros((n_warps, max(1, prog.shared_words)), np.int32)
+    for w in range(n_warps):
+        a, g, s = mod.make_random_input(warp, seed + w)
+        args[:, w] = a
+        gl[w] = g[: prog.global_words]
+        sh[w, : prog.shared_words] = s[: prog.shared_words]
+    sh = sh[:, : prog.shared_words].copy() if prog.shared_words else None
+    g_ref, s_ref = gl.copy(), None if sh is None else sh.copy()
+    rets, has, faults, stats = mod.execute_program(warp, n_warps, args, g_ref, s_ref, latency=latency,
+                                                   max_steps=max_steps or 10_000_000, threads=8)
+    import torch
+
+    g_gpu = torch.from_numpy(gl.copy()).cuda()
+    s_gpu = None if sh is None else torch.from_numpy(sh.copy()).cuda()
+    res = prog.execute_warps(warp, args, g_gpu, s_gpu, max_steps=max_steps, n_warps=n_warps)
+    torch.cuda.synchronize()
+    return (rets, has, faults, stats, g_ref, s_ref), res
+
+
+def _assert_equal(tag, ref, res):
+    rets, has, faults, stats, g_ref, s_ref = ref
+    assert (res.globals.cpu().numpy() == g_ref).all(), tag + ": global memory"
+    if s_ref is not None:
+        assert (res.shared.cpu().numpy() == s_ref).all(), tag + ": shared memory"
+    assert (res.faults.cpu().numpy() == faults).all(), tag + ": fault counts"
+    assert (res.ret_valid.cpu().numpy() == has).all(), tag + ": which lanes returned"
+    assert (np.where(has == 1, res.returns.cpu().numpy(), 0) == np.where(has == 1, rets, 0)).all(), tag + ": returns"
+    assert (res.stats.cpu().numpy() == stats).all(), (tag + ": stats", res.stats.cpu().numpy()[:2], stats[:2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("warp", [1, 4, 8, 32, 33, 64])
+def test_gpu_interpreter_equals_reference(reference, warp):
+    for tag, text in _texts(reference):
+        if "neg_multiret" in tag:
+            continue
+        for latency in (None, UNIT):
+            ref, res = _run_both(reference, text, warp, 64, 1000 + warp, latency)
+            _assert_equal(f"{tag} warp {warp} {'unit' if latency else 'default'}", ref, res)
+
+
+# The reference's interpreter known-answer tests (test_interp.cpp) as IR
+KAT = {
+    "wrap_shift_div": """
+global out[64]
+fn f(%n) {
+^a:
+  %t = tid
+  %x = add 2147483647 %t
+  %s = shl 1 33
+  %r = shr -1 %t
+  %d = div -7 2
+  %m = rem -7 2
+  %q = div -2147483648 -1
+  %y = add %x %s
+  %z = add %y %r
+  %w = add %z %d
+  %v = add %w %m
+  %u = add %v %q
+  store.global out %t %u
+  ret %u
+}
+""",
+    "div_by_zero_faults_lane": """
+fn f(%n) {
+^a:
+  %t = tid
+  %q = div 10 %t
+  ret %q
+}
+""",
+    "oob_store_faults_only_that_lane": """
+global out[4]
+fn f(%n) {
+^a:
+  %t = tid
+  store.global out %t %t
+  ret %t
+}
+""",
+    "same_address_last_lane_wins": """
+global out[4]
+fn f(%n) {
+^a:
+  %t = tid
+  store.global out 1 %t
+  %v = load.global out 1
+  ret %v
+}
+""",
+    "diamond_reconvergence": """
+fn f(%n) {
+^a:
+  %t = tid
+  %c = icmp.lt %t 2
+  condbr %c ^b ^c
+^b:
+  %x = mul %t 2
+  br ^d
+^c:
+  %y = add %t 100
+  br ^d
+^d:
+  %p = phi %x:^b, %y:^c
+  ret %p
+}
+""",
+    "undef_taint": """
+global out[64]
+fn f(%n) {
+^a:
+  %t = tid
+  %c = icmp.lt %t 8
+  condbr %c ^b ^d
+^b:
+  br ^d
+^d:
+  %p = phi 5:^b, undef:^a
+  %s = select %c %p 7
+  store.global out %t %s
+  ret %s
+}
+""",
+    "nontermination_budget": """
+fn f(%n) {
+^a:
+  br ^l
+^l:
+  %t = tid
+  %c = icmp.ge %t 0
+  condbr %c ^l ^x
+^x:
+  ret
+}
+""",
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", sorted(KAT))
+@pytest.mark.parametrize("warp", [4, 32, 64])
+def test_gpu_interpreter_known_answers(reference, case, warp):
+    max_steps = 1000 if case == "nontermination_budget" else 0
+    ref, res = _run_both(reference, KAT[case], warp, 8, 7, None, max_steps)
+    _assert_equal(f"{case} warp {warp}", ref, res)
+    if case == "diamond_reconvergence":
+        assert res.returns.cpu().numpy()[0, :4].tolist() == [0, 2, 102, 103]    # test_interp.cpp:89-104
+    if case == "nontermination_budget":
+        assert (res.stats.cpu().numpy()[:, 7] & 1).all()
+
+
+@pytest.mark.gpu
+def test_gpu_interpreter_execution_errors():
+    phi_without_incoming = """
+fn f(%n) {
+^a:
+  %t = tid
+  %c = icmp.lt %t 2
+  condbr %c ^b ^d
+^b:
+  br ^d
+^d:
+  %p = phi 1:^b, 2:^x
+  ret %p
+^x:
+  br ^d
+}
+"""
+    import torch
+
+    p = darm.Program(phi_without_incoming)
+    with pytest.raises(darm.DarmUserError):
+        p.execute_warps(4, np.zeros((1, 1), np.int32), torch.zeros((2, 0), dtype=torch.int32, device="cuda"),
+                        n_warps=2)
