@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "darm/interp.hpp"
+#include "darm/parser.hpp"
 #include "darm_gpu.h"
 
 namespace darm {
@@ -93,6 +94,94 @@ inline std::vector<WarpResult> executeWarps(const Module &m, const Function &f,
       r.globalFinal[decl.name] = std::move(v);
     }
     for (int i = 0; i < faults[size_t(w)]; ++i) r.faults.push_back({-1, "", "fault on the GPU"});
+  }
+  return out;
+}
+
+// executeWarp for a batch of warps of ANY function on the GPU interpreter
+// (darm_gpu_program_*): the module is printed with the reference's printModule
+// (parser.hpp) and lowered by the library; the WarpResults carry everything
+// executeWarp fills — returns, globalFinal, sharedFinal, stats (incl.
+// serializedCycles / utilization), fault count (lanes -1) and the
+// nonTerminated / taintedObservable flags — so compareRuns and the bench
+// statistics work unchanged.  `lm` supplies the 28 opcode latencies.
+inline std::vector<WarpResult> executeWarpsIR(const Module &m, const Function &f,
+                                              const std::vector<WarpInput> &ins, const LatencyModel &lm,
+                                              int64_t maxSteps = 10000000) {
+  std::vector<WarpResult> out(ins.size());
+  if (ins.empty()) return out;
+  Module one;
+  one.globals = m.globals;
+  one.functions.push_back(f);
+  const std::string text = printModule(one);
+  int64_t lat[28];
+  for (int k = 0; k <= int(Opcode::Barrier); ++k) lat[k] = lm.latency(Opcode(k));
+  darm_gpu_program *p = nullptr;
+  char err[512] = {0};
+  if (darm_gpu_program_load(text.c_str(), lat, &p, err, sizeof err) != DARM_OK)
+    throw std::runtime_error(std::string("darm_gpu: ") + err);
+  const int W = ins[0].warpSize;
+  const int64_t n = int64_t(ins.size());
+  int64_t gw = 0, sw = 0;
+  darm_gpu_program_shape(p, nullptr, nullptr, nullptr, &gw, &sw);
+  const size_t np = f.params.size();
+  std::vector<int32_t> args(np * size_t(n) * W);
+  std::vector<int32_t> gl(size_t(n * gw), 0), sh(size_t(n * sw), 0);
+  for (int64_t w = 0; w < n; ++w) {
+    const WarpInput &in = ins[size_t(w)];
+    if (in.warpSize != W) throw std::runtime_error("darm::gpu::executeWarpsIR: mixed warp sizes");
+    for (size_t q = 0; q < np; ++q)
+      for (int l = 0; l < W; ++l) args[q * n * W + w * W + l] = in.args[q].size() == 1 ? in.args[q][0] : in.args[q].at(size_t(l));
+    int64_t off = 0;
+    for (const auto &g : m.globals) {
+      auto it = in.globalInit.find(g.name);
+      if (it != in.globalInit.end()) std::copy(it->second.begin(), it->second.end(), gl.begin() + w * gw + off);
+      off += g.size;
+    }
+    off = 0;
+    for (const auto &s : f.sharedDecls) {
+      auto it = in.sharedInit.find(s.name);
+      if (it != in.sharedInit.end()) std::copy(it->second.begin(), it->second.end(), sh.begin() + w * sw + off);
+      off += s.size;
+    }
+  }
+  std::vector<int32_t> rets(static_cast<size_t>(n * W)), faults(static_cast<size_t>(n));
+  std::vector<uint8_t> valid(static_cast<size_t>(n * W));
+  std::vector<int64_t> st(static_cast<size_t>(n * 8));
+  const int rc = darm_gpu_program_execute(p, W, n, args.data(), n * W, gl.data(), sw ? sh.data() : nullptr,
+                                          rets.data(), valid.data(), faults.data(), st.data(), maxSteps,
+                                          DARM_MEM_HOST, nullptr, nullptr, err, sizeof err);
+  darm_gpu_program_free(p);
+  if (rc == DARM_USER_ERROR) throw std::runtime_error(std::string("darm_gpu: ") + err);
+  if (rc != DARM_OK) throw std::logic_error(std::string("darm_gpu: ") + err);
+  for (int64_t w = 0; w < n; ++w) {
+    WarpResult &r = out[size_t(w)];
+    r.returns.assign(size_t(W), std::nullopt);
+    for (int l = 0; l < W; ++l)
+      if (valid[size_t(w * W + l)]) r.returns[size_t(l)] = rets[size_t(w * W + l)];
+    int64_t off = 0;
+    for (const auto &g : m.globals) {
+      r.globalFinal[g.name] = std::vector<int32_t>(gl.begin() + w * gw + off, gl.begin() + w * gw + off + g.size);
+      off += g.size;
+    }
+    off = 0;
+    for (const auto &s : f.sharedDecls) {
+      r.sharedFinal[s.name] = std::vector<int32_t>(sh.begin() + w * sw + off, sh.begin() + w * sw + off + s.size);
+      off += s.size;
+    }
+    for (int i = 0; i < faults[size_t(w)]; ++i) r.faults.push_back({-1, "", "fault on the GPU"});
+    const int64_t *s8 = st.data() + w * 8;
+    r.stats.issuedInstructions = s8[0];
+    r.stats.threadCycles = s8[1];
+    r.stats.usefulThreadCycles = s8[2];
+    r.stats.serializedCycles = s8[3];
+    r.stats.divergentBranchCount = s8[4];
+    r.stats.sharedMemIssues = s8[5];
+    r.stats.globalMemIssues = s8[6];
+    r.stats.utilization = s8[1] == 0 ? 1.0 : double(s8[2]) / double(s8[1]);
+    r.nonTerminated = s8[7] & 1;
+    r.taintedObservable = (s8[7] & 2) != 0;
+    if (r.taintedObservable) r.taintNote = "undef-derived value observed (GPU interpreter)";
   }
   return out;
 }

@@ -14,6 +14,10 @@
 //   gpuLanes         lanes of the timed batch (warp x warps, config 1 shape)
 //   gpuUnmeldedUs / gpuMeldedUs / gpuSpeedup   kernel time (library events,
 //                    best of `reps`) for makeRandomInput batches
+//   gpuSimEqual      the simulator run on the GPU interpreter
+//                    (darm::gpu::executeWarpsIR, before and after the pass)
+//                    produced exactly the CPU interpreter's WarpResults,
+//                    statistics included; cpuSimMs / gpuSimMs time both
 // The JSON keys are the reference's (darm_cli.cpp:343-358) plus the gpu* keys,
 // so consumers of the reference's bench JSON read both side by side; the table
 // prints the reference's columns followed by the GPU ones.
@@ -23,6 +27,7 @@
 // Exit codes as the reference CLI (darm_cli.cpp:25-27): 0 ok, 2 usage,
 // 3 oracle failure or internal error.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -55,7 +60,8 @@ struct Row {
   std::vector<double> mpScores;
   double serBefore = 0, serAfter = 0, utilBefore = 1, utilAfter = 1;
   // GPU columns
-  bool gpu = false, gpuOracleOk = true;
+  bool gpu = false, gpuOracleOk = true, gpuSimEqual = true;
+  double cpuSimMs = 0, gpuSimMs = 0;
   std::string gpuOracleDiff;
   long long gpuLanes = 0;
   double gpuUnmeldedUs = 0, gpuMeldedUs = 0;
@@ -144,10 +150,37 @@ Row bench_one(const std::string &kernel, const char *text, const Row &opts, int 
     gu = gpu::executeWarps(m, f0, ins, gpu::Form::Unmelded);
     gm = gpu::executeWarps(m, f0, ins, gpu::Form::Melded);
   }
+  // the simulator itself on the GPU interpreter (executeWarpsIR): same stats?
+  std::vector<WarpResult> sim_b, sim_a;
+  if (use_gpu) {
+    const auto t0 = std::chrono::steady_clock::now();
+    sim_b = gpu::executeWarpsIR(m, f0, ins, lm);
+    sim_a = gpu::executeWarpsIR(melded, f1, ins, lm);
+    row.gpuSimMs = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   double sb = 0, sa = 0, ub = 0, ua = 0;
+  const auto c0 = std::chrono::steady_clock::now();
+  std::vector<WarpResult> cpu_b, cpu_a;
   for (int i = 0; i < fixtures; ++i) {
-    WarpResult before = executeWarp(m, f0, ins[size_t(i)], lm);
-    WarpResult after = executeWarp(melded, f1, ins[size_t(i)], lm);
+    cpu_b.push_back(executeWarp(m, f0, ins[size_t(i)], lm));
+    cpu_a.push_back(executeWarp(melded, f1, ins[size_t(i)], lm));
+  }
+  row.cpuSimMs = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+  auto same_stats = [](const WarpResult &x, const WarpResult &y) {
+    return x.stats.issuedInstructions == y.stats.issuedInstructions && x.stats.threadCycles == y.stats.threadCycles &&
+           x.stats.usefulThreadCycles == y.stats.usefulThreadCycles &&
+           x.stats.serializedCycles == y.stats.serializedCycles &&
+           x.stats.divergentBranchCount == y.stats.divergentBranchCount &&
+           x.stats.sharedMemIssues == y.stats.sharedMemIssues && x.stats.globalMemIssues == y.stats.globalMemIssues &&
+           x.returns == y.returns && x.globalFinal == y.globalFinal && x.sharedFinal == y.sharedFinal &&
+           x.faults.size() == y.faults.size() && x.nonTerminated == y.nonTerminated &&
+           x.taintedObservable == y.taintedObservable;
+  };
+  for (int i = 0; i < fixtures; ++i) {
+    const WarpResult &before = cpu_b[size_t(i)];
+    const WarpResult &after = cpu_a[size_t(i)];
+    if (use_gpu && !(same_stats(before, sim_b[size_t(i)]) && same_stats(after, sim_a[size_t(i)])))
+      row.gpuSimEqual = false;
     CompareVerdict v = compareRuns(before, after);
     if (!v.equal && row.oracleOk) {
       row.oracleOk = false;
@@ -215,8 +248,12 @@ json to_json(const Row &r) {
     j["gpuUnmeldedUs"] = r.gpuUnmeldedUs;
     j["gpuMeldedUs"] = r.gpuMeldedUs;
     j["gpuSpeedup"] = r.gpuMeldedUs > 0 ? r.gpuUnmeldedUs / r.gpuMeldedUs : 0.0;
+    j["gpuSimEqual"] = r.gpuSimEqual;
+    j["cpuSimMs"] = r.cpuSimMs;
+    j["gpuSimMs"] = r.gpuSimMs;
   } else {
-    for (const char *k : {"gpuOracleOk", "gpuOracleDiff", "gpuLanes", "gpuUnmeldedUs", "gpuMeldedUs", "gpuSpeedup"})
+    for (const char *k : {"gpuOracleOk", "gpuOracleDiff", "gpuLanes", "gpuUnmeldedUs", "gpuMeldedUs", "gpuSpeedup",
+                          "gpuSimEqual", "cpuSimMs", "gpuSimMs"})
       j[k] = nullptr;
   }
   return j;
@@ -280,8 +317,8 @@ int main(int argc, char **argv) {
       Row r = bench_one(k, text, opts, fixtures, warp, seed, use_gpu, gpu_warps, reps);
       std::string status = r.rejected ? "rejected" : (r.melds > 0 ? "melded" : "no-meld");
       if (!r.oracleOk) status = "ORACLE-FAIL";
-      const char *gst = !r.gpu ? "-" : (r.gpuOracleOk ? "ok" : "FAIL");
-      failed = failed || !r.oracleOk || (r.gpu && !r.gpuOracleOk);
+      const char *gst = !r.gpu ? "-" : (r.gpuOracleOk && r.gpuSimEqual ? "ok" : "FAIL");
+      failed = failed || !r.oracleOk || (r.gpu && (!r.gpuOracleOk || !r.gpuSimEqual));
       std::printf("%-14s %-13s %5.2f  %-8s %5d  %9.1f %9.1f %6.1f%%  %5.3f %5.3f  %-6s %9.2f %9.2f %6.3f\n",
                   r.kernel.c_str(), r.mode.c_str(), r.threshold, status.c_str(), r.melds, r.serBefore, r.serAfter,
                   reduction(r.serBefore, r.serAfter), r.utilBefore, r.utilAfter, gst, r.gpuUnmeldedUs,

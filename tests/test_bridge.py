@@ -27,7 +27,8 @@ GPU_BENCH = os.path.join(ROOT, "oracle", "_ref", "darm_gpu_bench")
 REFERENCE_ROW_KEYS = {"kernel", "mode", "threshold", "rejected", "melded", "melds", "converged", "mpScores",
                       "oracleOk", "oracleDiff", "serializedBefore", "serializedAfter",
                       "serializedReductionPercent", "utilizationBefore", "utilizationAfter"}
-GPU_ROW_KEYS = {"gpuOracleOk", "gpuOracleDiff", "gpuLanes", "gpuUnmeldedUs", "gpuMeldedUs", "gpuSpeedup"}
+GPU_ROW_KEYS = {"gpuOracleOk", "gpuOracleDiff", "gpuLanes", "gpuUnmeldedUs", "gpuMeldedUs", "gpuSpeedup",
+                "gpuSimEqual", "cpuSimMs", "gpuSimMs"}
 
 
 def _gpu_bench(args, tmp_path):
@@ -59,5 +60,6 @@ def test_stats_wire_format_gpu_rows(tmp_path):
     rows, _ = _gpu_bench(["--fixtures", "20", "--gpu-warps", "32768"], tmp_path)
     for r in rows:
         assert r["gpuOracleOk"], (r["kernel"], r["gpuOracleDiff"])
+        assert r["gpuSimEqual"], r["kernel"]      # the simulator statistics, computed on the GPU
         assert r["gpuLanes"] == 32 * 32768
         assert r["gpuUnmeldedUs"] > 0 and r["gpuMeldedUs"] > 0
