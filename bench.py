@@ -267,7 +267,35 @@ def cpu_baseline(args):
 
 # ------------------------------------------------------------------ per-kernel table
 CORPUS_LANE = ["sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "nested"]
-NQ_NODES_16 = 1141190303  # search nodes of the N=16 tree incl. root (tests pin it for small n)
+NQ_NODES_16 = 1141190303
+# A divergent diamond written for this row (not a corpus file): the GPU
+# interpreter runs it from IR text like any reference module.
+DIAMOND_IR = """global x[64]
+global y[64]
+global z[64]
+fn diamond(%n) {
+^e:
+  %t = tid
+  %c = icmp.lt %t %n
+  condbr %c ^l ^r
+^l:
+  %a = load.global x %t
+  %b = mul %a 5
+  %d = load.global y %t
+  %s = sub %b %d
+  store.global z %t %s
+  br ^j
+^r:
+  %a2 = load.global x %t
+  %b2 = shl %a2 2
+  %d2 = load.global y %t
+  %s2 = add %b2 %d2
+  store.global z %t %s2
+  br ^j
+^j:
+  ret
+}
+"""
 
 
 def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None, rank=0, world=1):
@@ -362,6 +390,24 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_keys_per_s"] = n / (row["melded_us"] * 1e-6)
     out["ms1m"] = row
+    # the GPU executeWarp for arbitrary IR (darm_gpu_program_execute): a diamond
+    # kernel given as IR text, 32768 warps of 32 lanes (config 1 shape)
+    row = {}
+    for vname in ("diamond",):
+        prog = darm.Program(DIAMOND_IR)
+        nwi = 1 << 15
+        gi = torch.randint(-128, 129, (nwi, prog.global_words), dtype=torch.int32, device="cuda", generator=g)
+        work_g = torch.empty_like(gi)
+        argv = np.full((1, 1), 16, np.int32)
+        ts = []
+        for i in range(warmup + steps):
+            work_g.copy_(gi)
+            res = prog.execute_warps(32, argv, work_g, n_warps=nwi)
+            if i >= warmup:
+                ts.append(res.call_stats["kernel_ms"])
+        row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(ts) / len(ts))
+        row[vname + "_warps_per_s"] = nwi / (row[vname + "_us"] * 1e-6)
+    out["interp_diamond_32k_warps"] = row
     # LUD 8192^2 fp32 (config 4): the whole decomposition (3 x 512 launches in one graph)
     n = 8192
     g = torch.Generator(device="cuda").manual_seed(4)
