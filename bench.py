@@ -338,7 +338,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
         for i in range(warmup + max(3, steps // 4)):
             if dist:
                 dist.barrier()
-            sols, _, st = darm.nqueens(16, 7, v, rank=rank, world=world, stream=stream.cuda_stream)
+            sols, _, st = darm.nqueens(16, 7, v, rank=rank, world=world, stream=stream.cuda_stream, mirror=True)
             if dist:
                 t = torch.tensor([sols], dtype=torch.int64, device="cuda")
                 dist.all_reduce(t)
@@ -349,8 +349,8 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
         row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
     tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
-    row["melded_nodes_per_s"] = NQ_NODES_16 / (row["melded_us"] * 1e-6)
-    row["prefix_rows"] = 7
+    row["melded_solutions_per_s"] = 14772512 / (row["melded_us"] * 1e-6)
+    row["prefix_rows"], row["mirror_symmetry"] = 7, True
     row["n_gpus"], row["scaling"] = world, "strong (prefixes sharded over the ranks)"
     out["nqueens16"] = row
     # PCM (Batcher odd-even merge sort of 64-key buckets, 2^24 keys) and MS (bottom-up

@@ -183,6 +183,17 @@ int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world,
                      int64_t *n_prefixes, void *stream, darm_gpu_stats *stats,
                      char *err, size_t errlen);
 
+/* Same, with flags: DARM_NQ_MIRROR counts by mirror symmetry — the row-0 queen
+ * only in columns < ceil(n/2), those left of the middle counted twice — which
+ * halves the search; the prefix set (and per_prefix) is then the reduced one. */
+#define DARM_NQ_MIRROR 1
+int darm_gpu_nqueens_ex(int variant, int n, int prefix_rows, int rank, int world,
+                        int flags, uint64_t *solutions, uint32_t *per_prefix,
+                        int64_t per_prefix_len, int64_t *n_prefixes, void *stream,
+                        darm_gpu_stats *stats, char *err, size_t errlen);
+int64_t darm_gpu_nqueens_prefix_count_ex(int n, int prefix_rows, int rank, int world,
+                                         int flags);
+
 /* ---- LUD (Rodinia lud, no reference code): blocked LU
  *      decomposition without pivoting, BLOCK = 16, in place ----------------
  * a: n x n row-major fp32 (n % 16 == 0, 16 <= n <= 46336); on return the

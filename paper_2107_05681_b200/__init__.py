@@ -54,6 +54,8 @@ ABI_SYMBOLS = (
     "darm_gpu_merge_sort",
     "darm_gpu_nqueens",
     "darm_gpu_nqueens_prefix_count",
+    "darm_gpu_nqueens_ex",
+    "darm_gpu_nqueens_prefix_count_ex",
     "darm_gpu_lud",
     "darm_gpu_srad",
     "darm_gpu_srad_roi_words",
@@ -158,6 +160,13 @@ def lib() -> ctypes.CDLL:
             ctypes.c_size_t]
         L.darm_gpu_nqueens_prefix_count.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.darm_gpu_nqueens_prefix_count.restype = ctypes.c_int64
+        L.darm_gpu_nqueens_ex.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int64,
+            ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.POINTER(Stats), ctypes.c_char_p,
+            ctypes.c_size_t]
+        L.darm_gpu_nqueens_prefix_count_ex.argtypes = [ctypes.c_int] * 5
+        L.darm_gpu_nqueens_prefix_count_ex.restype = ctypes.c_int64
         L.darm_gpu_lud.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.POINTER(Stats), ctypes.c_char_p, ctypes.c_size_t]
         I32P, F32P, F64P = c_i32p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)
@@ -520,11 +529,13 @@ class Program:
 
 
 def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int = 1,
-            per_prefix: bool = False, stream=None, want_stats: bool = True):
+            per_prefix: bool = False, stream=None, want_stats: bool = True, mirror: bool = False):
     """Count n-queens solutions below the prefixes i % world == rank.
 
+    ``mirror``: count by mirror symmetry (half the search, DARM_NQ_MIRROR).
     Returns ``(solutions, per_prefix_counts or None, stats)``.
     """
+    flags = 1 if mirror else 0
     if isinstance(variant, str):
         variant = VARIANTS[variant]
     sols = ctypes.c_uint64(0)
@@ -532,13 +543,13 @@ def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int 
     err = ctypes.create_string_buffer(512)
     per = None
     if per_prefix:
-        cnt = lib().darm_gpu_nqueens_prefix_count(n, prefix_rows, rank, world)
+        cnt = lib().darm_gpu_nqueens_prefix_count_ex(n, prefix_rows, rank, world, flags)
         if cnt < 0:
             raise DarmUserError("bad n-queens arguments")
         per = np.zeros(max(1, cnt), dtype=np.uint32)
     st = Stats()
-    rc = lib().darm_gpu_nqueens(
-        int(variant), n, prefix_rows, rank, world, ctypes.byref(sols),
+    rc = lib().darm_gpu_nqueens_ex(
+        int(variant), n, prefix_rows, rank, world, flags, ctypes.byref(sols),
         per.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)) if per is not None else None,
         per.size if per is not None else 0, ctypes.byref(npre), ctypes.c_void_p(stream or 0),
         ctypes.byref(st) if want_stats else None, err, 512)

@@ -36,6 +36,7 @@ namespace darm_gpu {
 struct NqParams {
   const uint32_t *prefix;          // n_prefix x {cols, d1, d2} (row-relative, as enumerated)
   uint32_t n_prefix;
+  uint32_t n_double;               // prefixes [0, n_double) count twice (mirror symmetry)
   uint32_t *per_prefix;            // solutions per prefix (may be null)
   unsigned long long *total;       // sum of solutions
   unsigned int *next;              // work counter
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
     if (row < P.base) {                                    // ^s: %done
       if (pidx != 0xffffffffu) {
         if (P.per_prefix) P.per_prefix[pidx] = sol;
-        acc += sol;
+        acc += pidx < P.n_double ? 2ull * sol : sol;
       }
       // the lanes refilling in this iteration take consecutive prefixes
       const unsigned act = __activemask();
@@ -169,12 +170,13 @@ cudaError_t launch_form(const NqParams &P, int sms, cudaStream_t s) {
 }
 }  // namespace
 
-cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, int n, int base,
+cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, uint32_t n_double, int n, int base,
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,
                            int sms, cudaStream_t s) {
   NqParams P;
   P.prefix = prefix;
   P.n_prefix = n_prefix;
+  P.n_double = n_double;
   P.per_prefix = per_prefix;
   P.total = total;
   P.next = counter;

@@ -572,12 +572,20 @@ int darm_gpu_merge_sort(int variant, int32_t *keys, int64_t n, int mem, void *st
 
 // N-Queens prefixes: every valid placement of the first `base` rows, lowest
 // free column first; prefix i goes to rank i % world.
-static void nqueens_prefixes(int n, int base, int rank, int world, std::vector<uint32_t> &out) {
+// symmetric: row 0 only in the columns < ceil(n/2) (mirror symmetry; the
+// placements with the row-0 queen left of the middle count twice, the middle
+// column of an odd n once); *n_double receives how many of the kept prefixes
+// (they come first) carry the factor 2.
+static void nqueens_prefixes(int n, int base, int rank, int world, std::vector<uint32_t> &out,
+                             bool symmetric = false, int64_t *n_double = nullptr) {
   const uint32_t mask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
   uint32_t cols[32], d1[32], d2[32], av[32];
   int row = 0;
   cols[0] = d1[0] = d2[0] = 0;
-  av[0] = mask;
+  av[0] = symmetric ? ((1u << ((n + 1) / 2)) - 1u) : mask;
+  const uint32_t left = (1u << (n / 2)) - 1u;   // row-0 columns that count twice
+  int64_t dbl = 0;
+  uint32_t first = 0;                           // the row-0 queen
   uint64_t idx = 0;
   while (row >= 0) {
     if (av[row] == 0) {
@@ -586,12 +594,14 @@ static void nqueens_prefixes(int n, int base, int rank, int world, std::vector<u
     }
     const uint32_t bit = av[row] & (0u - av[row]);
     av[row] ^= bit;
+    if (row == 0) first = bit;
     const uint32_t c = cols[row] | bit, e1 = (d1[row] | bit) << 1, e2 = (d2[row] | bit) >> 1;
     if (row + 1 == base) {
       if (int(idx % uint64_t(world)) == rank) {
         out.push_back(c);
         out.push_back(e1);
         out.push_back(e2);
+        if (symmetric && (first & left)) ++dbl;
       }
       ++idx;
       continue;
@@ -602,20 +612,34 @@ static void nqueens_prefixes(int n, int base, int rank, int world, std::vector<u
     d2[row] = e2;
     av[row] = ~(c | e1 | e2) & mask;
   }
+  if (n_double) *n_double = dbl;
 }
 
 int64_t darm_gpu_nqueens_prefix_count(int n, int prefix_rows, int rank, int world) {
-  if (n < 2 || n > 31 || prefix_rows < 1 || prefix_rows > n - 1 || world < 1 || rank < 0 || rank >= world)
+  return darm_gpu_nqueens_prefix_count_ex(n, prefix_rows, rank, world, 0);
+}
+
+int64_t darm_gpu_nqueens_prefix_count_ex(int n, int prefix_rows, int rank, int world, int flags) {
+  if (n < 2 || n > 31 || prefix_rows < 1 || prefix_rows > n - 1 || world < 1 || rank < 0 || rank >= world ||
+      (flags & ~DARM_NQ_MIRROR))
     return -1;
   std::vector<uint32_t> pre;
-  nqueens_prefixes(n, prefix_rows, rank, world, pre);
+  nqueens_prefixes(n, prefix_rows, rank, world, pre, (flags & DARM_NQ_MIRROR) != 0);
   return int64_t(pre.size() / 3);
 }
 
 int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world, uint64_t *solutions,
                      uint32_t *per_prefix, int64_t per_prefix_len, int64_t *n_prefixes, void *stream,
                      darm_gpu_stats *stats, char *err, size_t errlen) {
+  return darm_gpu_nqueens_ex(variant, n, prefix_rows, rank, world, 0, solutions, per_prefix, per_prefix_len,
+                             n_prefixes, stream, stats, err, errlen);
+}
+
+int darm_gpu_nqueens_ex(int variant, int n, int prefix_rows, int rank, int world, int flags, uint64_t *solutions,
+                        uint32_t *per_prefix, int64_t per_prefix_len, int64_t *n_prefixes, void *stream,
+                        darm_gpu_stats *stats, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
+    if (flags & ~DARM_NQ_MIRROR) user_error("unknown n-queens flags");
     if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
     if (n < 2 || n > 31) user_error("n must be in [2, 31]");
     if (prefix_rows < 1 || prefix_rows > n - 1) user_error("prefix_rows must be in [1, n-1]");
@@ -623,7 +647,8 @@ int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world, u
     if (!solutions) user_error("solutions is NULL");
     if (stats) std::memset(stats, 0, sizeof(*stats));
     std::vector<uint32_t> pre;
-    nqueens_prefixes(n, prefix_rows, rank, world, pre);
+    int64_t n_double = 0;
+    nqueens_prefixes(n, prefix_rows, rank, world, pre, (flags & DARM_NQ_MIRROR) != 0, &n_double);
     const int64_t np = int64_t(pre.size() / 3);
     if (n_prefixes) *n_prefixes = np;
     if (np >= (int64_t(1) << 32) - 1) user_error("too many prefixes; lower prefix_rows");
@@ -639,7 +664,7 @@ int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world, u
     if (!pre.empty()) DARM_CUDA(cudaMemcpyAsync(dpre, pre.data(), pre.size() * 4, cudaMemcpyHostToDevice, s));
     DARM_CUDA(cudaMemsetAsync(dctl, 0, 16, s));
     tl.mark(1);
-    if (np) DARM_CUDA(launch_nqueens(variant, dpre, uint32_t(np), n, prefix_rows, dper, dctl,
+    if (np) DARM_CUDA(launch_nqueens(variant, dpre, uint32_t(np), uint32_t(n_double), n, prefix_rows, dper, dctl,
                                      reinterpret_cast<unsigned int *>(dctl + 1), st.sms, s));
     tl.mark(2);
     unsigned long long total = 0;

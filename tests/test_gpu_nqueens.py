@@ -62,3 +62,18 @@ def test_nqueens_small_and_edge():
         darm.nqueens(8, 8)
     with pytest.raises(darm.DarmUserError):
         darm.nqueens(1, 1)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_nqueens_mirror_symmetry(variant):
+    """DARM_NQ_MIRROR: row-0 queen in the left half (x2) and the middle column of
+    an odd board (x1) — the same totals with half the search."""
+    for n in range(4, 15):
+        for base in (1, 2, min(4, n - 1)):
+            assert darm.nqueens(n, base, variant, mirror=True)[0] == NQUEENS[n], (n, base)
+    parts = [darm.nqueens(13, 4, variant, rank=r, world=3, mirror=True)[0] for r in range(3)]
+    assert sum(parts) == NQUEENS[13]
+    assert darm.nqueens(16, 7, variant, mirror=True)[0] == 14772512
+    _, per, _ = darm.nqueens(9, 3, variant, per_prefix=True, mirror=True)
+    _, per_full, _ = darm.nqueens(9, 3, variant, per_prefix=True)
+    assert len(per) < len(per_full)
