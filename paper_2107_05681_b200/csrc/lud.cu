@@ -287,6 +287,76 @@ __global__ void __launch_bounds__(256) lud_update_kernel(float *__restrict__ a, 
   for (int i = 0; i < 4; ++i) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
 }
 
+// The far trailing block's T-step update (the bulk of the FLOPs): 128x64
+// tiles, thread micro-tile 8 rows x 4 columns (two 16-byte L loads and one U
+// load per k for 32 FMAs), panels in dynamic shared memory; same per-element
+// operation sequence as lud_update_kernel.
+constexpr int kFarRows = 128, kFarCols = 64;
+
+__global__ void __launch_bounds__(256, 2) lud_far_kernel(float *__restrict__ a, int n, int o, int T, int lo) {
+  extern __shared__ __align__(16) float fsm[];
+  const int K = T * BS, K4 = K / 4;
+  float(*lt)[kFarRows + 4] = reinterpret_cast<float(*)[kFarRows + 4]>(fsm);                       // [K][132]
+  float(*up)[kFarCols + 4] = reinterpret_cast<float(*)[kFarCols + 4]>(fsm + K * (kFarRows + 4));   // [K][68]
+  const int r0 = lo + kFarRows * int(blockIdx.y), c0 = lo + kFarCols * int(blockIdx.x);
+  const int nr = min(kFarRows, n - r0), nc = min(kFarCols, n - c0);
+  for (int e = threadIdx.x; e < kFarRows * K4; e += 256) {
+    const int rr = e % kFarRows, k4 = e / kFarRows;
+    float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rr < nr) l = *reinterpret_cast<const float4 *>(a + size_t(r0 + rr) * n + o + 4 * k4);
+    lt[4 * k4][rr] = l.x;
+    lt[4 * k4 + 1][rr] = l.y;
+    lt[4 * k4 + 2][rr] = l.z;
+    lt[4 * k4 + 3][rr] = l.w;
+  }
+  for (int e = threadIdx.x; e < K * (kFarCols / 4); e += 256) {
+    const int kk = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * c4 < nc) u = *reinterpret_cast<const float4 *>(a + size_t(o + kk) * n + c0 + 4 * c4);
+    *reinterpret_cast<float4 *>(&up[kk][4 * c4]) = u;
+  }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int c = 4 * tx, rb = 8 * ty;
+  const bool live = c < nc && rb < nr;
+  float4 v[8];
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float4 *>(a + size_t(r0 + rb + i) * n + c0 + c);
+  }
+  __syncthreads();
+  if (!live) return;
+  for (int t = 0; t < T; ++t) {
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+#pragma unroll
+    for (int k = 0; k < BS; ++k) {
+      const float4 u = *reinterpret_cast<const float4 *>(&up[t * BS + k][c]);
+      const float4 l0 = *reinterpret_cast<const float4 *>(&lt[t * BS + k][rb]);
+      const float4 l1 = *reinterpret_cast<const float4 *>(&lt[t * BS + k][rb + 4]);
+      const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc[i][0] = fmaf(lv[i], u.x, acc[i][0]);
+        acc[i][1] = fmaf(lv[i], u.y, acc[i][1]);
+        acc[i][2] = fmaf(lv[i], u.z, acc[i][2]);
+        acc[i][3] = fmaf(lv[i], u.w, acc[i][3]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i].x -= acc[i][0];
+      v[i].y -= acc[i][1];
+      v[i].z -= acc[i][2];
+      v[i].w -= acc[i][3];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
+}
+
 namespace {
 cudaError_t launch_update(float *a, int n, int o, int T, Rect R0, Rect R1, const float *dsrc, int dofs,
                           cudaStream_t s) {
@@ -336,8 +406,19 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
       ++*launches;
     }
     if (E < n) {
-      const Rect far{E, n, E, n};
-      cudaError_t e = launch_update(a, n, O, T, far, Rect{0, 0, 0, 0}, nullptr, 0, s);
+      // the far trailing block [E, n)^2 takes the super-step's T updates
+      const int m = n - E;
+      const size_t shm = size_t(T * BS) * (kFarRows + 4 + kFarCols + 4) * sizeof(float);
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(lud_far_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(size_t(kLook * BS) * (kFarRows + 4 + kFarCols + 4) * sizeof(float)));
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      lud_far_kernel<<<dim3((m + kFarCols - 1) / kFarCols, (m + kFarRows - 1) / kFarRows), 256, shm, s>>>(a, n, O,
+                                                                                                       T, E);
+      cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       ++*launches;
     }
