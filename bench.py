@@ -426,41 +426,48 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     # halo exchange and the ROI all-reduce every iteration over NCCL
     n, iters = 16384, 100
     j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
-    row = {}
-    if world == 1:
-        j = torch.empty_like(j0)
-        for vname, v in (("unmelded", 0), ("melded", 1)):
-            call = darm.srad(j, iters, 0.5, darm.RODINIA_ROI, v, stream=stream.cuda_stream, want_stats=False,
-                             prepare_only=True)
-            t = time_steps(torch, stream, lambda: j.copy_(j0), call, 2, 1, flush)
-            row[vname + "_us"] = 1e3 * sum(t) / len(t)
-    else:
-        from paper_2107_05681_b200.srad_tiles import SradTiles
+    for key, fast in (("srad16384x100", False), ("srad16384x100_fast_math", True)):
+        row = {}
+        flag = darm.FAST_MATH if fast else 0
+        if world == 1:
+            j = torch.empty_like(j0)
+            for vname, v in (("unmelded", 0), ("melded", 1)):
+                call = darm.srad(j, iters, 0.5, darm.RODINIA_ROI, v, stream=stream.cuda_stream, want_stats=False,
+                                 prepare_only=True, fast=fast)
+                t = time_steps(torch, stream, lambda: j.copy_(j0), call, 2, 1, flush)
+                row[vname + "_us"] = 1e3 * sum(t) / len(t)
+            del j
+        else:
+            from paper_2107_05681_b200.srad_tiles import SradTiles
 
-        for vname, v in (("unmelded", 0), ("melded", 1)):
-            tiles = SradTiles(n, n, 0.5, darm.RODINIA_ROI, dist=dist, device=torch.device("cuda"), variant=v)
-            ts = []
-            for rep in range(2):
-                tiles.load(j0)
-                torch.cuda.synchronize()
-                dist.barrier()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                tiles.run(iters)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                if rep:
-                    ts.append(e0.elapsed_time(e1))
-            row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
-            del tiles
-    tmax(row)
-    row["speedup"] = row["unmelded_us"] / row["melded_us"]
-    # minimal traffic 8 B/px/iteration (one read of J, one write of J') + the in/out copies of the call
-    alg = 8.0 * n * n * iters + 8.0 * n * n
-    row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
-    row["melded_frac_hbm"] = row["melded_GBps"] / (peak * world)
-    row["n_gpus"], row["scaling"] = world, "strong (row tiles, NCCL halo exchange)" if world > 1 else "single GPU"
-    out["srad16384x100"] = row
+            for vname, v in (("unmelded", 0), ("melded", 1)):
+                tiles = SradTiles(n, n, 0.5, darm.RODINIA_ROI, dist=dist, device=torch.device("cuda"),
+                                  variant=v | flag)
+                ts = []
+                for rep in range(2):
+                    tiles.load(j0)
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    tiles.run(iters)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    if rep:
+                        ts.append(e0.elapsed_time(e1))
+                row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
+                del tiles
+        tmax(row)
+        row["speedup"] = row["unmelded_us"] / row["melded_us"]
+        # minimal traffic 8 B/px/iteration (one read of J, one write of J') + the in/out copies of the call
+        alg = 8.0 * n * n * iters + 8.0 * n * n
+        row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
+        row["melded_frac_hbm"] = row["melded_GBps"] / (peak * world)
+        row["n_gpus"], row["scaling"] = world, ("strong (row tiles, NCCL halo exchange)" if world > 1 else
+                                                "single GPU")
+        row["arithmetic"] = ("reciprocal-multiply divisions + FMA, within 1e-5 relative (DARM_FAST_MATH)" if fast
+                             else "IEEE, bit-exact vs the restatement")
+        out[key] = row
     return out
 
 

@@ -34,6 +34,7 @@ import numpy as np
 UNMELDED = 0
 MELDED = 1
 VARIANTS = {"unmelded": UNMELDED, "melded": MELDED}
+FAST_MATH = 0x100   # SRAD: OR into the variant (DARM_FAST_MATH, within 1e-5 relative)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libdarm_gpu.so")
@@ -589,10 +590,14 @@ def _roi_arr(roi):
 
 
 def srad(j, iters: int, lam: float = 0.5, roi=RODINIA_ROI, variant=MELDED, stream=None,
-         want_stats: bool = True, prepare_only: bool = False):
-    """SRAD on a 2-D fp32 image, in place (numpy -> HOST mode, torch CUDA -> DEVICE)."""
+         want_stats: bool = True, prepare_only: bool = False, fast: bool = False):
+    """SRAD on a 2-D fp32 image, in place (numpy -> HOST mode, torch CUDA -> DEVICE).
+    ``fast``: reciprocal-multiply divisions and FMAs (DARM_FAST_MATH; within
+    1e-5 relative of the IEEE path instead of bit-identical)."""
     if isinstance(variant, str):
         variant = VARIANTS[variant]
+    if fast:
+        variant |= FAST_MATH
     if _is_torch_cuda(j):
         import torch
 

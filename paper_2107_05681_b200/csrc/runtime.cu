@@ -550,7 +550,7 @@ int darm_gpu_merge_sort(int variant, int32_t *keys, int64_t n, int mem, void *st
     int launches = 0;
     tl.mark(1);
     if (n > 1) {
-      GraphEntry &g = cached_graph(st, 2, variant, dk, n, [&](cudaStream_t cs, int *l) {
+      GraphEntry &g = cached_graph(st, 4, variant, dk, n, [&](cudaStream_t cs, int *l) {
         return record_merge_sort(variant, dk, tmp, n, cs, l);
       });
       DARM_CUDA(cudaGraphLaunch(g.exec, s));
@@ -745,7 +745,8 @@ int64_t darm_gpu_srad_roi_words(int64_t cols, const int *roi) {
 int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, float lambda, const int *roi,
                   int mem, void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if ((variant & ~DARM_FAST_MATH) != DARM_UNMELDED && (variant & ~DARM_FAST_MATH) != DARM_MELDED)
+      user_error("variant must be 0 (unmelded) or 1 (melded), optionally | DARM_FAST_MATH");
     check_srad_args(rows, cols, roi, lambda);
     if (iters < 0) user_error("iters must be >= 0");
     if (!j) user_error("image is NULL");
@@ -769,7 +770,7 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
                                                                          : cudaMemcpyDeviceToDevice, s));
     tl.mark(1);
     const int it = iters;
-    GraphEntry &g = cached_graph(st, 2 + variant, it, b0, rows * 1000003 + cols * 7 + roi[0] * 131 + roi[1] * 17 +
+    GraphEntry &g = cached_graph(st, 16 + variant, it, b0, rows * 1000003 + cols * 7 + roi[0] * 131 + roi[1] * 17 +
                                                            roi[2] * 3 + roi[3] + int64_t(lambda * 1e6) * 97,
                                  [&](cudaStream_t cs, int *launches) {
       cudaError_t e = launch_srad_roi(b0, int(cols), 0, int(rows), R, roiA, cs);
@@ -821,7 +822,8 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, 
                             int64_t r0, int64_t rows, float lambda, const int *roi, const double *roi_in,
                             double *roi_out, float *q0_scratch, void *stream, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if ((variant & ~DARM_FAST_MATH) != DARM_UNMELDED && (variant & ~DARM_FAST_MATH) != DARM_MELDED)
+      user_error("variant must be 0 (unmelded) or 1 (melded), optionally | DARM_FAST_MATH");
     check_srad_args(rows, cols, roi, lambda);
     if (tile_rows < 1 || r0 < 0 || r0 + tile_rows > rows) user_error("tile outside the image");
     if (!tile_in || !tile_out || !roi_in || !q0_scratch) user_error("NULL buffer");

@@ -51,17 +51,42 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 
 // c for one pixel from its centre and 4 neighbour values (Rodinia SRAD,
 // restated).  R_D is the clamp.
-template <bool M>
+// FAST (DARM_FAST_MATH): the five divisions as a multiply by the MUFU
+// reciprocal (rcp.approx.ftz: no range fix-up, the operands here are normal
+// numbers of moderate size) and the sums of products contracted to FMAs; the
+// result stays within the north star's 1e-5 relative tolerance of the IEEE
+// path (tests/test_srad.py) instead of matching it bit for bit.
+__device__ __forceinline__ float rcp_approx(float b) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+  return r;
+}
+
+template <bool FAST>
+__device__ __forceinline__ float sdiv(float a, float b) {
+  if constexpr (FAST) return a * rcp_approx(b);
+  else return a / b;
+}
+
+template <bool M, bool FAST>
 __device__ __forceinline__ float srad_coeff(float jc, float n, float s, float w, float e, float q0sqr,
                                             float q0den) {
   const float dN = n - jc, dS = s - jc, dW = w - jc, dE = e - jc;
-  const float g2 = (((dN * dN + dS * dS) + dW * dW) + dE * dE) / (jc * jc);
-  const float l = (((dN + dS) + dW) + dE) / jc;
-  const float num = (0.5f * g2) - ((1.0f / 16.0f) * (l * l));
-  float den = 1.0f + (0.25f * l);
-  const float qsqr = num / (den * den);
-  den = (qsqr - q0sqr) / q0den;
-  float c = 1.0f / (1.0f + den);
+  float g2, l, num, den;
+  if constexpr (FAST) {
+    g2 = sdiv<FAST>(__fmaf_rn(dE, dE, __fmaf_rn(dW, dW, __fmaf_rn(dS, dS, dN * dN))), jc * jc);
+    l = sdiv<FAST>(((dN + dS) + dW) + dE, jc);
+    num = __fmaf_rn(-1.0f / 16.0f, l * l, 0.5f * g2);
+    den = __fmaf_rn(0.25f, l, 1.0f);
+  } else {
+    g2 = (((dN * dN + dS * dS) + dW * dW) + dE * dE) / (jc * jc);
+    l = (((dN + dS) + dW) + dE) / jc;
+    num = (0.5f * g2) - ((1.0f / 16.0f) * (l * l));
+    den = 1.0f + (0.25f * l);
+  }
+  const float qsqr = sdiv<FAST>(num, den * den);
+  den = sdiv<FAST>(qsqr - q0sqr, q0den);
+  float c = FAST ? rcp_approx(1.0f + den) : 1.0f / (1.0f + den);
   if constexpr (!M) {
     if (c < 0.0f) {                      // R_D: three-way, data dependent
       DARM_ARM("srad.rd.lo");
@@ -76,7 +101,7 @@ __device__ __forceinline__ float srad_coeff(float jc, float n, float s, float w,
   return c;
 }
 
-template <bool M>
+template <bool M, bool FAST>
 __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
   const int lane = threadIdx.x & 31;
   const int wcol = blockIdx.x * 8 + (threadIdx.x >> 5);   // warp column group
@@ -124,7 +149,7 @@ __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
   float jm1 = row(g0 - 1)[jc], j0 = row(g0)[jc], jp1 = row(g0 + 1)[jc];
   float w0, e0;
   west_east(row(g0), j0, w0, e0);
-  float c0 = srad_coeff<M>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
+  float c0 = srad_coeff<M, FAST>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
   float jp2 = row(g0 + 2)[jc];
   // sliding row pointers: p1 -> row g+1 (lane 31's east value), pn -> the
   // next row to prefetch (g+3, held at the last row the buffer/image has)
@@ -141,14 +166,20 @@ __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
     // c at row g+1 (clamped: at the last image row it is c(g) itself)
     float w1, e1;
     west_east(p1, jp1, w1, e1);
-    const float c1 = (g + 1 <= gmax) ? srad_coeff<M>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
+    const float c1 = (g + 1 <= gmax) ? srad_coeff<M, FAST>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
     // east neighbour's c at row g
     float ce = __shfl_down_sync(0xffffffffu, c0, 1);
     if (j >= cols - 1) ce = c0;
     // update row g
     const float dN = jm1 - j0, dS = jp1 - j0, dW = w0 - j0, dE = e0 - j0;
-    const float d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
-    const float jn = j0 + P.lq * d;
+    float d, jn;
+    if constexpr (FAST) {
+      d = __fmaf_rn(ce, dE, __fmaf_rn(c0, dW, __fmaf_rn(c1, dS, c0 * dN)));
+      jn = __fmaf_rn(P.lq, d, j0);
+    } else {
+      d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
+      jn = j0 + P.lq * d;
+    }
     if (out_lane) *outp = jn;
     outp += cols;
     if (roi_warp && g >= P.roi_r1 && g <= P.roi_r2) {
@@ -272,10 +303,12 @@ cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const 
   P.roi_groups = roi.groups;
   const int wgroups = (cols + 29) / 30;
   dim3 grid((wgroups + 7) / 8, (tile_rows + P.rs - 1) / P.rs);
-  if (variant)
-    srad_sweep_kernel<true><<<grid, 256, 0, s>>>(P);
+  const bool fast = variant & 0x100;   // DARM_FAST_MATH
+  if (variant & 1)
+    fast ? srad_sweep_kernel<true, true><<<grid, 256, 0, s>>>(P) : srad_sweep_kernel<true, false><<<grid, 256, 0, s>>>(P);
   else
-    srad_sweep_kernel<false><<<grid, 256, 0, s>>>(P);
+    fast ? srad_sweep_kernel<false, true><<<grid, 256, 0, s>>>(P)
+         : srad_sweep_kernel<false, false><<<grid, 256, 0, s>>>(P);
   return cudaGetLastError();
 }
 

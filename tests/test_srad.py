@@ -237,3 +237,38 @@ def test_gpu_config5_16384(restatement):
     got = one.cpu().numpy()
     assert np.max(np.abs(got - want) / np.abs(want)) <= 1e-5
     assert (got.view(np.int32) == want.view(np.int32)).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("rows,cols,iters,roi", [(256, 256, 100, ROI), (513, 377, 30, (10, 200, 31, 300)),
+                                                  (2049, 1000, 20, ROI)])
+def test_gpu_fast_math_within_tolerance(restatement, variant, rows, cols, iters, roi):
+    """DARM_FAST_MATH: the north star's 1e-5 relative tolerance against the
+    IEEE restatement, after up to 100 iterations; the two forms agree bit for
+    bit with each other."""
+    j0 = image(rows, cols, rows + 1)
+    want = j0.copy()
+    restatement.srad(want, iters, 0.5, roi)
+    j = j0.copy()
+    darm.srad(j, iters, 0.5, roi, variant, fast=True)
+    rel = np.max(np.abs(j - want) / np.abs(want))
+    assert rel <= 1e-5, rel
+    other = j0.copy()
+    darm.srad(other, iters, 0.5, roi, 1 - variant, fast=True)
+    assert (other.view(np.int32) == j.view(np.int32)).all()
+
+
+@pytest.mark.gpu
+def test_gpu_fast_math_config5(restatement):
+    """16384^2: 100 fast iterations stay within 1e-5 relative of 100 IEEE
+    iterations on the GPU (the IEEE path is bit-exact to the restatement)."""
+    n = 16384
+    g = torch.Generator(device="cuda").manual_seed(5)
+    j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
+    a, b = j0.clone(), j0.clone()
+    darm.srad(a, 100, 0.5, ROI, 1)
+    darm.srad(b, 100, 0.5, ROI, 1, fast=True)
+    torch.cuda.synchronize()
+    rel = float(((a - b).abs() / a.abs()).max())
+    assert rel <= 1e-5, rel

@@ -29,9 +29,10 @@ def main(which, bucket=64):
         n = 16384
         g = torch.Generator(device="cuda").manual_seed(5)
         j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
-        for v in (darm.UNMELDED, darm.MELDED):
-            j = j0.clone()
-            darm.srad(j, 2, 0.5, darm.RODINIA_ROI, v, want_stats=False)
+        for fast in (False, True):
+            for v in (darm.UNMELDED, darm.MELDED):
+                j = j0.clone()
+                darm.srad(j, 2, 0.5, darm.RODINIA_ROI, v, want_stats=False, fast=fast)
         torch.cuda.synchronize()
         return
     if which == "nqueens":
