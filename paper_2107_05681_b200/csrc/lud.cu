@@ -31,6 +31,20 @@ namespace darm_gpu {
 
 namespace {
 constexpr int BS = 16;
+
+// Two fp32 FMAs in one instruction (sm_100 FFMA2, fma.rn.f32x2): each half is
+// an IEEE fma with one rounding, so the results equal two fmaf calls bit for
+// bit; the FMA pipe issues half as many instructions.
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra, rb, rc, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+  return d;
+}
 constexpr int LD = BS + 1;  // padded shared row: conflict-free column walks
 }  // namespace
 
@@ -287,74 +301,117 @@ __global__ void __launch_bounds__(256) lud_update_kernel(float *__restrict__ a, 
   for (int i = 0; i < 4; ++i) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
 }
 
-// The far trailing block's T-step update (the bulk of the FLOPs): 128x64
-// tiles, thread micro-tile 8 rows x 4 columns (two 16-byte L loads and one U
-// load per k for 32 FMAs), panels in dynamic shared memory; same per-element
-// operation sequence as lud_update_kernel.
-constexpr int kFarRows = 128, kFarCols = 64;
+constexpr int kFarRows = 128, kFarCols = 64;   // far-update tile
 
-__global__ void __launch_bounds__(256, 2) lud_far_kernel(float *__restrict__ a, int n, int o, int T, int lo) {
-  extern __shared__ __align__(16) float fsm[];
+// The far trailing block's T-step update (the bulk of the FLOPs), persistent:
+// one CTA per SM walks the 128x64 tiles
+// of the far block; every tile's L rows (non-transposed, 16-byte chunks along
+// k), U rows and the tile of A itself are brought into shared memory with
+// cp.async while the previous tile computes (two stages).  Per 4 k's a thread
+// reads 8 float4 of L (its 8 rows) and 4 float4 of U (its 4 columns) for 64
+// FFMA2.  Same per-element operation sequence as lud_update_kernel.
+constexpr int kPipeK = kLook * BS;                 // 64
+constexpr int kLdL = kPipeK + 4;                   // lp[r][k] row pitch
+constexpr int kLdU = kFarCols + 4;                 // up[k][c]
+constexpr int kLdV = kFarCols + 4;                 // vt[r][c]
+constexpr int kStageWords = kFarRows * kLdL + kPipeK * kLdU + kFarRows * kLdV;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 16 : 0;                // 0: zero-fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(256, 1) lud_far_pipe_kernel(float *__restrict__ a, int n, int o, int T, int lo) {
+  extern __shared__ __align__(16) float psm[];
+  const int m = n - lo;
+  const int tiles_c = (m + kFarCols - 1) / kFarCols, tiles_r = (m + kFarRows - 1) / kFarRows;
+  const int tiles = tiles_c * tiles_r;
   const int K = T * BS, K4 = K / 4;
-  float(*lt)[kFarRows + 4] = reinterpret_cast<float(*)[kFarRows + 4]>(fsm);                       // [K][132]
-  float(*up)[kFarCols + 4] = reinterpret_cast<float(*)[kFarCols + 4]>(fsm + K * (kFarRows + 4));   // [K][68]
-  const int r0 = lo + kFarRows * int(blockIdx.y), c0 = lo + kFarCols * int(blockIdx.x);
-  const int nr = min(kFarRows, n - r0), nc = min(kFarCols, n - c0);
-  for (int e = threadIdx.x; e < kFarRows * K4; e += 256) {
-    const int rr = e % kFarRows, k4 = e / kFarRows;
-    float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (rr < nr) l = *reinterpret_cast<const float4 *>(a + size_t(r0 + rr) * n + o + 4 * k4);
-    lt[4 * k4][rr] = l.x;
-    lt[4 * k4 + 1][rr] = l.y;
-    lt[4 * k4 + 2][rr] = l.z;
-    lt[4 * k4 + 3][rr] = l.w;
-  }
-  for (int e = threadIdx.x; e < K * (kFarCols / 4); e += 256) {
-    const int kk = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
-    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * c4 < nc) u = *reinterpret_cast<const float4 *>(a + size_t(o + kk) * n + c0 + 4 * c4);
-    *reinterpret_cast<float4 *>(&up[kk][4 * c4]) = u;
-  }
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int c = 4 * tx, rb = 8 * ty;
-  const bool live = c < nc && rb < nr;
-  float4 v[8];
-  if (live) {
+  auto stage_ptr = [&](int st) { return psm + size_t(st) * kStageWords; };
+  auto issue = [&](int tile, int st) {
+    float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL, *vt = up + kPipeK * kLdU;
+    const int r0 = lo + kFarRows * (tile / tiles_c), c0 = lo + kFarCols * (tile % tiles_c);
+    const int nr = min(kFarRows, n - r0), nc = min(kFarCols, n - c0);
+    for (int e = threadIdx.x; e < kFarRows * K4; e += 256) {          // L rows of the tile, k along
+      const int r = e / K4, k4 = e % K4;
+      const bool ok = r < nr;
+      cp_async16(lp + r * kLdL + 4 * k4, a + size_t(ok ? r0 + r : r0) * n + o + 4 * k4, ok);
+    }
+    for (int e = threadIdx.x; e < K * (kFarCols / 4); e += 256) {      // U rows, columns of the tile
+      const int kk = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
+      const bool ok = 4 * c4 < nc;
+      cp_async16(up + kk * kLdU + 4 * c4, a + size_t(o + kk) * n + (ok ? c0 + 4 * c4 : c0), ok);
+    }
+    for (int e = threadIdx.x; e < kFarRows * (kFarCols / 4); e += 256) {   // the tile of A
+      const int r = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
+      const bool ok = r < nr && 4 * c4 < nc;
+      cp_async16(vt + r * kLdV + 4 * c4, a + size_t(ok ? r0 + r : r0) * n + (ok ? c0 + 4 * c4 : c0), ok);
+    }
+    cp_async_commit();
+  };
+  int tile = blockIdx.x;
+  if (tile < tiles) issue(tile, 0);
+  for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
+    const int st = it & 1;
+    const int next = tile + gridDim.x;
+    if (next < tiles) {
+      issue(next, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL, *vt = up + kPipeK * kLdU;
+    const int r0 = lo + kFarRows * (tile / tiles_c), c0 = lo + kFarCols * (tile % tiles_c);
+    const int nr = min(kFarRows, n - r0), nc = min(kFarCols, n - c0);
+    float4 v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float4 *>(a + size_t(r0 + rb + i) * n + c0 + c);
-  }
-  __syncthreads();
-  if (!live) return;
-  for (int t = 0; t < T; ++t) {
-    float acc[8][4];
+    for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float4 *>(vt + (rb + i) * kLdV + c);
+    for (int t = 0; t < T; ++t) {
+      float2 acc[8][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+      for (int k4 = 0; k4 < BS / 4; ++k4) {
+        const int kb = t * BS + 4 * k4;
+        float4 l[8], u[4];
 #pragma unroll
-    for (int k = 0; k < BS; ++k) {
-      const float4 u = *reinterpret_cast<const float4 *>(&up[t * BS + k][c]);
-      const float4 l0 = *reinterpret_cast<const float4 *>(&lt[t * BS + k][rb]);
-      const float4 l1 = *reinterpret_cast<const float4 *>(&lt[t * BS + k][rb + 4]);
-      const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        for (int i = 0; i < 8; ++i) l[i] = *reinterpret_cast<const float4 *>(lp + (rb + i) * kLdL + kb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = *reinterpret_cast<const float4 *>(up + (kb + q) * kLdU + c);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 u01 = make_float2(u[q].x, u[q].y), u23 = make_float2(u[q].z, u[q].w);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float li = q == 0 ? l[i].x : q == 1 ? l[i].y : q == 2 ? l[i].z : l[i].w;
+            const float2 ll = make_float2(li, li);
+            acc[i][0] = fma2(ll, u01, acc[i][0]);
+            acc[i][1] = fma2(ll, u23, acc[i][1]);
+          }
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        acc[i][0] = fmaf(lv[i], u.x, acc[i][0]);
-        acc[i][1] = fmaf(lv[i], u.y, acc[i][1]);
-        acc[i][2] = fmaf(lv[i], u.z, acc[i][2]);
-        acc[i][3] = fmaf(lv[i], u.w, acc[i][3]);
+        v[i].x -= acc[i][0].x;
+        v[i].y -= acc[i][0].y;
+        v[i].z -= acc[i][1].x;
+        v[i].w -= acc[i][1].y;
       }
     }
+    if (c < nc) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      v[i].x -= acc[i][0];
-      v[i].y -= acc[i][1];
-      v[i].z -= acc[i][2];
-      v[i].w -= acc[i][3];
+      for (int i = 0; i < 8; ++i)
+        if (rb + i < nr) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
     }
+    __syncthreads();   // this stage is refilled by the next iteration's issue
   }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
 }
 
 namespace {
@@ -408,16 +465,19 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
     if (E < n) {
       // the far trailing block [E, n)^2 takes the super-step's T updates
       const int m = n - E;
-      const size_t shm = size_t(T * BS) * (kFarRows + 4 + kFarCols + 4) * sizeof(float);
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lud_far_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(size_t(kLook * BS) * (kFarRows + 4 + kFarCols + 4) * sizeof(float)));
+      const size_t shm = 2 * size_t(kStageWords) * sizeof(float);
+      static int sms = 0;
+      if (!sms) {
+        cudaError_t e = cudaFuncSetAttribute(lud_far_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(shm));
         if (e != cudaSuccess) return e;
-        attr = true;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
       }
-      lud_far_kernel<<<dim3((m + kFarCols - 1) / kFarCols, (m + kFarRows - 1) / kFarRows), 256, shm, s>>>(a, n, O,
-                                                                                                       T, E);
+      const int tiles = ((m + kFarCols - 1) / kFarCols) * ((m + kFarRows - 1) / kFarRows);
+      lud_far_pipe_kernel<<<min(tiles, sms), 256, shm, s>>>(a, n, O, T, E);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       ++*launches;
