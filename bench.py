@@ -480,12 +480,19 @@ def our_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
 
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # DARM_DIST_BACKEND=gloo: a functional run of the multi-rank logic with
+        # several ranks on one GPU (NCCL refuses two ranks per device)
+        backend = os.environ.get("DARM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist_mod.init_process_group(backend)
         dist = dist_mod
     darm.init()
     stream = torch.cuda.current_stream()
@@ -504,7 +511,7 @@ def our_arm(args):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        with ClockSampler(local) as clk:
+        with ClockSampler(dev_index) as clk:
             times = time_steps(torch, stream, prepare, step, args.steps, args.warmup, flush)
         torch.cuda.synchronize()
         if not torch.equal(work, want):

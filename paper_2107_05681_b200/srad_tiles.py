@@ -92,20 +92,26 @@ class SradTiles:
         if self.world == 1:
             return
         d = self.dist
+        # gloo moves host buffers only (NCCL moves device memory directly)
+        stage = self.device.type == "cuda" and d.get_backend() == "gloo"
+        to_wire = (lambda t: t.cpu()) if stage else (lambda t: t.contiguous())  # noqa: E731
         ops = []
         up, down = self.rank - 1, self.rank + 1
+        top = bottom = None
         if up >= 0:
-            ops.append(d.P2POp(d.isend, self.tin[1:3].contiguous(), up))
-            ops.append(d.P2POp(d.irecv, self.halo_top, up))
+            top = self.halo_top.cpu() if stage else self.halo_top
+            ops.append(d.P2POp(d.isend, to_wire(self.tin[1:3]), up))
+            ops.append(d.P2POp(d.irecv, top, up))
         if down < self.world:
-            ops.append(d.P2POp(d.isend, self.tin[self.n:self.n + 1].contiguous(), down))
-            ops.append(d.P2POp(d.irecv, self.halo_bottom, down))
+            bottom = self.halo_bottom.cpu() if stage else self.halo_bottom
+            ops.append(d.P2POp(d.isend, to_wire(self.tin[self.n:self.n + 1]), down))
+            ops.append(d.P2POp(d.irecv, bottom, down))
         for req in d.batch_isend_irecv(ops):
             req.wait()
         if up >= 0:
-            self.tin[0:1].copy_(self.halo_top)
+            self.tin[0:1].copy_(top)
         if down < self.world:
-            self.tin[self.n + 1:self.n + 3].copy_(self.halo_bottom)
+            self.tin[self.n + 1:self.n + 3].copy_(bottom)
 
     @property
     def halo_top(self):
@@ -138,14 +144,16 @@ class SradTiles:
         torch = self.torch
         if self.world == 1:
             return self.tile().clone()
-        parts = [torch.empty((n, self.cols), dtype=torch.float32, device=self.device)
+        stage = self.device.type == "cuda" and self.dist.get_backend() == "gloo"
+        dev = torch.device("cpu") if stage else self.device
+        parts = [torch.empty((n, self.cols), dtype=torch.float32, device=dev)
                  for _, n in split_rows(self.rows, self.world)]
-        own = self.tile().contiguous()
+        own = self.tile().contiguous().to(dev)
         if self.rank == 0:
             out = [own.clone()]
             for k in range(1, self.world):
                 self.dist.recv(parts[k], src=k)
                 out.append(parts[k])
-            return torch.cat(out, dim=0)
+            return torch.cat(out, dim=0).to(self.device)
         self.dist.send(own, dst=0)
         return None
