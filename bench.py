@@ -48,6 +48,41 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+LANE_KEYS = {"nqueens16": "nqueens", "pcm": "pcm_16kpt", "pcm_1key": "pcm_1kpt", "ms1m": "ms",
+             "lud8192": "lud_panel", "srad16384x100": "srad", "srad16384x100_fast_math": "srad_fast",
+             "bitonic": "bitonic_sort_16kpt", "bitonic_1key": "bitonic_sort_1kpt"}
+
+
+def attach_lane_efficiency(per_kernel):
+    """SIMT lane efficiency of every per-kernel row from the committed ncu sweep
+    (profiles/r<NN>_lane_efficiency.json, tools/lane_eff.sh) and, for the corpus
+    kernels, the reference simulator's unit-latency utilisation in the same
+    configuration (profiles/r<NN>_simulator_util.json, oracle/sim_util.py)."""
+    import glob
+
+    def latest(stem):
+        paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r[0-9][0-9]_{stem}.json")))
+        if not paths:
+            return None, None
+        with open(paths[-1]) as f:
+            return json.load(f), os.path.relpath(paths[-1], ROOT)
+
+    le, le_src = latest("lane_efficiency")
+    sim, sim_src = latest("simulator_util")
+    for key, row in per_kernel.items():
+        k = LANE_KEYS.get(key, key)
+        if le and k in le["kernels"]:
+            e = le["kernels"][k]
+            row["lane_efficiency"] = {
+                form: {"thread_inst_per_inst_div32": round(e[form]["lane_efficiency"], 4),
+                       "pred_on_div32": round(e[form]["lane_efficiency_pred_on"], 4)}
+                for form in ("unmelded", "melded") if form in e}
+            row["lane_efficiency"]["source"] = le_src
+        sk = "bitonic_step" if key == "bitonic_step" else key
+        if sim and sk in sim["utilization"]:
+            row["reference_simulator_utilization"] = dict(sim["utilization"][sk], source=sim_src)
+
+
 def ncu_kernel_summary(stem, pattern):
     """Latest committed ncu summary profiles/r<NN>_ncu_<stem>.json -> entry whose
     kernel name contains `pattern` (None when absent)."""
@@ -604,6 +639,7 @@ def our_arm(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     if per_kernel is not None:
+        attach_lane_efficiency(per_kernel)
         line["per_kernel"] = per_kernel
     print(json.dumps(line))
     if dist:
