@@ -31,6 +31,7 @@ namespace darm_gpu {
 
 namespace {
 constexpr int BS = 16;
+constexpr int kLook = 4;   // steps per look-ahead super-step
 
 // Two fp32 FMAs in one instruction (sm_100 FFMA2, fma.rn.f32x2): each half is
 // an IEEE fma with one rounding, so the results equal two fmaf calls bit for
@@ -67,21 +68,61 @@ constexpr int LD = BS + 1;  // padded shared row: conflict-free column walks
 //      warp only at BLOCK = 16);
 //   5. results go back through shared memory as coalesced float4 stores.
 // The factored diagonal block goes to `dst` (CTA 0, row stride `dstride`):
-// a scratch block while CTAs of this launch may still be reading the
-// unfactored block from `a` (the next launch, lud_update_kernel, moves it
-// into place), or straight into `a` for the last block (one CTA).
+// a scratch slot while CTAs of this launch may still be reading the
+// unfactored block from `a` (lud_scatter_diag_kernel moves them all into place
+// at the end; no later kernel reads a factored diagonal block), or straight
+// into `a` for the last block (one CTA).
 constexpr int kPairs = 4;
 
+// Pending updates (left-looking inside a super-step): the blocks a panel
+// reads still lack the updates of the earlier steps O, O+16, .., o-16 of its
+// super-step; the panel applies them itself, per element in step order as
+// sum = fma(L, U, sum) over k = 0..15 then a -= sum — the per-element sequence
+// of the separate update kernel it replaces.  L / U come from the earlier
+// steps' column / row blocks, already final.  Shared layout (dynamic):
+//   Lp[16][kLdP]   rows o..o+15, columns O..o   (the diagonal rows' L)
+//   Ud[48][LD]     rows O..o, columns o..o+15   (U above the diagonal block)
+//   per warp Ur[48][LD] (U above its row block), Lc[16][kLdP] (its column block's L)
+constexpr int kMaxPend = kLook - 1;
+constexpr int kLdP = kMaxPend * BS + 1;
+constexpr int kPendFloats = BS * kLdP + kMaxPend * BS * LD + kPairs * (kMaxPend * BS * LD + BS * kLdP);
+
 template <bool M>
-__global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs,
+__global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs, int O,
                                                                float *__restrict__ dst, int dstride) {
   __shared__ float dia[kPairs][BS][LD];
   __shared__ float diaT[kPairs][BS][LD];      // diaT[i][j] = dia[j][i]
   __shared__ float blk[kPairs][2][BS][LD];    // [0] row block R[i][c]; [1] column block transposed C[i][r]
+  extern __shared__ float pend[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * kPairs + warp;
   const bool have = p < npairs;                             // warp-uniform
   const size_t cb = size_t(o) + size_t(BS) * (p + 1);       // column of the row block = row of the column block
+  const int P = (o - O) / BS;                               // pending steps (block-uniform)
+  float(*Lp)[kLdP] = reinterpret_cast<float(*)[kLdP]>(pend);
+  float(*Ud)[LD] = reinterpret_cast<float(*)[LD]>(pend + BS * kLdP);
+  float(*Ur)[LD] = reinterpret_cast<float(*)[LD]>(pend + BS * kLdP + kMaxPend * BS * LD +
+                                                  warp * (kMaxPend * BS * LD + BS * kLdP));
+  float(*Lc)[kLdP] = reinterpret_cast<float(*)[kLdP]>(reinterpret_cast<float *>(Ur) + kMaxPend * BS * LD);
+  if (P > 0) {
+    const int K = P * BS;
+    for (int e = threadIdx.x; e < BS * K; e += 32 * kPairs) {
+      const int rr = e / K, k = e % K;
+      Lp[rr][k] = a[(size_t(o) + rr) * n + O + k];
+    }
+    for (int e = threadIdx.x; e < K * BS; e += 32 * kPairs) {
+      const int k = e / BS, c = e % BS;
+      Ud[k][c] = a[(size_t(O) + k) * n + o + c];
+    }
+    if (have) {
+      for (int e = lane; e < K * BS; e += 32) {
+        const int k = e / BS, c = e % BS;
+        Ur[k][c] = a[(size_t(O) + k) * n + cb + c];
+        Lc[c][k] = a[(cb + c) * n + O + k];
+      }
+    }
+    __syncthreads();
+  }
   // 1. requests in flight: the pair (2 float4 per lane per block) and the diagonal row of lane r
   float4 rv[2], cv[2];
   if (have) {
@@ -103,6 +144,16 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
       v[4 * q + 1] = t.y;
       v[4 * q + 2] = t.z;
       v[4 * q + 3] = t.w;
+    }
+  }
+  // the diagonal block's pending updates (lane r holds row r)
+  for (int st = 0; st < P; ++st) {
+#pragma unroll
+    for (int c = 0; c < BS; ++c) {
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < BS; ++k) sum = fmaf(Lp[r][st * BS + k], Ud[st * BS + k][c], sum);
+      v[c] = v[c] - sum;
     }
   }
   // 2. diagonal factorisation in registers
@@ -143,6 +194,22 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
     C[c + 1][i] = cv[h].y;
     C[c + 2][i] = cv[h].z;
     C[c + 3][i] = cv[h].w;
+  }
+  __syncwarp();
+  // the pair's pending updates: R[i][c] (row block) and C[j][rr] (column block)
+  for (int st = 0; st < P; ++st) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int x = lane & (BS - 1), y = (lane >> 4) + 2 * q;
+      float sr = 0.f, sc = 0.f;
+#pragma unroll
+      for (int k = 0; k < BS; ++k) {
+        sr = fmaf(Lp[y][st * BS + k], Ur[st * BS + k][x], sr);   // L[o+y][o_st+k] U[o_st+k][cb+x]
+        sc = fmaf(Lc[x][st * BS + k], Ud[st * BS + k][y], sc);   // L[cb+x][o_st+k] U[o_st+k][o+y]
+      }
+      R[y][x] = R[y][x] - sr;
+      C[y][x] = C[y][x] - sc;
+    }
   }
   __syncwarp();
   const float(*Dg)[LD] = dia[warp];
@@ -205,102 +272,18 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int q = lane + 32 * h, i = q >> 2, c = 4 * (q & 3);
-    if (i > 0) *reinterpret_cast<float4 *>(a + (size_t(o) + i) * n + cb + c) = make_float4(R[i][c], R[i][c + 1], R[i][c + 2], R[i][c + 3]);
+    *reinterpret_cast<float4 *>(a + (size_t(o) + i) * n + cb + c) = make_float4(R[i][c], R[i][c + 1], R[i][c + 2], R[i][c + 3]);
     *reinterpret_cast<float4 *>(a + (cb + i) * n + o + c) = make_float4(C[c][i], C[c + 1][i], C[c + 2][i], C[c + 3][i]);
   }
 }
 
 // ------------------------------------------------------------------ update
-// Trailing updates A[r][c] -= sum_k L_t[r][k] U_t[k][c] for the T consecutive
-// 16-column steps t at offsets o + 16t, applied in step order to every element
-// of up to two rectangles (rows [r_lo, r_hi) x cols [c_lo, c_hi), multiples of
-// 16): per element and step, sum = fma(L[r][k], U[k][c], sum) for k = 0..15
-// and then a = a - sum — exactly the per-element sequence of one
-// 16-column step after another, so deferring the far trailing block's T
-// updates into one pass over it (look-ahead) leaves every bit unchanged while
-// the trailing matrix crosses HBM once per 64 columns instead of once per 16.
-// 64x64 tile per CTA, L (transposed) and U panels staged in shared memory;
-// thread (tx, ty) owns the 4x4 micro-tile rows 4ty.., columns 4tx.., so each
-// k costs two 16-byte shared loads for 16 FMAs; the element stays in registers
-// across t.  CTA (0,0,0) also moves the previous panel launch's factored
-// diagonal block from `dsrc` into place (nothing this launch touches reads it).
-constexpr int kLook = 4;   // steps per look-ahead super-step
-
-struct Rect {
-  int r_lo, r_hi, c_lo, c_hi;
-};
-
-__global__ void __launch_bounds__(256) lud_update_kernel(float *__restrict__ a, int n, int o, int T, Rect R0,
-                                                         Rect R1, const float *__restrict__ dsrc, int dofs) {
-  __shared__ __align__(16) float lt[kLook * BS][64 + 4];      // lt[(t,k)][r] = L_t[r][k]
-  __shared__ __align__(16) float up[kLook * BS][64 + 4];      // up[(t,k)][c] = U_t[k][c]
-  if (dsrc && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-    const int e = threadIdx.x;                                  // 256 = 16 x 16
-    a[size_t(dofs + e / BS) * n + dofs + e % BS] = dsrc[e];
-  }
-  const Rect R = blockIdx.z ? R1 : R0;
-  const int r0 = R.r_lo + 64 * int(blockIdx.y), c0 = R.c_lo + 64 * int(blockIdx.x);
-  if (r0 >= R.r_hi || c0 >= R.c_hi) return;                    // CTA-uniform
-  const int nr = min(64, R.r_hi - r0), nc = min(64, R.c_hi - c0);
-  const int K = T * BS, K4 = K / 4;
-  // L: float4 along k from row r (lanes walk rows: conflict-free transposed stores)
-  for (int e = threadIdx.x; e < 64 * K4; e += 256) {
-    const int rr = e & 63, k4 = e >> 6;
-    float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (rr < nr) l = *reinterpret_cast<const float4 *>(a + size_t(r0 + rr) * n + o + 4 * k4);
-    lt[4 * k4][rr] = l.x;
-    lt[4 * k4 + 1][rr] = l.y;
-    lt[4 * k4 + 2][rr] = l.z;
-    lt[4 * k4 + 3][rr] = l.w;
-  }
-  // U: float4 along c
-  for (int e = threadIdx.x; e < K * 16; e += 256) {
-    const int kk = e >> 4, c4 = e & 15;
-    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * c4 < nc) u = *reinterpret_cast<const float4 *>(a + size_t(o + kk) * n + c0 + 4 * c4);
-    *reinterpret_cast<float4 *>(&up[kk][4 * c4]) = u;
-  }
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int c = 4 * tx, rb = 4 * ty;
-  const bool live = c < nc && rb < nr;
-  float4 v[4];
-  if (live) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = *reinterpret_cast<const float4 *>(a + size_t(r0 + rb + i) * n + c0 + c);
-  }
-  __syncthreads();
-  if (!live) return;
-  for (int t = 0; t < T; ++t) {
-    float acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
-#pragma unroll
-    for (int k = 0; k < BS; ++k) {
-      const float4 u = *reinterpret_cast<const float4 *>(&up[t * BS + k][c]);
-      const float4 l = *reinterpret_cast<const float4 *>(&lt[t * BS + k][rb]);
-      const float lv[4] = {l.x, l.y, l.z, l.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[i][0] = fmaf(lv[i], u.x, acc[i][0]);
-        acc[i][1] = fmaf(lv[i], u.y, acc[i][1]);
-        acc[i][2] = fmaf(lv[i], u.z, acc[i][2]);
-        acc[i][3] = fmaf(lv[i], u.w, acc[i][3]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v[i].x -= acc[i][0];
-      v[i].y -= acc[i][1];
-      v[i].z -= acc[i][2];
-      v[i].w -= acc[i][3];
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
-}
-
+// Trailing update of the far block [O+64, n)^2 by the T steps of a super-step:
+// per element and step, sum = fma(L[r][k], U[k][c], sum) for k = 0..15 and then
+// a = a - sum, in step order — exactly the per-element sequence of one
+// 16-column step after another (and of the restatement), so deferring the far
+// block's T updates into one pass over it leaves every bit unchanged while the
+// trailing matrix crosses HBM once per 64 columns instead of once per 16.
 constexpr int kFarRows = 128, kFarCols = 64;   // far-update tile
 
 // The far trailing block's T-step update (the bulk of the FLOPs), persistent:
@@ -309,7 +292,7 @@ constexpr int kFarRows = 128, kFarCols = 64;   // far-update tile
 // k), U rows and the tile of A itself are brought into shared memory with
 // cp.async while the previous tile computes (two stages).  Per 4 k's a thread
 // reads 8 float4 of L (its 8 rows) and 4 float4 of U (its 4 columns) for 64
-// FFMA2.  Same per-element operation sequence as lud_update_kernel.
+// FFMA2.  Per element the operation sequence above.
 constexpr int kPipeK = kLook * BS;                 // 64
 constexpr int kLdL = kPipeK + 4;                   // lp[r][k] row pitch
 constexpr int kLdU = kFarCols + 4;                 // up[k][c]
@@ -414,32 +397,34 @@ __global__ void __launch_bounds__(256, 1) lud_far_pipe_kernel(float *__restrict_
   }
 }
 
-namespace {
-cudaError_t launch_update(float *a, int n, int o, int T, Rect R0, Rect R1, const float *dsrc, int dofs,
-                          cudaStream_t s) {
-  auto tiles = [](int lo, int hi) { return hi > lo ? (hi - lo + 63) / 64 : 0; };
-  int gx = max(tiles(R0.c_lo, R0.c_hi), tiles(R1.c_lo, R1.c_hi));
-  int gy = max(tiles(R0.r_lo, R0.r_hi), tiles(R1.r_lo, R1.r_hi));
-  const int gz = (R1.r_hi > R1.r_lo && R1.c_hi > R1.c_lo) ? 2 : 1;
-  if (gx == 0 || gy == 0) {
-    if (!dsrc) return cudaSuccess;
-    gx = gy = 1;                                   // still move the diagonal block
-  }
-  lud_update_kernel<<<dim3(gx, gy, gz), 256, 0, s>>>(a, n, o, T, R0, R1, dsrc, dofs);
-  return cudaGetLastError();
-}
-}  // namespace
 
 // ------------------------------------------------------------------ driver
 // Super-steps of kLook 16-column steps at offset O.  For each step t in the
-// super-step: the panel kernel (diagonal + perimeter over everything right of
-// / below the diagonal block), then step t's update restricted to what the
-// later steps of the super-step read — the panel columns [o_t+16, O+64) for
-// all rows below, and the super-row rows [o_t+16, O+64) for all columns to
-// the right.  The far trailing block [O+64, n)^2 then takes the super-step's
-// kLook updates in one pass (lud_update_kernel with T = kLook).
+// super-step one panel launch: it first applies to the blocks it reads the
+// updates of the steps O..o-16 before it (left-looking inside the
+// super-step), then factors the diagonal block and solves the perimeter.  The
+// far trailing block [O+64, n)^2 then takes the super-step's kLook updates in
+// one pass (lud_far_pipe_kernel); the factored diagonal blocks are scattered
+// into place at the end.  n/16 + n/64 + 1 launches.
+// Scatter of the factored diagonal blocks (kept in scratch while later steps
+// may still read the unfactored blocks) into the matrix: block j of dscr to
+// a[16j.., 16j..].
+__global__ void lud_scatter_diag_kernel(float *__restrict__ a, int n, const float *__restrict__ dscr) {
+  const int j = blockIdx.x, e = threadIdx.x;   // 256 threads
+  a[size_t(BS * j + e / BS) * n + BS * j + e % BS] = dscr[size_t(j) * BS * BS + e];
+}
+
 cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches) {
   const int nb = n / BS;
+  static bool attr = false;
+  if (!attr) {
+    for (auto k : {lud_panel_kernel<false>, lud_panel_kernel<true>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(kPendFloats * sizeof(float)));
+      if (e != cudaSuccess) return e;
+    }
+    attr = true;
+  }
   for (int O = 0; O < n; O += kLook * BS) {
     const int T = min(kLook, (n - O) / BS);
     const int E = O + T * BS;   // end of the super-step's columns / rows
@@ -447,20 +432,17 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
       const int o = O + t * BS;
       const int m = nb - o / BS - 1;   // blocks right of / below the diagonal
       const int grid = m > 0 ? (m + kPairs - 1) / kPairs : 1;
-      // the last diagonal block has no other reader: factor it in place
-      float *dst = m > 0 ? dscr : a + size_t(o) * n + o;
+      // the factored diagonal block goes to scratch slot o/16 (CTAs of this launch
+      // still read the unfactored one); the last one, with no other reader, in place
+      float *dst = m > 0 ? dscr + size_t(o / BS) * BS * BS : a + size_t(o) * n + o;
       const int dstride = m > 0 ? BS : n;
+      const size_t shm = (t > 0 ? kPendFloats : 0) * sizeof(float);
       if (variant)
-        lud_panel_kernel<true><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m, dst, dstride);
+        lud_panel_kernel<true><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride);
       else
-        lud_panel_kernel<false><<<grid, 32 * kPairs, 0, s>>>(a, n, o, m, dst, dstride);
+        lud_panel_kernel<false><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride);
       ++*launches;
       if (m == 0) break;
-      const Rect panel_cols{o + BS, n, o + BS, E};   // rows below, panel columns
-      const Rect super_row{o + BS, E, E, n};         // super-row rows, columns right
-      cudaError_t e = launch_update(a, n, o, 1, panel_cols, super_row, dscr, o, s);
-      if (e != cudaSuccess) return e;
-      ++*launches;
     }
     if (E < n) {
       // the far trailing block [E, n)^2 takes the super-step's T updates
@@ -482,6 +464,10 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
       if (e != cudaSuccess) return e;
       ++*launches;
     }
+  }
+  if (nb > 1) {
+    lud_scatter_diag_kernel<<<nb - 1, BS * BS, 0, s>>>(a, n, dscr);
+    ++*launches;
   }
   return cudaGetLastError();
 }

@@ -703,7 +703,7 @@ int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream, darm_g
       d = static_cast<float *>(slot(st, 0, bytes));
       DARM_CUDA(cudaMemcpyAsync(d, a, bytes, cudaMemcpyHostToDevice, s));
     }
-    auto *dscr = static_cast<float *>(slot(st, 7, 256 * sizeof(float)));
+    auto *dscr = static_cast<float *>(slot(st, 7, size_t(n / 16) * 256 * sizeof(float)));   // factored diagonals
     GraphEntry &g = cached_graph(st, 1, variant, d, n, [&](cudaStream_t cs, int *launches) {
       return record_lud(variant, d, int(n), dscr, cs, launches);
     });
