@@ -254,7 +254,7 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out,
  * reference interpreter's: per-lane returns, final global / shared memory,
  * fault counts, and the WarpExecStats counters (latencies: the reference's
  * defaults, ir.cpp:235-244, or `latency`, 28 entries in the opcode order of
- * ir.hpp:17-46).  Limits: 160 values per function, 16 phis per block, SIMT
+ * ir.hpp:17-46).  Limits: 256 values per function, 16 phis per block, SIMT
  * stack depth 48.
  *
  * Buffers (HOST or DEVICE per `mem`):

@@ -31,7 +31,7 @@
 
 namespace darm_gpu {
 
-constexpr int kMaxRegs = 160;      // values per function (registers per lane)
+constexpr int kMaxRegs = 256;      // values per function (registers per lane)
 constexpr int kMaxPhis = 16;       // phis per block
 constexpr int kMaxDepth = 48;      // SIMT stack frames
 constexpr int kWarpsPerCta = 4;

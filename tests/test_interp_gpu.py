@@ -234,3 +234,27 @@ fn f(%n) {
     with pytest.raises(darm.DarmUserError):
         p.execute_warps(4, np.zeros((1, 1), np.int32), torch.zeros((2, 0), dtype=torch.int32, device="cuda"),
                         n_warps=2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("warp", [5, 32, 64])
+def test_gpu_interpreter_fuzz(reference, warp):
+    """Random structured IR functions (tests/irgen.py: divergent diamonds and
+    loops, faulting divisions and out-of-bounds accesses, undef phis) — the GPU
+    interpreter equals the reference interpreter on every field, under a small
+    step budget so non-termination is exercised too."""
+    from irgen import random_function
+
+    ran = 0
+    for seed in range(150):
+        text = random_function(1000 * warp + seed)
+        if text.count("%v") > 400:      # well past the interpreter's 256 values
+            continue
+        try:
+            ref, res = _run_both(reference, text, warp, 8, seed, None, max_steps=3000)
+        except darm.DarmUserError as e:
+            assert "at most" in str(e)   # a documented limit, not a wrong result
+            continue
+        _assert_equal(f"fuzz seed {1000 * warp + seed} warp {warp}", ref, res)
+        ran += 1
+    assert ran >= 140
