@@ -44,6 +44,7 @@ struct SradParams {
   double *roi_out;       // [roi_rows][roi_groups][2] partial sums of J' (may be null)
   int cols, tile_rows, r0, R, rs;
   float lq;              // lambda / 4
+  float nz;              // -0.0f (opaque to ptxas: see mulx)
   int roi_r1, roi_r2, roi_c1, roi_c2, roi_w0, roi_groups;
 };
 
@@ -101,7 +102,97 @@ __device__ __forceinline__ float srad_coeff(float jc, float n, float s, float w,
   return c;
 }
 
-template <bool M, bool FAST>
+// ---- two pixels per instruction: packed fp32 pairs (sm_100 f32x2).  Every
+// half is the IEEE operation of the scalar code.  ptxas (12.9) contracts a
+// mul.rn.f32x2 feeding an add.rn.f32x2 into FFMA2 even under -fmad=false, so
+// the IEEE path forms products as mulx = fma(a, b, z) with z = -0.0f from a
+// kernel parameter (exact: a*b + -0 == a*b, and not foldable).
+__device__ __forceinline__ unsigned long long pk(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+#define DARM_F2(NAME, OP)                                                                     \
+  __device__ __forceinline__ float2 NAME(float2 a, float2 b) {                                \
+    unsigned long long r;                                                                     \
+    asm(OP ".rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));                       \
+    return upk(r);                                                                            \
+  }
+DARM_F2(add2, "add")
+DARM_F2(sub2, "sub")
+DARM_F2(mul2, "mul")
+#undef DARM_F2
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+  return upk(r);
+}
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+
+__device__ __forceinline__ float2 mulx(float2 a, float2 b, float2 z) { return fma2(a, b, z); }
+// (the fast form's product feeds a subtraction / addition: mulx, not mul2)
+template <bool FAST>
+__device__ __forceinline__ float2 sdiv2(float2 a, float2 b, float2 z) {
+  if constexpr (FAST) return mulx(a, make_float2(rcp_approx(b.x), rcp_approx(b.y)), z);
+  else return make_float2(a.x / b.x, a.y / b.y);
+}
+
+// R_D for one pixel of a pair (same arms as srad_coeff's)
+template <bool M>
+__device__ __forceinline__ float clamp_rd(float c) {
+  if constexpr (!M) {
+    if (c < 0.0f) {
+      DARM_ARM("srad.rd2.lo");
+      c = 0.0f;
+    } else if (c > 1.0f) {
+      DARM_ARM("srad.rd2.hi");
+      c = 1.0f;
+    }
+    return c;
+  } else {
+    return c < 0.0f ? 0.0f : (c > 1.0f ? 1.0f : c);
+  }
+}
+
+// srad_coeff for two pixels at once (rows i and i+1 of one column)
+template <bool M, bool FAST, bool PACK>
+__device__ __forceinline__ float2 srad_coeff2(float2 jc, float2 n, float2 s, float2 w, float2 e, float q0sqr,
+                                              float q0den, float2 z) {
+  if constexpr (!PACK)
+    return make_float2(srad_coeff<M, FAST>(jc.x, n.x, s.x, w.x, e.x, q0sqr, q0den),
+                       srad_coeff<M, FAST>(jc.y, n.y, s.y, w.y, e.y, q0sqr, q0den));
+  const float2 dN = sub2(n, jc), dS = sub2(s, jc), dW = sub2(w, jc), dE = sub2(e, jc);
+  float2 g2, l, num, den, qsqr;
+  if constexpr (FAST) {
+    g2 = sdiv2<FAST>(fma2(dE, dE, fma2(dW, dW, fma2(dS, dS, mul2(dN, dN)))), mul2(jc, jc), z);
+    l = sdiv2<FAST>(add2(add2(add2(dN, dS), dW), dE), jc, z);
+    num = fma2(f2(-1.0f / 16.0f), mul2(l, l), mul2(f2(0.5f), g2));
+    den = fma2(f2(0.25f), l, f2(1.0f));
+    qsqr = sdiv2<FAST>(num, mul2(den, den), z);
+  } else {
+    g2 = sdiv2<FAST>(add2(add2(add2(mulx(dN, dN, z), mulx(dS, dS, z)), mulx(dW, dW, z)), mulx(dE, dE, z)),
+                     mulx(jc, jc, z), z);
+    l = sdiv2<FAST>(add2(add2(add2(dN, dS), dW), dE), jc, z);
+    num = sub2(mulx(f2(0.5f), g2, z), mulx(f2(1.0f / 16.0f), mulx(l, l, z), z));
+    den = add2(f2(1.0f), mulx(f2(0.25f), l, z));
+    qsqr = sdiv2<FAST>(num, mulx(den, den, z), z);
+  }
+  den = sdiv2<FAST>(sub2(qsqr, f2(q0sqr)), f2(q0den), z);
+  const float2 one_den = add2(f2(1.0f), den);
+  float2 c;
+  if constexpr (FAST)
+    c = make_float2(rcp_approx(one_den.x), rcp_approx(one_den.y));
+  else
+    c = make_float2(1.0f / one_den.x, 1.0f / one_den.y);
+  return make_float2(clamp_rd<M>(c.x), clamp_rd<M>(c.y));
+}
+
+template <bool M, bool FAST, bool PACK>
 __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
   const int lane = threadIdx.x & 31;
   const int wcol = blockIdx.x * 8 + (threadIdx.x >> 5);   // warp column group
@@ -145,43 +236,8 @@ __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
     }
   };
   const int g0 = P.r0 + seg0;
-  // window at the segment start: rows g0-1, g0, g0+1
-  float jm1 = row(g0 - 1)[jc], j0 = row(g0)[jc], jp1 = row(g0 + 1)[jc];
-  float w0, e0;
-  west_east(row(g0), j0, w0, e0);
-  float c0 = srad_coeff<M, FAST>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
-  float jp2 = row(g0 + 2)[jc];
-  // sliding row pointers: p1 -> row g+1 (lane 31's east value), pn -> the
-  // next row to prefetch (g+3, held at the last row the buffer/image has)
-  const int glim = min(gmax, P.r0 + P.tile_rows + 1);
-  const float *p1 = row(g0 + 1);
-  int g1 = min(g0 + 1, gmax);
-  int gn = min(g0 + 3, glim);
-  const float *pn = row(gn);
   const bool roi_warp = P.roi_out && wcol >= P.roi_w0 && wcol < P.roi_w0 + P.roi_groups;
-  float *outp = P.jout + size_t(seg0 + 1) * cols + j;
-  for (int i = seg0; i < seg1; ++i) {
-    const int g = P.r0 + i;
-    const float jp3 = pn[jc];                              // prefetch
-    // c at row g+1 (clamped: at the last image row it is c(g) itself)
-    float w1, e1;
-    west_east(p1, jp1, w1, e1);
-    const float c1 = (g + 1 <= gmax) ? srad_coeff<M, FAST>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
-    // east neighbour's c at row g
-    float ce = __shfl_down_sync(0xffffffffu, c0, 1);
-    if (j >= cols - 1) ce = c0;
-    // update row g
-    const float dN = jm1 - j0, dS = jp1 - j0, dW = w0 - j0, dE = e0 - j0;
-    float d, jn;
-    if constexpr (FAST) {
-      d = __fmaf_rn(ce, dE, __fmaf_rn(c0, dW, __fmaf_rn(c1, dS, c0 * dN)));
-      jn = __fmaf_rn(P.lq, d, j0);
-    } else {
-      d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
-      jn = j0 + P.lq * d;
-    }
-    if (out_lane) *outp = jn;
-    outp += cols;
+  auto roi_row = [&](int g, float jn) {
     if (roi_warp && g >= P.roi_r1 && g <= P.roi_r2) {
       const bool in = out_lane && j >= P.roi_c1 && j <= P.roi_c2;
       double s = in ? double(jn) : 0.0, s2 = in ? double(jn) * double(jn) : 0.0;
@@ -196,22 +252,92 @@ __global__ void __launch_bounds__(256) srad_sweep_kernel(SradParams P) {
         dst[1] = s2;
       }
     }
-    // slide the window
-    jm1 = j0;
-    j0 = jp1;
-    jp1 = jp2;
-    jp2 = jp3;
-    w0 = w1;
-    e0 = e1;
-    c0 = c1;
-    if (g1 < gmax) {
-      ++g1;
-      p1 += cols;
+  };
+  // rows past the image clamp to its last row; the buffer holds rows up to glim
+  const int glim = min(gmax, P.r0 + P.tile_rows + 1);
+  auto rowc = [&](int g) { return row(min(g, glim)); };
+  // window at the segment start: rows g0-1 .. g0+3, c and west / east of row g0
+  float jm1 = row(g0 - 1)[jc], j0 = row(g0)[jc], jp1 = rowc(g0 + 1)[jc], jp2 = rowc(g0 + 2)[jc];
+  float jp3 = rowc(g0 + 3)[jc];
+  float w0, e0;
+  west_east(row(g0), j0, w0, e0);
+  float c0 = srad_coeff<M, FAST>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
+  float *outp = P.jout + size_t(seg0 + 1) * cols + j;
+  const float2 z = f2(P.nz);
+  int i = seg0;
+  // two rows (g, g+1) per iteration, their arithmetic in f32x2 pairs
+  for (; i + 1 < seg1; i += 2) {
+    const int g = P.r0 + i;
+    const float q4 = rowc(g + 4)[jc], q5 = rowc(g + 5)[jc];   // next iteration's rows, in flight
+    float w1, e1, w2, e2;
+    west_east(rowc(g + 1), jp1, w1, e1);
+    west_east(rowc(g + 2), jp2, w2, e2);
+    const float2 cc = srad_coeff2<M, FAST, PACK>(make_float2(jp1, jp2), make_float2(j0, jp1), make_float2(jp2, jp3),
+                                           make_float2(w1, w2), make_float2(e1, e2), q0sqr, q0den, z);
+    const float c1 = (g + 1 <= gmax) ? cc.x : c0;           // c at the rows below (clamped at the bottom)
+    const float c2 = (g + 2 <= gmax) ? cc.y : c1;
+    float ce0 = __shfl_down_sync(0xffffffffu, c0, 1), ce1 = __shfl_down_sync(0xffffffffu, c1, 1);
+    if (j >= cols - 1) {
+      ce0 = c0;
+      ce1 = c1;
     }
-    if (gn < glim) {
-      ++gn;
-      pn += cols;
+    const float2 jv = make_float2(j0, jp1), cv = make_float2(c0, c1), cs = make_float2(c1, c2);
+    const float2 dN = sub2(make_float2(jm1, j0), jv), dS = sub2(make_float2(jp1, jp2), jv);
+    const float2 dW = sub2(make_float2(w0, w1), jv), dE = sub2(make_float2(e0, e1), jv);
+    const float2 ce = make_float2(ce0, ce1);
+    float2 jn;
+    if constexpr (!PACK) {
+      if constexpr (FAST) {
+        const float dx = __fmaf_rn(ce.x, dE.x, __fmaf_rn(cv.x, dW.x, __fmaf_rn(cs.x, dS.x, cv.x * dN.x)));
+        const float dy = __fmaf_rn(ce.y, dE.y, __fmaf_rn(cv.y, dW.y, __fmaf_rn(cs.y, dS.y, cv.y * dN.y)));
+        jn = make_float2(__fmaf_rn(P.lq, dx, jv.x), __fmaf_rn(P.lq, dy, jv.y));
+      } else {
+        const float dx = ((cv.x * dN.x + cs.x * dS.x) + cv.x * dW.x) + ce.x * dE.x;
+        const float dy = ((cv.y * dN.y + cs.y * dS.y) + cv.y * dW.y) + ce.y * dE.y;
+        jn = make_float2(jv.x + P.lq * dx, jv.y + P.lq * dy);
+      }
+    } else if constexpr (FAST) {
+      const float2 d = fma2(ce, dE, fma2(cv, dW, fma2(cs, dS, mul2(cv, dN))));
+      jn = fma2(f2(P.lq), d, jv);
+    } else {
+      const float2 d = add2(add2(add2(mulx(cv, dN, z), mulx(cs, dS, z)), mulx(cv, dW, z)), mulx(ce, dE, z));
+      jn = add2(jv, mulx(f2(P.lq), d, z));
     }
+    if (out_lane) {
+      outp[0] = jn.x;
+      outp[cols] = jn.y;
+    }
+    outp += 2 * cols;
+    roi_row(g, jn.x);
+    roi_row(g + 1, jn.y);
+    // slide by two rows
+    jm1 = jp1;
+    j0 = jp2;
+    jp1 = jp3;
+    jp2 = q4;
+    jp3 = q5;
+    w0 = w2;
+    e0 = e2;
+    c0 = c2;
+  }
+  if (i < seg1) {   // an odd last row
+    const int g = P.r0 + i;
+    float w1, e1;
+    west_east(rowc(g + 1), jp1, w1, e1);
+    const float c1 = (g + 1 <= gmax) ? srad_coeff<M, FAST>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
+    float ce = __shfl_down_sync(0xffffffffu, c0, 1);
+    if (j >= cols - 1) ce = c0;
+    const float dN = jm1 - j0, dS = jp1 - j0, dW = w0 - j0, dE = e0 - j0;
+    float d, jn;
+    if constexpr (FAST) {
+      d = __fmaf_rn(ce, dE, __fmaf_rn(c0, dW, __fmaf_rn(c1, dS, c0 * dN)));
+      jn = __fmaf_rn(P.lq, d, j0);
+    } else {
+      d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
+      jn = j0 + P.lq * d;
+    }
+    if (out_lane) *outp = jn;
+    roi_row(g, jn);
   }
 }
 
@@ -295,6 +421,7 @@ cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const 
   P.R = R;
   P.rs = 128;
   P.lq = 0.25f * lambda;
+  P.nz = -0.0f;
   P.roi_r1 = roi.r1;
   P.roi_r2 = roi.r2;
   P.roi_c1 = roi.c1;
@@ -304,11 +431,17 @@ cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const 
   const int wgroups = (cols + 29) / 30;
   dim3 grid((wgroups + 7) / 8, (tile_rows + P.rs - 1) / P.rs);
   const bool fast = variant & 0x100;   // DARM_FAST_MATH
+  // f32x2 pairs only where they pay (measured, 16384^2 x 100): the melded
+  // fast path (105.2 -> 101.8 ms).  The unmelded form's per-pixel R_D branches
+  // split every pair (126 -> 147 ms) and the IEEE path's scalar divisions
+  // around packed products lose too (157 -> 184 ms): both run two rows per
+  // iteration in scalar code.
   if (variant & 1)
-    fast ? srad_sweep_kernel<true, true><<<grid, 256, 0, s>>>(P) : srad_sweep_kernel<true, false><<<grid, 256, 0, s>>>(P);
+    fast ? srad_sweep_kernel<true, true, true><<<grid, 256, 0, s>>>(P)
+         : srad_sweep_kernel<true, false, false><<<grid, 256, 0, s>>>(P);
   else
-    fast ? srad_sweep_kernel<false, true><<<grid, 256, 0, s>>>(P)
-         : srad_sweep_kernel<false, false><<<grid, 256, 0, s>>>(P);
+    fast ? srad_sweep_kernel<false, true, false><<<grid, 256, 0, s>>>(P)
+         : srad_sweep_kernel<false, false, false><<<grid, 256, 0, s>>>(P);
   return cudaGetLastError();
 }
 

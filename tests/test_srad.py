@@ -139,6 +139,9 @@ class _ThreadDist:
     def get_world_size(self):
         return self.world
 
+    def get_backend(self):
+        return "nccl"   # device tensors straight through, like NCCL
+
     def get_rank(self):
         return self.local.rank
 
