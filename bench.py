@@ -591,6 +591,22 @@ def our_arm(args):
         row["speedup"] = row["unmelded_us"] / row["melded_us"]
         row["keys_per_thread"] = 1
         per_kernel["bitonic_1key"] = row
+        # bucket sweep (B = 256 .. 4096; 16 keys per
+        # thread, buckets over 512 keys span warps and exchange through shared memory)
+        for Bs in (256, 1024, 4096):
+            want_s = torch.sort(pristine.view(-1, Bs), dim=1).values.view(-1)
+            row = {}
+            for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
+                step = darm.bitonic_sort(work, Bs, variant, stream=stream.cuda_stream, want_stats=False,
+                                         prepare_only=True)
+                t = time_steps(torch, stream, lambda: work.copy_(pristine), step, args.steps, args.warmup, flush)
+                if not torch.equal(work, want_s):
+                    raise SystemExit(f"bitonic B={Bs} {vname}: result is not the bucket-sorted input")
+                row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(t) / len(t))
+            row["speedup"] = row["unmelded_us"] / row["melded_us"]
+            row["keys_per_thread"] = 16
+            row["melded_hbm_gbs"] = 8 * n / (row["melded_us"] * 1e-6) / 1e9
+            per_kernel[f"bitonic_B{Bs}"] = row
 
     if rank != 0:
         if dist:

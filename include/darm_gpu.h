@@ -122,19 +122,22 @@ int darm_gpu_execute_warps(const char *kernel, int variant, int warp,
 /* ---- bitonic sort: the corpus compare-exchange step (corpus/bitonic.ir:6-43)
  *      chained over every stage dir = 2..bucket and stride k = dir/2..1 -------
  * Sorts each of the n/bucket consecutive buckets ascending, in place.
- * bucket: power of two in [2, 1024]; n % bucket == 0.  The chained-step
+ * bucket: power of two in [2, 4096]; n % bucket == 0.  The chained-step
  * semantics equal the reference driver's executeWarp chain for bucket <= 64
- * (oracle: oracle/ref_shim.cpp ref_bitonic_sort). */
+ * (oracle: oracle/ref_shim.cpp ref_bitonic_sort); larger buckets are pinned by
+ * sortedness and the C restatement. */
 int darm_gpu_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket,
                           int mem, void *stream, darm_gpu_stats *stats,
                           char *err, size_t errlen);
 
 /* Same, choosing how many IR lanes (keys) one hardware thread carries:
  *   1        one key per thread: an IR warp of `bucket` lanes is `bucket`
- *            threads (the shape the reference interpreter runs);
+ *            threads (the shape the reference interpreter runs; bucket <= 1024);
  *   4, 8, 16 register-blocked: a thread holds that many consecutive keys of a
- *            bucket, strides below it are exchanged inside the thread
- *            (needs bucket / keys_per_thread <= 32, 16-byte aligned keys);
+ *            bucket, strides below it are exchanged inside the thread, across
+ *            threads of a warp by shuffles, across warps (buckets over
+ *            32 * keys_per_thread) through shared memory (needs
+ *            bucket / keys_per_thread <= 256, 16-byte aligned keys);
  *   0        the fastest supported (what darm_gpu_bitonic_sort uses).
  * stats->reserved receives the keys per thread used.
  * HOST mode with n >= 2^22 keys pipelines 2^21-key chunks over three internal
@@ -149,7 +152,8 @@ int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket,
  *      chained over p = 1..bucket/2, k = p..1 ----------------------------------
  * Sorts each of the n/bucket consecutive buckets ascending, in place; the
  * arguments, shapes (keys_per_thread), HOST-mode pipelining and stats are those
- * of darm_gpu_bitonic_sort_ex.  The chained-step semantics equal the
+ * of darm_gpu_bitonic_sort_ex, with bucket <= 1024 and
+ * bucket / keys_per_thread <= 32 (a bucket stays inside a warp).  The chained-step semantics equal the
  * reference interpreter's executeWarp chain of the IR step for bucket <= 64
  * (oracle: oracle/ref_shim.cpp ref_chain_sort). */
 int darm_gpu_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket,
@@ -168,7 +172,7 @@ int darm_gpu_merge_sort(int variant, int32_t *keys, int64_t n, int mem,
                         size_t errlen);
 
 /* ---- N-Queens (NQU; the reference has no code for it):
- *      paper_2107_05681_b200/ir/nqueens_step.ir run to completion per thread -
+ *      paper_2107_05681_b200/ir/nqueens_sym.ir run to completion per thread -
  * Counts the placements of n non-attacking queens on an n x n board (2 <= n
  * <= 31).  The search space is split into the valid placements of the first
  * prefix_rows rows (1 <= prefix_rows <= n-1), enumerated lowest free column

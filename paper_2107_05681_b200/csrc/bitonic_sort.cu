@@ -155,23 +155,29 @@ __device__ __forceinline__ void load_keys(int32_t (&v)[R], const int32_t *__rest
 template <bool M, int B, int R, bool PF>
 __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
   constexpr int LB = __builtin_ctz(B), LR = __builtin_ctz(R), P = B / R;
-  static_assert(R >= 4 && R <= B && P <= 32, "R keys per thread, at most 32 threads per bucket");
-  constexpr uint32_t kTile = 32u * R;
+  static_assert(R >= 4 && R <= B && P <= 256, "R keys per thread, at most 256 threads per bucket");
+  // kCta: a bucket spans warps (B > 32 R, up to 4096 keys): the CTA walks
+  // 256 R-key tiles and strides k >= 32 R exchange through shared memory
+  constexpr bool kCta = P > 32;
+  constexpr uint32_t kTile = (kCta ? 256u : 32u) * R;
+  __shared__ int32_t xch[kCta ? 2 : 1][kCta ? R : 1][kCta ? 256 : 1];   // [buffer][register][thread]: conflict-free
   const int lane = int(threadIdx.x) & 31;
-  const int tib = lane & (P - 1);                       // thread index within the bucket
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const int tid = kCta ? int(threadIdx.x) : lane;       // thread index within the tile
+  const int tib = tid & (P - 1);                        // thread index within the bucket
+  const uint32_t units = kCta ? gridDim.x : (gridDim.x * blockDim.x) >> 5;   // tile walkers (CTAs or warps)
   const uint32_t tiles = (n + kTile - 1) / kTile;
-  uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t tile = kCta ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int par = 0;
   int32_t nxt[R];
-  if (PF && tile < tiles) load_keys<R>(nxt, keys, tile * kTile + uint32_t(lane) * R, n);
-  for (; tile < tiles; tile += warps) {
-    const uint32_t base = tile * kTile + uint32_t(lane) * R;
+  if (PF && tile < tiles) load_keys<R>(nxt, keys, tile * kTile + uint32_t(tid) * R, n);
+  for (; tile < tiles; tile += units) {
+    const uint32_t base = tile * kTile + uint32_t(tid) * R;
     const bool live = base < n;
     int32_t v[R];
     if constexpr (PF) {
 #pragma unroll
       for (int j = 0; j < R; ++j) v[j] = nxt[j];
-      if (tile + warps < tiles) load_keys<R>(nxt, keys, base + warps * kTile, n);   // next tile in flight
+      if (tile + units < tiles) load_keys<R>(nxt, keys, base + units * kTile, n);   // next tile in flight
     } else {
       load_keys<R>(v, keys, base, n);
     }
@@ -224,12 +230,22 @@ __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32
             }
           }
         } else {
-          // partner thread lane ^ k/R holds the partner keys in the same registers
+          // partner thread tib ^ k/R holds the partner keys in the same registers
           const int pk = k / R;
           const bool keep = !(tib & pk);                  // icmp.lt %t %j
           int32_t b0[R];
+          if (pk < 32) {
 #pragma unroll
-          for (int j = 0; j < R; ++j) b0[j] = __shfl_xor_sync(0xffffffffu, v[j], pk);   // load.shared buf %j
+            for (int j = 0; j < R; ++j) b0[j] = __shfl_xor_sync(0xffffffffu, v[j], pk);   // load.shared buf %j
+          } else if constexpr (kCta) {
+            // another warp: one exchange through double-buffered shared memory
+#pragma unroll
+            for (int j = 0; j < R; ++j) xch[par][j][threadIdx.x] = v[j];
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < R; ++j) b0[j] = xch[par][j][threadIdx.x ^ pk];
+            par ^= 1;
+          }
           if constexpr (M) {
 #pragma unroll
             for (int j = 0; j < R; ++j) {
@@ -320,23 +336,45 @@ cudaError_t launch_reg_pf(int32_t *keys, int64_t n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Buckets that span warps: CTAs walk 256*R-key tiles, as many CTAs as fit
+// (each with the same tile count, up to one).
+template <bool M, int B, int R>
+cudaError_t launch_reg_cta(int32_t *keys, int64_t n, cudaStream_t s) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bitonic_sort_reg_kernel<M, B, R, true>, 256, 0);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+  }
+  const int64_t tiles = (n + 256 * R - 1) / (256 * R);
+  const int64_t max_ctas = int64_t(sm_count()) * per_sm;
+  const int64_t iters = (tiles + max_ctas - 1) / max_ctas;
+  int64_t grid = (tiles + iters - 1) / iters;
+  if (grid < 1) grid = 1;
+  bitonic_sort_reg_kernel<M, B, R, true><<<int(grid), 256, 0, s>>>(keys, uint32_t(n));
+  return cudaGetLastError();
+}
+
 template <bool M, int B, int R>
 cudaError_t launch_reg(int32_t *keys, int64_t n, cudaStream_t s) {
-  return launch_reg_pf<M, B, R, true>(keys, n, s);
+  if constexpr (B / R > 32) return launch_reg_cta<M, B, R>(keys, n, s);
+  else return launch_reg_pf<M, B, R, true>(keys, n, s);
 }
 
 template <bool M, int B>
 cudaError_t launch_r(int32_t *keys, int64_t n, int r, cudaStream_t s) {
-  if constexpr (B >= 4 && B / 4 <= 32) {
+  if constexpr (B >= 4 && B / 4 <= 256) {
     if (r == 4) return launch_reg<M, B, 4>(keys, n, s);
   }
-  if constexpr (B >= 8 && B / 8 <= 32) {
+  if constexpr (B >= 8 && B / 8 <= 256) {
     if (r == 8) return launch_reg<M, B, 8>(keys, n, s);
   }
-  if constexpr (B >= 16 && B / 16 <= 32) {
+  if constexpr (B >= 16 && B / 16 <= 256) {
     if (r == 16) return launch_reg<M, B, 16>(keys, n, s);
   }
-  if (r == 1) return launch_b<M, B>(keys, n, s);
+  if constexpr (B <= 1024) {
+    if (r == 1) return launch_b<M, B>(keys, n, s);
+  }
   return cudaErrorInvalidValue;
 }
 
@@ -353,6 +391,8 @@ cudaError_t launch_m(int32_t *keys, int64_t n, int bucket, int r, cudaStream_t s
     case 256: return launch_r<M, 256>(keys, n, r, s);
     case 512: return launch_r<M, 512>(keys, n, r, s);
     case 1024: return launch_r<M, 1024>(keys, n, r, s);
+    case 2048: return launch_r<M, 2048>(keys, n, r, s);
+    case 4096: return launch_r<M, 4096>(keys, n, r, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -360,23 +400,24 @@ cudaError_t launch_m(int32_t *keys, int64_t n, int bucket, int r, cudaStream_t s
 }  // namespace
 
 bool bitonic_sort_supported(int bucket) {
-  return bucket >= 2 && bucket <= 1024 && (bucket & (bucket - 1)) == 0;
+  return bucket >= 2 && bucket <= 4096 && (bucket & (bucket - 1)) == 0;
 }
 
-// keys_per_thread: 1 = one key per thread (the IR warp shape), 4 / 8 / 16 =
-// register-blocked (needs 16-byte aligned keys and bucket / r <= 32), 0 = the
-// fastest supported: 16 for buckets 32..512, the bucket itself for 4..16.
-int bitonic_keys_per_thread(int bucket, int keys_per_thread, const void *keys) {
+// keys_per_thread: 1 = one key per thread (the IR warp shape, buckets up to
+// 1024), 4 / 8 / 16 = register-blocked (needs 16-byte aligned keys and
+// bucket / r <= max_threads: 256 for bitonic, 32 for PCM), 0 = the fastest
+// supported: 16 where bucket / 16 fits, the bucket itself for 4..16, else 1.
+// -1: not supported.
+int bitonic_keys_per_thread(int bucket, int keys_per_thread, const void *keys, int max_threads) {
   const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
   if (keys_per_thread == 0) {
-    if (!aligned) return 1;
-    if (bucket >= 32 && bucket <= 512) return 16;
-    if (bucket >= 4 && bucket <= 16) return bucket;
-    return 1;
+    if (bucket >= 32 && bucket / 16 <= max_threads && aligned) return 16;
+    if (bucket >= 4 && bucket <= 16 && aligned) return bucket;
+    return bucket <= 1024 ? 1 : -1;
   }
-  if (keys_per_thread == 1) return 1;
+  if (keys_per_thread == 1) return bucket <= 1024 ? 1 : -1;
   if (keys_per_thread != 4 && keys_per_thread != 8 && keys_per_thread != 16) return -1;
-  if (!aligned || keys_per_thread > bucket || bucket / keys_per_thread > 32) return -1;
+  if (!aligned || keys_per_thread > bucket || bucket / keys_per_thread > max_threads) return -1;
   return keys_per_thread;
 }
 

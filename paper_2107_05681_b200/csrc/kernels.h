@@ -34,8 +34,9 @@ extern const int kCorpusCount;
 
 // bitonic_sort.cu
 bool bitonic_sort_supported(int bucket);
-// resolves keys_per_thread (0 = auto) for this bucket / pointer; -1 = unsupported
-int bitonic_keys_per_thread(int bucket, int keys_per_thread, const void *keys);
+// resolves keys_per_thread (0 = auto) for this bucket / pointer, at most
+// max_threads threads per bucket; -1 = unsupported
+int bitonic_keys_per_thread(int bucket, int keys_per_thread, const void *keys, int max_threads);
 cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread,
                                 cudaStream_t s, int *launches);
 

@@ -436,21 +436,26 @@ using NetworkLaunch = cudaError_t (*)(int, int32_t *, int64_t, int, int, cudaStr
 
 // Bucket sorts built from a one-warp network step (bitonic.ir, oddeven_step.ir):
 // argument checks, HOST-mode staging (pipelined for large inputs), stats.
-static int network_sort(NetworkLaunch launch, int variant, int32_t *keys, int64_t n, int bucket,
-                        int keys_per_thread, int mem, void *stream, darm_gpu_stats *stats, char *err,
-                        size_t errlen) {
+// max_bucket / max_threads: the largest bucket and threads per bucket the
+// network's kernels take (bitonic 4096 / 256: buckets may span warps; PCM
+// 1024 / 32).
+static int network_sort(NetworkLaunch launch, int max_bucket, int max_threads, int variant, int32_t *keys,
+                        int64_t n, int bucket, int keys_per_thread, int mem, void *stream, darm_gpu_stats *stats,
+                        char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
-    if (!bitonic_sort_supported(bucket)) user_error("bucket must be a power of two in [2, 1024]");
+    if (!bitonic_sort_supported(bucket) || bucket > max_bucket)
+      user_error("bucket must be a power of two in [2, " + std::to_string(max_bucket) + "]");
     if (n < 0 || n % bucket) user_error("n must be a non-negative multiple of the bucket size");
     if (n >= (int64_t(1) << 31)) user_error("too many keys (limit 2^31 - 1)");
     if (n && !keys) user_error("keys is NULL");
     if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
     // HOST mode stages through a cudaMalloc'd (aligned) buffer
-    const int kpt = bitonic_keys_per_thread(bucket, keys_per_thread, mem == DARM_MEM_DEVICE ? keys : nullptr);
+    const int kpt =
+        bitonic_keys_per_thread(bucket, keys_per_thread, mem == DARM_MEM_DEVICE ? keys : nullptr, max_threads);
     if (kpt < 0)
-      user_error("keys_per_thread must be 0, 1, 4, 8 or 16, with bucket / keys_per_thread <= 32 and "
-                 "16-byte aligned keys");
+      user_error("keys_per_thread must be 0, 1 (bucket <= 1024), 4, 8 or 16, with bucket / keys_per_thread <= " +
+                 std::to_string(max_threads) + " and 16-byte aligned keys");
     if (stats) std::memset(stats, 0, sizeof(*stats));
     DeviceState &st = device_state(nullptr);
     std::lock_guard<std::mutex> lk(st.mu);
@@ -517,13 +522,13 @@ static int network_sort(NetworkLaunch launch, int variant, int32_t *keys, int64_
 
 int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
                              void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
-  return network_sort(launch_bitonic_sort, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
+  return network_sort(launch_bitonic_sort, 4096, 256, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
                       errlen);
 }
 
 int darm_gpu_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
                           void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
-  return network_sort(launch_oddeven_sort, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
+  return network_sort(launch_oddeven_sort, 1024, 32, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
                       errlen);
 }
 

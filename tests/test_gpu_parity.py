@@ -150,7 +150,8 @@ def test_bitonic_sort_golden(kpt):
                 assert st["keys_per_thread"] == kpt
 
 
-BUCKET_KPT = [(B, r) for B in (4, 8, 16, 32, 64, 128, 256, 512) for r in (4, 8, 16) if r <= B and B // r <= 32]
+BUCKET_KPT = [(B, r) for B in (4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096) for r in (4, 8, 16)
+              if r <= B and B // r <= 256]
 
 
 @pytest.mark.parametrize("bucket,kpt", BUCKET_KPT)
@@ -184,11 +185,22 @@ def test_bitonic_sort_keys_per_thread_contract():
     with pytest.raises(darm.DarmError):
         darm.bitonic_sort(buf[:64 * 4], 64, 1, keys_per_thread=2)
     with pytest.raises(darm.DarmError):
-        darm.bitonic_sort(buf[:64 * 4], 1024, 1, keys_per_thread=16)
+        darm.bitonic_sort(buf[:64 * 3], 128, 1, keys_per_thread=16)   # n not a multiple of the bucket
+    big = torch.zeros(8192, dtype=torch.int32, device="cuda")
+    with pytest.raises(darm.DarmError):
+        darm.bitonic_sort(big, 4096, 1, keys_per_thread=8)            # 512 threads per bucket
+    with pytest.raises(darm.DarmError):
+        darm.bitonic_sort(big, 2048, 1, keys_per_thread=1)            # one key per thread: bucket <= 1024
+    with pytest.raises(darm.DarmError):
+        darm.bitonic_sort(big, 8192, 1)
+    with pytest.raises(darm.DarmError):
+        darm.oddeven_sort(big, 2048, 1)                               # PCM: bucket <= 1024
+    assert darm.oddeven_sort(big[:4096], 1024, 1)["keys_per_thread"] == 1
+    assert darm.bitonic_sort(big, 4096, 1)["keys_per_thread"] == 16
     assert darm.bitonic_sort(buf[:64 * 4], 64, 1)["keys_per_thread"] == 16
 
 
-@pytest.mark.parametrize("bucket", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("bucket", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
 def test_bitonic_sort_buckets(bucket, restatement):
     rng = np.random.default_rng(bucket)
     n = 1 << 20

@@ -24,8 +24,11 @@ def main(*buckets, sort=None):
     flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
     for B in buckets or (64,):
         want = torch.sort(pristine.view(-1, B), dim=1).values.view(-1)
+        wide = 256 if sort is darm.bitonic_sort else 32
         for kpt in (1, 4, 8, 16):
-            if kpt > 1 and (kpt > B or B // kpt > 32):
+            if kpt == 1 and B > 1024:
+                continue
+            if kpt > 1 and (kpt > B or B // kpt > wide):
                 continue
             res = {}
             for v in (darm.UNMELDED, darm.MELDED):
