@@ -87,7 +87,7 @@ constexpr int kMaxPend = kLook - 1;
 constexpr int kLdP = kMaxPend * BS + 1;
 constexpr int kPendFloats = BS * kLdP + kMaxPend * BS * LD + kPairs * (kMaxPend * BS * LD + BS * kLdP);
 
-template <bool M>
+template <bool M, int P>   // P: pending steps of the super-step (0..kLook-1), compile-time
 __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs, int O,
                                                                float *__restrict__ dst, int dstride) {
   __shared__ float dia[kPairs][BS][LD];
@@ -98,32 +98,14 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
   const int p = blockIdx.x * kPairs + warp;
   const bool have = p < npairs;                             // warp-uniform
   const size_t cb = size_t(o) + size_t(BS) * (p + 1);       // column of the row block = row of the column block
-  const int P = (o - O) / BS;                               // pending steps (block-uniform)
   float(*Lp)[kLdP] = reinterpret_cast<float(*)[kLdP]>(pend);
   float(*Ud)[LD] = reinterpret_cast<float(*)[LD]>(pend + BS * kLdP);
   float(*Ur)[LD] = reinterpret_cast<float(*)[LD]>(pend + BS * kLdP + kMaxPend * BS * LD +
                                                   warp * (kMaxPend * BS * LD + BS * kLdP));
   float(*Lc)[kLdP] = reinterpret_cast<float(*)[kLdP]>(reinterpret_cast<float *>(Ur) + kMaxPend * BS * LD);
-  if (P > 0) {
-    const int K = P * BS;
-    for (int e = threadIdx.x; e < BS * K; e += 32 * kPairs) {
-      const int rr = e / K, k = e % K;
-      Lp[rr][k] = a[(size_t(o) + rr) * n + O + k];
-    }
-    for (int e = threadIdx.x; e < K * BS; e += 32 * kPairs) {
-      const int k = e / BS, c = e % BS;
-      Ud[k][c] = a[(size_t(O) + k) * n + o + c];
-    }
-    if (have) {
-      for (int e = lane; e < K * BS; e += 32) {
-        const int k = e / BS, c = e % BS;
-        Ur[k][c] = a[(size_t(O) + k) * n + cb + c];
-        Lc[c][k] = a[(cb + c) * n + O + k];
-      }
-    }
-    __syncthreads();
-  }
-  // 1. requests in flight: the pair (2 float4 per lane per block) and the diagonal row of lane r
+  // 1. every global read of the launch in flight at once (one memory round
+  //    trip): the pair (2 float4 per lane per block), the diagonal row of lane
+  //    r, and the pending updates' L and U (float4 chunks, fixed counts)
   float4 rv[2], cv[2];
   if (have) {
 #pragma unroll
@@ -145,6 +127,56 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
       v[4 * q + 2] = t.z;
       v[4 * q + 3] = t.w;
     }
+  }
+  if constexpr (P > 0) {
+    constexpr int K = P * BS, K4 = K / 4, NT = 32 * kPairs;
+    constexpr int nL = BS * K4, nU = K * (BS / 4);            // float4 chunks of Lp / Ud (CTA-wide)
+    constexpr int nW = K * (BS / 4) / 32;                     // chunks of Ur and of Lc per lane
+    static_assert(nW * 32 == K * (BS / 4) && BS * K4 == K * (BS / 4), "chunk counts");
+    float4 lb[(nL + NT - 1) / NT], ub[(nU + NT - 1) / NT], urb[nW], lcb[nW];
+#pragma unroll
+    for (int j = 0; j < (nL + NT - 1) / NT; ++j) {
+      const int e = int(threadIdx.x) + NT * j;
+      if (e < nL) lb[j] = *reinterpret_cast<const float4 *>(a + (size_t(o) + e / K4) * n + O + 4 * (e % K4));
+    }
+#pragma unroll
+    for (int j = 0; j < (nU + NT - 1) / NT; ++j) {
+      const int e = int(threadIdx.x) + NT * j;
+      if (e < nU) ub[j] = *reinterpret_cast<const float4 *>(a + (size_t(O) + e / 4) * n + o + 4 * (e % 4));
+    }
+    if (have) {
+#pragma unroll
+      for (int j = 0; j < nW; ++j) {
+        const int e = lane + 32 * j;
+        urb[j] = *reinterpret_cast<const float4 *>(a + (size_t(O) + e / 4) * n + cb + 4 * (e % 4));
+        lcb[j] = *reinterpret_cast<const float4 *>(a + (cb + e / K4) * n + O + 4 * (e % K4));
+      }
+    }
+    auto put = [](float *d, float4 x) {
+      d[0] = x.x;
+      d[1] = x.y;
+      d[2] = x.z;
+      d[3] = x.w;
+    };
+#pragma unroll
+    for (int j = 0; j < (nL + NT - 1) / NT; ++j) {
+      const int e = int(threadIdx.x) + NT * j;
+      if (e < nL) put(&Lp[e / K4][4 * (e % K4)], lb[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < (nU + NT - 1) / NT; ++j) {
+      const int e = int(threadIdx.x) + NT * j;
+      if (e < nU) put(&Ud[e / 4][4 * (e % 4)], ub[j]);
+    }
+    if (have) {
+#pragma unroll
+      for (int j = 0; j < nW; ++j) {
+        const int e = lane + 32 * j;
+        put(&Ur[e / 4][4 * (e % 4)], urb[j]);
+        put(&Lc[e / K4][4 * (e % K4)], lcb[j]);
+      }
+    }
+    __syncthreads();
   }
   // the diagonal block's pending updates (lane r holds row r)
   for (int st = 0; st < P; ++st) {
@@ -284,20 +316,22 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
 // 16-column step after another (and of the restatement), so deferring the far
 // block's T updates into one pass over it leaves every bit unchanged while the
 // trailing matrix crosses HBM once per 64 columns instead of once per 16.
-constexpr int kFarRows = 128, kFarCols = 64;   // far-update tile
+constexpr int kFarRows = 128, kFarCols = 128;  // far-update tile
+constexpr int kFarThreads = 512;               // 16 warps: 4 per SMSP hide the shared-memory latency
 
 // The far trailing block's T-step update (the bulk of the FLOPs), persistent:
-// one CTA per SM walks the 128x64 tiles
-// of the far block; every tile's L rows (non-transposed, 16-byte chunks along
-// k), U rows and the tile of A itself are brought into shared memory with
-// cp.async while the previous tile computes (two stages).  Per 4 k's a thread
-// reads 8 float4 of L (its 8 rows) and 4 float4 of U (its 4 columns) for 64
-// FFMA2.  Per element the operation sequence above.
+// one 512-thread CTA per SM walks the 128x128 tiles of the far block.  A
+// tile's L rows (k along, 16-byte chunks) and U rows go to shared memory with
+// cp.async while the previous tile computes (two stages); the tile of A itself
+// goes straight to registers (thread = 8 rows x 4 columns), its loads in
+// flight during the first step's FMAs, which do not need it.  A warp shares
+// its 8 rows: L reads are broadcasts, U reads 512 contiguous bytes.  Per 4 k's
+// a thread reads 8 float4 of L and 4 float4 of U for 64 FFMA2 (the L operand
+// broadcast to both halves).  Per element the operation sequence above.
 constexpr int kPipeK = kLook * BS;                 // 64
 constexpr int kLdL = kPipeK + 4;                   // lp[r][k] row pitch
 constexpr int kLdU = kFarCols + 4;                 // up[k][c]
-constexpr int kLdV = kFarCols + 4;                 // vt[r][c]
-constexpr int kStageWords = kFarRows * kLdL + kPipeK * kLdU + kFarRows * kLdV;
+constexpr int kStageWords = kFarRows * kLdL + kPipeK * kLdU;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -308,33 +342,63 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(256, 1) lud_far_pipe_kernel(float *__restrict__ a, int n, int o, int T, int lo) {
+// The region a launch updates: up to two rectangles of the trailing matrix
+// (the look-ahead strips, or the far block), tiles numbered rectangle by
+// rectangle, row-major inside each.
+struct FarRects {
+  int rlo[2], rhi[2], clo[2], chi[2];
+  int tiles_c[2], first[2];   // tiles per row of tiles; first tile index of each rectangle
+  int tiles;
+};
+
+static FarRects far_rects(int n_rects, const int (*r)[4]) {
+  FarRects f{};
+  f.tiles = 0;
+  for (int i = 0; i < 2; ++i) {
+    const bool on = i < n_rects && r[i][1] > r[i][0] && r[i][3] > r[i][2];
+    f.rlo[i] = on ? r[i][0] : 0;
+    f.rhi[i] = on ? r[i][1] : 0;
+    f.clo[i] = on ? r[i][2] : 0;
+    f.chi[i] = on ? r[i][3] : 0;
+    f.tiles_c[i] = on ? (f.chi[i] - f.clo[i] + kFarCols - 1) / kFarCols : 1;
+    f.first[i] = f.tiles;
+    if (on) f.tiles += f.tiles_c[i] * ((f.rhi[i] - f.rlo[i] + kFarRows - 1) / kFarRows);
+  }
+  return f;
+}
+
+template <int T>   // steps in the super-step (kLook but for the last one): compile-time address math
+__global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__restrict__ a, int n, int o, FarRects R) {
   extern __shared__ __align__(16) float psm[];
-  const int m = n - lo;
-  const int tiles_c = (m + kFarCols - 1) / kFarCols, tiles_r = (m + kFarRows - 1) / kFarRows;
-  const int tiles = tiles_c * tiles_r;
-  const int K = T * BS, K4 = K / 4;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int tiles = R.tiles;
+  // tile -> its origin (r0, c0) and extent (nr, nc)
+  auto place = [&](int tile, int &r0, int &c0, int &nr, int &nc) {
+    const int i = tile >= R.first[1] && R.first[1] < R.tiles ? 1 : 0;
+    const int t = tile - R.first[i];
+    r0 = R.rlo[i] + kFarRows * (t / R.tiles_c[i]);
+    c0 = R.clo[i] + kFarCols * (t % R.tiles_c[i]);
+    nr = min(kFarRows, R.rhi[i] - r0);
+    nc = min(kFarCols, R.chi[i] - c0);
+  };
+  constexpr int K = T * BS, K4 = K / 4;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = 4 * tx, rb = 8 * ty;
   auto stage_ptr = [&](int st) { return psm + size_t(st) * kStageWords; };
   auto issue = [&](int tile, int st) {
-    float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL, *vt = up + kPipeK * kLdU;
-    const int r0 = lo + kFarRows * (tile / tiles_c), c0 = lo + kFarCols * (tile % tiles_c);
-    const int nr = min(kFarRows, n - r0), nc = min(kFarCols, n - c0);
-    for (int e = threadIdx.x; e < kFarRows * K4; e += 256) {          // L rows of the tile, k along
+    float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL;
+    int r0, c0, nr, nc;
+    place(tile, r0, c0, nr, nc);
+#pragma unroll
+    for (int e = threadIdx.x; e < kFarRows * K4; e += kFarThreads) {   // L rows of the tile, k along
       const int r = e / K4, k4 = e % K4;
       const bool ok = r < nr;
       cp_async16(lp + r * kLdL + 4 * k4, a + size_t(ok ? r0 + r : r0) * n + o + 4 * k4, ok);
     }
-    for (int e = threadIdx.x; e < K * (kFarCols / 4); e += 256) {      // U rows, columns of the tile
+#pragma unroll
+    for (int e = threadIdx.x; e < K * (kFarCols / 4); e += kFarThreads) {   // U rows, columns of the tile
       const int kk = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
       const bool ok = 4 * c4 < nc;
       cp_async16(up + kk * kLdU + 4 * c4, a + size_t(o + kk) * n + (ok ? c0 + 4 * c4 : c0), ok);
-    }
-    for (int e = threadIdx.x; e < kFarRows * (kFarCols / 4); e += 256) {   // the tile of A
-      const int r = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
-      const bool ok = r < nr && 4 * c4 < nc;
-      cp_async16(vt + r * kLdV + 4 * c4, a + size_t(ok ? r0 + r : r0) * n + (ok ? c0 + 4 * c4 : c0), ok);
     }
     cp_async_commit();
   };
@@ -342,6 +406,15 @@ __global__ void __launch_bounds__(256, 1) lud_far_pipe_kernel(float *__restrict_
   if (tile < tiles) issue(tile, 0);
   for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
     const int st = it & 1;
+    int r0, c0, nr, nc;
+    place(tile, r0, c0, nr, nc);
+    // this tile of A: in flight during step 0
+    const bool cok = c < nc;
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = (cok && rb + i < nr) ? *reinterpret_cast<const float4 *>(a + size_t(r0 + rb + i) * n + c0 + c)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
     const int next = tile + gridDim.x;
     if (next < tiles) {
       issue(next, st ^ 1);
@@ -350,33 +423,27 @@ __global__ void __launch_bounds__(256, 1) lud_far_pipe_kernel(float *__restrict_
       cp_async_wait<0>();
     }
     __syncthreads();
-    const float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL, *vt = up + kPipeK * kLdU;
-    const int r0 = lo + kFarRows * (tile / tiles_c), c0 = lo + kFarCols * (tile % tiles_c);
-    const int nr = min(kFarRows, n - r0), nc = min(kFarCols, n - c0);
-    float4 v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float4 *>(vt + (rb + i) * kLdV + c);
-    for (int t = 0; t < T; ++t) {
+    const float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL;
+#pragma unroll 1
+    for (int t = 0; t < (rb < nr ? T : 0); ++t) {   // warps with no rows in the tile (a band's edge) skip
       float2 acc[8][2];
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int k4 = 0; k4 < BS / 4; ++k4) {
         const int kb = t * BS + 4 * k4;
-        float4 l[8], u[4];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) l[i] = *reinterpret_cast<const float4 *>(lp + (rb + i) * kLdL + kb);
+        float4 u[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) u[q] = *reinterpret_cast<const float4 *>(up + (kb + q) * kLdU + c);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 u01 = make_float2(u[q].x, u[q].y), u23 = make_float2(u[q].z, u[q].w);
+        for (int i = 0; i < 8; ++i) {
+          const float4 l = *reinterpret_cast<const float4 *>(lp + (rb + i) * kLdL + kb);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float li = q == 0 ? l[i].x : q == 1 ? l[i].y : q == 2 ? l[i].z : l[i].w;
+          for (int q = 0; q < 4; ++q) {
+            const float li = q == 0 ? l.x : q == 1 ? l.y : q == 2 ? l.z : l.w;
             const float2 ll = make_float2(li, li);
-            acc[i][0] = fma2(ll, u01, acc[i][0]);
-            acc[i][1] = fma2(ll, u23, acc[i][1]);
+            acc[i][0] = fma2(ll, make_float2(u[q].x, u[q].y), acc[i][0]);
+            acc[i][1] = fma2(ll, make_float2(u[q].z, u[q].w), acc[i][1]);
           }
         }
       }
@@ -388,7 +455,7 @@ __global__ void __launch_bounds__(256, 1) lud_far_pipe_kernel(float *__restrict_
         v[i].w -= acc[i][1].y;
       }
     }
-    if (c < nc) {
+    if (cok) {
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (rb + i < nr) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
@@ -414,55 +481,134 @@ __global__ void lud_scatter_diag_kernel(float *__restrict__ a, int n, const floa
   a[size_t(BS * j + e / BS) * n + BS * j + e % BS] = dscr[size_t(j) * BS * BS + e];
 }
 
-cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches) {
+namespace {
+
+template <bool M>
+void launch_panel(float *a, int n, int o, int O, float *dscr, cudaStream_t s) {
   const int nb = n / BS;
+  const int m = nb - o / BS - 1;   // blocks right of / below the diagonal
+  const int grid = m > 0 ? (m + kPairs - 1) / kPairs : 1;
+  // the factored diagonal block goes to scratch slot o/16 (CTAs of this launch
+  // still read the unfactored one); the last one, with no other reader, in place
+  float *dst = m > 0 ? dscr + size_t(o / BS) * BS * BS : a + size_t(o) * n + o;
+  const int dstride = m > 0 ? BS : n;
+  const size_t shm = (o > O ? kPendFloats : 0) * sizeof(float);
+  switch ((o - O) / BS) {
+    case 0: lud_panel_kernel<M, 0><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride); break;
+    case 1: lud_panel_kernel<M, 1><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride); break;
+    case 2: lud_panel_kernel<M, 2><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride); break;
+    default: lud_panel_kernel<M, 3><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride); break;
+  }
+}
+
+// The panel launches of the super-step at O (T steps).
+void launch_panels(int variant, float *a, int n, int O, float *dscr, cudaStream_t s, int *launches) {
+  const int T = min(kLook, (n - O) / BS);
+  for (int t = 0; t < T; ++t) {
+    const int o = O + t * BS;
+    if (variant)
+      launch_panel<true>(a, n, o, O, dscr, s);
+    else
+      launch_panel<false>(a, n, o, O, dscr, s);
+    ++*launches;
+  }
+}
+
+cudaError_t launch_far(float *a, int n, int O, int T, const FarRects &R, int grid, cudaStream_t s) {
+  if (R.tiles == 0) return cudaSuccess;
+  const size_t shm = 2 * size_t(kStageWords) * sizeof(float);
+  grid = max(1, min(grid, R.tiles));
+  switch (T) {
+    case 1: lud_far_pipe_kernel<1><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
+    case 2: lud_far_pipe_kernel<2><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
+    case 3: lud_far_pipe_kernel<3><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
+    default: lud_far_pipe_kernel<4><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
+  }
+  return cudaGetLastError();
+}
+
+struct LudSide {       // per device: the panel stream of the look-ahead and its fork / join events
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+}  // namespace
+
+// Look-ahead across super-steps (two streams inside the captured graph):
+//   main   ... far strips(g) -> far block(g) -> [join] -> far strips(g+1) ...
+//   panel       [fork] -> panels(g+1) (4 launches) -> join
+// The strips are the rows and columns the next super-step's panels read
+// (the 64-wide L-shaped band at E = end of super-step g); once they hold
+// super-step g's updates the next panels run on the side stream while the
+// far block [E+64, n)^2 takes them on all but kPanelSMs SMs.  Disjoint
+// regions, and every element still receives its updates in step order.
+// SMs the far block leaves to the concurrent panels (measured at 8192:
+// 0 -> 15.65 ms, 4 -> 14.98, 8 -> 14.72, 16 -> 14.89, 32 -> 16.13)
+constexpr int kPanelSMs = 8;
+
+cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches) {
   static bool attr = false;
+  static int sms = 0;
   if (!attr) {
-    for (auto k : {lud_panel_kernel<false>, lud_panel_kernel<true>}) {
+    for (auto k : {lud_panel_kernel<false, 0>, lud_panel_kernel<false, 1>, lud_panel_kernel<false, 2>,
+                   lud_panel_kernel<false, 3>, lud_panel_kernel<true, 0>, lud_panel_kernel<true, 1>,
+                   lud_panel_kernel<true, 2>, lud_panel_kernel<true, 3>}) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(kPendFloats * sizeof(float)));
       if (e != cudaSuccess) return e;
     }
+    const int shm = int(2 * size_t(kStageWords) * sizeof(float));
+    for (auto k : {lud_far_pipe_kernel<1>, lud_far_pipe_kernel<2>, lud_far_pipe_kernel<3>, lud_far_pipe_kernel<4>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, shm);
+      if (e != cudaSuccess) return e;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
     attr = true;
   }
-  for (int O = 0; O < n; O += kLook * BS) {
+  static LudSide side[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  LudSide &sd = side[dev & 63];
+  if (!sd.s) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaError_t e = cudaStreamCreateWithPriority(&sd.s, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  const int nb = n / BS;
+  const int G = kLook * BS;
+  launch_panels(variant, a, n, 0, dscr, s, launches);   // super-step 0: nothing to overlap with
+  for (int O = 0; O < n; O += G) {
     const int T = min(kLook, (n - O) / BS);
-    const int E = O + T * BS;   // end of the super-step's columns / rows
-    for (int t = 0; t < T; ++t) {
-      const int o = O + t * BS;
-      const int m = nb - o / BS - 1;   // blocks right of / below the diagonal
-      const int grid = m > 0 ? (m + kPairs - 1) / kPairs : 1;
-      // the factored diagonal block goes to scratch slot o/16 (CTAs of this launch
-      // still read the unfactored one); the last one, with no other reader, in place
-      float *dst = m > 0 ? dscr + size_t(o / BS) * BS * BS : a + size_t(o) * n + o;
-      const int dstride = m > 0 ? BS : n;
-      const size_t shm = (t > 0 ? kPendFloats : 0) * sizeof(float);
-      if (variant)
-        lud_panel_kernel<true><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride);
-      else
-        lud_panel_kernel<false><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride);
-      ++*launches;
-      if (m == 0) break;
-    }
-    if (E < n) {
-      // the far trailing block [E, n)^2 takes the super-step's T updates
-      const int m = n - E;
-      const size_t shm = 2 * size_t(kStageWords) * sizeof(float);
-      static int sms = 0;
-      if (!sms) {
-        cudaError_t e = cudaFuncSetAttribute(lud_far_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(shm));
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-      }
-      const int tiles = ((m + kFarCols - 1) / kFarCols) * ((m + kFarRows - 1) / kFarRows);
-      lud_far_pipe_kernel<<<min(tiles, sms), 256, shm, s>>>(a, n, O, T, E);
-      cudaError_t e = cudaGetLastError();
+    const int E = O + T * BS;
+    if (E >= n) break;
+    const int Tn = min(kLook, (n - E) / BS);   // the next super-step's steps
+    const int F = E + Tn * BS;                  // end of its band
+    // the band the next panels read: rows [E, F) x cols [E, n), rows [F, n) x cols [E, F)
+    const int band[2][4] = {{E, F, E, n}, {F, n, E, F}};
+    cudaError_t e = launch_far(a, n, O, T, far_rects(2, band), sms, s);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    if (F < n) {
+      e = cudaEventRecord(sd.fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(sd.s, sd.fork, 0);
+      if (e != cudaSuccess) return e;
+      launch_panels(variant, a, n, E, dscr, sd.s, launches);
+      e = cudaEventRecord(sd.join, sd.s);
+      if (e != cudaSuccess) return e;
+      const int far[1][4] = {{F, n, F, n}};
+      e = launch_far(a, n, O, T, far_rects(1, far), sms - kPanelSMs, s);
       if (e != cudaSuccess) return e;
       ++*launches;
+      e = cudaStreamWaitEvent(s, sd.join, 0);
+      if (e != cudaSuccess) return e;
+    } else {
+      launch_panels(variant, a, n, E, dscr, s, launches);   // the last super-step: no far block left
     }
   }
   if (nb > 1) {
