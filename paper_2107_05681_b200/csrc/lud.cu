@@ -317,21 +317,26 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
 // block's T updates into one pass over it leaves every bit unchanged while the
 // trailing matrix crosses HBM once per 64 columns instead of once per 16.
 constexpr int kFarRows = 128, kFarCols = 128;  // far-update tile
-constexpr int kFarThreads = 512;               // 16 warps: 4 per SMSP hide the shared-memory latency
+constexpr int kFarThreads = 256;               // thread = 8 rows x 8 columns of the tile
 
 // The far trailing block's T-step update (the bulk of the FLOPs), persistent:
-// one 512-thread CTA per SM walks the 128x128 tiles of the far block.  A
-// tile's L rows (k along, 16-byte chunks) and U rows go to shared memory with
-// cp.async while the previous tile computes (two stages); the tile of A itself
-// goes straight to registers (thread = 8 rows x 4 columns), its loads in
-// flight during the first step's FMAs, which do not need it.  A warp shares
-// its 8 rows: L reads are broadcasts, U reads 512 contiguous bytes.  Per 4 k's
-// a thread reads 8 float4 of L and 4 float4 of U for 64 FFMA2 (the L operand
-// broadcast to both halves).  Per element the operation sequence above.
+// one 256-thread CTA per SM walks the 128x128 tiles of its region.  A tile's
+// L rows (k along, 16-byte chunks) and U rows go to shared memory with
+// cp.async while the previous tile computes (two stages), and so does the
+// tile of A (one buffer: copied to registers at the tile's start, then
+// refilled with the next tile's).  Thread (tx, ty) owns rows ty + 16 i (i < 8) and
+// columns 4 tx .. +3 and 64 + 4 tx .. +3: a warp's L reads are two rows 68
+// words apart (one wavefront), its U reads 256 contiguous bytes per half.
+// Per 4 k's a thread reads 8 float4 of L and 8 of U for 128 FFMA2 (the L
+// operand broadcast to both halves); the accumulators and the tile take 128
+// registers.  Band tiles (64 rows or 64 columns) run a half-size variant.
+// Per element the operation sequence above.
 constexpr int kPipeK = kLook * BS;                 // 64
 constexpr int kLdL = kPipeK + 4;                   // lp[r][k] row pitch
 constexpr int kLdU = kFarCols + 4;                 // up[k][c]
 constexpr int kStageWords = kFarRows * kLdL + kPipeK * kLdU;
+constexpr int kLdA = kFarCols + 4;                 // the A tile's staging buffer (single)
+constexpr int kFarSmemWords = 2 * kStageWords + kFarRows * kLdA;   // 205 KB
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -341,6 +346,53 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool va
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// T steps on one tile: NI row groups (of 16 rows: 8 = all, 4 = a 64-row band)
+// and NH column halves (2 = all, 1 = a 64-column band).
+template <int T, int NI, int NH>
+__device__ __forceinline__ void far_tile(const float *__restrict__ lp, const float *__restrict__ up, float4 (&v)[8][2],
+                                         int ty, int c1) {
+#pragma unroll 1
+  for (int t = 0; t < T; ++t) {
+    float2 acc[NI][2 * NH];
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+      for (int j = 0; j < 2 * NH; ++j) acc[i][j] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k4 = 0; k4 < BS / 4; ++k4) {
+      const int kb = t * BS + 4 * k4;
+      float4 l[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) l[i] = *reinterpret_cast<const float4 *>(lp + (ty + 16 * i) * kLdL + kb);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4 u[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) u[h] = *reinterpret_cast<const float4 *>(up + (kb + q) * kLdU + c1 + 64 * h);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const float li = q == 0 ? l[i].x : q == 1 ? l[i].y : q == 2 ? l[i].z : l[i].w;
+          const float2 ll = make_float2(li, li);
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            acc[i][2 * h] = fma2(ll, make_float2(u[h].x, u[h].y), acc[i][2 * h]);
+            acc[i][2 * h + 1] = fma2(ll, make_float2(u[h].z, u[h].w), acc[i][2 * h + 1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        v[i][h].x -= acc[i][2 * h].x;
+        v[i][h].y -= acc[i][2 * h].y;
+        v[i][h].z -= acc[i][2 * h + 1].x;
+        v[i][h].w -= acc[i][2 * h + 1].y;
+      }
+  }
+}
 
 // The region a launch updates: up to two rectangles of the trailing matrix
 // (the look-ahead strips, or the far block), tiles numbered rectangle by
@@ -381,9 +433,10 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
     nc = min(kFarCols, R.chi[i] - c0);
   };
   constexpr int K = T * BS, K4 = K / 4;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int c = 4 * tx, rb = 8 * ty;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int c1 = 4 * tx;
   auto stage_ptr = [&](int st) { return psm + size_t(st) * kStageWords; };
+  float *const ap = psm + 2 * size_t(kStageWords);
   auto issue = [&](int tile, int st) {
     float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL;
     int r0, c0, nr, nc;
@@ -400,6 +453,12 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
       const bool ok = 4 * c4 < nc;
       cp_async16(up + kk * kLdU + 4 * c4, a + size_t(o + kk) * n + (ok ? c0 + 4 * c4 : c0), ok);
     }
+#pragma unroll
+    for (int e = threadIdx.x; e < kFarRows * (kFarCols / 4); e += kFarThreads) {   // the tile of A
+      const int r = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
+      const bool ok = r < nr && 4 * c4 < nc;
+      cp_async16(ap + r * kLdA + 4 * c4, a + size_t(ok ? r0 + r : r0) * n + (ok ? c0 + 4 * c4 : c0), ok);
+    }
     cp_async_commit();
   };
   int tile = blockIdx.x;
@@ -408,59 +467,33 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
     const int st = it & 1;
     int r0, c0, nr, nc;
     place(tile, r0, c0, nr, nc);
-    // this tile of A: in flight during step 0
-    const bool cok = c < nc;
-    float4 v[8];
+    cp_async_wait<0>();
+    __syncthreads();
+    // the tile of A into registers, then the A buffer takes the next tile's
+    float4 v[8][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      v[i] = (cok && rb + i < nr) ? *reinterpret_cast<const float4 *>(a + size_t(r0 + rb + i) * n + c0 + c)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-    const int next = tile + gridDim.x;
-    if (next < tiles) {
-      issue(next, st ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) v[i][h] = *reinterpret_cast<const float4 *>(ap + (ty + 16 * i) * kLdA + c1 + 64 * h);
     __syncthreads();
+    const int next = tile + gridDim.x;
+    if (next < tiles) issue(next, st ^ 1);
     const float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL;
-#pragma unroll 1
-    for (int t = 0; t < (rb < nr ? T : 0); ++t) {   // warps with no rows in the tile (a band's edge) skip
-      float2 acc[8][2];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int k4 = 0; k4 < BS / 4; ++k4) {
-        const int kb = t * BS + 4 * k4;
-        float4 u[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) u[q] = *reinterpret_cast<const float4 *>(up + (kb + q) * kLdU + c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 l = *reinterpret_cast<const float4 *>(lp + (rb + i) * kLdL + kb);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float li = q == 0 ? l.x : q == 1 ? l.y : q == 2 ? l.z : l.w;
-            const float2 ll = make_float2(li, li);
-            acc[i][0] = fma2(ll, make_float2(u[q].x, u[q].y), acc[i][0]);
-            acc[i][1] = fma2(ll, make_float2(u[q].z, u[q].w), acc[i][1]);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i].x -= acc[i][0].x;
-        v[i].y -= acc[i][0].y;
-        v[i].z -= acc[i][1].x;
-        v[i].w -= acc[i][1].y;
-      }
+    // nr, nc are multiples of 16: rows ty + 16 i are in the tile iff i < nr / 16
+    if (nr > 64) {
+      if (nc > 64) far_tile<T, 8, 2>(lp, up, v, ty, c1);
+      else far_tile<T, 8, 1>(lp, up, v, ty, c1);
+    } else {
+      if (nc > 64) far_tile<T, 4, 2>(lp, up, v, ty, c1);
+      else far_tile<T, 4, 1>(lp, up, v, ty, c1);
     }
-    if (cok) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (rb + i < nr) *reinterpret_cast<float4 *>(a + size_t(r0 + rb + i) * n + c0 + c) = v[i];
-    }
-    __syncthreads();   // this stage is refilled by the next iteration's issue
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = ty + 16 * i, c = c1 + 64 * h;
+        if (r < nr && c < nc) *reinterpret_cast<float4 *>(a + size_t(r0 + r) * n + c0 + c) = v[i][h];
+      }
   }
 }
 
@@ -516,7 +549,7 @@ void launch_panels(int variant, float *a, int n, int O, float *dscr, cudaStream_
 
 cudaError_t launch_far(float *a, int n, int O, int T, const FarRects &R, int grid, cudaStream_t s) {
   if (R.tiles == 0) return cudaSuccess;
-  const size_t shm = 2 * size_t(kStageWords) * sizeof(float);
+  const size_t shm = size_t(kFarSmemWords) * sizeof(float);
   grid = max(1, min(grid, R.tiles));
   switch (T) {
     case 1: lud_far_pipe_kernel<1><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
@@ -557,7 +590,7 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
                                            int(kPendFloats * sizeof(float)));
       if (e != cudaSuccess) return e;
     }
-    const int shm = int(2 * size_t(kStageWords) * sizeof(float));
+    const int shm = int(size_t(kFarSmemWords) * sizeof(float));
     for (auto k : {lud_far_pipe_kernel<1>, lud_far_pipe_kernel<2>, lud_far_pipe_kernel<3>, lud_far_pipe_kernel<4>}) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, shm);
       if (e != cudaSuccess) return e;
