@@ -5,13 +5,14 @@
 // (oracle/darm_oracle.c, oracle_lud) performs the same floating-point
 // operations in the same order, so GPU and CPU results agree bit for bit.
 //
-// Per 16-column step at offset o (two launches):
-//   panel      factor A[o:o+16, o:o+16] (every CTA, in shared memory), then
-//              U12 = L11^-1 A12 for every block right of the diagonal and
-//              L21 = A21 U11^-1 for every block below it          (melded kernel)
-//   update     A22 -= L21 U12, 16-term fp32 FMA chains             (64x64 tiles)
-// with a look-ahead: four steps form a super-step and the far trailing block
-// takes their four updates in one pass (same per-element operation order).
+// Per 16-column step at offset o, one panel launch: apply the step's pending
+// updates to the blocks it reads, factor A[o:o+16, o:o+16] (every warp, in
+// registers), then U12 = L11^-1 A12 for every block right of the diagonal and
+// L21 = A21 U11^-1 for every block below it (the melded kernel).  Four steps
+// form a super-step; the trailing matrix takes their four updates in one
+// pass (A22 -= L21 U12 as 16-term fp32 FMA chains, same per-element operation
+// order), first the 64-wide band the next super-step's panels read, then the
+// far block while those panels run beside it (record_lud).
 // The perimeter kernel is the paper's melding target: each warp owns one
 // block pair, lanes 0-15 the row block and lanes 16-31 the column block, so
 // the thread-ID test `lane < 16` splits every warp in half (divergent on a
@@ -20,8 +21,8 @@
 //   melded:   hand-melded as the paper did for LUD: one load,
 //             one solve and one store sequence whose addresses, shared-memory
 //             operands and the role-only division are chosen per lane.
-// The 2 x (n/16) launches are recorded once into a CUDA graph per (n, form,
-// buffer) and replayed.
+// The n/16 + 2 n/64 + 1 launches are recorded once into a CUDA graph per (n,
+// form, buffer) and replayed.
 #include <cstdint>
 
 #include "common.cuh"
@@ -503,9 +504,9 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
 // super-step one panel launch: it first applies to the blocks it reads the
 // updates of the steps O..o-16 before it (left-looking inside the
 // super-step), then factors the diagonal block and solves the perimeter.  The
-// far trailing block [O+64, n)^2 then takes the super-step's kLook updates in
-// one pass (lud_far_pipe_kernel); the factored diagonal blocks are scattered
-// into place at the end.  n/16 + n/64 + 1 launches.
+// trailing matrix then takes the super-step's kLook updates in one pass
+// (lud_far_pipe_kernel: the band, then the far block); the factored diagonal
+// blocks are scattered into place at the end.
 // Scatter of the factored diagonal blocks (kept in scratch while later steps
 // may still read the unfactored blocks) into the matrix: block j of dscr to
 // a[16j.., 16j..].
