@@ -64,7 +64,7 @@ def test_gpu_exact_known_answer(variant, n):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", [0, 1])
-@pytest.mark.parametrize("n", [16, 80, 256, 1024, 2048])
+@pytest.mark.parametrize("n", [16, 80, 144, 208, 256, 336, 1024, 1200, 2048])
 def test_gpu_bit_exact_vs_restatement(restatement, variant, n):
     a = dominant(n, seed=n)
     want = a.copy()
