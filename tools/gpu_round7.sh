@@ -1,0 +1,23 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench (+ reference arm), launch list, ncu
+# captures, the lane-efficiency sweep and the per-kernel timing tools.
+set -x
+mkdir -p gpurun_out
+nproc > gpurun_out/nproc.txt
+timeout 1800 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-per-kernel > gpurun_out/bench_under_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:bitonic_sort -c 4 -o gpurun_out/prof_bitonic python tools/profile_driver.py bitonic > gpurun_out/ncu_bitonic.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:srad_sweep -c 4 -o gpurun_out/prof_srad python tools/profile_driver.py srad > gpurun_out/ncu_srad.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lud_far -s 21 -c 1 -o gpurun_out/prof_lud_far python tools/profile_driver.py lud > gpurun_out/ncu_lud_far.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lud_panel -s 100 -c 1 -o gpurun_out/prof_lud_unmelded python tools/profile_driver.py lud > gpurun_out/ncu_lud_u.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lud_panel -s 612 -c 1 -o gpurun_out/prof_lud_melded python tools/profile_driver.py lud > gpurun_out/ncu_lud_m.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_lud8192.csv python tools/profile_driver.py lud > gpurun_out/ncu_lud_list.log 2>&1
+bash tools/lane_eff.sh
+timeout 300 python tools/trace_lud.py 8192 > gpurun_out/trace_lud.log 2>&1
+timeout 300 python tools/time_lud.py 2048 4096 8192 > gpurun_out/time_lud.log 2>&1
+timeout 300 python tools/time_srad.py > gpurun_out/time_srad.log 2>&1
+timeout 600 python tools/time_bitonic.py 64 256 1024 4096 > gpurun_out/time_bitonic.log 2>&1
+ls -la gpurun_out
