@@ -91,8 +91,8 @@ constexpr int kPendFloats = BS * kLdP + kMaxPend * BS * LD + kPairs * (kMaxPend 
 template <bool M, int P>   // P: pending steps of the super-step (0..kLook-1), compile-time
 __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs, int O,
                                                                float *__restrict__ dst, int dstride) {
-  __shared__ float dia[kPairs][BS][LD];
-  __shared__ float diaT[kPairs][BS][LD];      // diaT[i][j] = dia[j][i]
+  __shared__ float dia[BS][LD];               // the factored diagonal block (warp 0 of the CTA)
+  __shared__ float diaT[BS][LD];              // diaT[i][j] = dia[j][i]
   __shared__ float blk[kPairs][2][BS][LD];    // [0] row block R[i][c]; [1] column block transposed C[i][r]
   extern __shared__ float pend[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
   }
   const int r = lane & (BS - 1);
   float v[BS];
-  {
+  if (warp == 0) {
     const float4 *src = reinterpret_cast<const float4 *>(a + (size_t(o) + r) * n + o);
 #pragma unroll
     for (int q = 0; q < BS / 4; ++q) {
@@ -179,73 +179,78 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
     }
     __syncthreads();
   }
-  // the diagonal block's pending updates (lane r holds row r)
-  for (int st = 0; st < P; ++st) {
+  // 2. warp 0: the diagonal block's pending updates (lane r holds row r) and
+  //    its factorisation in registers, into shared memory for the CTA;
+  //    meanwhile the other warps stage their pairs and apply theirs
+  if (warp == 0) {
+    for (int st = 0; st < P; ++st) {
 #pragma unroll
-    for (int c = 0; c < BS; ++c) {
-      float sum = 0.f;
+      for (int c = 0; c < BS; ++c) {
+        float sum = 0.f;
 #pragma unroll
-      for (int k = 0; k < BS; ++k) sum = fmaf(Lp[r][st * BS + k], Ud[st * BS + k][c], sum);
-      v[c] = v[c] - sum;
+        for (int k = 0; k < BS; ++k) sum = fmaf(Lp[r][st * BS + k], Ud[st * BS + k][c], sum);
+        v[c] = v[c] - sum;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < BS - 1; ++k) {
+      const float ukk = __shfl_sync(0xffffffffu, v[k], k);
+      if (r > k) v[k] = v[k] / ukk;                           // L[r][k]
+#pragma unroll
+      for (int c = k + 1; c < BS; ++c) {
+        const float ukc = __shfl_sync(0xffffffffu, v[c], k);  // U[k][c]
+        if (r > k) v[c] = fmaf(-v[k], ukc, v[c]);
+      }
+    }
+    if (lane < BS) {
+#pragma unroll
+      for (int c = 0; c < BS; ++c) {
+        dia[r][c] = v[c];
+        diaT[c][r] = v[c];
+      }
+      if (blockIdx.x == 0) {
+        float4 *d4 = reinterpret_cast<float4 *>(dst + size_t(r) * dstride);
+#pragma unroll
+        for (int q = 0; q < BS / 4; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
     }
   }
-  // 2. diagonal factorisation in registers
-#pragma unroll
-  for (int k = 0; k < BS - 1; ++k) {
-    const float ukk = __shfl_sync(0xffffffffu, v[k], k);
-    if (r > k) v[k] = v[k] / ukk;                           // L[r][k]
-#pragma unroll
-    for (int c = k + 1; c < BS; ++c) {
-      const float ukc = __shfl_sync(0xffffffffu, v[c], k);  // U[k][c]
-      if (r > k) v[c] = fmaf(-v[k], ukc, v[c]);
-    }
-  }
-  if (lane < BS) {
-#pragma unroll
-    for (int c = 0; c < BS; ++c) {
-      dia[warp][r][c] = v[c];
-      diaT[warp][c][r] = v[c];
-    }
-    if (blockIdx.x == 0 && warp == 0) {
-      float4 *d4 = reinterpret_cast<float4 *>(dst + size_t(r) * dstride);
-#pragma unroll
-      for (int q = 0; q < BS / 4; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    }
-  }
-  if (!have) return;                                        // warp-uniform
   // 3. stage the pair
   float(*R)[LD] = blk[warp][0];
   float(*C)[LD] = blk[warp][1];
+  if (have) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int q = lane + 32 * h, i = q >> 2, c = 4 * (q & 3);
-    R[i][c] = rv[h].x;
-    R[i][c + 1] = rv[h].y;
-    R[i][c + 2] = rv[h].z;
-    R[i][c + 3] = rv[h].w;
-    C[c][i] = cv[h].x;
-    C[c + 1][i] = cv[h].y;
-    C[c + 2][i] = cv[h].z;
-    C[c + 3][i] = cv[h].w;
-  }
-  __syncwarp();
-  // the pair's pending updates: R[i][c] (row block) and C[j][rr] (column block)
-  for (int st = 0; st < P; ++st) {
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h, i = q >> 2, c = 4 * (q & 3);
+      R[i][c] = rv[h].x;
+      R[i][c + 1] = rv[h].y;
+      R[i][c + 2] = rv[h].z;
+      R[i][c + 3] = rv[h].w;
+      C[c][i] = cv[h].x;
+      C[c + 1][i] = cv[h].y;
+      C[c + 2][i] = cv[h].z;
+      C[c + 3][i] = cv[h].w;
+    }
+    __syncwarp();
+    // the pair's pending updates: R[i][c] (row block) and C[j][rr] (column block)
+    for (int st = 0; st < P; ++st) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int x = lane & (BS - 1), y = (lane >> 4) + 2 * q;
-      float sr = 0.f, sc = 0.f;
+      for (int q = 0; q < 8; ++q) {
+        const int x = lane & (BS - 1), y = (lane >> 4) + 2 * q;
+        float sr = 0.f, sc = 0.f;
 #pragma unroll
-      for (int k = 0; k < BS; ++k) {
-        sr = fmaf(Lp[y][st * BS + k], Ur[st * BS + k][x], sr);   // L[o+y][o_st+k] U[o_st+k][cb+x]
-        sc = fmaf(Lc[x][st * BS + k], Ud[st * BS + k][y], sc);   // L[cb+x][o_st+k] U[o_st+k][o+y]
+        for (int k = 0; k < BS; ++k) {
+          sr = fmaf(Lp[y][st * BS + k], Ur[st * BS + k][x], sr);   // L[o+y][o_st+k] U[o_st+k][cb+x]
+          sc = fmaf(Lc[x][st * BS + k], Ud[st * BS + k][y], sc);   // L[cb+x][o_st+k] U[o_st+k][o+y]
+        }
+        R[y][x] = R[y][x] - sr;
+        C[y][x] = C[y][x] - sc;
       }
-      R[y][x] = R[y][x] - sr;
-      C[y][x] = C[y][x] - sc;
     }
   }
-  __syncwarp();
-  const float(*Dg)[LD] = dia[warp];
+  __syncthreads();                                          // the diagonal block is in dia / diaT
+  if (!have) return;                                        // warp-uniform
+  const float(*Dg)[LD] = dia;
   // 4. the perimeter solve
   if constexpr (!M) {
     if (lane < BS) {                                        // U12 = L11^-1 A12, column idx
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
     const bool col = lane >= BS;
     const int idx = lane & (BS - 1);
     float(*S)[LD] = col ? C : R;
-    const float(*D)[LD] = col ? diaT[warp] : dia[warp];
+    const float(*D)[LD] = col ? diaT : dia;
     float x[BS];
 #pragma unroll
     for (int i = 0; i < BS; ++i) x[i] = S[i][idx];
