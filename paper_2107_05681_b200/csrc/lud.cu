@@ -82,11 +82,13 @@ constexpr int kPairs = 4;
 // of the separate update kernel it replaces.  L / U come from the earlier
 // steps' column / row blocks, already final.  Shared layout (dynamic):
 //   Lp[16][kLdP]   rows o..o+15, columns O..o   (the diagonal rows' L)
-//   Ud[48][LD]     rows O..o, columns o..o+15   (U above the diagonal block)
-//   per warp Ur[48][LD] (U above its row block), Lc[16][kLdP] (its column block's L)
+//   UdT[16][kLdP]  U above the diagonal block, transposed: UdT[c][k] = U[O+k][o+c]
+//   per warp UrT[16][kLdP] (U above its row block, transposed) and Lc[16][kLdP]
+//   (its column block's L)
+// Every operand row is contiguous along k, so the sums read float4s.
 constexpr int kMaxPend = kLook - 1;
-constexpr int kLdP = kMaxPend * BS + 1;
-constexpr int kPendFloats = BS * kLdP + kMaxPend * BS * LD + kPairs * (kMaxPend * BS * LD + BS * kLdP);
+constexpr int kLdP = kMaxPend * BS + 4;   // 52: float4 rows, 16 rows on distinct bank quads but for pairs
+constexpr int kPendFloats = 2 * BS * kLdP + kPairs * 2 * BS * kLdP;
 
 template <bool M, int P>   // P: pending steps of the super-step (0..kLook-1), compile-time
 __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restrict__ a, int n, int o, int npairs, int O,
@@ -100,10 +102,9 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
   const bool have = p < npairs;                             // warp-uniform
   const size_t cb = size_t(o) + size_t(BS) * (p + 1);       // column of the row block = row of the column block
   float(*Lp)[kLdP] = reinterpret_cast<float(*)[kLdP]>(pend);
-  float(*Ud)[LD] = reinterpret_cast<float(*)[LD]>(pend + BS * kLdP);
-  float(*Ur)[LD] = reinterpret_cast<float(*)[LD]>(pend + BS * kLdP + kMaxPend * BS * LD +
-                                                  warp * (kMaxPend * BS * LD + BS * kLdP));
-  float(*Lc)[kLdP] = reinterpret_cast<float(*)[kLdP]>(reinterpret_cast<float *>(Ur) + kMaxPend * BS * LD);
+  float(*UdT)[kLdP] = reinterpret_cast<float(*)[kLdP]>(pend + BS * kLdP);
+  float(*UrT)[kLdP] = reinterpret_cast<float(*)[kLdP]>(pend + 2 * BS * kLdP + warp * 2 * BS * kLdP);
+  float(*Lc)[kLdP] = reinterpret_cast<float(*)[kLdP]>(pend + 3 * BS * kLdP + warp * 2 * BS * kLdP);
   // 1. every global read of the launch in flight at once (one memory round
   //    trip): the pair (2 float4 per lane per block), the diagonal row of lane
   //    r, and the pending updates' L and U (float4 chunks, fixed counts)
@@ -153,11 +154,12 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
         lcb[j] = *reinterpret_cast<const float4 *>(a + (cb + e / K4) * n + O + 4 * (e % K4));
       }
     }
-    auto put = [](float *d, float4 x) {
-      d[0] = x.x;
-      d[1] = x.y;
-      d[2] = x.z;
-      d[3] = x.w;
+    auto put = [](float *d, float4 x) { *reinterpret_cast<float4 *>(d) = x; };
+    auto put_t = [](float (*d)[kLdP], int c, int k, float4 x) {   // d[c + i][k] = x[i]
+      d[c][k] = x.x;
+      d[c + 1][k] = x.y;
+      d[c + 2][k] = x.z;
+      d[c + 3][k] = x.w;
     };
 #pragma unroll
     for (int j = 0; j < (nL + NT - 1) / NT; ++j) {
@@ -167,13 +169,13 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
 #pragma unroll
     for (int j = 0; j < (nU + NT - 1) / NT; ++j) {
       const int e = int(threadIdx.x) + NT * j;
-      if (e < nU) put(&Ud[e / 4][4 * (e % 4)], ub[j]);
+      if (e < nU) put_t(UdT, 4 * (e % 4), e / 4, ub[j]);
     }
     if (have) {
 #pragma unroll
       for (int j = 0; j < nW; ++j) {
         const int e = lane + 32 * j;
-        put(&Ur[e / 4][4 * (e % 4)], urb[j]);
+        put_t(UrT, 4 * (e % 4), e / 4, urb[j]);
         put(&Lc[e / K4][4 * (e % K4)], lcb[j]);
       }
     }
@@ -184,11 +186,26 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
   //    meanwhile the other warps stage their pairs and apply theirs
   if (warp == 0) {
     for (int st = 0; st < P; ++st) {
+      float l[BS];                                          // L[o+r][O+16st+k], k ascending
+#pragma unroll
+      for (int q = 0; q < BS / 4; ++q) {
+        const float4 t = *reinterpret_cast<const float4 *>(&Lp[r][st * BS + 4 * q]);
+        l[4 * q] = t.x;
+        l[4 * q + 1] = t.y;
+        l[4 * q + 2] = t.z;
+        l[4 * q + 3] = t.w;
+      }
 #pragma unroll
       for (int c = 0; c < BS; ++c) {
         float sum = 0.f;
 #pragma unroll
-        for (int k = 0; k < BS; ++k) sum = fmaf(Lp[r][st * BS + k], Ud[st * BS + k][c], sum);
+        for (int q = 0; q < BS / 4; ++q) {
+          const float4 u = *reinterpret_cast<const float4 *>(&UdT[c][st * BS + 4 * q]);   // broadcast
+          sum = fmaf(l[4 * q], u.x, sum);
+          sum = fmaf(l[4 * q + 1], u.y, sum);
+          sum = fmaf(l[4 * q + 2], u.z, sum);
+          sum = fmaf(l[4 * q + 3], u.w, sum);
+        }
         v[c] = v[c] - sum;
       }
     }
@@ -233,15 +250,38 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
     }
     __syncwarp();
     // the pair's pending updates: R[i][c] (row block) and C[j][rr] (column block)
+    const int x = lane & (BS - 1);
     for (int st = 0; st < P; ++st) {
+      float ur[BS], lc[BS];                                 // U[O+16st+k][cb+x], L[cb+x][O+16st+k]
+#pragma unroll
+      for (int q = 0; q < BS / 4; ++q) {
+        const float4 t = *reinterpret_cast<const float4 *>(&UrT[x][st * BS + 4 * q]);
+        const float4 w = *reinterpret_cast<const float4 *>(&Lc[x][st * BS + 4 * q]);
+        ur[4 * q] = t.x;
+        ur[4 * q + 1] = t.y;
+        ur[4 * q + 2] = t.z;
+        ur[4 * q + 3] = t.w;
+        lc[4 * q] = w.x;
+        lc[4 * q + 1] = w.y;
+        lc[4 * q + 2] = w.z;
+        lc[4 * q + 3] = w.w;
+      }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int x = lane & (BS - 1), y = (lane >> 4) + 2 * q;
+        const int y = (lane >> 4) + 2 * q;
         float sr = 0.f, sc = 0.f;
 #pragma unroll
-        for (int k = 0; k < BS; ++k) {
-          sr = fmaf(Lp[y][st * BS + k], Ur[st * BS + k][x], sr);   // L[o+y][o_st+k] U[o_st+k][cb+x]
-          sc = fmaf(Lc[x][st * BS + k], Ud[st * BS + k][y], sc);   // L[cb+x][o_st+k] U[o_st+k][o+y]
+        for (int k4 = 0; k4 < BS / 4; ++k4) {
+          const float4 lp = *reinterpret_cast<const float4 *>(&Lp[y][st * BS + 4 * k4]);   // L[o+y][..]
+          const float4 ud = *reinterpret_cast<const float4 *>(&UdT[y][st * BS + 4 * k4]);  // U[..][o+y]
+          sr = fmaf(lp.x, ur[4 * k4], sr);
+          sc = fmaf(lc[4 * k4], ud.x, sc);
+          sr = fmaf(lp.y, ur[4 * k4 + 1], sr);
+          sc = fmaf(lc[4 * k4 + 1], ud.y, sc);
+          sr = fmaf(lp.z, ur[4 * k4 + 2], sr);
+          sc = fmaf(lc[4 * k4 + 2], ud.z, sc);
+          sr = fmaf(lp.w, ur[4 * k4 + 3], sr);
+          sc = fmaf(lc[4 * k4 + 3], ud.w, sc);
         }
         R[y][x] = R[y][x] - sr;
         C[y][x] = C[y][x] - sc;
