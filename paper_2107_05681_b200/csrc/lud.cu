@@ -471,12 +471,15 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
   const int tiles = R.tiles;
   // tile -> its origin (r0, c0) and extent (nr, nc)
   auto place = [&](int tile, int &r0, int &c0, int &nr, int &nc) {
-    const int i = tile >= R.first[1] && R.first[1] < R.tiles ? 1 : 0;
-    const int t = tile - R.first[i];
-    r0 = R.rlo[i] + kFarRows * (t / R.tiles_c[i]);
-    c0 = R.clo[i] + kFarCols * (t % R.tiles_c[i]);
-    nr = min(kFarRows, R.rhi[i] - r0);
-    nc = min(kFarCols, R.chi[i] - c0);
+    // selects, not an indexed parameter array (which would go to local memory)
+    const bool second = tile >= R.first[1] && R.first[1] < R.tiles;
+    const unsigned t = unsigned(tile - (second ? R.first[1] : 0));
+    const unsigned tc = unsigned(second ? R.tiles_c[1] : R.tiles_c[0]);
+    const unsigned q = t / tc;
+    r0 = (second ? R.rlo[1] : R.rlo[0]) + kFarRows * int(q);
+    c0 = (second ? R.clo[1] : R.clo[0]) + kFarCols * int(t - q * tc);
+    nr = min(kFarRows, (second ? R.rhi[1] : R.rhi[0]) - r0);
+    nc = min(kFarCols, (second ? R.chi[1] : R.chi[0]) - c0);
   };
   constexpr int K = T * BS, K4 = K / 4;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
