@@ -23,6 +23,9 @@
 //             operands and the role-only division are chosen per lane.
 // The n/16 + 2 n/64 + 1 launches are recorded once into a CUDA graph per (n,
 // form, buffer) and replayed.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 
 #include "common.cuh"
@@ -378,20 +381,39 @@ constexpr int kFarThreads = 256;               // thread = 8 rows x 8 columns of
 // registers.  Band tiles (64 rows or 64 columns) run a half-size variant.
 // Per element the operation sequence above.
 constexpr int kPipeK = kLook * BS;                 // 64
-constexpr int kLdL = kPipeK + 4;                   // lp[r][k] row pitch
-constexpr int kLdU = kFarCols + 4;                 // up[k][c]
+// dense tiles as the tensor memory accelerator writes them (no padding)
+constexpr int kLdL = kPipeK;                       // lp[r][k] row pitch
+constexpr int kLdU = kFarCols;                     // up[k][c]
 constexpr int kStageWords = kFarRows * kLdL + kPipeK * kLdU;
-constexpr int kLdA = kFarCols + 4;                 // the A tile's staging buffer (single)
-constexpr int kFarSmemWords = 2 * kStageWords + kFarRows * kLdA;   // 205 KB
+constexpr int kLdA = kFarCols;                     // the A tile's buffer (single)
+constexpr int kFarSmemWords = 2 * kStageWords + kFarRows * kLdA;   // 192 KB
+constexpr unsigned kStageBytes = unsigned(kStageWords) * 4, kTileABytes = unsigned(kFarRows * kLdA) * 4;
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int bytes = valid ? 16 : 0;                // 0: zero-fill
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+// TMA (cp.async.bulk.tensor) and mbarrier primitives
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(float *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
 
 // T steps on one tile: NI row groups (of 16 rows: 8 = all, 4 = a 64-row band)
 // and NH column halves (2 = all, 1 = a 64-column band).
@@ -465,9 +487,15 @@ static FarRects far_rects(int n_rects, const int (*r)[4]) {
   return f;
 }
 
-template <int T>   // steps in the super-step (kLook but for the last one): compile-time address math
-__global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__restrict__ a, int n, int o, FarRects R) {
-  extern __shared__ __align__(16) float psm[];
+struct FarMaps {                 // tensor maps of A (n x n fp32, row-major): three box shapes
+  CUtensorMap l, u, t;           // L rows (64 x 128), U rows (128 x 64), the tile (128 x 128)
+};
+
+template <int T>   // steps in the super-step (kLook but for the last one)
+__global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__restrict__ a, int n, int o, FarRects R,
+                                                                      const __grid_constant__ FarMaps maps) {
+  extern __shared__ __align__(128) float psm[];
+  __shared__ __align__(8) uint64_t bar[3];   // stage 0 / stage 1 (L, U) landed; the A tile landed
   const int tiles = R.tiles;
   // tile -> its origin (r0, c0) and extent (nr, nc)
   auto place = [&](int tile, int &r0, int &c0, int &nr, int &nc) {
@@ -481,44 +509,40 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
     nr = min(kFarRows, (second ? R.rhi[1] : R.rhi[0]) - r0);
     nc = min(kFarCols, (second ? R.chi[1] : R.chi[0]) - c0);
   };
-  constexpr int K = T * BS, K4 = K / 4;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int c1 = 4 * tx;
   auto stage_ptr = [&](int st) { return psm + size_t(st) * kStageWords; };
   float *const ap = psm + 2 * size_t(kStageWords);
+  // one thread issues a tile's three boxes: L (rows r0.., columns o..o+63), U
+  // (rows o..o+63, columns c0..), A (rows r0.., columns c0..).  Box parts past
+  // the region (a band's edge) load neighbouring data that is computed on but
+  // never stored; parts past the matrix are zero-filled.
   auto issue = [&](int tile, int st) {
-    float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL;
     int r0, c0, nr, nc;
     place(tile, r0, c0, nr, nc);
-#pragma unroll
-    for (int e = threadIdx.x; e < kFarRows * K4; e += kFarThreads) {   // L rows of the tile, k along
-      const int r = e / K4, k4 = e % K4;
-      const bool ok = r < nr;
-      cp_async16(lp + r * kLdL + 4 * k4, a + size_t(ok ? r0 + r : r0) * n + o + 4 * k4, ok);
-    }
-#pragma unroll
-    for (int e = threadIdx.x; e < K * (kFarCols / 4); e += kFarThreads) {   // U rows, columns of the tile
-      const int kk = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
-      const bool ok = 4 * c4 < nc;
-      cp_async16(up + kk * kLdU + 4 * c4, a + size_t(o + kk) * n + (ok ? c0 + 4 * c4 : c0), ok);
-    }
-#pragma unroll
-    for (int e = threadIdx.x; e < kFarRows * (kFarCols / 4); e += kFarThreads) {   // the tile of A
-      const int r = e / (kFarCols / 4), c4 = e % (kFarCols / 4);
-      const bool ok = r < nr && 4 * c4 < nc;
-      cp_async16(ap + r * kLdA + 4 * c4, a + size_t(ok ? r0 + r : r0) * n + (ok ? c0 + 4 * c4 : c0), ok);
-    }
-    cp_async_commit();
+    float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL;
+    mbar_expect_tx(&bar[st], kStageBytes);
+    tma_load_2d(lp, &maps.l, o, r0, &bar[st]);
+    tma_load_2d(up, &maps.u, c0, o, &bar[st]);
+    mbar_expect_tx(&bar[2], kTileABytes);
+    tma_load_2d(ap, &maps.t, c0, r0, &bar[2]);
   };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   int tile = blockIdx.x;
-  if (tile < tiles) issue(tile, 0);
+  if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
   for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
     const int st = it & 1;
     int r0, c0, nr, nc;
     place(tile, r0, c0, nr, nc);
-    cp_async_wait<0>();
-    __syncthreads();
-    // the tile of A into registers, then the A buffer takes the next tile's
+    mbar_wait(&bar[st], unsigned(it >> 1) & 1u);
+    mbar_wait(&bar[2], unsigned(it) & 1u);
+    // the tile of A into registers; then the buffer and the other stage take the next tile's
     float4 v[8][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -526,7 +550,10 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
       for (int h = 0; h < 2; ++h) v[i][h] = *reinterpret_cast<const float4 *>(ap + (ty + 16 * i) * kLdA + c1 + 64 * h);
     __syncthreads();
     const int next = tile + gridDim.x;
-    if (next < tiles) issue(next, st ^ 1);
+    if (threadIdx.x == 0 && next < tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+      issue(next, st ^ 1);
+    }
     const float *lp = stage_ptr(st), *up = lp + kFarRows * kLdL;
     // nr, nc are multiples of 16: rows ty + 16 i are in the tile iff i < nr / 16
     if (nr > 64) {
@@ -596,15 +623,39 @@ void launch_panels(int variant, float *a, int n, int O, float *dscr, cudaStream_
   }
 }
 
-cudaError_t launch_far(float *a, int n, int O, int T, const FarRects &R, int grid, cudaStream_t s) {
+// The three tensor maps of the matrix (host-encoded through the driver entry point).
+cudaError_t far_maps(float *a, int n, FarMaps &m) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&encode),
+                                            cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !encode) return cudaErrorNotSupported;
+  }
+  const cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(n)};
+  const cuuint64_t strides[1] = {cuuint64_t(n) * sizeof(float)};
+  const cuuint32_t es[2] = {1, 1};
+  auto one = [&](CUtensorMap &t, unsigned bx, unsigned by) {
+    const cuuint32_t box[2] = {bx, by};
+    return encode(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  if (one(m.l, kPipeK, kFarRows) != CUDA_SUCCESS || one(m.u, kFarCols, kPipeK) != CUDA_SUCCESS ||
+      one(m.t, kFarCols, kFarRows) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  return cudaSuccess;
+}
+
+cudaError_t launch_far(float *a, int n, int O, int T, const FarRects &R, const FarMaps &maps, int grid,
+                       cudaStream_t s) {
   if (R.tiles == 0) return cudaSuccess;
   const size_t shm = size_t(kFarSmemWords) * sizeof(float);
   grid = max(1, min(grid, R.tiles));
   switch (T) {
-    case 1: lud_far_pipe_kernel<1><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
-    case 2: lud_far_pipe_kernel<2><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
-    case 3: lud_far_pipe_kernel<3><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
-    default: lud_far_pipe_kernel<4><<<grid, kFarThreads, shm, s>>>(a, n, O, R); break;
+    case 1: lud_far_pipe_kernel<1><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
+    case 2: lud_far_pipe_kernel<2><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
+    case 3: lud_far_pipe_kernel<3><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
+    default: lud_far_pipe_kernel<4><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
   }
   return cudaGetLastError();
 }
@@ -664,6 +715,11 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
   }
   const int nb = n / BS;
   const int G = kLook * BS;
+  FarMaps maps;
+  if (n > G) {
+    cudaError_t e = far_maps(a, n, maps);
+    if (e != cudaSuccess) return e;
+  }
   launch_panels(variant, a, n, 0, dscr, s, launches);   // super-step 0: nothing to overlap with
   for (int O = 0; O < n; O += G) {
     const int T = min(kLook, (n - O) / BS);
@@ -673,7 +729,7 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
     const int F = E + Tn * BS;                  // end of its band
     // the band the next panels read: rows [E, F) x cols [E, n), rows [F, n) x cols [E, F)
     const int band[2][4] = {{E, F, E, n}, {F, n, E, F}};
-    cudaError_t e = launch_far(a, n, O, T, far_rects(2, band), sms, s);
+    cudaError_t e = launch_far(a, n, O, T, far_rects(2, band), maps, sms, s);
     if (e != cudaSuccess) return e;
     ++*launches;
     if (F < n) {
@@ -684,7 +740,7 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
       e = cudaEventRecord(sd.join, sd.s);
       if (e != cudaSuccess) return e;
       const int far[1][4] = {{F, n, F, n}};
-      e = launch_far(a, n, O, T, far_rects(1, far), sms - kPanelSMs, s);
+      e = launch_far(a, n, O, T, far_rects(1, far), maps, sms - kPanelSMs, s);
       if (e != cudaSuccess) return e;
       ++*launches;
       e = cudaStreamWaitEvent(s, sd.join, 0);
