@@ -317,13 +317,17 @@ struct Sb4T {
       const bool sel2 = sel ? c1 : true;
       int32_t w2u = 0;
       if (sel2) w2u = ir_add(v2e, 1);                      // ^d4.r.m.g1.m
-      int32_t w5u = 0, oldu = 0;
+      int32_t w5u = 0;
       if (!sel) {                                          // ^d4.r.m.u1.m.g
         int32_t v5 = in[g];
         w5u = ir_xor(v5, 7);
-        oldu = out[g];
+        // runDarm's block also loads out[t] (the predicated store's old value)
+        // for sel3 = select sel w2 old; that value reaches the store only when
+        // c1, where sel is true, so it is dead.  The reference's dead-code pass
+        // keeps it because an IR load may fault (post_opt.cpp:209-220); here
+        // t < warp <= the declared size, so it cannot, and it is not issued.
       }
-      int32_t sel3 = sel ? w2u : oldu;
+      int32_t sel3 = w2u;                                  // select sel w2 old, sel true where used
       int32_t sel4 = sel ? w4u : w5u;
       out[g] = c1 ? sel3 : sel4;
     }

@@ -680,9 +680,18 @@ struct LudSide {       // per device: the panel stream of the look-ahead and its
 constexpr int kPanelSMs = 8;
 
 cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches) {
-  static bool attr = false;
-  static int sms = 0;
-  if (!attr) {
+  // per device: kernel attributes, SM count, the panel stream (callers hold
+  // the device's lock)
+  struct LudDevice {
+    bool attr = false;
+    int sms = 0;
+    LudSide side;
+  };
+  static LudDevice devs[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  LudDevice &D = devs[dev & 63];
+  if (!D.attr) {
     for (auto k : {lud_panel_kernel<false, 0>, lud_panel_kernel<false, 1>, lud_panel_kernel<false, 2>,
                    lud_panel_kernel<false, 3>, lud_panel_kernel<true, 0>, lud_panel_kernel<true, 1>,
                    lud_panel_kernel<true, 2>, lud_panel_kernel<true, 3>}) {
@@ -695,16 +704,12 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, shm);
       if (e != cudaSuccess) return e;
     }
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-    attr = true;
+    cudaDeviceGetAttribute(&D.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (D.sms <= 0) D.sms = 148;
+    D.attr = true;
   }
-  static LudSide side[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  LudSide &sd = side[dev & 63];
+  const int sms = D.sms;
+  LudSide &sd = D.side;
   if (!sd.s) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
