@@ -92,8 +92,15 @@ __device__ __forceinline__ int32_t oe_one_step(int32_t v, int lane, uint64_t lo,
     b0 = xch[par][lower ? threadIdx.x + k : (upper ? threadIdx.x - k : threadIdx.x)];
     par ^= 1;
   }
-  if constexpr (M)
-    return lower ? min(v, b0) : max(v, b0);                // %sel = select %lower %g1 %g2; one store
+  if constexpr (M) {
+    // %sel = select %lower %g1 %g2; one store.  Issued as a complementary
+    // predicated pair: for the plain select ptxas emits min; @!P max, whose
+    // write-after-write on one register stalls every serial step.
+    asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p min.s32 %0, %0, %2;\n @!p max.s32 %0, %0, %2;\n}"
+        : "+r"(v)
+        : "r"(int(lower)), "r"(b0));
+    return v;
+  }
   else
     return oe_exchange_unmelded(v, b0, lower);
 }
