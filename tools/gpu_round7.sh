@@ -20,4 +20,6 @@ timeout 300 python tools/trace_lud.py 8192 > gpurun_out/trace_lud.log 2>&1
 timeout 300 python tools/time_lud.py 2048 4096 8192 > gpurun_out/time_lud.log 2>&1
 timeout 300 python tools/time_srad.py > gpurun_out/time_srad.log 2>&1
 timeout 600 python tools/time_bitonic.py 64 256 1024 4096 > gpurun_out/time_bitonic.log 2>&1
+timeout 600 python tools/time_bitonic.py --oddeven 64 256 > gpurun_out/time_oddeven.log 2>&1
+timeout 300 python tools/time_corpus.py > gpurun_out/time_corpus.log 2>&1
 ls -la gpurun_out
