@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
 #pragma unroll
     for (int k = 0; k < BS - 1; ++k) {
       const float ukk = __shfl_sync(0xffffffffu, v[k], k);
-      if (r > k) v[k] = v[k] / ukk;                           // L[r][k]
+      const float lk = v[k] / ukk;                            // L[r][k] (rows r > k keep it;
+      v[k] = r > k ? lk : v[k];                               //  a select, not a guarded division)
 #pragma unroll
       for (int c = k + 1; c < BS; ++c) {
         const float ukc = __shfl_sync(0xffffffffu, v[c], k);  // U[k][c]
@@ -331,7 +332,8 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
     // read [i][idx]) and the diagonal operand (dia or its transpose, so both
     // read D[i][j]); fmaf(a,b,c) == fmaf(b,a,c), so -x[j] * D[i][j] is the same
     // operation as either arm's.  The column role's division is the only
-    // one-sided run.
+    // one-sided run: all lanes divide and a select keeps it for the column
+    // role (a guarded division would branch around the IEEE sequence 16 times).
     const bool col = lane >= BS;
     const int idx = lane & (BS - 1);
     float(*S)[LD] = col ? C : R;
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
     for (int i = 0; i < BS; ++i) {
 #pragma unroll
       for (int j = 0; j < i; ++j) x[i] = fmaf(-x[j], D[i][j], x[i]);
-      if (col) x[i] = x[i] / D[i][i];
+      const float q = x[i] / D[i][i];                     // every lane divides; the row role
+      x[i] = col ? q : x[i];                                // discards it (select, no branch)
     }
 #pragma unroll
     for (int i = 0; i < BS; ++i) S[i][idx] = x[i];
