@@ -39,6 +39,14 @@ METRIC = "Melded vs unmelded speedup & SIMT lane efficiency per kernel, 1-8 B200
 L2_FLUSH_BYTES = 256 << 20
 
 
+def sm_max_mhz():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        return 1965.0
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -387,6 +395,11 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     row["melded_solutions_per_s"] = 14772512 / (row["melded_us"] * 1e-6)
     row["prefix_rows"], row["mirror_symmetry"] = 7, True
     row["n_gpus"], row["scaling"] = world, "strong (prefixes sharded over the ranks)"
+    prof, src = ncu_kernel_summary("nqueens", "nqueens_kernel<1")
+    row["roofline"] = {"bound": "ALU pipe (integer issue)", "nodes": 1141190303,
+                       "alu_pipe_pct": prof.get("alu_pipe_pct") if prof else None,
+                       "issue_active_pct": prof.get("issue_active_pct") if prof else None,
+                       "source": src}
     out["nqueens16"] = row
     # PCM (Batcher odd-even merge sort of 64-key buckets, 2^24 keys) and MS (bottom-up
     # merge sort of 2^20 keys, the paper's input size)
@@ -424,6 +437,10 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_keys_per_s"] = n / (row["melded_us"] * 1e-6)
+    passes = 1 + max(0, (n // 4096).bit_length() - 1)        # tile pass + one per width >= 4096
+    row["melded_GBps"] = 8.0 * n * passes / (row["melded_us"] * 1e-6) / 1e9
+    row["melded_frac_hbm"] = row["melded_GBps"] / peak
+    row["roofline_note"] = f"8 B/key per pass x {passes} passes; at 2^20 keys (4 MiB) the passes run from L2"
     out["ms1m"] = row
     # the GPU executeWarp for arbitrary IR (darm_gpu_program_execute): a diamond
     # kernel given as IR text, 32768 warps of 32 lanes (config 1 shape)
@@ -442,8 +459,9 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
                 ts.append(res.call_stats["kernel_ms"])
         row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(ts) / len(ts))
         row[vname + "_warps_per_s"] = nwi / (row[vname + "_us"] * 1e-6)
+    row["roofline_note"] = "an interpreter: bound by issue per IR instruction, not by bytes"
     out["interp_diamond_32k_warps"] = row
-    # LUD 8192^2 fp32 (config 4): the whole decomposition (3 x 512 launches in one graph)
+    # LUD 8192^2 fp32 (config 4): the whole decomposition (n/16 + 2n/64 + 1 launches in one graph)
     n = 8192
     g = torch.Generator(device="cuda").manual_seed(4)
     a0 = torch.rand((n, n), generator=g, device="cuda") + n * torch.eye(n, device="cuda")
@@ -456,6 +474,10 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_TFLOPs"] = (2.0 / 3.0) * n ** 3 / (row["melded_us"] * 1e-6) / 1e12
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    roof = sms * 256 * sm_max_mhz() * 1e6 / 1e12             # fp32 FMA: 128 lanes x 2 flop per SM per clock
+    row["fp32_roof_TFLOPs"] = roof
+    row["melded_frac_fp32"] = row["melded_TFLOPs"] / roof
     out["lud8192"] = row
     # SRAD 16384^2 fp32 x 100 iterations (config 5): one GPU, or row tiles with a
     # halo exchange and the ROI all-reduce every iteration over NCCL
@@ -578,7 +600,8 @@ def our_arm(args):
         per_kernel["bitonic"] = {"unmelded_us": 1e3 * results["unmelded"]["kernel_ms_mean"],
                                  "melded_us": 1e3 * results["melded"]["kernel_ms_mean"],
                                  "speedup": results["unmelded"]["total_ms"] / results["melded"]["total_ms"],
-                                 "keys_per_thread": kpt}
+                                 "keys_per_thread": kpt,
+                                 "melded_frac_hbm": 8 * n / results["melded"]["kernel_ms_mean"] / 1e6 / peak0}
         # the IR warp shape: one key (one IR lane) per hardware thread
         row = {}
         for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
@@ -590,6 +613,7 @@ def our_arm(args):
             row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(t) / len(t))
         row["speedup"] = row["unmelded_us"] / row["melded_us"]
         row["keys_per_thread"] = 1
+        row["melded_frac_hbm"] = 8 * n / (row["melded_us"] * 1e-6) / 1e9 / peak0
         per_kernel["bitonic_1key"] = row
         # bucket sweep (B = 256 .. 4096; 16 keys per
         # thread, buckets over 512 keys span warps and exchange through shared memory)
@@ -606,6 +630,7 @@ def our_arm(args):
             row["speedup"] = row["unmelded_us"] / row["melded_us"]
             row["keys_per_thread"] = 16
             row["melded_hbm_gbs"] = 8 * n / (row["melded_us"] * 1e-6) / 1e9
+            row["melded_frac_hbm"] = row["melded_hbm_gbs"] / peak0
             per_kernel[f"bitonic_B{Bs}"] = row
 
     if rank != 0:
