@@ -224,6 +224,21 @@ def test_bitonic_sort_buckets(bucket, restatement):
     assert (k == want).all()
 
 
+@pytest.mark.parametrize("bucket", [64, 4096])
+def test_bitonic_sort_host_pipeline(bucket):
+    """HOST mode at 2^22 keys: 2^21-key chunks pipelined over three streams
+    (copy in / sort / copy out); every bucket sorted, both forms, including
+    4096-key buckets whose strides cross warps."""
+    rng = np.random.default_rng(bucket)
+    keys = rng.integers(-(2 ** 31), 2 ** 31, size=1 << 22, dtype=np.int64).astype(np.int32)
+    want = np.sort(keys.reshape(-1, bucket), axis=1).reshape(-1)
+    for variant in (0, 1):
+        k = keys.copy()
+        st = darm.bitonic_sort(k, bucket, variant)
+        assert st["launches"] == 2 and st["keys_per_thread"] == 16
+        assert (k == want).all(), (bucket, variant)
+
+
 def test_bitonic_sort_config2_full_size():
     """BASELINE config 2: 2^24 int32 keys on one GPU, 64-key buckets; the
     size-independent properties: every bucket sorted and a permutation of its input."""
