@@ -222,7 +222,7 @@ def kernel_info(kernel: str) -> dict:
 
 
 def _i32p(a: np.ndarray):
-    assert a.dtype == np.int32 and a.flags["C_CONTIGUOUS"]
+    _require(a.dtype == np.int32 and a.flags["C_CONTIGUOUS"], "expected a C-contiguous int32 array")
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
 
 
@@ -278,8 +278,29 @@ class WarpBatchResult:
     stats: dict
 
 
+def _require(ok, what):
+    """Argument check of the public wrappers: a DarmUserError (the C-ABI's
+    user-error class, code 2), not an assert, so it holds under python -O."""
+    if not ok:
+        raise DarmUserError(what)
+
+
 def _is_torch_cuda(x) -> bool:
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
+
+
+def _require_i32(x, name, min_words=0):
+    """A DEVICE (torch CUDA) or HOST (numpy) int32 buffer the C-ABI may walk
+    as ``min_words`` contiguous words."""
+    if _is_torch_cuda(x):
+        import torch
+
+        _require(x.dtype == torch.int32 and x.is_contiguous(), f"{name}: expected a contiguous int32 CUDA tensor")
+        _require(x.numel() >= min_words, f"{name}: {x.numel()} words, at least {min_words} needed")
+    else:
+        _require(isinstance(x, np.ndarray) and x.dtype == np.int32 and x.flags["C_CONTIGUOUS"],
+                 f"{name}: expected a C-contiguous int32 numpy array or int32 CUDA tensor")
+        _require(x.size >= min_words, f"{name}: {x.size} words, at least {min_words} needed")
 
 
 def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, object],
@@ -304,6 +325,15 @@ def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, obje
     n_lanes = int(first.numel() if device else first.size)
     if n_warps is None:
         n_warps = n_lanes // warp
+    for n in names:   # compact batch layout: word w*warp + t of every global
+        _require(n in globals, f"missing global {n}")
+        _require(_is_torch_cuda(globals[n]) == device, f"{n}: globals must all be numpy or all CUDA tensors")
+        _require_i32(globals[n], n, n_warps * warp)
+    for n, size in info["shared"]:
+        if shared:
+            _require_i32(shared[n], n, n_warps * size) if device else None
+    if faults is not None:
+        _require_i32(faults, "faults", n_warps)
     if device:
         import torch
 
@@ -331,9 +361,6 @@ def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, obje
         args_np = np.ascontiguousarray(np.asarray(args, dtype=np.int32).reshape(len(info["params"]), -1))
         acount = args_np.shape[1]
         aptr = _i32p(args_np)
-        for n in names:
-            g = globals[n]
-            assert g.dtype == np.int32 and g.flags["C_CONTIGUOUS"], n
         gl_ptrs = [globals[n].ctypes.data for n in names]
         sh_ptrs = [np.ascontiguousarray(shared[n], dtype=np.int32).ctypes.data for n in snames] if shared else []
         if faults is None:
@@ -370,6 +397,7 @@ class PreparedCall:
 def _network_sort(fn, keys, bucket, variant, stream, want_stats, prepare_only, keys_per_thread):
     if isinstance(variant, str):
         variant = VARIANTS[variant]
+    _require_i32(keys, "keys")
     if _is_torch_cuda(keys):
         import torch
 
@@ -377,7 +405,6 @@ def _network_sort(fn, keys, bucket, variant, stream, want_stats, prepare_only, k
         if stream is None:
             stream = torch.cuda.current_stream(keys.device).cuda_stream
     else:
-        assert keys.dtype == np.int32 and keys.flags["C_CONTIGUOUS"]
         ptr, n, mem = keys.ctypes.data, keys.size, 0
     call = PreparedCall(fn, (int(variant), ctypes.c_void_p(ptr), int(n), int(bucket), int(keys_per_thread), mem,
                              ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
@@ -413,6 +440,7 @@ def merge_sort(keys, variant=MELDED, stream=None, want_stats: bool = True, prepa
     (``darm_gpu_merge_sort``)."""
     if isinstance(variant, str):
         variant = VARIANTS[variant]
+    _require_i32(keys, "keys")
     if _is_torch_cuda(keys):
         import torch
 
@@ -420,7 +448,6 @@ def merge_sort(keys, variant=MELDED, stream=None, want_stats: bool = True, prepa
         if stream is None:
             stream = torch.cuda.current_stream(keys.device).cuda_stream
     else:
-        assert keys.dtype == np.int32 and keys.flags["C_CONTIGUOUS"]
         ptr, n, mem = keys.ctypes.data, keys.size, 0
     call = PreparedCall(lib().darm_gpu_merge_sort, (int(variant), ctypes.c_void_p(ptr), int(n), mem,
                                                     ctypes.c_void_p(stream or 0)), want_stats, keepalive=(keys,))
@@ -493,6 +520,10 @@ class Program:
         dev = _is_torch_cuda(globals_)
         if n_warps is None:
             n_warps = int(globals_.shape[0])
+        _require_i32(globals_, "globals", n_warps * self.global_words)
+        if shared is not None:
+            _require(_is_torch_cuda(shared) == dev, "shared: same memory kind as globals")
+            _require_i32(shared, "shared", n_warps * self.shared_words)
         if dev:
             import torch
 
@@ -569,12 +600,14 @@ def lud(a, variant=MELDED, stream=None, want_stats: bool = True, prepare_only: b
     if _is_torch_cuda(a):
         import torch
 
-        assert a.dtype == torch.float32 and a.is_contiguous() and a.dim() == 2 and a.shape[0] == a.shape[1]
+        _require(a.dtype == torch.float32 and a.is_contiguous() and a.dim() == 2 and a.shape[0] == a.shape[1],
+                 "a: expected a contiguous square float32 CUDA tensor")
         ptr, n, mem = a.data_ptr(), a.shape[0], 1
         if stream is None:
             stream = torch.cuda.current_stream(a.device).cuda_stream
     else:
-        assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"] and a.ndim == 2 and a.shape[0] == a.shape[1]
+        _require(a.dtype == np.float32 and a.flags["C_CONTIGUOUS"] and a.ndim == 2 and a.shape[0] == a.shape[1],
+                 "a: expected a C-contiguous square float32 array")
         ptr, n, mem = a.ctypes.data, a.shape[0], 0
     call = PreparedCall(lib().darm_gpu_lud, (int(variant), ctypes.c_void_p(ptr), int(n), mem,
                                              ctypes.c_void_p(stream or 0)), want_stats, keepalive=(a,))
@@ -601,12 +634,14 @@ def srad(j, iters: int, lam: float = 0.5, roi=RODINIA_ROI, variant=MELDED, strea
     if _is_torch_cuda(j):
         import torch
 
-        assert j.dtype == torch.float32 and j.is_contiguous() and j.dim() == 2
+        _require(j.dtype == torch.float32 and j.is_contiguous() and j.dim() == 2,
+                 "j: expected a contiguous 2-D float32 CUDA tensor")
         ptr, (rows, cols), mem = j.data_ptr(), j.shape, 1
         if stream is None:
             stream = torch.cuda.current_stream(j.device).cuda_stream
     else:
-        assert j.dtype == np.float32 and j.flags["C_CONTIGUOUS"] and j.ndim == 2
+        _require(j.dtype == np.float32 and j.flags["C_CONTIGUOUS"] and j.ndim == 2,
+                 "j: expected a C-contiguous 2-D float32 array")
         ptr, (rows, cols), mem = j.ctypes.data, j.shape, 0
     r = _roi_arr(roi)
     call = PreparedCall(lib().darm_gpu_srad, (int(variant), ctypes.c_void_p(ptr), int(rows), int(cols), int(iters),

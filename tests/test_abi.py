@@ -106,6 +106,23 @@ def test_user_errors_are_reported_before_device_use():
         darm.bitonic_sort(np.zeros(100, np.int32), 64)
 
 
+def test_wrapper_rejects_bad_buffers():
+    """The Python wrappers check dtype, contiguity and size before any pointer
+    crosses the C-ABI (the library cannot see a buffer's extent)."""
+    with pytest.raises(darm.DarmUserError):
+        darm.bitonic_sort(np.zeros(128, np.float32), 64)
+    with pytest.raises(darm.DarmUserError):
+        darm.bitonic_sort(np.zeros(256, np.int32)[::2], 64)
+    with pytest.raises(darm.DarmUserError):
+        darm.merge_sort(np.zeros(16, np.int64))
+    g = {n: np.zeros(64, np.int32) for n in ["in", "aux2", "aux3", "out"]}
+    g["aux3"] = np.zeros(32, np.int32)   # two warps need 64 words
+    with pytest.raises(darm.DarmUserError):
+        darm.execute_warps("sb1", 0, 32, [[16]], g, n_warps=2)
+    with pytest.raises(darm.DarmUserError):
+        darm.lud(np.zeros((32, 16), np.float32))
+
+
 def _have_gpu():
     try:
         import torch
