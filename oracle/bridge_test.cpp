@@ -11,9 +11,16 @@
 //   c = darm::gpu::executeWarps(..., Unmelded)  sm_100a unmelded form
 //   d = darm::gpu::executeWarps(..., Melded)    sm_100a melded form
 // and compareRuns(a, b), compareRuns(a, c), compareRuns(a, d) must all be equal.
+// Then acceptance criteria 5 and 6 (acceptance.cpp:243-310) with every
+// executeWarp replaced by darm::gpu::executeWarpsIR (the GPU warp
+// interpreter): serialized cycles drop on the structured kernels at a
+// half-warp split (sb3 / sb4 more than sb1, sb3 with >= 2 melds) and bitonic
+// issues fewer shared-memory accesses after melding; the GPU's statistics are
+// also checked equal to the reference interpreter's on every fixture.
 // Exit 0 on success, 1 on the first mismatch (with the reference's diff).
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -28,6 +35,80 @@ using namespace darm;
 // corpus kernels embedded at build time (oracle/embed_corpus.py)
 extern "C" const char *const ref_corpus_names[];
 extern "C" const char *const ref_corpus_texts[];
+
+static const char *corpus_text(const char *k) {
+  for (int i = 0; ref_corpus_names[i]; ++i)
+    if (std::string(ref_corpus_names[i]) == k) return ref_corpus_texts[i];
+  return nullptr;
+}
+
+// Sum of one WarpExecStats counter over `seeds` fixtures, on the GPU
+// interpreter; every fixture's counters must equal the reference's.
+template <class Get>
+static bool gpu_stat_sum(const Module &m, std::vector<WarpInput> ins, Get get, int64_t &sum) {
+  const Function &f = m.functions[0];
+  const LatencyModel lm = LatencyModel::defaults();
+  auto g = gpu::executeWarpsIR(m, f, ins, lm);
+  sum = 0;
+  for (size_t i = 0; i < ins.size(); ++i) {
+    WarpResult c = executeWarp(m, f, ins[i], lm);
+    if (get(g[i].stats) != get(c.stats) || g[i].stats.serializedCycles != c.stats.serializedCycles ||
+        g[i].stats.sharedMemIssues != c.stats.sharedMemIssues) {
+      std::printf("MISMATCH stats fixture %zu\n", i);
+      return false;
+    }
+    sum += get(g[i].stats);
+  }
+  return true;
+}
+
+static bool criteria5and6() {
+  const LatencyModel lm = LatencyModel::defaults();
+  std::map<std::string, double> rel;
+  std::map<std::string, size_t> melds;
+  for (const char *k : {"sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r"}) {
+    Module pre = parseModule(corpus_text(k));
+    Module post = pre;
+    melds[k] = runDarm(post.functions[0], MeldConfig{}, lm).melds.size();
+    std::vector<WarpInput> ins;
+    for (uint64_t s = 0; s < 10; ++s) {
+      WarpInput in = makeRandomInput(pre, pre.functions[0], 32, 3000 + s);
+      in.args[0] = {16};                                   // half-warp split (acceptance.cpp:251-257)
+      if (in.args.size() > 1) in.args[1] = {24};
+      ins.push_back(in);
+    }
+    int64_t before = 0, after = 0;
+    auto ser = [](const WarpExecStats &st) { return st.serializedCycles; };
+    if (!gpu_stat_sum(pre, ins, ser, before) || !gpu_stat_sum(post, ins, ser, after)) return false;
+    if (before <= 0 || after >= before) {
+      std::printf("C5 FAIL %s: serialized %lld -> %lld\n", k, (long long)before, (long long)after);
+      return false;
+    }
+    rel[k] = double(before - after) / double(before);
+  }
+  if (melds["sb3"] < 2 || rel["sb3"] <= rel["sb1"] || rel["sb4"] <= rel["sb1"]) {
+    std::printf("C5 FAIL: sb3 melds %zu, reductions sb1 %.3f sb3 %.3f sb4 %.3f\n", melds["sb3"], rel["sb1"],
+                rel["sb3"], rel["sb4"]);
+    return false;
+  }
+  std::printf("C5 (GPU interpreter): ok, serialized-cycle reduction sb1 %.3f sb3 %.3f sb4 %.3f\n", rel["sb1"],
+              rel["sb3"], rel["sb4"]);
+  Module pre = parseModule(corpus_text("bitonic"));
+  Module post = pre;
+  runDarm(post.functions[0], MeldConfig{}, lm);
+  std::vector<WarpInput> ins;
+  for (uint64_t s = 0; s < 10; ++s) ins.push_back(makeRandomInput(pre, pre.functions[0], 32, 5000 + s));
+  int64_t before = 0, after = 0;
+  auto shm = [](const WarpExecStats &st) { return st.sharedMemIssues; };
+  if (!gpu_stat_sum(pre, ins, shm, before) || !gpu_stat_sum(post, ins, shm, after)) return false;
+  if (after >= before) {
+    std::printf("C6 FAIL: shared-memory issues %lld -> %lld\n", (long long)before, (long long)after);
+    return false;
+  }
+  std::printf("C6 (GPU interpreter): ok, bitonic shared-memory issues %lld -> %lld\n", (long long)before,
+              (long long)after);
+  return true;
+}
 
 int main(int argc, char **argv) {
   const int fixtures = argc > 1 ? std::atoi(argv[1]) : 100;
@@ -72,5 +153,5 @@ int main(int argc, char **argv) {
     std::printf("%s: ok\n", k);
   }
   std::printf("bridge: %lld compareRuns verdicts equal\n", compared);
-  return 0;
+  return criteria5and6() ? 0 : 1;
 }

@@ -2,7 +2,9 @@
 reference-side C++ binding include/darm_gpu.hpp: for every positive corpus
 kernel, warp sizes {4, 8, 32, 64} and 100 makeRandomInput fixtures, the
 reference's compareRuns finds the sm_100a unmelded and melded results equal
-to the reference interpreter's (oracle/bridge_test.cpp)."""
+to the reference interpreter's; then criteria 5 and 6 (acceptance.cpp:243-310)
+with executeWarp replaced by the GPU warp interpreter
+(oracle/bridge_test.cpp)."""
 import os
 import subprocess
 
@@ -20,6 +22,8 @@ def test_acceptance_c1_on_gpu_through_reference_types():
     r = subprocess.run([BRIDGE, "100"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "compareRuns verdicts equal" in r.stdout
+    # acceptance criteria 5 and 6 with executeWarp replaced by the GPU interpreter
+    assert "C5 (GPU interpreter): ok" in r.stdout and "C6 (GPU interpreter): ok" in r.stdout, r.stdout
 
 
 GPU_BENCH = os.path.join(ROOT, "oracle", "_ref", "darm_gpu_bench")
