@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "darm/fixtures.hpp"
 #include "darm/interp.hpp"
 #include "darm/parser.hpp"
 #include "darm_gpu.h"
@@ -184,6 +185,28 @@ inline std::vector<WarpResult> executeWarpsIR(const Module &m, const Function &f
     if (r.taintedObservable) r.taintNote = "undef-derived value observed (GPU interpreter)";
   }
   return out;
+}
+
+// The result oracle on the GPU: the reference's testing::oracleCompare
+// (tests/helpers.hpp:156-174) — makeRandomInput fixtures seed .. seed +
+// fixtures - 1 at each warp size, both functions run, compareRuns per fixture —
+// with the two executeWarp loops replaced by one executeWarpsIR batch each.
+// Returns "" when every verdict is equal, else the first diff as the
+// reference formats it.
+inline std::string oracleCompare(const Module &m1, const Function &f1, const Module &m2, const Function &f2,
+                                 int fixtures, uint64_t seed, const std::vector<int> &warps = {4, 8, 32}) {
+  const LatencyModel lm = LatencyModel::defaults();
+  for (int w : warps) {
+    std::vector<WarpInput> ins;
+    for (int i = 0; i < fixtures; ++i) ins.push_back(makeRandomInput(m1, f1, w, seed + uint64_t(i)));
+    auto a = executeWarpsIR(m1, f1, ins, lm);
+    auto b = executeWarpsIR(m2, f2, ins, lm);
+    for (int i = 0; i < fixtures; ++i) {
+      CompareVerdict v = compareRuns(a[size_t(i)], b[size_t(i)]);
+      if (!v.equal) return f1.name + " warp " + std::to_string(w) + " fixture " + std::to_string(i) + ": " + v.diff;
+    }
+  }
+  return "";
 }
 
 }  // namespace gpu

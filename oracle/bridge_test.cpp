@@ -110,6 +110,56 @@ static bool criteria5and6() {
   return true;
 }
 
+// The reference's testing::oracleCompare (helpers.hpp:156-174), the result
+// oracle of criterion 1 and test_pipeline, run on the GPU
+// (darm::gpu::oracleCompare): every positive kernel against its runDarm
+// output, 100 fixtures x warps {4, 8, 32} -> no diff; and a mutated melded
+// sb1 (`mul %v 3` -> `mul %v 4`) -> the same first diff the CPU oracle reports.
+static std::string cpu_oracle(const Module &m1, const Function &f1, const Module &m2, const Function &f2,
+                              int fixtures, uint64_t seed) {
+  for (int w : {4, 8, 32})
+    for (int i = 0; i < fixtures; ++i) {
+      WarpInput in = makeRandomInput(m1, f1, w, seed + uint64_t(i));
+      CompareVerdict v = compareRuns(executeWarp(m1, f1, in, LatencyModel::defaults()),
+                                     executeWarp(m2, f2, in, LatencyModel::defaults()));
+      if (!v.equal) return f1.name + " warp " + std::to_string(w) + " fixture " + std::to_string(i) + ": " + v.diff;
+    }
+  return "";
+}
+
+static bool gpu_oracle() {
+  for (const char *k : {"sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "bitonic", "nested"}) {
+    Module orig = parseModule(corpus_text(k));
+    Module melded = orig;
+    runDarm(melded.functions[0], MeldConfig{}, LatencyModel::defaults());
+    const std::string d = gpu::oracleCompare(orig, orig.functions[0], melded, melded.functions[0], 100, 7000);
+    if (!d.empty()) {
+      std::printf("GPU oracle MISMATCH %s: %s\n", k, d.c_str());
+      return false;
+    }
+  }
+  std::string text = corpus_text("sb1");
+  Module orig = parseModule(text);
+  Module melded = orig;
+  runDarm(melded.functions[0], MeldConfig{}, LatencyModel::defaults());
+  std::string mt = printModule(melded);
+  const size_t at = mt.find("mul ");
+  if (at == std::string::npos) return false;
+  const size_t three = mt.find(" 3", at);
+  if (three == std::string::npos) return false;
+  mt.replace(three, 2, " 4");
+  Module bad = parseModule(mt);
+  const std::string g = gpu::oracleCompare(orig, orig.functions[0], bad, bad.functions[0], 20, 7000);
+  const std::string c = cpu_oracle(orig, orig.functions[0], bad, bad.functions[0], 20, 7000);
+  if (g.empty() || g != c) {
+    std::printf("GPU oracle on a mutated kernel: gpu '%s' cpu '%s'\n", g.c_str(), c.c_str());
+    return false;
+  }
+  std::printf("GPU oracle (oracleCompare on executeWarpsIR): ok, 10 kernels x 300 fixtures equal; mutated sb1 "
+              "caught with the CPU oracle's diff\n");
+  return true;
+}
+
 int main(int argc, char **argv) {
   const int fixtures = argc > 1 ? std::atoi(argv[1]) : 100;
   const char *kernels[] = {"sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "bitonic", "nested"};
@@ -153,5 +203,5 @@ int main(int argc, char **argv) {
     std::printf("%s: ok\n", k);
   }
   std::printf("bridge: %lld compareRuns verdicts equal\n", compared);
-  return criteria5and6() ? 0 : 1;
+  return criteria5and6() && gpu_oracle() ? 0 : 1;
 }

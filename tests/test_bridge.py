@@ -24,6 +24,8 @@ def test_acceptance_c1_on_gpu_through_reference_types():
     assert "compareRuns verdicts equal" in r.stdout
     # acceptance criteria 5 and 6 with executeWarp replaced by the GPU interpreter
     assert "C5 (GPU interpreter): ok" in r.stdout and "C6 (GPU interpreter): ok" in r.stdout, r.stdout
+    # the result oracle itself (testing::oracleCompare) on the GPU, incl. a mutated kernel it must catch
+    assert "GPU oracle (oracleCompare on executeWarpsIR): ok" in r.stdout, r.stdout
 
 
 GPU_BENCH = os.path.join(ROOT, "oracle", "_ref", "darm_gpu_bench")
