@@ -45,6 +45,16 @@ __device__ __forceinline__ bool oe_is_upper(int x) {
   else return !(x & k) && (x & (2 * p - 1)) >= k;
 }
 
+// lower ? min(v, b) : max(v, b) issued as a complementary predicated pair:
+// for the plain select ptxas emits min; @!P max, whose write-after-write on
+// one register stalls every serial step.
+__device__ __forceinline__ int32_t oe_select_minmax(int32_t v, int32_t b, bool lower) {
+  asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p min.s32 %0, %0, %2;\n @!p max.s32 %0, %0, %2;\n}"
+      : "+r"(v)
+      : "r"(int(lower)), "r"(b));
+  return v;
+}
+
 __device__ __forceinline__ int32_t oe_exchange_unmelded(int32_t v, int32_t b0, bool lower) {
   if (lower) {                                             // condbr %lower ^lo ^up
     DARM_ARM("oddeven.lo");
@@ -92,15 +102,8 @@ __device__ __forceinline__ int32_t oe_one_step(int32_t v, int lane, uint64_t lo,
     b0 = xch[par][lower ? threadIdx.x + k : (upper ? threadIdx.x - k : threadIdx.x)];
     par ^= 1;
   }
-  if constexpr (M) {
-    // %sel = select %lower %g1 %g2; one store.  Issued as a complementary
-    // predicated pair: for the plain select ptxas emits min; @!P max, whose
-    // write-after-write on one register stalls every serial step.
-    asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p min.s32 %0, %0, %2;\n @!p max.s32 %0, %0, %2;\n}"
-        : "+r"(v)
-        : "r"(int(lower)), "r"(b0));
-    return v;
-  }
+  if constexpr (M)
+    return oe_select_minmax(v, b0, lower);   // %sel = select %lower %g1 %g2; one store
   else
     return oe_exchange_unmelded(v, b0, lower);
 }
@@ -151,8 +154,11 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
 #pragma unroll
     for (int j = 0; j < R; ++j) b0[j] = __shfl_sync(0xffffffffu, v[j], src);
     if constexpr (M) {
+      // the select as a complementary predicated pair (see oe_one_step) from 8
+      // keys per thread up; at 4 the plain select schedules better (57 vs 63 µs)
 #pragma unroll
-      for (int j = 0; j < R; ++j) v[j] = lower ? min(v[j], b0[j]) : max(v[j], b0[j]);
+      for (int j = 0; j < R; ++j)
+        v[j] = R >= 8 ? oe_select_minmax(v[j], b0[j], lower) : (lower ? min(v[j], b0[j]) : max(v[j], b0[j]));
     } else {
       if (lower) {                                         // condbr %lower ^lo ^up
         DARM_ARM("oddeven.reg.lo");
