@@ -30,6 +30,16 @@ __device__ __forceinline__ int32_t flip_fma(int32_t x, int32_t m) {
   return int32_t(uint32_t(x) * uint32_t(1 + 2 * m) + uint32_t(m));
 }
 
+// bit ? max(v, b) : min(v, b) issued as a complementary predicated pair; for
+// the plain select ptxas emits min; @P max (a write-after-write on one
+// register in every serial step of the one-key network).
+__device__ __forceinline__ int32_t select_maxmin(int32_t v, int32_t b, bool bit) {
+  asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p max.s32 %0, %0, %2;\n @!p min.s32 %0, %0, %2;\n}"
+      : "+r"(v)
+      : "r"(int(bit)), "r"(b));
+  return v;
+}
+
 template <int B>
 struct Network {
   static constexpr int kSteps = __builtin_ctz(B) * (__builtin_ctz(B) + 1) / 2;
@@ -104,7 +114,7 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
             // need1 = (keep == up) ? cv > b0 : cv < b0 with up folded into the data:
             // need1 = (keep == up) ? gt : lt with up folded into the data: the
             // lower slot keeps the smaller key — one predicated min/max
-            v[u] = bit[kb] ? max(v[u], b0[u]) : min(v[u], b0[u]);   // ^e.m: the single melded store
+            v[u] = select_maxmin(v[u], b0[u], bit[kb]);   // ^e.m: the single melded store
           }
         }
       }
