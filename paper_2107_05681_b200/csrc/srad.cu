@@ -192,11 +192,12 @@ __device__ __forceinline__ float2 srad_coeff2(float2 jc, float2 n, float2 s, flo
   return make_float2(clamp_rd<M>(c.x), clamp_rd<M>(c.y));
 }
 
-// IEEE path: 5 CTAs per SM (48 registers, a 16-byte spill) hide more load
-// latency than 4 (160.6 / 151.0 ms against 169.6 / 157.5); the fast path keeps
-// the compiler's choice (63 registers, 4 CTAs: bounding it to 4 or 5 is slower)
+// CTAs per SM, each form at its best (16384^2 x 100): 5 (48 registers, a
+// small spill) for the IEEE forms (unmelded 169.6 -> 160.6 ms, melded 157.5 ->
+// 151.0) and the unmelded fast form (126.7 -> 121.1); the melded fast form
+// keeps the compiler's 63 registers and 4 CTAs (102.9 ms; bounded to 5: 105.5)
 template <bool M, bool FAST, bool PACK>
-__global__ void __launch_bounds__(256, FAST ? 0 : 5) srad_sweep_kernel(SradParams P) {
+__global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(SradParams P) {
   const int lane = threadIdx.x & 31;
   const int wcol = blockIdx.x * 8 + (threadIdx.x >> 5);   // warp column group
   const int j = wcol * 30 + lane - 1;                      // this lane's column
