@@ -11,6 +11,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-per-kernel > gpurun_out/bench_under_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bitonic_sort -c 4 -o gpurun_out/prof_bitonic python tools/profile_driver.py bitonic > gpurun_out/ncu_bitonic.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:srad_sweep -c 4 -o gpurun_out/prof_srad python tools/profile_driver.py srad > gpurun_out/ncu_srad.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:srad_sweep -s 4 -c 4 -o gpurun_out/prof_srad_fast python tools/profile_driver.py srad > gpurun_out/ncu_srad_fast.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:oddeven_sort -c 4 -o gpurun_out/prof_oddeven python tools/profile_driver.py oddeven > gpurun_out/ncu_oddeven.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_sort -c 4 -o gpurun_out/prof_merge python tools/profile_driver.py merge 1048576 > gpurun_out/ncu_merge.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:nqueens -c 2 -o gpurun_out/prof_nqueens python tools/profile_driver.py nqueens > gpurun_out/ncu_nqueens.log 2>&1

@@ -11,7 +11,7 @@ cp $O/launches.csv $P/${R}_launches_bench.csv
 python tools/launch_share.py $O/launches.csv > $P/${R}_launches_bench_summary.txt
 cp $O/launches_lud8192.csv $P/${R}_launches_lud8192.csv
 python tools/launch_share.py $O/launches_lud8192.csv > $P/${R}_launches_lud8192_summary.txt
-for k in bitonic srad lud_far lud_melded lud_unmelded oddeven merge nqueens; do
+for k in bitonic srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens; do
   python tools/ncu_summary.py $O/prof_$k.ncu-rep > $P/${R}_ncu_$k.json
 done
 cp $O/lane_eff.csv $P/${R}_lane_efficiency_ncu.csv
