@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
   auto row = [&](int g) { return P.jin + size_t(clampi(g, 0, gmax) - P.r0 + 1) * cols; };
   // R_B: the west/east neighbour of this lane at image borders and lane 31's
   // east value (no lane to its right).
-  auto west_east = [&](const float *rp, float v, float &w, float &e) {
+  auto west_east = [&](const float *rp, float v, float &w, float &e) {   // rp -> (row, jc)
     const float sw = __shfl_up_sync(0xffffffffu, v, 1);
     const float se = __shfl_down_sync(0xffffffffu, v, 1);
     if constexpr (!M) {
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
       } else if (lane == 31 || j == cols - 1) {
         DARM_ARM("srad.rb.east");
         w = sw;
-        e = j >= cols - 1 ? v : rp[min(jc + 1, cols - 1)];
+        e = j >= cols - 1 ? v : rp[1];                     // j < cols - 1: jc + 1 is in the row
       } else {
         DARM_ARM("srad.rb.mid");
         w = sw;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
     } else {
       const bool edge_e = lane == 31 || j >= cols - 1;
       float ee = v;
-      if (lane == 31 && j < cols - 1) ee = rp[jc + 1];   // the only one-sided run
+      if (lane == 31 && j < cols - 1) ee = rp[1];         // the only one-sided run
       w = j == 0 ? v : sw;
       e = edge_e ? ee : se;
     }
@@ -264,18 +264,39 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
   float jm1 = row(g0 - 1)[jc], j0 = row(g0)[jc], jp1 = rowc(g0 + 1)[jc], jp2 = rowc(g0 + 2)[jc];
   float jp3 = rowc(g0 + 3)[jc];
   float w0, e0;
-  west_east(row(g0), j0, w0, e0);
+  west_east(row(g0) + jc, j0, w0, e0);
   float c0 = srad_coeff<M, FAST>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
   float *outp = P.jout + size_t(seg0 + 1) * cols + j;
   const float2 z = f2(P.nz);
+  // per-lane row pointers slide two rows per iteration: row g, and from it the
+  // rows g+1, g+2 (lane 31's east values) and g+4, g+5 (the prefetch) while
+  // g + 5 <= glim; a tile's last iterations clamp through rowc (IEEE melded
+  // 151.3 -> 147.4 ms)
+  const size_t cs = size_t(cols);
+  const float *pg = row(g0) + jc;
   int i = seg0;
   // two rows (g, g+1) per iteration, their arithmetic in f32x2 pairs
   for (; i + 1 < seg1; i += 2) {
     const int g = P.r0 + i;
-    const float q4 = rowc(g + 4)[jc], q5 = rowc(g + 5)[jc];   // next iteration's rows, in flight
+    const float *p1, *p2, *p4, *p5;
+    // (the fast melded form's register budget has no room for the pointers: it
+    // recomputes them, 102 vs 106 ms)
+    if (!(FAST && M) && g + 5 <= glim) {
+      p1 = pg + cs;
+      p2 = p1 + cs;
+      p4 = p2 + 2 * cs;
+      p5 = p4 + cs;
+    } else {
+      p1 = rowc(g + 1) + jc;
+      p2 = rowc(g + 2) + jc;
+      p4 = rowc(g + 4) + jc;
+      p5 = rowc(g + 5) + jc;
+    }
+    pg += 2 * cs;
+    const float q4 = *p4, q5 = *p5;                         // next iteration's rows, in flight
     float w1, e1, w2, e2;
-    west_east(rowc(g + 1), jp1, w1, e1);
-    west_east(rowc(g + 2), jp2, w2, e2);
+    west_east(p1, jp1, w1, e1);
+    west_east(p2, jp2, w2, e2);
     const float2 cc = srad_coeff2<M, FAST, PACK>(make_float2(jp1, jp2), make_float2(j0, jp1), make_float2(jp2, jp3),
                                            make_float2(w1, w2), make_float2(e1, e2), q0sqr, q0den, z);
     const float c1 = (g + 1 <= gmax) ? cc.x : c0;           // c at the rows below (clamped at the bottom)
@@ -327,7 +348,7 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
   if (i < seg1) {   // an odd last row
     const int g = P.r0 + i;
     float w1, e1;
-    west_east(rowc(g + 1), jp1, w1, e1);
+    west_east(rowc(g + 1) + jc, jp1, w1, e1);
     const float c1 = (g + 1 <= gmax) ? srad_coeff<M, FAST>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
     float ce = __shfl_down_sync(0xffffffffu, c0, 1);
     if (j >= cols - 1) ce = c0;
