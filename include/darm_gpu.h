@@ -222,6 +222,10 @@ int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream,
  * relative, the tolerance BASELINE.json's north star states for SRAD, instead
  * of bit for bit. */
 #define DARM_FAST_MATH 0x100
+/* SRAD only: force the 64-bit row addressing that tiles of 2^31 or more
+ * elements take (32-bit element indices otherwise); results are identical —
+ * a testing aid for that path. */
+#define DARM_SRAD_INDEX64 0x200
 
 int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters,
                   float lambda, const int *roi, int mem, void *stream,

@@ -35,6 +35,7 @@ UNMELDED = 0
 MELDED = 1
 VARIANTS = {"unmelded": UNMELDED, "melded": MELDED}
 FAST_MATH = 0x100   # SRAD: OR into the variant (DARM_FAST_MATH, within 1e-5 relative)
+SRAD_INDEX64 = 0x200   # SRAD: force the 64-bit row addressing of very large tiles (testing aid)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libdarm_gpu.so")

@@ -750,7 +750,8 @@ int64_t darm_gpu_srad_roi_words(int64_t cols, const int *roi) {
 int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, float lambda, const int *roi,
                   int mem, void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if ((variant & ~DARM_FAST_MATH) != DARM_UNMELDED && (variant & ~DARM_FAST_MATH) != DARM_MELDED)
+    if ((variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_UNMELDED &&
+        (variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_MELDED)
       user_error("variant must be 0 (unmelded) or 1 (melded), optionally | DARM_FAST_MATH");
     check_srad_args(rows, cols, roi, lambda);
     if (iters < 0) user_error("iters must be >= 0");
@@ -827,7 +828,8 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, 
                             int64_t r0, int64_t rows, float lambda, const int *roi, const double *roi_in,
                             double *roi_out, float *q0_scratch, void *stream, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if ((variant & ~DARM_FAST_MATH) != DARM_UNMELDED && (variant & ~DARM_FAST_MATH) != DARM_MELDED)
+    if ((variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_UNMELDED &&
+        (variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_MELDED)
       user_error("variant must be 0 (unmelded) or 1 (melded), optionally | DARM_FAST_MATH");
     check_srad_args(rows, cols, roi, lambda);
     if (tile_rows < 1 || r0 < 0 || r0 + tile_rows > rows) user_error("tile outside the image");

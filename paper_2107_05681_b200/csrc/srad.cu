@@ -196,7 +196,7 @@ __device__ __forceinline__ float2 srad_coeff2(float2 jc, float2 n, float2 s, flo
 // small spill) for the IEEE forms (unmelded 169.6 -> 160.6 ms, melded 157.5 ->
 // 151.0) and the unmelded fast form (126.7 -> 121.1); the melded fast form
 // keeps the compiler's 63 registers and 4 CTAs (102.9 ms; bounded to 5: 105.5)
-template <bool M, bool FAST, bool PACK>
+template <bool M, bool FAST, bool PACK, bool IDX32>
 __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(SradParams P) {
   const int lane = threadIdx.x & 31;
   const int wcol = blockIdx.x * 8 + (threadIdx.x >> 5);   // warp column group
@@ -268,20 +268,29 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
   float c0 = srad_coeff<M, FAST>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
   float *outp = P.jout + size_t(seg0 + 1) * cols + j;
   const float2 z = f2(P.nz);
-  // per-lane row pointers slide two rows per iteration: row g, and from it the
-  // rows g+1, g+2 (lane 31's east values) and g+4, g+5 (the prefetch) while
-  // g + 5 <= glim; a tile's last iterations clamp through rowc (IEEE melded
-  // 151.3 -> 147.4 ms)
+  // Row addressing in the two-row loop (rows g+1, g+2 for lane 31's east
+  // values, g+4, g+5 for the prefetch): tiles under 2^31 elements use 32-bit
+  // element indices (clamp + multiply-add, one wide multiply-add for the
+  // address: 16384^2 x 100 IEEE melded 147.4 -> 135.2 ms, fast melded 101.3 ->
+  // 92.6); larger tiles slide 64-bit row pointers two rows per iteration
+  // (clamping through rowc for a tile's last iterations)
   const size_t cs = size_t(cols);
   const float *pg = row(g0) + jc;
+  const int off32 = (1 - P.r0) * cols + jc;                  // IDX32: row g's element index = g * cols + off32
   int i = seg0;
   // two rows (g, g+1) per iteration, their arithmetic in f32x2 pairs
   for (; i + 1 < seg1; i += 2) {
     const int g = P.r0 + i;
     const float *p1, *p2, *p4, *p5;
-    // (the fast melded form's register budget has no room for the pointers: it
-    // recomputes them, 102 vs 106 ms)
-    if (!(FAST && M) && g + 5 <= glim) {
+    if constexpr (IDX32) {
+      // the tile buffer has < 2^31 elements: a 32-bit element index per row
+      // (clamp, multiply-add) and one wide multiply-add for the address
+      auto at = [&](int gg) { return P.jin + (min(gg, glim) * cols + off32); };
+      p1 = at(g + 1);
+      p2 = at(g + 2);
+      p4 = at(g + 4);
+      p5 = at(g + 5);
+    } else if (!(FAST && M) && g + 5 <= glim) {   // (no register room in the melded fast form)
       p1 = pg + cs;
       p2 = p1 + cs;
       p4 = p2 + 2 * cs;
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
       p4 = rowc(g + 4) + jc;
       p5 = rowc(g + 5) + jc;
     }
-    pg += 2 * cs;
+    if constexpr (!IDX32) pg += 2 * cs;
     const float q4 = *p4, q5 = *p5;                         // next iteration's rows, in flight
     float w1, e1, w2, e2;
     west_east(p1, jp1, w1, e1);
@@ -461,12 +470,17 @@ cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const 
   // split every pair (126 -> 147 ms) and the IEEE path's scalar divisions
   // around packed products lose too (157 -> 184 ms): both run two rows per
   // iteration in scalar code.
+  // 32-bit element indices while the tile buffer (tile_rows + 3 rows) has
+  // fewer than 2^31 elements (16384^2 on one GPU: 2.7e8)
+  const bool idx32 = int64_t(tile_rows + 3) * cols < (int64_t(1) << 31) && !(variant & 0x200);   // DARM_SRAD_INDEX64
+#define SRAD_L(Mm, F, PK)                                                                                   \
+  (idx32 ? srad_sweep_kernel<Mm, F, PK, true><<<grid, 256, 0, s>>>(P)                                    \
+         : srad_sweep_kernel<Mm, F, PK, false><<<grid, 256, 0, s>>>(P))
   if (variant & 1)
-    fast ? srad_sweep_kernel<true, true, true><<<grid, 256, 0, s>>>(P)
-         : srad_sweep_kernel<true, false, false><<<grid, 256, 0, s>>>(P);
+    fast ? SRAD_L(true, true, true) : SRAD_L(true, false, false);
   else
-    fast ? srad_sweep_kernel<false, true, false><<<grid, 256, 0, s>>>(P)
-         : srad_sweep_kernel<false, false, false><<<grid, 256, 0, s>>>(P);
+    fast ? SRAD_L(false, true, false) : SRAD_L(false, false, false);
+#undef SRAD_L
   return cudaGetLastError();
 }
 
