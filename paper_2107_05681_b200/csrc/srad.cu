@@ -279,6 +279,11 @@ __global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(Sr
   const int off32 = (1 - P.r0) * cols + jc;                  // IDX32: row g's element index = g * cols + off32
   int i = seg0;
   // two rows (g, g+1) per iteration, their arithmetic in f32x2 pairs
+  // unrolled twice for the unmelded fast form only (108.7 -> 104.9 ms; the
+  // other forms lose: IEEE melded 135 -> 140, fast melded 93 -> 112 at 80
+  // registers) — each form at its best
+  constexpr int kUnroll = (FAST && !M) ? 2 : 1;
+#pragma unroll kUnroll
   for (; i + 1 < seg1; i += 2) {
     const int g = P.r0 + i;
     const float *p1, *p2, *p4, *p5;
