@@ -26,4 +26,9 @@ timeout 300 python tools/time_srad.py > gpurun_out/time_srad.log 2>&1
 timeout 600 python tools/time_bitonic.py 64 256 1024 4096 > gpurun_out/time_bitonic.log 2>&1
 timeout 600 python tools/time_bitonic.py --oddeven 64 256 > gpurun_out/time_oddeven.log 2>&1
 timeout 300 python tools/time_corpus.py > gpurun_out/time_corpus.log 2>&1
+# summarise the ncu reports here and drop them (gpurun copies back at most 64 MiB)
+for k in bitonic srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens; do
+  python tools/ncu_summary.py gpurun_out/prof_$k.ncu-rep > gpurun_out/ncusum_$k.json && rm -f gpurun_out/prof_$k.ncu-rep
+done
+rm -f gpurun_out/trace_lud.json
 ls -la gpurun_out

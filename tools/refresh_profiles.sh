@@ -12,7 +12,8 @@ python tools/launch_share.py $O/launches.csv > $P/${R}_launches_bench_summary.tx
 cp $O/launches_lud8192.csv $P/${R}_launches_lud8192.csv
 python tools/launch_share.py $O/launches_lud8192.csv > $P/${R}_launches_lud8192_summary.txt
 for k in bitonic srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens; do
-  python tools/ncu_summary.py $O/prof_$k.ncu-rep > $P/${R}_ncu_$k.json
+  if [ -f $O/ncusum_$k.json ]; then cp $O/ncusum_$k.json $P/${R}_ncu_$k.json
+  else python tools/ncu_summary.py $O/prof_$k.ncu-rep > $P/${R}_ncu_$k.json; fi
 done
 cp $O/lane_eff.csv $P/${R}_lane_efficiency_ncu.csv
 python tools/lane_eff.py $O/lane_eff.csv > /dev/null
