@@ -51,6 +51,18 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
   const int T = blockDim.x;
   const int lane = int(threadIdx.x) & 31;
   uint32_t *const stk = sk_b + (int(threadIdx.x) - (P.base - 1) * T);  // row r's slot: stk[r * T]
+  // the same slot as a 32-bit shared-window address (row r: sa0 + r * 4T), so
+  // the loop does not re-derive the generic window base every iteration
+  const uint32_t sa0 = static_cast<uint32_t>(__cvta_generic_to_shared(stk));
+  const uint32_t sstride = 4u * uint32_t(T);
+  auto ld_stk = [&](int r) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sa0 + uint32_t(r) * sstride) : "memory");
+    return v;
+  };
+  auto st_stk = [&](int r, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa0 + uint32_t(r) * sstride), "r"(v) : "memory");
+  };
   const int n = P.n, nm1 = P.n - 1;
   const uint32_t mask = P.mask;
   int row = P.base - 1;
@@ -88,7 +100,7 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
       if (av == 0) {
         DARM_ARM("nq.pop");                                // ^pop
         const int r1 = row - 1;
-        const uint32_t b1 = stk[r1 * T];
+        const uint32_t b1 = ld_stk(r1);
         cols ^= b1;
         d1 ^= W(b1) << r1;
         const int k1 = nm1 - r1;
@@ -100,7 +112,7 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
       } else {
         DARM_ARM("nq.push");                               // ^push
         const uint32_t b2 = av & (0u - av);
-        stk[row * T] = b2;
+        st_stk(row, b2);
         cols ^= b2;
         d1 ^= W(b2) << row;
         const int k2 = nm1 - row;
@@ -119,10 +131,15 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
       uint32_t b2 = 0;
       if (!z) b2 = av & uint32_t(r1);                      // ^pop.m.g
       const int rr = z ? r1 : row;                         // the stack row both arms touch
-      uint32_t *const slot = stk + rr * T;
-      if (!z) *slot = b2;                                  // ^pop.m.g1
+      const uint32_t slot = sa0 + uint32_t(rr) * sstride;
       uint32_t b1 = 0;
-      if (z) b1 = *slot;                                   // ^pop.m.g2
+      // ^pop.m.g1: if (!z) slot = b2;  ^pop.m.g2: if (z) b1 = slot  (predicated)
+      asm volatile(
+          "{\n .reg .pred p, q;\n setp.ne.b32 p, %2, 0;\n setp.eq.b32 q, %2, 0;\n"
+          " @q st.shared.u32 [%1], %3;\n @p ld.shared.u32 %0, [%1];\n}"
+          : "+r"(b1)
+          : "r"(slot), "r"(int(z)), "r"(b2)
+          : "memory");
       const uint32_t b = z ? b1 : b2;                      // %sel3
       cols ^= b;
       d1 ^= W(b) << rr;
