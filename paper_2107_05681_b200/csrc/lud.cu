@@ -99,7 +99,10 @@ __global__ void __launch_bounds__(32 * kPairs) lud_panel_kernel(float *__restric
   __shared__ float dia[BS][LD];               // the factored diagonal block (warp 0 of the CTA)
   __shared__ float diaT[BS][LD];              // diaT[i][j] = dia[j][i]
   __shared__ float blk[kPairs][2][BS][LD];    // [0] row block R[i][c]; [1] column block transposed C[i][r]
-  extern __shared__ float pend[];
+  // pending-update operands, static (sized for kMaxPend): the compiler then
+  // addresses them in the shared window directly instead of re-deriving a
+  // generic base for a dynamic array at every access
+  __shared__ __align__(16) float pend[kPendFloats];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * kPairs + warp;
   const bool have = p < npairs;                             // warp-uniform
@@ -604,7 +607,7 @@ void launch_panel(float *a, int n, int o, int O, float *dscr, cudaStream_t s) {
   // still read the unfactored one); the last one, with no other reader, in place
   float *dst = m > 0 ? dscr + size_t(o / BS) * BS * BS : a + size_t(o) * n + o;
   const int dstride = m > 0 ? BS : n;
-  const size_t shm = (o > O ? kPendFloats : 0) * sizeof(float);
+  const size_t shm = 0;
   switch ((o - O) / BS) {
     case 0: lud_panel_kernel<M, 0><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride); break;
     case 1: lud_panel_kernel<M, 1><<<grid, 32 * kPairs, shm, s>>>(a, n, o, m, O, dst, dstride); break;
@@ -695,13 +698,6 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
   cudaGetDevice(&dev);
   LudDevice &D = devs[dev & 63];
   if (!D.attr) {
-    for (auto k : {lud_panel_kernel<false, 0>, lud_panel_kernel<false, 1>, lud_panel_kernel<false, 2>,
-                   lud_panel_kernel<false, 3>, lud_panel_kernel<true, 0>, lud_panel_kernel<true, 1>,
-                   lud_panel_kernel<true, 2>, lud_panel_kernel<true, 3>}) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(kPendFloats * sizeof(float)));
-      if (e != cudaSuccess) return e;
-    }
     const int shm = int(size_t(kFarSmemWords) * sizeof(float));
     for (auto k : {lud_far_pipe_kernel<1>, lud_far_pipe_kernel<2>, lud_far_pipe_kernel<3>, lud_far_pipe_kernel<4>}) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, shm);
