@@ -40,6 +40,28 @@ __device__ __forceinline__ int32_t select_maxmin(int32_t v, int32_t b, bool bit)
   return v;
 }
 
+// In-register compare-exchange (lo, hi) = (min, max) of (a, b).  For the pairs
+// with f set the larger key is rebuilt on the FMA pipe as a + b - lo (exact in
+// wrapping 32-bit arithmetic): two IMADs by the runtime unit `one` / `mone`
+// (gridDim.y = 1, opaque to both compilers) replace one VIMNMX on the ALU pipe,
+// which the compare-exchanges saturate.  DARM_CX_FMA_MOD = 0 turns it off.
+#ifndef DARM_CX_FMA_MOD
+#define DARM_CX_FMA_MOD 2
+#endif
+__device__ __forceinline__ void cx_pair(bool f, int32_t a, int32_t b, int32_t &lo, int32_t &hi, uint32_t one,
+                                        uint32_t mone) {
+  lo = min(a, b);
+  if (f) {   // compile-time after unrolling
+    uint32_t s, h;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(a), "r"(one), "r"(b));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(lo), "r"(mone), "r"(s));
+    hi = int32_t(h);
+  } else {
+    hi = max(a, b);
+  }
+}
+__host__ __device__ constexpr bool cx_on_fma(int j) { return DARM_CX_FMA_MOD > 0 && j % (DARM_CX_FMA_MOD > 0 ? DARM_CX_FMA_MOD : 1) == 0; }
+
 template <int B>
 struct Network {
   static constexpr int kSteps = __builtin_ctz(B) * (__builtin_ctz(B) + 1) / 2;
@@ -148,6 +170,11 @@ template <int R>
 __device__ __forceinline__ void load_keys(int32_t (&v)[R], const int32_t *__restrict__ keys, uint32_t base, uint32_t n) {
   if (base < n) {                                         // whole bucket in or out (n % B == 0)
     const int4 *src = reinterpret_cast<const int4 *>(keys + base);
+    if (R % 8 == 0 && aligned32(keys)) {
+#pragma unroll
+      for (int q = 0; q < R / 8; ++q) ld_v8(keys + base + 8 * q, &v[8 * q]);
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < R / 4; ++q) {
       const int4 x = src[q];
@@ -178,6 +205,7 @@ __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32
   const uint32_t tiles = (n + kTile - 1) / kTile;
   uint32_t tile = kCta ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int par = 0;
+  const uint32_t one = gridDim.y, mone = 0u - one;   // 1 and -1, opaque (cx_pair)
   int32_t nxt[R];
   if (PF && tile < tiles) load_keys<R>(nxt, keys, tile * kTile + uint32_t(tid) * R, n);
   for (; tile < tiles; tile += units) {
@@ -212,7 +240,8 @@ __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32
             for (int j = 0; j < R; ++j) {
               if (j & k) continue;
               const bool up = d < LR ? !((j >> d) & 1) : true;   // compile-time (or folded) direction
-              const int32_t lo = min(v[j], v[j | k]), hi = max(v[j], v[j | k]);
+              int32_t lo, hi;
+              cx_pair(cx_on_fma(j), v[j], v[j | k], lo, hi, one, mone);
               v[j] = up ? lo : hi;
               v[j | k] = up ? hi : lo;
             }
@@ -222,7 +251,8 @@ __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32
 #pragma unroll
               for (int j = 0; j < R; ++j) {
                 if (j & k) continue;
-                const int32_t lo = min(v[j], v[j | k]), hi = max(v[j], v[j | k]);
+                int32_t lo, hi;
+                cx_pair(cx_on_fma(j), v[j], v[j | k], lo, hi, one, mone);
                 v[j] = lo;
                 v[j | k] = hi;
               }
@@ -232,7 +262,8 @@ __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32
 #pragma unroll
               for (int j = 0; j < R; ++j) {
                 if (j & k) continue;
-                const int32_t lo = min(v[j], v[j | k]), hi = max(v[j], v[j | k]);
+                int32_t lo, hi;
+                cx_pair(cx_on_fma(j), v[j], v[j | k], lo, hi, one, mone);
                 v[j] = hi;
                 v[j | k] = lo;
               }
@@ -281,7 +312,12 @@ __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32
         }
       }
     }
-    if (live) {
+    if (live && R % 8 == 0 && aligned32(keys)) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) v[j] = flip_fma(v[j], neg);
+#pragma unroll
+      for (int q = 0; q < R / 8; ++q) st_v8(keys + base + 8 * q, &v[8 * q]);
+    } else if (live) {
       int4 *dst = reinterpret_cast<int4 *>(keys + base);
 #pragma unroll
       for (int q = 0; q < R / 4; ++q)

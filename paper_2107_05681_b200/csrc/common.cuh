@@ -29,6 +29,21 @@ __device__ __forceinline__ int32_t ir_shr(int32_t a, int32_t b) { return int32_t
 // sinking nor if-conversion in NVVM can cross it; it emits no SASS.
 #define DARM_ARM(tag) asm volatile("// arm " tag ::: "memory")
 
+// 32-byte vectors (LDG/STG.E.ENL2.256): with R >= 8 consecutive keys per thread
+// each warp instruction covers whole sectors; 16-byte vectors at a 64-byte
+// thread stride touch every sector twice (2x the L1 sector traffic).
+__device__ __forceinline__ bool aligned32(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
+__device__ __forceinline__ void ld_v8(const int32_t *p, int32_t *v) {
+  asm("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void st_v8(int32_t *p, const int32_t *v) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 // Lane -> (warp, tid) split for a logical warp of W lanes (1..64).  WT is the
 // compile-time warp size when it is a power of two, 0 for a runtime W.
 template <int WT>

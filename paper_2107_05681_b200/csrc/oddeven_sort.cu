@@ -235,7 +235,10 @@ __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__res
   for (uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < tiles; tile += warps) {
     const uint32_t base = tile * kTile + uint32_t(lane) * R;
     int32_t v[R];
-    if (base < n) {                                        // whole bucket in or out (n % B == 0)
+    if (base < n && R % 8 == 0 && aligned32(keys)) {       // whole sectors per warp instruction
+#pragma unroll
+      for (int q = 0; q < R / 8; ++q) ld_v8(keys + base + 8 * q, &v[8 * q]);
+    } else if (base < n) {                                 // whole bucket in or out (n % B == 0)
       const int4 *src = reinterpret_cast<const int4 *>(keys + base);
 #pragma unroll
       for (int q = 0; q < R / 4; ++q) {
@@ -250,7 +253,10 @@ __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__res
       for (int j = 0; j < R; ++j) v[j] = INT_MAX;
     }
     oe_reg_network<M, B, R, 1, 1>(v, lane, tib, x0);
-    if (base < n) {
+    if (base < n && R % 8 == 0 && aligned32(keys)) {
+#pragma unroll
+      for (int q = 0; q < R / 8; ++q) st_v8(keys + base + 8 * q, &v[8 * q]);
+    } else if (base < n) {
       int4 *dst = reinterpret_cast<int4 *>(keys + base);
 #pragma unroll
       for (int q = 0; q < R / 4; ++q) dst[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
