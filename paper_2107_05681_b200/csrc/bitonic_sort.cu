@@ -196,14 +196,15 @@ __global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32
   // kCta: a bucket spans warps (B > 32 R, up to 4096 keys): the CTA walks
   // 256 R-key tiles and strides k >= 32 R exchange through shared memory
   constexpr bool kCta = P > 32;
-  constexpr uint32_t kTile = (kCta ? 256u : 32u) * R;
+  // The CTA walks 256 R-key tiles (CTA-uniform loop: ptxas knows every shuffle
+  // runs converged, no WARPSYNC around them).
+  constexpr uint32_t kTile = 256u * R;
   __shared__ int32_t xch[kCta ? 2 : 1][kCta ? R : 1][kCta ? 256 : 1];   // [buffer][register][thread]: conflict-free
-  const int lane = int(threadIdx.x) & 31;
-  const int tid = kCta ? int(threadIdx.x) : lane;       // thread index within the tile
+  const int tid = int(threadIdx.x);                     // thread index within the tile
   const int tib = tid & (P - 1);                        // thread index within the bucket
-  const uint32_t units = kCta ? gridDim.x : (gridDim.x * blockDim.x) >> 5;   // tile walkers (CTAs or warps)
+  const uint32_t units = gridDim.x;
   const uint32_t tiles = (n + kTile - 1) / kTile;
-  uint32_t tile = kCta ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t tile = blockIdx.x;
   int par = 0;
   const uint32_t one = gridDim.y, mone = 0u - one;   // 1 and -1, opaque (cx_pair)
   int32_t nxt[R];
@@ -362,21 +363,17 @@ int sm_count() {
 // are launched, spread evenly over the SMs.
 template <bool M, int B, int R, bool PF>
 cudaError_t launch_reg_pf(int32_t *keys, int64_t n, cudaStream_t s) {
-  constexpr int CTA = 256, WPC = CTA / 32;
+  constexpr int CTA = 256;
   static int per_sm = 0;                          // resident CTAs per SM (registers bound it)
   if (!per_sm) {
     cudaError_t e =
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bitonic_sort_reg_kernel<M, B, R, PF>, CTA, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
-  const int sms = sm_count();
-  const int64_t tiles = (n + 32 * R - 1) / (32 * R);
-  const int64_t max_warps = int64_t(sms) * per_sm * WPC;
-  const int64_t iters = (tiles + max_warps - 1) / max_warps;
-  const int64_t warps_per_sm = (tiles + int64_t(sms) * iters - 1) / (int64_t(sms) * iters);
-  int64_t grid = int64_t(sms) * ((warps_per_sm + WPC - 1) / WPC);
-  const int64_t need = (tiles + WPC - 1) / WPC;
-  if (grid > need) grid = need;
+  const int64_t tiles = (n + CTA * R - 1) / (CTA * R);
+  const int64_t max_ctas = int64_t(sm_count()) * per_sm;
+  const int64_t iters = (tiles + max_ctas - 1) / max_ctas;
+  int64_t grid = (tiles + iters - 1) / iters;
   if (grid < 1) grid = 1;
   bitonic_sort_reg_kernel<M, B, R, PF><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
