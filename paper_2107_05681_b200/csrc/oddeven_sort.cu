@@ -226,14 +226,14 @@ template <bool M, int B, int R>
 __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
   constexpr int P = B / R;
   static_assert(R >= 4 && R <= B && P <= 32, "R keys per thread, at most 32 threads per bucket");
-  constexpr uint32_t kTile = 32u * R;
+  // CTA-uniform walk over 256 R-key tiles: ptxas sees every shuffle converged
+  constexpr uint32_t kTile = 256u * R;
   const int lane = int(threadIdx.x) & 31;
   const int tib = lane & (P - 1);
   const int x0 = tib * R;                                  // bucket index of register 0
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t tiles = (n + kTile - 1) / kTile;
-  for (uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < tiles; tile += warps) {
-    const uint32_t base = tile * kTile + uint32_t(lane) * R;
+  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint32_t base = tile * kTile + uint32_t(threadIdx.x) * R;
     int32_t v[R];
     if (base < n && R % 8 == 0 && aligned32(keys)) {       // whole sectors per warp instruction
 #pragma unroll
@@ -291,19 +291,16 @@ cudaError_t launch_one(int32_t *keys, int64_t n, cudaStream_t s) {
 
 template <bool M, int B, int R>
 cudaError_t launch_reg(int32_t *keys, int64_t n, cudaStream_t s) {
-  constexpr int CTA = 256, WPC = CTA / 32;
+  constexpr int CTA = 256;
   static int per_sm = 0;
   if (!per_sm) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oddeven_sort_reg_kernel<M, B, R>, CTA, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
-  const int64_t tiles = (n + 32 * R - 1) / (32 * R);
-  const int64_t max_warps = int64_t(sms()) * per_sm * WPC;
-  const int64_t iters = (tiles + max_warps - 1) / max_warps;
-  const int64_t warps_per_sm = (tiles + int64_t(sms()) * iters - 1) / (int64_t(sms()) * iters);
-  int64_t grid = int64_t(sms()) * ((warps_per_sm + WPC - 1) / WPC);
-  const int64_t need = (tiles + WPC - 1) / WPC;
-  if (grid > need) grid = need;
+  const int64_t tiles = (n + CTA * R - 1) / (CTA * R);
+  const int64_t max_ctas = int64_t(sms()) * per_sm;
+  const int64_t iters = (tiles + max_ctas - 1) / max_ctas;
+  int64_t grid = (tiles + iters - 1) / iters;
   if (grid < 1) grid = 1;
   oddeven_sort_reg_kernel<M, B, R><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
