@@ -222,6 +222,28 @@ __device__ __forceinline__ void oe_reg_network(int32_t (&v)[R], int lane, int ti
   }
 }
 
+// R consecutive keys of one thread (INT_MAX past the end; n % B == 0)
+template <int R>
+__device__ __forceinline__ void oe_load_keys(int32_t (&v)[R], const int32_t *__restrict__ keys, uint32_t base, uint32_t n) {
+  if (base < n && R % 8 == 0 && aligned32(keys)) {         // whole sectors per warp instruction
+#pragma unroll
+    for (int q = 0; q < R / 8; ++q) ld_v8(keys + base + 8 * q, &v[8 * q]);
+  } else if (base < n) {
+    const int4 *src = reinterpret_cast<const int4 *>(keys + base);
+#pragma unroll
+    for (int q = 0; q < R / 4; ++q) {
+      const int4 x = src[q];
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = INT_MAX;
+  }
+}
+
 template <bool M, int B, int R>
 __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
   constexpr int P = B / R;
@@ -232,26 +254,15 @@ __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__res
   const int tib = lane & (P - 1);
   const int x0 = tib * R;                                  // bucket index of register 0
   const uint32_t tiles = (n + kTile - 1) / kTile;
-  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  int32_t nxt[R];                                          // the next tile's keys, in flight
+  uint32_t tile = blockIdx.x;
+  if (tile < tiles) oe_load_keys<R>(nxt, keys, tile * kTile + uint32_t(threadIdx.x) * R, n);
+  for (; tile < tiles; tile += gridDim.x) {
     const uint32_t base = tile * kTile + uint32_t(threadIdx.x) * R;
     int32_t v[R];
-    if (base < n && R % 8 == 0 && aligned32(keys)) {       // whole sectors per warp instruction
 #pragma unroll
-      for (int q = 0; q < R / 8; ++q) ld_v8(keys + base + 8 * q, &v[8 * q]);
-    } else if (base < n) {                                 // whole bucket in or out (n % B == 0)
-      const int4 *src = reinterpret_cast<const int4 *>(keys + base);
-#pragma unroll
-      for (int q = 0; q < R / 4; ++q) {
-        const int4 x = src[q];
-        v[4 * q] = x.x;
-        v[4 * q + 1] = x.y;
-        v[4 * q + 2] = x.z;
-        v[4 * q + 3] = x.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < R; ++j) v[j] = INT_MAX;
-    }
+    for (int j = 0; j < R; ++j) v[j] = nxt[j];
+    if (tile + gridDim.x < tiles) oe_load_keys<R>(nxt, keys, base + gridDim.x * kTile, n);
     oe_reg_network<M, B, R, 1, 1>(v, lane, tib, x0);
     if (base < n && R % 8 == 0 && aligned32(keys)) {
 #pragma unroll
