@@ -669,8 +669,9 @@ def our_arm(args):
                      "kernel": kname.format("true"),
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "alu_pipe_pct": (prof_m or {}).get("alu_pipe_pct"),
-                     "note": "ALU-pipe-bound (VIMNMX compare-exchanges, 21 steps per key) at about the HBM "
-                             "time; see DESIGN.md §5"},
+                     "note": "instruction-issue-bound (83% issue-active in ncu: VIMNMX compare-exchanges on the "
+                             "ALU pipe, half the in-register maxima as IMADs on the FMA pipe, 21 steps per key); "
+                             "see DESIGN.md §5"},
         "e2e": {"value": n * world / (e2e_total / args.steps / 1e3), "unit": "keys/s",
                 "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                 "how": "darm_gpu_bitonic_sort(mem=HOST) on pinned numpy buffers; library CUDA events t0..t3"},

@@ -45,6 +45,10 @@ __device__ __forceinline__ int32_t select_maxmin(int32_t v, int32_t b, bool bit)
 // wrapping 32-bit arithmetic): two IMADs by the runtime unit `one` / `mone`
 // (gridDim.y = 1, opaque to both compilers) replace one VIMNMX on the ALU pipe,
 // which the compare-exchanges saturate.  DARM_CX_FMA_MOD = 0 turns it off.
+// resident 256-thread CTAs per SM the prefetching register kernel is built for
+#ifndef DARM_BITONIC_MIN_CTAS
+#define DARM_BITONIC_MIN_CTAS 4
+#endif
 #ifndef DARM_CX_FMA_MOD
 #define DARM_CX_FMA_MOD 2
 #endif
@@ -190,7 +194,7 @@ __device__ __forceinline__ void load_keys(int32_t (&v)[R], const int32_t *__rest
 }
 
 template <bool M, int B, int R, bool PF>
-__global__ void __launch_bounds__(256, PF ? 4 : 1) bitonic_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
+__global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
   constexpr int LB = __builtin_ctz(B), LR = __builtin_ctz(R), P = B / R;
   static_assert(R >= 4 && R <= B && P <= 256, "R keys per thread, at most 256 threads per bucket");
   // kCta: a bucket spans warps (B > 32 R, up to 4096 keys): the CTA walks
