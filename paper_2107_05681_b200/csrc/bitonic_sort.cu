@@ -40,32 +40,6 @@ __device__ __forceinline__ int32_t select_maxmin(int32_t v, int32_t b, bool bit)
   return v;
 }
 
-// In-register compare-exchange (lo, hi) = (min, max) of (a, b).  For the pairs
-// with f set the larger key is rebuilt on the FMA pipe as a + b - lo (exact in
-// wrapping 32-bit arithmetic): two IMADs by the runtime unit `one` / `mone`
-// (gridDim.y = 1, opaque to both compilers) replace one VIMNMX on the ALU pipe,
-// which the compare-exchanges saturate.  DARM_CX_FMA_MOD = 0 turns it off.
-// resident 256-thread CTAs per SM the prefetching register kernel is built for
-#ifndef DARM_BITONIC_MIN_CTAS
-#define DARM_BITONIC_MIN_CTAS 4
-#endif
-#ifndef DARM_CX_FMA_MOD
-#define DARM_CX_FMA_MOD 2
-#endif
-__device__ __forceinline__ void cx_pair(bool f, int32_t a, int32_t b, int32_t &lo, int32_t &hi, uint32_t one,
-                                        uint32_t mone) {
-  lo = min(a, b);
-  if (f) {   // compile-time after unrolling
-    uint32_t s, h;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(a), "r"(one), "r"(b));
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(lo), "r"(mone), "r"(s));
-    hi = int32_t(h);
-  } else {
-    hi = max(a, b);
-  }
-}
-__host__ __device__ constexpr bool cx_on_fma(int j) { return DARM_CX_FMA_MOD > 0 && j % (DARM_CX_FMA_MOD > 0 ? DARM_CX_FMA_MOD : 1) == 0; }
-
 template <int B>
 struct Network {
   static constexpr int kSteps = __builtin_ctz(B) * (__builtin_ctz(B) + 1) / 2;

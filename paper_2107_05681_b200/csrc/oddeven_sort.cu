@@ -179,7 +179,8 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
       constexpr int kp = k == p ? 0 : k;
       const int y = j % (2 * p);
       if (!(y >= kp && ((y - kp) & k) == 0 && y + k < 2 * p)) continue;
-      const int32_t lo = min(v[j], v[j + k]), hi = max(v[j], v[j + k]);
+      int32_t lo, hi;
+      cx_pair(cx_on_fma(j), v[j], v[j + k], lo, hi, gridDim.y, 0u - gridDim.y);   // half the maxima on the FMA pipe
       v[j] = lo;
       v[j + k] = hi;
     }
@@ -198,7 +199,8 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
 #pragma unroll
     for (int j = 0; j + k < R; ++j) {
       if (!(j & k)) continue;
-      const int32_t lo = min(v[j], v[j + k]), hi = max(v[j], v[j + k]);
+      int32_t lo, hi;
+      cx_pair(cx_on_fma(j), v[j], v[j + k], lo, hi, gridDim.y, 0u - gridDim.y);
       v[j] = lo;
       v[j + k] = hi;
     }
