@@ -174,6 +174,31 @@ def test_bitonic_sort_register_blocked(bucket, kpt):
                 assert (k.cpu().numpy() == want).all(), (bucket, kpt, n, dup, variant)
 
 
+@pytest.mark.parametrize("sort", ["bitonic", "oddeven"])
+@pytest.mark.parametrize("kpt", [8, 16])
+def test_register_sorts_16_byte_aligned_keys(sort, kpt):
+    """The register-blocked kernels move keys as 32-byte vectors when the key
+    pointer is 32-byte aligned and as 16-byte vectors otherwise: a pointer 16
+    bytes past a 256-byte allocation takes the second path; both agree with
+    np.sort (and a tail of partial CTA tiles)."""
+    import torch
+
+    fn = darm.bitonic_sort if sort == "bitonic" else darm.oddeven_sort
+    rng = np.random.default_rng(kpt)
+    for bucket in (64, 256):
+        n = bucket * 1031
+        keys = rng.integers(-(2 ** 31), 2 ** 31, size=n, dtype=np.int64).astype(np.int32)
+        want = np.sort(keys.reshape(-1, bucket), axis=1).reshape(-1)
+        for variant in (0, 1):
+            buf = torch.zeros(n + 4, dtype=torch.int32, device="cuda")
+            k = buf[4:]
+            assert k.data_ptr() % 32 == 16
+            k.copy_(torch.from_numpy(keys))
+            assert fn(k, bucket, variant, keys_per_thread=kpt)["keys_per_thread"] == kpt
+            assert (k.cpu().numpy() == want).all(), (sort, bucket, kpt, variant)
+            assert (buf[:4].cpu().numpy() == 0).all()
+
+
 def test_bitonic_sort_keys_per_thread_contract():
     import torch
 
