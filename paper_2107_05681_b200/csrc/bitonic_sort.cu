@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
   // have under the 64-register cap (64 B of stack: 180 -> 1490 us); it keeps
   // both halves of every pair on the ALU pipe
   constexpr bool kCxFma = M || B < 4096;
+  constexpr int kCxMod = M ? DARM_CX_FMA_MOD_MELDED : DARM_CX_FMA_MOD;
   int32_t nxt[R];
   if (PF && tile < tiles) load_keys<R>(nxt, keys, tile * kTile + uint32_t(tid) * R, n);
   for (; tile < tiles; tile += units) {
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
               if (j & k) continue;
               const bool up = d < LR ? !((j >> d) & 1) : true;   // compile-time (or folded) direction
               int32_t lo, hi;
-              cx_pair(kCxFma && cx_on_fma(j), v[j], v[j | k], lo, hi, one, mone);
+              cx_pair(kCxFma && cx_on_fma(j, kCxMod), v[j], v[j | k], lo, hi, one, mone);
               v[j] = up ? lo : hi;
               v[j | k] = up ? hi : lo;
             }
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
               for (int j = 0; j < R; ++j) {
                 if (j & k) continue;
                 int32_t lo, hi;
-                cx_pair(kCxFma && cx_on_fma(j), v[j], v[j | k], lo, hi, one, mone);
+                cx_pair(kCxFma && cx_on_fma(j, kCxMod), v[j], v[j | k], lo, hi, one, mone);
                 v[j] = lo;
                 v[j | k] = hi;
               }
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
               for (int j = 0; j < R; ++j) {
                 if (j & k) continue;
                 int32_t lo, hi;
-                cx_pair(kCxFma && cx_on_fma(j), v[j], v[j | k], lo, hi, one, mone);
+                cx_pair(kCxFma && cx_on_fma(j, kCxMod), v[j], v[j | k], lo, hi, one, mone);
                 v[j] = hi;
                 v[j | k] = lo;
               }

@@ -68,7 +68,11 @@ __device__ __forceinline__ void cx_pair(bool f, int32_t a, int32_t b, int32_t &l
     hi = max(a, b);
   }
 }
-__host__ __device__ constexpr bool cx_on_fma(int j) { return DARM_CX_FMA_MOD > 0 && j % (DARM_CX_FMA_MOD > 0 ? DARM_CX_FMA_MOD : 1) == 0; }
+__host__ __device__ constexpr bool cx_on_fma(int j, int mod = DARM_CX_FMA_MOD) { return mod > 0 && j % (mod > 0 ? mod : 1) == 0; }
+// the melded bitonic register kernel (issue-bound rather than ALU-bound)
+#ifndef DARM_CX_FMA_MOD_MELDED
+#define DARM_CX_FMA_MOD_MELDED DARM_CX_FMA_MOD
+#endif
 
 // Lane -> (warp, tid) split for a logical warp of W lanes (1..64).  WT is the
 // compile-time warp size when it is a power of two, 0 for a runtime W.
