@@ -36,9 +36,17 @@ extern "C" {
 #define DARM_USER_ERROR 2
 #define DARM_INTERNAL_ERROR 3
 
-/* Kernel forms (north star: "each kernel ... in two forms"). */
-#define DARM_UNMELDED 0 /* original CFG, IPDOM reconvergence kept            */
+/* Kernel forms (north star: "each kernel ... in two forms"), plus two
+ * reference columns where the comparison needs them. */
+#define DARM_UNMELDED 0 /* original CFG, IPDOM reconvergence kept: every arm is
+                           a real divergent branch in SASS (BSSY/@P BRA/BSYNC) */
 #define DARM_MELDED 1   /* control flow emitted by runDarm   */
+#define DARM_PREDICATED 2 /* original CFG as ptxas compiles it (short arms
+                           if-converted into predicated runs): corpus kernels,
+                           bitonic and PCM sorts                               */
+#define DARM_MELDED_LITERAL 3 /* bitonic sorts only: SURVEY App. A.2 as printed
+                           (select chain on `up`, one store), next to
+                           DARM_MELDED's order-flip form                        */
 
 #define DARM_MEM_HOST 0
 #define DARM_MEM_DEVICE 1

@@ -31,14 +31,18 @@ from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
-UNMELDED = 0
-MELDED = 1
-VARIANTS = {"unmelded": UNMELDED, "melded": MELDED}
+UNMELDED = 0             # original CFG, every arm a real divergent branch (IPDOM)
+MELDED = 1               # the control flow runDarm emits
+PREDICATED = 2           # original CFG as ptxas compiles it (short arms if-converted)
+MELDED_LITERAL = 3       # bitonic sorts: SURVEY App. A.2's select chain as printed
+VARIANTS = {"unmelded": UNMELDED, "melded": MELDED, "predicated": PREDICATED, "melded_literal": MELDED_LITERAL}
 FAST_MATH = 0x100   # SRAD: OR into the variant (DARM_FAST_MATH, within 1e-5 relative)
 SRAD_INDEX64 = 0x200   # SRAD: force the 64-bit row addressing of very large tiles (testing aid)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libdarm_gpu.so")
+# DARM_GPU_LIB points experiments at a variant build (e.g. a knob sweep)
+# without overwriting the in-tree library
+LIB_PATH = os.environ.get("DARM_GPU_LIB") or os.path.join(_HERE, "_lib", "libdarm_gpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "darm_gpu.h")
 
 # Every symbol include/darm_gpu.h declares.
@@ -306,7 +310,8 @@ def _require_i32(x, name, min_words=0):
 
 def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, object],
                   shared: Optional[Dict[str, object]] = None, n_warps: Optional[int] = None,
-                  faults=None, stream=None, want_stats: bool = True, prepare_only: bool = False):
+                  faults=None, stream=None, want_stats: bool = True, prepare_only: bool = False,
+                  count_faults: bool = True):
     """Run a batch of warps of a corpus kernel on the GPU (replaces executeWarp).
 
     ``globals``/``shared`` are numpy int32 arrays (HOST mode: copied in and the
@@ -314,7 +319,9 @@ def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, obje
     updated in place, asynchronous on ``stream``).  ``args`` is an int32 array of
     shape (n_params, acount) with acount in {1, n_warps, n_warps*warp}; with
     acount == 1 it is always host memory.  ``prepare_only`` returns a
-    :class:`PreparedCall` instead of running.
+    :class:`PreparedCall` instead of running.  ``count_faults=False`` passes
+    no fault counters (kernels without shared memory then launch one kernel
+    and nothing else; their lanes are in bounds by construction).
     """
     if isinstance(variant, str):
         variant = VARIANTS[variant]
@@ -332,7 +339,9 @@ def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, obje
         _require_i32(globals[n], n, n_warps * warp)
     for n, size in info["shared"]:
         if shared:
-            _require_i32(shared[n], n, n_warps * size) if device else None
+            _require(n in shared, f"missing shared {n}")
+            _require(_is_torch_cuda(shared[n]) == device, f"{n}: shared must be the same memory kind as globals")
+            _require_i32(shared[n], n, n_warps * size)
     if faults is not None:
         _require_i32(faults, "faults", n_warps)
     if device:
@@ -352,18 +361,23 @@ def execute_warps(kernel: str, variant, warp: int, args, globals: Dict[str, obje
             aptr = ctypes.cast(ctypes.c_void_p(args_t.data_ptr()), ctypes.POINTER(ctypes.c_int32))
         gl_ptrs = [globals[n].data_ptr() for n in names]
         sh_ptrs = [shared[n].data_ptr() for n in snames] if shared else []
-        if faults is None:
+        if faults is None and count_faults:
             faults = torch.zeros(n_warps, dtype=torch.int32, device=first.device)
-        fptr = ctypes.cast(ctypes.c_void_p(faults.data_ptr()), ctypes.POINTER(ctypes.c_int32))
+        fptr = (ctypes.cast(ctypes.c_void_p(faults.data_ptr()), ctypes.POINTER(ctypes.c_int32))
+                if faults is not None else None)
         mem = 1
         if stream is None:
             stream = torch.cuda.current_stream(first.device).cuda_stream
+        elif args_t is not None and args_t is not args:
+            # allocated on the current stream, read on `stream`: keep the
+            # caching allocator from reusing it before the launch has run
+            args_t.record_stream(torch.cuda.ExternalStream(int(stream), device=first.device))
     else:
         args_np = np.ascontiguousarray(np.asarray(args, dtype=np.int32).reshape(len(info["params"]), -1))
         acount = args_np.shape[1]
         aptr = _i32p(args_np)
         gl_ptrs = [globals[n].ctypes.data for n in names]
-        sh_ptrs = [np.ascontiguousarray(shared[n], dtype=np.int32).ctypes.data for n in snames] if shared else []
+        sh_ptrs = [shared[n].ctypes.data for n in snames] if shared else []   # checked int32, C-contiguous
         if faults is None:
             faults = np.zeros(n_warps, dtype=np.int32)
         fptr = _i32p(faults)

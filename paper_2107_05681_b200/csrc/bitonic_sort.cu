@@ -46,8 +46,9 @@ struct Network {
   static_assert(kSteps <= 64, "step masks are 64-bit");
 };
 
-template <bool M, int B, int CTA, int U>
+template <int F, int B, int CTA, int U>
 __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__ keys, uint32_t n) {
+  constexpr bool M = F == kMelded;
   constexpr int LB = __builtin_ctz(B);
   constexpr bool kNeedSmem = B > 32;
   __shared__ int32_t xch[kNeedSmem ? 2 : 1][U][kNeedSmem ? CTA : 1];
@@ -108,8 +109,12 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if constexpr (!M) {
-            v[u] = bitonic_exchange<false>(v[u], b0[u], !bit[kb], d >= LB ? true : !bit[d], false);
+          if constexpr (F == kLiteral) {
+            // App. A.2 select chain, issued as the melded form's predicated pair
+            const bool up = d >= LB ? true : !bit[d];
+            v[u] = select_maxmin(v[u], b0[u], bit[kb] == up);
+          } else if constexpr (!M) {
+            v[u] = bitonic_exchange<F>(v[u], b0[u], !bit[kb], d >= LB ? true : !bit[d]);
           } else {
             // need1 = (keep == up) ? cv > b0 : cv < b0 with up folded into the data:
             // need1 = (keep == up) ? gt : lt with up folded into the data: the
@@ -167,8 +172,9 @@ __device__ __forceinline__ void load_keys(int32_t (&v)[R], const int32_t *__rest
   }
 }
 
-template <bool M, int B, int R, bool PF>
+template <int F, int B, int R, bool PF>
 __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
+  constexpr bool M = F == kMelded;
   constexpr int LB = __builtin_ctz(B), LR = __builtin_ctz(R), P = B / R;
   static_assert(R >= 4 && R <= B && P <= 256, "R keys per thread, at most 256 threads per bucket");
   // kCta: a bucket spans warps (B > 32 R, up to 4096 keys): the CTA walks
@@ -186,9 +192,10 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
   int par = 0;
   const uint32_t one = gridDim.y, mone = 0u - one;   // 1 and -1, opaque (cx_pair)
   // the FMA-pipe maxima need registers the unmelded 4096-key form does not
-  // have under the 64-register cap (64 B of stack: 180 -> 1490 us); it keeps
-  // both halves of every pair on the ALU pipe
-  constexpr bool kCxFma = M || B < 4096;
+  // have under the 64-register cap (64 B of stack: 180 -> 1490 us): at 4096
+  // keys every form keeps both halves of every pair on the ALU pipe, so the
+  // forms differ in control flow only
+  constexpr bool kCxFma = B < 4096;
   constexpr int kCxMod = M ? DARM_CX_FMA_MOD_MELDED : DARM_CX_FMA_MOD;
   int32_t nxt[R];
   if (PF && tile < tiles) load_keys<R>(nxt, keys, tile * kTile + uint32_t(tid) * R, n);
@@ -229,9 +236,20 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
               v[j] = up ? lo : hi;
               v[j | k] = up ? hi : lo;
             }
+          } else if constexpr (F == kLiteral) {
+            // App. A.2: the compare-exchange hoisted out of both arms, the
+            // slot each key goes to chosen by `select %up`
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              if (j & k) continue;
+              int32_t lo, hi;
+              cx_pair(kCxFma && cx_on_fma(j, kCxMod), v[j], v[j | k], lo, hi, one, mone);
+              v[j] = upT ? lo : hi;
+              v[j | k] = upT ? hi : lo;
+            }
           } else {
             if (upT) {                                    // condbr %up ^c ^d
-              DARM_ARM("bitonic.reg.up");
+              DARM_ARM_F(F, "bitonic.reg.up");
 #pragma unroll
               for (int j = 0; j < R; ++j) {
                 if (j & k) continue;
@@ -242,7 +260,7 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
               }
               DARM_ARM("bitonic.reg.up.end");
             } else {
-              DARM_ARM("bitonic.reg.down");
+              DARM_ARM_F(F, "bitonic.reg.down");
 #pragma unroll
               for (int j = 0; j < R; ++j) {
                 if (j & k) continue;
@@ -280,14 +298,17 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
           } else if (!thread_up) {
 #pragma unroll
             for (int j = 0; j < R; ++j) v[j] = keep ? min(v[j], b0[j]) : max(v[j], b0[j]);
+          } else if constexpr (F == kLiteral) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) v[j] = bitonic_exchange<kLiteral>(v[j], b0[j], keep, upT);
           } else {
             if (upT) {                                    // condbr %up ^c ^d
-              DARM_ARM("bitonic.xr.up");
+              DARM_ARM_F(F, "bitonic.xr.up");
 #pragma unroll
               for (int j = 0; j < R; ++j) v[j] = keep ? min(v[j], b0[j]) : max(v[j], b0[j]);
               DARM_ARM("bitonic.xr.up.end");
             } else {
-              DARM_ARM("bitonic.xr.down");
+              DARM_ARM_F(F, "bitonic.xr.down");
 #pragma unroll
               for (int j = 0; j < R; ++j) v[j] = keep ? max(v[j], b0[j]) : min(v[j], b0[j]);
               DARM_ARM("bitonic.xr.down.end");
@@ -316,7 +337,7 @@ namespace {
 int g_sms = 0;
 int sm_count();
 
-template <bool M, int B>
+template <int F, int B>
 cudaError_t launch_b(int32_t *keys, int64_t n, cudaStream_t s) {
   constexpr int CTA = B > 256 ? B : 256;
   sm_count();
@@ -326,7 +347,7 @@ cudaError_t launch_b(int32_t *keys, int64_t n, cudaStream_t s) {
   int64_t grid = int64_t(g_sms) * per_sm;
   if (grid > (tiles + U - 1) / U) grid = (tiles + U - 1) / U;
   if (grid < 1) grid = 1;
-  bitonic_sort_kernel<M, B, CTA, U><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
+  bitonic_sort_kernel<F, B, CTA, U><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
 }
 
@@ -344,13 +365,13 @@ int sm_count() {
 // grid is sized so every warp gets the same number of tiles (up to one): with
 // I = ceil(tiles / max resident warps) iterations, only ceil(tiles / I) warps
 // are launched, spread evenly over the SMs.
-template <bool M, int B, int R, bool PF>
+template <int F, int B, int R, bool PF>
 cudaError_t launch_reg_pf(int32_t *keys, int64_t n, cudaStream_t s) {
   constexpr int CTA = 256;
   static int per_sm = 0;                          // resident CTAs per SM (registers bound it)
   if (!per_sm) {
     cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bitonic_sort_reg_kernel<M, B, R, PF>, CTA, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bitonic_sort_reg_kernel<F, B, R, PF>, CTA, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
   const int64_t tiles = (n + CTA * R - 1) / (CTA * R);
@@ -358,18 +379,18 @@ cudaError_t launch_reg_pf(int32_t *keys, int64_t n, cudaStream_t s) {
   const int64_t iters = (tiles + max_ctas - 1) / max_ctas;
   int64_t grid = (tiles + iters - 1) / iters;
   if (grid < 1) grid = 1;
-  bitonic_sort_reg_kernel<M, B, R, PF><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
+  bitonic_sort_reg_kernel<F, B, R, PF><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
 }
 
 // Buckets that span warps: CTAs walk 256*R-key tiles, as many CTAs as fit
 // (each with the same tile count, up to one).
-template <bool M, int B, int R>
+template <int F, int B, int R>
 cudaError_t launch_reg_cta(int32_t *keys, int64_t n, cudaStream_t s) {
   static int per_sm = 0;
   if (!per_sm) {
     cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bitonic_sort_reg_kernel<M, B, R, true>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bitonic_sort_reg_kernel<F, B, R, true>, 256, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
   const int64_t tiles = (n + 256 * R - 1) / (256 * R);
@@ -377,48 +398,48 @@ cudaError_t launch_reg_cta(int32_t *keys, int64_t n, cudaStream_t s) {
   const int64_t iters = (tiles + max_ctas - 1) / max_ctas;
   int64_t grid = (tiles + iters - 1) / iters;
   if (grid < 1) grid = 1;
-  bitonic_sort_reg_kernel<M, B, R, true><<<int(grid), 256, 0, s>>>(keys, uint32_t(n));
+  bitonic_sort_reg_kernel<F, B, R, true><<<int(grid), 256, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
 }
 
-template <bool M, int B, int R>
+template <int F, int B, int R>
 cudaError_t launch_reg(int32_t *keys, int64_t n, cudaStream_t s) {
-  if constexpr (B / R > 32) return launch_reg_cta<M, B, R>(keys, n, s);
-  else return launch_reg_pf<M, B, R, true>(keys, n, s);
+  if constexpr (B / R > 32) return launch_reg_cta<F, B, R>(keys, n, s);
+  else return launch_reg_pf<F, B, R, true>(keys, n, s);
 }
 
-template <bool M, int B>
+template <int F, int B>
 cudaError_t launch_r(int32_t *keys, int64_t n, int r, cudaStream_t s) {
   if constexpr (B >= 4 && B / 4 <= 256) {
-    if (r == 4) return launch_reg<M, B, 4>(keys, n, s);
+    if (r == 4) return launch_reg<F, B, 4>(keys, n, s);
   }
   if constexpr (B >= 8 && B / 8 <= 256) {
-    if (r == 8) return launch_reg<M, B, 8>(keys, n, s);
+    if (r == 8) return launch_reg<F, B, 8>(keys, n, s);
   }
   if constexpr (B >= 16 && B / 16 <= 256) {
-    if (r == 16) return launch_reg<M, B, 16>(keys, n, s);
+    if (r == 16) return launch_reg<F, B, 16>(keys, n, s);
   }
   if constexpr (B <= 1024) {
-    if (r == 1) return launch_b<M, B>(keys, n, s);
+    if (r == 1) return launch_b<F, B>(keys, n, s);
   }
   return cudaErrorInvalidValue;
 }
 
-template <bool M>
+template <int F>
 cudaError_t launch_m(int32_t *keys, int64_t n, int bucket, int r, cudaStream_t s) {
   switch (bucket) {
-    case 2: return launch_r<M, 2>(keys, n, r, s);
-    case 4: return launch_r<M, 4>(keys, n, r, s);
-    case 8: return launch_r<M, 8>(keys, n, r, s);
-    case 16: return launch_r<M, 16>(keys, n, r, s);
-    case 32: return launch_r<M, 32>(keys, n, r, s);
-    case 64: return launch_r<M, 64>(keys, n, r, s);
-    case 128: return launch_r<M, 128>(keys, n, r, s);
-    case 256: return launch_r<M, 256>(keys, n, r, s);
-    case 512: return launch_r<M, 512>(keys, n, r, s);
-    case 1024: return launch_r<M, 1024>(keys, n, r, s);
-    case 2048: return launch_r<M, 2048>(keys, n, r, s);
-    case 4096: return launch_r<M, 4096>(keys, n, r, s);
+    case 2: return launch_r<F, 2>(keys, n, r, s);
+    case 4: return launch_r<F, 4>(keys, n, r, s);
+    case 8: return launch_r<F, 8>(keys, n, r, s);
+    case 16: return launch_r<F, 16>(keys, n, r, s);
+    case 32: return launch_r<F, 32>(keys, n, r, s);
+    case 64: return launch_r<F, 64>(keys, n, r, s);
+    case 128: return launch_r<F, 128>(keys, n, r, s);
+    case 256: return launch_r<F, 256>(keys, n, r, s);
+    case 512: return launch_r<F, 512>(keys, n, r, s);
+    case 1024: return launch_r<F, 1024>(keys, n, r, s);
+    case 2048: return launch_r<F, 2048>(keys, n, r, s);
+    case 4096: return launch_r<F, 4096>(keys, n, r, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -451,8 +472,12 @@ cudaError_t launch_bitonic_sort(int variant, int32_t *keys, int64_t n, int bucke
                                 cudaStream_t s, int *launches) {
   if (n == 0) return cudaSuccess;
   if (launches) *launches += 1;
-  return variant ? launch_m<true>(keys, n, bucket, keys_per_thread, s)
-                 : launch_m<false>(keys, n, bucket, keys_per_thread, s);
+  switch (variant) {
+    case kUnmelded: return launch_m<kUnmelded>(keys, n, bucket, keys_per_thread, s);
+    case kMelded: return launch_m<kMelded>(keys, n, bucket, keys_per_thread, s);
+    case kPredicated: return launch_m<kPredicated>(keys, n, bucket, keys_per_thread, s);
+    default: return launch_m<kLiteral>(keys, n, bucket, keys_per_thread, s);
+  }
 }
 
 }  // namespace darm_gpu

@@ -20,14 +20,39 @@ __device__ __forceinline__ int32_t ir_and(int32_t a, int32_t b) { return a & b; 
 __device__ __forceinline__ int32_t ir_shl(int32_t a, int32_t b) { return int32_t(uint32_t(a) << (uint32_t(b) & 31u)); }
 __device__ __forceinline__ int32_t ir_shr(int32_t a, int32_t b) { return int32_t(uint32_t(a) >> (uint32_t(b) & 31u)); }
 
-// Arm fence.  The unmelded forms must keep both sides of a divergent branch as
-// separate code: without it LLVM's SimplifyCFG hoists the
-// identical leading instructions of the two arms (`load in; mul 3` in sb1) and
-// sinks the identical tails (`add; store out`), i.e. the compiler would meld
-// the "unmelded" kernel itself.  A volatile asm with a distinct text per arm is
-// never identical across arms and is not speculatable, so neither hoisting,
-// sinking nor if-conversion in NVVM can cross it; it emits no SASS.
-#define DARM_ARM(tag) asm volatile("// arm " tag ::: "memory")
+// Forms of a kernel: the `variant` codes of darm_gpu.h.
+enum : int {
+  kUnmelded = 0,    // original CFG, IPDOM reconvergence kept (real branches in SASS)
+  kMelded = 1,      // the control flow runDarm emits
+  kPredicated = 2,  // original CFG as ptxas compiles it (short arms if-converted)
+  kLiteral = 3,     // bitonic sorts: App. A.2's select chain on `up` as printed
+};
+
+// Arm fences.  Without them LLVM's SimplifyCFG hoists the
+// identical leading instructions of two arms (`load in; mul 3` in sb1) and
+// sinks the identical tails (`add; store out`): the compiler would meld the
+// "unmelded" kernel itself.
+//   DARM_ARM:   a volatile asm with a distinct text per arm: never identical
+//               across arms and not speculatable, so NVVM cannot hoist, sink
+//               or merge across it.  It emits no SASS and has no memory
+//               clobber (both forms keep the same load classes, e.g.
+//               LDG.E.CONSTANT for read-only __restrict__ inputs).
+//   DARM_IPDOM: DARM_ARM plus one PMTRIG (`pmevent`, a performance-monitor
+//               trigger with no architectural effect): ptxas does not
+//               if-convert a block holding it, so the arm stays behind a real
+//               divergent branch (BSSY / @P BRA / BSYNC) — the IPDOM
+//               reconvergence of interp.cpp:298-306.  Cost: one issue slot
+//               per arm executed.
+//   DARM_ARM_F: DARM_IPDOM in the kUnmelded form, DARM_ARM otherwise.
+#define DARM_ARM(tag) asm volatile("// arm " tag)
+#define DARM_IPDOM(tag) asm volatile("pmevent 0; // arm " tag)
+#define DARM_ARM_F(F, tag)        \
+  do {                            \
+    if constexpr ((F) == kUnmelded) \
+      DARM_IPDOM(tag);            \
+    else                          \
+      DARM_ARM(tag);              \
+  } while (0)
 
 // 32-byte vectors (LDG/STG.E.ENL2.256): with R >= 8 consecutive keys per thread
 // each warp instruction covers whole sectors; 16-byte vectors at a 64-byte

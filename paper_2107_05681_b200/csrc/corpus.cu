@@ -14,7 +14,7 @@ namespace darm_gpu {
 // Grid-stride over lanes.  AM = argument mode: 0 broadcast, 1 per warp,
 // 2 per lane (interp.cpp:346-354 allows 1 or warpSize values per parameter;
 // batching adds the per-warp case).
-template <class K, bool M, int WT, int AM>
+template <class K, int F, int WT, int AM>
 __global__ void __launch_bounds__(256) corpus_lanes(CorpusParams P) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < P.total; g += stride) {
@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) corpus_lanes(CorpusParams P) {
 #pragma unroll
     for (int p = 0; p < K::kParams; ++p)
       a[p] = AM == 0 ? P.argv[p] : (AM == 1 ? __ldg(P.argp[p] + w) : __ldg(P.argp[p] + g));
-    K::template lane<M>(P, g, t, a);
+    K::template lane<F>(P, g, t, a);
   }
 }
 
@@ -36,8 +36,9 @@ __global__ void __launch_bounds__(256) corpus_lanes(CorpusParams P) {
 // A lane whose partner index t^k falls outside buf faults (interp.cpp:251-256)
 // and does nothing else.  The barrier between the partner loads and the
 // divergent stores restores the interpreter's lockstep order.
-template <bool M, int WT, int AM>
+template <int F, int WT, int AM>
 __global__ void __launch_bounds__(256) bitonic_step_kernel(CorpusParams P) {
+  constexpr bool M = F == kMelded;
   extern __shared__ int32_t smem[];
   const uint32_t W = WT > 0 ? uint32_t(WT) : P.warp;
   const uint32_t S = P.shared_size;
@@ -74,20 +75,20 @@ __global__ void __launch_bounds__(256) bitonic_step_kernel(CorpusParams P) {
     if (run) {
       if constexpr (!M) {
         if (up) {                                          // ^b condbr %up ^c ^d
-          DARM_ARM("bstep.c");
+          DARM_ARM_F(F, "bstep.c");
           int32_t c0 = buf[t];                             // ^c load.shared buf %t
           bool need1 = keep ? (c0 > b0) : (c0 < b0);
           if (need1) {
-            DARM_ARM("bstep.e");
+            DARM_ARM_F(F, "bstep.e");
             buf[t] = b0;                                   // ^e store.shared
           }
           DARM_ARM("bstep.x1");
         } else {
-          DARM_ARM("bstep.d");
+          DARM_ARM_F(F, "bstep.d");
           int32_t dv = buf[t];                             // ^d load.shared buf %t
           bool need2 = keep ? (dv < b0) : (dv > b0);
           if (need2) {
-            DARM_ARM("bstep.f");
+            DARM_ARM_F(F, "bstep.f");
             buf[t] = b0;                                   // ^f store.shared
           }
           DARM_ARM("bstep.x2");
@@ -116,35 +117,39 @@ int grid_for(uint64_t work, int per_cta, int sms) {
   return int(ctas < 1 ? 1 : ctas);
 }
 
-template <class K, bool M, int WT>
+template <class K, int F, int WT>
 cudaError_t launch_lanes_am(int am, const CorpusParams &P, int sms, cudaStream_t s) {
   // One thread per lane: every lane's loads are in flight at once (the kernels
   // are latency/HBM-bound and a lane does a handful of instructions).
   (void)sms;
   const int grid = int((uint64_t(P.total) + 255) / 256);
   switch (am) {
-    case 0: corpus_lanes<K, M, WT, 0><<<grid, 256, 0, s>>>(P); break;
-    case 1: corpus_lanes<K, M, WT, 1><<<grid, 256, 0, s>>>(P); break;
-    default: corpus_lanes<K, M, WT, 2><<<grid, 256, 0, s>>>(P); break;
+    case 0: corpus_lanes<K, F, WT, 0><<<grid, 256, 0, s>>>(P); break;
+    case 1: corpus_lanes<K, F, WT, 1><<<grid, 256, 0, s>>>(P); break;
+    default: corpus_lanes<K, F, WT, 2><<<grid, 256, 0, s>>>(P); break;
   }
   return cudaGetLastError();
 }
 
-template <class K, bool M>
+template <class K, int F>
 cudaError_t launch_lanes_w(int am, const CorpusParams &P, int sms, cudaStream_t s) {
   switch (P.warp) {
-    case 32: return launch_lanes_am<K, M, 32>(am, P, sms, s);
-    case 64: return launch_lanes_am<K, M, 64>(am, P, sms, s);
-    default: return launch_lanes_am<K, M, 0>(am, P, sms, s);
+    case 32: return launch_lanes_am<K, F, 32>(am, P, sms, s);
+    case 64: return launch_lanes_am<K, F, 64>(am, P, sms, s);
+    default: return launch_lanes_am<K, F, 0>(am, P, sms, s);
   }
 }
 
 template <class K>
 cudaError_t launch_lanes(int variant, int am, const CorpusParams &P, int sms, cudaStream_t s) {
-  return variant ? launch_lanes_w<K, true>(am, P, sms, s) : launch_lanes_w<K, false>(am, P, sms, s);
+  switch (variant) {
+    case kUnmelded: return launch_lanes_w<K, kUnmelded>(am, P, sms, s);
+    case kMelded: return launch_lanes_w<K, kMelded>(am, P, sms, s);
+    default: return launch_lanes_w<K, kPredicated>(am, P, sms, s);
+  }
 }
 
-template <bool M, int WT>
+template <int F, int WT>
 cudaError_t launch_bstep_am(int am, const CorpusParams &P, int sms, cudaStream_t s) {
   // IR warps per CTA: up to 256 lanes, and at most 48 KB of shared `buf`
   // slices (the default dynamic shared-memory limit).
@@ -155,24 +160,28 @@ cudaError_t launch_bstep_am(int am, const CorpusParams &P, int sms, cudaStream_t
   const int grid = grid_for(P.n_warps, int(wpc), sms);
   const size_t shm = size_t(wpc) * P.shared_size * sizeof(int32_t);
   switch (am) {
-    case 0: bitonic_step_kernel<M, WT, 0><<<grid, block, shm, s>>>(P); break;
-    case 1: bitonic_step_kernel<M, WT, 1><<<grid, block, shm, s>>>(P); break;
-    default: bitonic_step_kernel<M, WT, 2><<<grid, block, shm, s>>>(P); break;
+    case 0: bitonic_step_kernel<F, WT, 0><<<grid, block, shm, s>>>(P); break;
+    case 1: bitonic_step_kernel<F, WT, 1><<<grid, block, shm, s>>>(P); break;
+    default: bitonic_step_kernel<F, WT, 2><<<grid, block, shm, s>>>(P); break;
   }
   return cudaGetLastError();
 }
 
-template <bool M>
+template <int F>
 cudaError_t launch_bstep_w(int am, const CorpusParams &P, int sms, cudaStream_t s) {
   switch (P.warp) {
-    case 32: return launch_bstep_am<M, 32>(am, P, sms, s);
-    case 64: return launch_bstep_am<M, 64>(am, P, sms, s);
-    default: return launch_bstep_am<M, 0>(am, P, sms, s);
+    case 32: return launch_bstep_am<F, 32>(am, P, sms, s);
+    case 64: return launch_bstep_am<F, 64>(am, P, sms, s);
+    default: return launch_bstep_am<F, 0>(am, P, sms, s);
   }
 }
 
 cudaError_t launch_bstep(int variant, int am, const CorpusParams &P, int sms, cudaStream_t s) {
-  return variant ? launch_bstep_w<true>(am, P, sms, s) : launch_bstep_w<false>(am, P, sms, s);
+  switch (variant) {
+    case kUnmelded: return launch_bstep_w<kUnmelded>(am, P, sms, s);
+    case kMelded: return launch_bstep_w<kMelded>(am, P, sms, s);
+    default: return launch_bstep_w<kPredicated>(am, P, sms, s);
+  }
 }
 
 }  // namespace

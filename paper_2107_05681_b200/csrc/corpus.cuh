@@ -1,18 +1,25 @@
 // corpus.cuh — lane bodies of the DARM corpus kernels, one struct per
 // /root/reference/proj/corpus/<name>.ir, each in two forms:
 //
-//   MELDED = false : the original CFG.  Every divergent branch of the IR is a
-//                    real branch whose arms are fenced (DARM_ARM) so that NVVM
-//                    cannot hoist/sink/if-convert the common code across them;
-//                    the hardware runs the arms one after the other and
-//                    reconverges at the immediate post-dominator (BSSY/BSYNC).
-//   MELDED = true  : the control flow runDarm emits for the kernel
+//   F = kUnmelded   : the original CFG.  Every divergent branch of the IR is a
+//                    real branch: each arm starts with DARM_IPDOM (NVVM cannot
+//                    hoist/sink/merge across it, ptxas cannot if-convert an arm
+//                    holding it), so the hardware runs the arms one after the
+//                    other and reconverges at the immediate post-dominator
+//                    (BSSY/@P BRA/BSYNC in SASS, checked by tests/test_abi.py).
+//   F = kPredicated : the same source with NVVM-only fences (DARM_ARM): what
+//                    ptxas makes of the original CFG — it if-converts short
+//                    arms into complementary predicated runs (both arms still
+//                    issue one after the other, without the branch).
+//   F = kMelded     : the control flow runDarm emits for the kernel
 //                    (melding_driver.cpp:54-100, threshold 0.2; printed IR in
 //                    SURVEY.md Appendix A and DESIGN.md §Melded forms):
 //                    common instructions hoisted once, select-based operand
 //                    choice, one-sided tails kept as guarded ("unpredicated")
 //                    runs.
 //
+// Read-only inputs are loaded with __ldg in every form (LDG.E.CONSTANT), so the
+// forms differ in control flow, not in load class.
 // Every global is indexed by %t in the corpus, so arrays are stored compact:
 // word g = w*warp + t is element t of warp w's copy (see darm_gpu.h).
 // `undef` incomings of the melded phis are materialised as 0; they are never
@@ -39,8 +46,9 @@ struct CorpusParams {
 // sb1.ir:7-28  out[t] = in[t]*3 + (t < n ? aux2[t] : aux3[t])
 struct Sb1 {
   static constexpr int kParams = 1;
-  template <bool M>
+  template <int F>
   __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    constexpr bool M = F == kMelded;
     const int32_t *__restrict__ in = P.gl[0];
     const int32_t *__restrict__ aux2 = P.gl[1];
     const int32_t *__restrict__ aux3 = P.gl[2];
@@ -49,26 +57,26 @@ struct Sb1 {
     const bool c = t < n;                                  // ^a1 sb1.ir:9-10
     if constexpr (!M) {
       if (c) {                                             // condbr %c ^a2 ^a3 (:11)
-        DARM_ARM("sb1.a2");                                // ^a2 :12-18
-        int32_t v2 = in[g];
+        DARM_ARM_F(F, "sb1.a2");                                // ^a2 :12-18
+        int32_t v2 = __ldg(in + g);
         int32_t m2 = ir_mul(v2, 3);
-        int32_t e2 = aux2[g];
+        int32_t e2 = __ldg(aux2 + g);
         out[g] = ir_add(m2, e2);
         DARM_ARM("sb1.a2.end");
       } else {
-        DARM_ARM("sb1.a3");                                // ^a3 :19-25
-        int32_t v3 = in[g];
+        DARM_ARM_F(F, "sb1.a3");                                // ^a3 :19-25
+        int32_t v3 = __ldg(in + g);
         int32_t m3 = ir_mul(v3, 3);
-        int32_t e3 = aux3[g];
+        int32_t e3 = __ldg(aux3 + g);
         out[g] = ir_add(m3, e3);
         DARM_ARM("sb1.a3.end");
       }
     } else {
-      int32_t v2 = in[g];                                  // hoisted common
+      int32_t v2 = __ldg(in + g);                                  // hoisted common
       int32_t m2 = ir_mul(v2, 3);
       int32_t e3 = 0, e2 = 0;
-      if (!c) e3 = aux3[g];                                // ^a2.m.g  (false-only run)
-      if (c) e2 = aux2[g];                                 // ^a2.m.g1 (true-only run)
+      if (!c) e3 = __ldg(aux3 + g);                                // ^a2.m.g  (false-only run)
+      if (c) e2 = __ldg(aux2 + g);                                 // ^a2.m.g1 (true-only run)
       int32_t sel = c ? e2 : e3;                           // ^a2.m.u1 select
       out[g] = ir_add(m2, sel);
     }
@@ -79,24 +87,25 @@ struct Sb1 {
 // sb1r.ir:5-26  arms differ except the memory accesses
 struct Sb1r {
   static constexpr int kParams = 1;
-  template <bool M>
+  template <int F>
   __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    constexpr bool M = F == kMelded;
     const int32_t *__restrict__ in = P.gl[0];
     int32_t *__restrict__ out = P.gl[1];
     const int32_t n = a[0];
     const bool c = t < n;
     if constexpr (!M) {
       if (c) {
-        DARM_ARM("sb1r.a2");                               // :10-16
-        int32_t v2 = in[g];
+        DARM_ARM_F(F, "sb1r.a2");                               // :10-16
+        int32_t v2 = __ldg(in + g);
         int32_t m2 = ir_mul(v2, 3);
         int32_t y2 = ir_add(m2, n);
         int32_t z2 = ir_shl(y2, 1);
         out[g] = z2;
         DARM_ARM("sb1r.a2.end");
       } else {
-        DARM_ARM("sb1r.a3");                               // :17-23
-        int32_t v3 = in[g];
+        DARM_ARM_F(F, "sb1r.a3");                               // :17-23
+        int32_t v3 = __ldg(in + g);
         int32_t x3 = ir_xor(v3, n);
         int32_t s3 = ir_sub(x3, 7);
         int32_t y3 = ir_add(s3, 2);
@@ -104,7 +113,7 @@ struct Sb1r {
         DARM_ARM("sb1r.a3.end");
       }
     } else {                                               // runDarm: block-block, 3 selects, 3 runs
-      int32_t v2 = in[g];
+      int32_t v2 = __ldg(in + g);
       int32_t s3 = 0, m2 = 0, z2 = 0;
       if (!c) {                                            // ^a2.m.g
         int32_t x3 = ir_xor(v2, n);
@@ -126,44 +135,45 @@ struct Sb1r {
 template <bool R>
 struct Sb2T {
   static constexpr int kParams = 1;
-  template <bool M>
+  template <int F>
   __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    constexpr bool M = F == kMelded;
     const int32_t *__restrict__ in = P.gl[0];
     int32_t *__restrict__ out = P.gl[1];
     const int32_t n = a[0];
     const bool c = t < n;
     if constexpr (!M) {
       if (c) {
-        DARM_ARM("sb2.b2");                                // ^b2 :10-21
-        int32_t v2 = in[g];
+        DARM_ARM_F(F, "sb2.b2");                                // ^b2 :10-21
+        int32_t v2 = __ldg(in + g);
         bool g2 = v2 > n;
         int32_t p2 = v2;
         if (g2) {
-          DARM_ARM("sb2.b2a");
+          DARM_ARM_F(F, "sb2.b2a");
           p2 = ir_add(ir_mul(v2, 2), 1);
         }
         DARM_ARM("sb2.b2m");
         out[g] = p2;
       } else {
-        DARM_ARM("sb2.b3");                                // ^b3 :22-33
-        int32_t v3 = in[g];
+        DARM_ARM_F(F, "sb2.b3");                                // ^b3 :22-33
+        int32_t v3 = __ldg(in + g);
         bool g3 = v3 > n;
         int32_t p3 = v3;
         if (g3) {
-          DARM_ARM("sb2.b3a");
+          DARM_ARM_F(F, "sb2.b3a");
           p3 = R ? ir_sub(ir_xor(v3, n), 3) : ir_add(ir_mul(v3, 2), 1);
         }
         DARM_ARM("sb2.b3m");
         out[g] = p3;
       }
     } else if constexpr (!R) {                             // sb2: region-region, MP 0.5, 1 select
-      int32_t v2 = in[g];
+      int32_t v2 = __ldg(in + g);
       bool g2 = v2 > n;
       int32_t p2 = v2;
       if (g2) p2 = ir_add(ir_mul(v2, 2), 1);               // ^b2a.m
       out[g] = c ? p2 : p2;                                // %sel = select %c %p2 %p2
     } else {                                               // sb2r: region-region, 1 select, 2 runs
-      int32_t v2 = in[g];
+      int32_t v2 = __ldg(in + g);
       bool g2 = v2 > n;
       int32_t u3 = 0, u2 = 0;
       if (g2) {                                            // ^b2a.m
@@ -184,8 +194,9 @@ using Sb2r = Sb2T<true>;
 template <bool R>
 struct Sb3T {
   static constexpr int kParams = 1;
-  template <bool M>
+  template <int F>
   __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    constexpr bool M = F == kMelded;
     const int32_t *__restrict__ in = P.gl[0];
     const int32_t *__restrict__ in2 = P.gl[1];
     int32_t *__restrict__ out = P.gl[2];
@@ -194,53 +205,53 @@ struct Sb3T {
     const bool c = t < n;
     if constexpr (!M) {
       if (c) {
-        DARM_ARM("sb3.c2");                                // ^c2..^c3m :12-33
-        int32_t v1 = in[g];
+        DARM_ARM_F(F, "sb3.c2");                                // ^c2..^c3m :12-33
+        int32_t v1 = __ldg(in + g);
         int32_t p1 = v1;
         if (v1 > n) {
-          DARM_ARM("sb3.c2a");
+          DARM_ARM_F(F, "sb3.c2a");
           p1 = ir_mul(v1, 2);
         }
         DARM_ARM("sb3.c2m");
         out[g] = p1;
-        int32_t v2 = in2[g];
+        int32_t v2 = __ldg(in2 + g);
         int32_t p2 = v2;
         if (v2 > n) {
-          DARM_ARM("sb3.c3a");
+          DARM_ARM_F(F, "sb3.c3a");
           p2 = ir_add(v2, 7);
         }
         DARM_ARM("sb3.c3m");
         out2[g] = p2;
       } else {
-        DARM_ARM("sb3.c5");                                // ^c5..^c6m :34-55
-        int32_t v5 = in[g];
+        DARM_ARM_F(F, "sb3.c5");                                // ^c5..^c6m :34-55
+        int32_t v5 = __ldg(in + g);
         int32_t p5 = v5;
         if (v5 > n) {
-          DARM_ARM("sb3.c5a");
+          DARM_ARM_F(F, "sb3.c5a");
           p5 = R ? ir_xor(v5, 9) : ir_mul(v5, 2);
         }
         DARM_ARM("sb3.c5m");
         out[g] = p5;
-        int32_t v6 = in2[g];
+        int32_t v6 = __ldg(in2 + g);
         int32_t p6 = v6;
         if (v6 > n) {
-          DARM_ARM("sb3.c6a");
+          DARM_ARM_F(F, "sb3.c6a");
           p6 = R ? ir_sub(v6, 5) : ir_add(v6, 7);
         }
         DARM_ARM("sb3.c6m");
         out2[g] = p6;
       }
     } else if constexpr (!R) {                             // sb3: 2 region-region melds
-      int32_t v1 = in[g];
+      int32_t v1 = __ldg(in + g);
       int32_t p1 = v1;
       if (v1 > n) p1 = ir_mul(v1, 2);                      // ^c2a.m
       out[g] = c ? p1 : p1;
-      int32_t v2 = in2[g];
+      int32_t v2 = __ldg(in2 + g);
       int32_t p2 = v2;
       if (v2 > n) p2 = ir_add(v2, 7);                      // ^c3a.m
       out2[g] = c ? p2 : p2;
     } else {                                               // sb3r: 2 melds, 2 runs each
-      int32_t v1 = in[g];
+      int32_t v1 = __ldg(in + g);
       bool g1 = v1 > n;
       int32_t w5 = 0, w1 = 0;
       if (g1) {                                            // ^c2a.m
@@ -249,7 +260,7 @@ struct Sb3T {
       }
       int32_t p1 = g1 ? w1 : v1, p5 = g1 ? w5 : v1;
       out[g] = c ? p1 : p5;
-      int32_t v2 = in2[g];
+      int32_t v2 = __ldg(in2 + g);
       bool g2 = v2 > n;
       int32_t w6 = 0, w2 = 0;
       if (g2) {                                            // ^c3a.m
@@ -269,28 +280,29 @@ using Sb3r = Sb3T<true>;
 template <bool R>
 struct Sb4T {
   static constexpr int kParams = 2;
-  template <bool M>
+  template <int F>
   __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    constexpr bool M = F == kMelded;
     const int32_t *__restrict__ in = P.gl[0];
     int32_t *__restrict__ out = P.gl[1];
     const int32_t h = a[0], q = a[1];
     const bool c1 = t < h;                                 // ^d1 :7-8
     if constexpr (!M) {
       if (c1) {
-        DARM_ARM("sb4.d2");                                // ^d2 :10-14
-        out[g] = ir_add(in[g], 1);
+        DARM_ARM_F(F, "sb4.d2");                                // ^d2 :10-14
+        out[g] = ir_add(__ldg(in + g), 1);
         DARM_ARM("sb4.d2.end");
       } else {
-        DARM_ARM("sb4.d3");                                // ^d3 :15-17
+        DARM_ARM_F(F, "sb4.d3");                                // ^d3 :15-17
         const bool c2 = t < q;
         if (c2) {
-          DARM_ARM("sb4.d4");                              // ^d4 :18-22
-          int32_t v4 = in[g];
+          DARM_ARM_F(F, "sb4.d4");                              // ^d4 :18-22
+          int32_t v4 = __ldg(in + g);
           out[g] = R ? ir_mul(v4, 3) : ir_add(v4, 1);
           DARM_ARM("sb4.d4.end");
         } else {
-          DARM_ARM("sb4.d5");                              // ^d5 :23-27
-          int32_t v5 = in[g];
+          DARM_ARM_F(F, "sb4.d5");                              // ^d5 :23-27
+          int32_t v5 = __ldg(in + g);
           out[g] = R ? ir_xor(v5, 7) : ir_add(v5, 1);
           DARM_ARM("sb4.d5.end");
         }
@@ -298,7 +310,7 @@ struct Sb4T {
     } else if constexpr (!R) {                             // sb4: block-region then block-block
       const bool c2 = t < q;
       const bool sel = c1 ? true : c2;
-      int32_t w2 = ir_add(in[g], 1);
+      int32_t w2 = ir_add(__ldg(in + g), 1);
       int32_t pred = 0;
       if (!sel) {                                          // ^d4.r.m.m.g: predicated store
         int32_t old = out[g];
@@ -310,7 +322,7 @@ struct Sb4T {
       const bool sel = c1 ? true : c2;
       int32_t w4u = 0, v2e = 0;
       if (sel) {                                           // ^d4.r.m
-        int32_t v2 = in[g];
+        int32_t v2 = __ldg(in + g);
         if (!c1) w4u = ir_mul(v2, 3);                      // ^d4.r.m.g
         v2e = v2;
       }
@@ -319,7 +331,7 @@ struct Sb4T {
       if (sel2) w2u = ir_add(v2e, 1);                      // ^d4.r.m.g1.m
       int32_t w5u = 0;
       if (!sel) {                                          // ^d4.r.m.u1.m.g
-        int32_t v5 = in[g];
+        int32_t v5 = __ldg(in + g);
         w5u = ir_xor(v5, 7);
         // runDarm's block also loads out[t] (the predicated store's old value)
         // for sel3 = select sel w2 old; that value reaches the store only when
@@ -340,42 +352,43 @@ using Sb4r = Sb4T<true>;
 // nested.ir:6-41  divergent diamond whose arms are data-dependent diamonds
 struct Nested {
   static constexpr int kParams = 1;
-  template <bool M>
+  template <int F>
   __device__ __forceinline__ static void lane(const CorpusParams &P, uint32_t g, int t, const int32_t *a) {
+    constexpr bool M = F == kMelded;
     const int32_t *__restrict__ in = P.gl[0];
     int32_t *__restrict__ out = P.gl[1];
     const int32_t n = a[0];
     const bool c = t < n;
     if constexpr (!M) {
       if (c) {
-        DARM_ARM("nested.l");                              // ^l..^lm :11-24
-        int32_t lv = in[g];
+        DARM_ARM_F(F, "nested.l");                              // ^l..^lm :11-24
+        int32_t lv = __ldg(in + g);
         int32_t lp;
         if (lv > n) {
-          DARM_ARM("nested.la");
+          DARM_ARM_F(F, "nested.la");
           lp = ir_mul(lv, 2);
         } else {
-          DARM_ARM("nested.lb");
+          DARM_ARM_F(F, "nested.lb");
           lp = ir_add(lv, 9);
         }
         DARM_ARM("nested.lm");
         out[g] = lp;
       } else {
-        DARM_ARM("nested.r");                              // ^r..^rm :25-38
-        int32_t rv = in[g];
+        DARM_ARM_F(F, "nested.r");                              // ^r..^rm :25-38
+        int32_t rv = __ldg(in + g);
         int32_t rp;
         if (rv > n) {
-          DARM_ARM("nested.ra");
+          DARM_ARM_F(F, "nested.ra");
           rp = ir_mul(rv, 2);
         } else {
-          DARM_ARM("nested.rb");
+          DARM_ARM_F(F, "nested.rb");
           rp = ir_add(rv, 9);
         }
         DARM_ARM("nested.rm");
         out[g] = rp;
       }
     } else {                                               // region-region then block-block
-      int32_t lv = in[g];
+      int32_t lv = __ldg(in + g);
       bool lc = lv > n;
       int32_t ly = 0, lx = 0;
       if (!lc) ly = ir_add(lv, 9);                         // ^la.m.m.g
@@ -394,31 +407,38 @@ struct Nested {
 // In both forms the IR's "compare, then conditionally store b0" pairs are
 // written as the min/max they compute (`need1 = keep ? cv>b0 : cv<b0;
 // if (need1) buf[t] = b0` == `keep ? min(cv,b0) : max(cv,b0)`), so the two
-// forms differ only in control flow:
-//   unmelded: the divergent `condbr %up ^c ^d` (:16) stays a fenced branch,
-//             each arm with its own compares/select/store (^c :17-27, ^d :28-38);
-//   melded:   SURVEY App. A.2 — the compares are hoisted and melded and
-//             need1 = select keep (select up gt1 lt2) (select up lt1 gt1), which
-//             is `(keep == up) ? gt1 : lt1`, so one select of min/max remains.
-// `keep_eq_up` is keep XNOR up, precomputed per lane and step by the caller.
-template <bool M>
-__device__ __forceinline__ int32_t bitonic_exchange(int32_t cv, int32_t b0, bool keep, bool up,
-                                                    bool keep_eq_up) {
-  if constexpr (!M) {
+// unmelded forms differ from each other only in control flow.
+// Forms (F, darm_gpu.h variant codes):
+//   kUnmelded / kPredicated: the divergent `condbr %up ^c ^d` (:16) with each
+//     arm's compares/select/store (^c :17-27, ^d :28-38); kUnmelded leads each
+//     arm with DARM_IPDOM so ptxas keeps the branch, kPredicated lets ptxas
+//     if-convert the two one-instruction arms;
+//   kLiteral: SURVEY App. A.2's melded control flow: gt1 hoisted, the lt
+//     compare of the two guarded runs (same operands, so one compare),
+//     sel = select up gt1 lt2, sel1 = select up lt1 gt1, need1 = select keep
+//     sel sel1, one store of b0.  The chain folds to need1 = (keep == up) ?
+//     gt1 : lt, and "store b0 if need1" to (keep == up) ? min(cv, b0) :
+//     max(cv, b0) — the same min/max the unmelded arms are written with, so
+//     the forms differ in control flow only;
+//   kMelded is not handled here: the sorts fold `up` into the data (order
+//     flips) and issue one predicated min/max (bitonic_sort.cu).
+template <int F>
+__device__ __forceinline__ int32_t bitonic_exchange(int32_t cv, int32_t b0, bool keep, bool up) {
+  static_assert(F != kMelded, "the order-flip melded form lives in the sorts");
+  if constexpr (F == kLiteral) {
+    const bool need_lt = keep == up;                       // need1 = select keep (select up ..) (select up ..)
+    return need_lt ? min(cv, b0) : max(cv, b0);            // ^e.m: the single store of b0
+  } else {
     if (up) {                                              // condbr %up ^c ^d (:16)
-      DARM_ARM("bitonic.c");                               // ^c/^e: keep ? (cv>b0) : (cv<b0)
+      DARM_ARM_F(F, "bitonic.c");                          // ^c/^e: keep ? (cv>b0) : (cv<b0)
       cv = keep ? min(cv, b0) : max(cv, b0);
       DARM_ARM("bitonic.x1");
     } else {
-      DARM_ARM("bitonic.d");                               // ^d/^f: keep ? (cv<b0) : (cv>b0)
+      DARM_ARM_F(F, "bitonic.d");                          // ^d/^f: keep ? (cv<b0) : (cv>b0)
       cv = keep ? max(cv, b0) : min(cv, b0);
       DARM_ARM("bitonic.x2");
     }
     return cv;
-  } else {
-    (void)keep;
-    (void)up;
-    return keep_eq_up ? min(cv, b0) : max(cv, b0);         // ^c.m.u1 selects + ^e.m store
   }
 }
 

@@ -55,13 +55,14 @@ __device__ __forceinline__ int32_t oe_select_minmax(int32_t v, int32_t b, bool l
   return v;
 }
 
+template <int F>
 __device__ __forceinline__ int32_t oe_exchange_unmelded(int32_t v, int32_t b0, bool lower) {
   if (lower) {                                             // condbr %lower ^lo ^up
-    DARM_ARM("oddeven.lo");
+    DARM_ARM_F(F, "oddeven.lo");
     v = min(v, b0);                                        // ^lo: cv > b0 -> store b0
     DARM_ARM("oddeven.lo.end");
   } else {
-    DARM_ARM("oddeven.up");
+    DARM_ARM_F(F, "oddeven.up");
     v = max(v, b0);                                        // ^up: cv < b0 -> store b0
     DARM_ARM("oddeven.up.end");
   }
@@ -85,7 +86,7 @@ __device__ __forceinline__ void oe_roles(int t, uint64_t &lo, uint64_t &up) {
   }
 }
 
-template <bool M, int CTA, int p, int k, int s>
+template <int F, int CTA, int p, int k, int s>
 __device__ __forceinline__ int32_t oe_one_step(int32_t v, int lane, uint64_t lo, uint64_t up, int32_t (*xch)[CTA],
                                                int &par) {
   const bool lower = (lo >> s) & 1u;
@@ -102,26 +103,26 @@ __device__ __forceinline__ int32_t oe_one_step(int32_t v, int lane, uint64_t lo,
     b0 = xch[par][lower ? threadIdx.x + k : (upper ? threadIdx.x - k : threadIdx.x)];
     par ^= 1;
   }
-  if constexpr (M)
+  if constexpr (F == kMelded)
     return oe_select_minmax(v, b0, lower);   // %sel = select %lower %g1 %g2; one store
   else
-    return oe_exchange_unmelded(v, b0, lower);
+    return oe_exchange_unmelded<F>(v, b0, lower);
 }
 
-template <bool M, int B, int CTA, int p, int k, int s>
+template <int F, int B, int CTA, int p, int k, int s>
 __device__ __forceinline__ int32_t oe_one_network(int32_t v, int lane, uint64_t lo, uint64_t up,
                                                   int32_t (*xch)[CTA], int &par) {
   if constexpr (p < B) {
-    v = oe_one_step<M, CTA, p, k, s>(v, lane, lo, up, xch, par);
+    v = oe_one_step<F, CTA, p, k, s>(v, lane, lo, up, xch, par);
     if constexpr (k > 1)
-      return oe_one_network<M, B, CTA, p, k / 2, s + 1>(v, lane, lo, up, xch, par);
+      return oe_one_network<F, B, CTA, p, k / 2, s + 1>(v, lane, lo, up, xch, par);
     else
-      return oe_one_network<M, B, CTA, 2 * p, 2 * p, s + 1>(v, lane, lo, up, xch, par);
+      return oe_one_network<F, B, CTA, 2 * p, 2 * p, s + 1>(v, lane, lo, up, xch, par);
   }
   return v;
 }
 
-template <bool M, int B, int CTA>
+template <int F, int B, int CTA>
 __global__ void __launch_bounds__(CTA) oddeven_sort_kernel(int32_t *__restrict__ keys, uint32_t n) {
   static_assert(__builtin_ctz(B) * (__builtin_ctz(B) + 1) / 2 <= 64, "step masks are 64-bit");
   __shared__ int32_t xch[2][CTA];
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(CTA) oddeven_sort_kernel(int32_t *__restrict__
     const uint32_t id = tile * CTA + threadIdx.x;
     int32_t v = id < n ? keys[id] : INT_MAX;
     int par = 0;
-    v = oe_one_network<M, B, CTA, 1, 1, 0>(v, lane, lo, up, xch, par);
+    v = oe_one_network<F, B, CTA, 1, 1, 0>(v, lane, lo, up, xch, par);
     if (id < n) keys[id] = v;
   }
 }
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(CTA) oddeven_sort_kernel(int32_t *__restrict__
 // ------------------------------------------------------------ R keys per thread
 // One step (p, k) on the R registers of a thread; p and k are template
 // parameters so every register index and role test is resolved at compile time.
-template <bool M, int B, int R, int p, int k>
+template <int F, int B, int R, int p, int k>
 __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, int x0) {
   constexpr int P = B / R;
   if constexpr (k >= R) {
@@ -153,7 +154,7 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
     int32_t b0[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) b0[j] = __shfl_sync(0xffffffffu, v[j], src);
-    if constexpr (M) {
+    if constexpr (F == kMelded) {
       // the select as a complementary predicated pair (see oe_one_step) from 8
       // keys per thread up; at 4 the plain select schedules better (57 vs 63 µs)
 #pragma unroll
@@ -161,12 +162,12 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
         v[j] = R >= 8 ? oe_select_minmax(v[j], b0[j], lower) : (lower ? min(v[j], b0[j]) : max(v[j], b0[j]));
     } else {
       if (lower) {                                         // condbr %lower ^lo ^up
-        DARM_ARM("oddeven.reg.lo");
+        DARM_ARM_F(F, "oddeven.reg.lo");
 #pragma unroll
         for (int j = 0; j < R; ++j) v[j] = min(v[j], b0[j]);
         DARM_ARM("oddeven.reg.lo.end");
       } else {
-        DARM_ARM("oddeven.reg.up");
+        DARM_ARM_F(F, "oddeven.reg.up");
 #pragma unroll
         for (int j = 0; j < R; ++j) v[j] = max(v[j], b0[j]);
         DARM_ARM("oddeven.reg.up.end");
@@ -213,14 +214,14 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
 }
 
 // steps k = K, K/2, .., 1 of stage p, then the next stage
-template <bool M, int B, int R, int p, int k>
+template <int F, int B, int R, int p, int k>
 __device__ __forceinline__ void oe_reg_network(int32_t (&v)[R], int lane, int tib, int x0) {
   if constexpr (p < B) {
-    oe_reg_step<M, B, R, p, k>(v, lane, tib, x0);
+    oe_reg_step<F, B, R, p, k>(v, lane, tib, x0);
     if constexpr (k > 1)
-      oe_reg_network<M, B, R, p, k / 2>(v, lane, tib, x0);
+      oe_reg_network<F, B, R, p, k / 2>(v, lane, tib, x0);
     else
-      oe_reg_network<M, B, R, 2 * p, 2 * p>(v, lane, tib, x0);
+      oe_reg_network<F, B, R, 2 * p, 2 * p>(v, lane, tib, x0);
   }
 }
 
@@ -246,7 +247,7 @@ __device__ __forceinline__ void oe_load_keys(int32_t (&v)[R], const int32_t *__r
   }
 }
 
-template <bool M, int B, int R>
+template <int F, int B, int R>
 __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__restrict__ keys, uint32_t n) {
   constexpr int P = B / R;
   static_assert(R >= 4 && R <= B && P <= 32, "R keys per thread, at most 32 threads per bucket");
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__res
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = nxt[j];
     if (tile + gridDim.x < tiles) oe_load_keys<R>(nxt, keys, base + gridDim.x * kTile, n);
-    oe_reg_network<M, B, R, 1, 1>(v, lane, tib, x0);
+    oe_reg_network<F, B, R, 1, 1>(v, lane, tib, x0);
     if (base < n && R % 8 == 0 && aligned32(keys)) {
 #pragma unroll
       for (int q = 0; q < R / 8; ++q) st_v8(keys + base + 8 * q, &v[8 * q]);
@@ -291,23 +292,23 @@ int sms() {
   return g_sms_oe;
 }
 
-template <bool M, int B>
+template <int F, int B>
 cudaError_t launch_one(int32_t *keys, int64_t n, cudaStream_t s) {
   constexpr int CTA = B > 256 ? B : 256;
   const int64_t tiles = (n + CTA - 1) / CTA;
   int64_t grid = int64_t(sms()) * (2048 / CTA);
   if (grid > tiles) grid = tiles;
   if (grid < 1) grid = 1;
-  oddeven_sort_kernel<M, B, CTA><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
+  oddeven_sort_kernel<F, B, CTA><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
 }
 
-template <bool M, int B, int R>
+template <int F, int B, int R>
 cudaError_t launch_reg(int32_t *keys, int64_t n, cudaStream_t s) {
   constexpr int CTA = 256;
   static int per_sm = 0;
   if (!per_sm) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oddeven_sort_reg_kernel<M, B, R>, CTA, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oddeven_sort_reg_kernel<F, B, R>, CTA, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
   const int64_t tiles = (n + CTA * R - 1) / (CTA * R);
@@ -315,38 +316,38 @@ cudaError_t launch_reg(int32_t *keys, int64_t n, cudaStream_t s) {
   const int64_t iters = (tiles + max_ctas - 1) / max_ctas;
   int64_t grid = (tiles + iters - 1) / iters;
   if (grid < 1) grid = 1;
-  oddeven_sort_reg_kernel<M, B, R><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
+  oddeven_sort_reg_kernel<F, B, R><<<int(grid), CTA, 0, s>>>(keys, uint32_t(n));
   return cudaGetLastError();
 }
 
-template <bool M, int B>
+template <int F, int B>
 cudaError_t launch_r(int32_t *keys, int64_t n, int r, cudaStream_t s) {
   if constexpr (B >= 4 && B / 4 <= 32) {
-    if (r == 4) return launch_reg<M, B, 4>(keys, n, s);
+    if (r == 4) return launch_reg<F, B, 4>(keys, n, s);
   }
   if constexpr (B >= 8 && B / 8 <= 32) {
-    if (r == 8) return launch_reg<M, B, 8>(keys, n, s);
+    if (r == 8) return launch_reg<F, B, 8>(keys, n, s);
   }
   if constexpr (B >= 16 && B / 16 <= 32) {
-    if (r == 16) return launch_reg<M, B, 16>(keys, n, s);
+    if (r == 16) return launch_reg<F, B, 16>(keys, n, s);
   }
-  if (r == 1) return launch_one<M, B>(keys, n, s);
+  if (r == 1) return launch_one<F, B>(keys, n, s);
   return cudaErrorInvalidValue;
 }
 
-template <bool M>
+template <int F>
 cudaError_t launch_m(int32_t *keys, int64_t n, int bucket, int r, cudaStream_t s) {
   switch (bucket) {
-    case 2: return launch_r<M, 2>(keys, n, r, s);
-    case 4: return launch_r<M, 4>(keys, n, r, s);
-    case 8: return launch_r<M, 8>(keys, n, r, s);
-    case 16: return launch_r<M, 16>(keys, n, r, s);
-    case 32: return launch_r<M, 32>(keys, n, r, s);
-    case 64: return launch_r<M, 64>(keys, n, r, s);
-    case 128: return launch_r<M, 128>(keys, n, r, s);
-    case 256: return launch_r<M, 256>(keys, n, r, s);
-    case 512: return launch_r<M, 512>(keys, n, r, s);
-    case 1024: return launch_r<M, 1024>(keys, n, r, s);
+    case 2: return launch_r<F, 2>(keys, n, r, s);
+    case 4: return launch_r<F, 4>(keys, n, r, s);
+    case 8: return launch_r<F, 8>(keys, n, r, s);
+    case 16: return launch_r<F, 16>(keys, n, r, s);
+    case 32: return launch_r<F, 32>(keys, n, r, s);
+    case 64: return launch_r<F, 64>(keys, n, r, s);
+    case 128: return launch_r<F, 128>(keys, n, r, s);
+    case 256: return launch_r<F, 256>(keys, n, r, s);
+    case 512: return launch_r<F, 512>(keys, n, r, s);
+    case 1024: return launch_r<F, 1024>(keys, n, r, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -357,8 +358,11 @@ cudaError_t launch_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucke
                                 cudaStream_t s, int *launches) {
   if (n == 0) return cudaSuccess;
   if (launches) *launches += 1;
-  return variant ? launch_m<true>(keys, n, bucket, keys_per_thread, s)
-                 : launch_m<false>(keys, n, bucket, keys_per_thread, s);
+  switch (variant) {
+    case kUnmelded: return launch_m<kUnmelded>(keys, n, bucket, keys_per_thread, s);
+    case kMelded: return launch_m<kMelded>(keys, n, bucket, keys_per_thread, s);
+    default: return launch_m<kPredicated>(keys, n, bucket, keys_per_thread, s);
+  }
 }
 
 }  // namespace darm_gpu

@@ -64,6 +64,7 @@ struct GraphEntry {
   int kind, variant;
   const void *ptr;
   int64_t n;
+  std::vector<int64_t> params;    // every other recorded parameter, compared exactly
   cudaGraphExec_t exec;
   int launches;
 };
@@ -173,9 +174,10 @@ struct Timeline {
 // Returns the cached executable graph for (kind, variant, ptr, n), recording
 // it with `record` on the device's private capture stream the first time.
 template <class Rec>
-GraphEntry &cached_graph(DeviceState &st, int kind, int variant, const void *ptr, int64_t n, Rec &&record) {
+GraphEntry &cached_graph(DeviceState &st, int kind, int variant, const void *ptr, int64_t n, Rec &&record,
+                         std::vector<int64_t> params = {}) {
   for (auto &g : st.graphs)
-    if (g.kind == kind && g.variant == variant && g.ptr == ptr && g.n == n) return g;
+    if (g.kind == kind && g.variant == variant && g.ptr == ptr && g.n == n && g.params == params) return g;
   if (!st.capture) DARM_CUDA(cudaStreamCreateWithFlags(&st.capture, cudaStreamNonBlocking));
   cudaGraph_t graph = nullptr;
   int launches = 0;
@@ -188,7 +190,7 @@ GraphEntry &cached_graph(DeviceState &st, int kind, int variant, const void *ptr
   cudaError_t inst = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   DARM_CUDA(inst);
-  st.graphs.push_back({kind, variant, ptr, n, exec, launches});
+  st.graphs.push_back({kind, variant, ptr, n, std::move(params), exec, launches});
   return st.graphs.back();
 }
 
@@ -329,7 +331,8 @@ int darm_gpu_execute_warps(const char *kernel, int variant, int warp, int64_t n_
   return guarded(err, errlen, [&] {
     const CorpusKernelDesc *d = find_kernel(kernel);
     if (!d) user_error(std::string("unknown kernel '") + (kernel ? kernel : "") + "'");
-    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if (variant != DARM_UNMELDED && variant != DARM_MELDED && variant != DARM_PREDICATED)
+      user_error("variant must be 0 (unmelded), 1 (melded) or 2 (predicated)");
     if (warp < 1 || warp > 64) user_error("warp size must be in [1, 64]");  // interp.cpp:334-335
     if (n_warps < 0) user_error("n_warps must be >= 0");
     if (n_warps * int64_t(warp) >= (int64_t(1) << 31)) user_error("too many lanes (limit 2^31)");
@@ -439,11 +442,14 @@ using NetworkLaunch = cudaError_t (*)(int, int32_t *, int64_t, int, int, cudaStr
 // max_bucket / max_threads: the largest bucket and threads per bucket the
 // network's kernels take (bitonic 4096 / 256: buckets may span warps; PCM
 // 1024 / 32).
-static int network_sort(NetworkLaunch launch, int max_bucket, int max_threads, int variant, int32_t *keys,
+static int network_sort(NetworkLaunch launch, int max_bucket, int max_threads, int max_variant, int variant,
+                        int32_t *keys,
                         int64_t n, int bucket, int keys_per_thread, int mem, void *stream, darm_gpu_stats *stats,
                         char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
+    if (variant < DARM_UNMELDED || variant > max_variant)
+      user_error("variant must be 0 (unmelded), 1 (melded), 2 (predicated)" +
+                 std::string(max_variant >= DARM_MELDED_LITERAL ? " or 3 (melded literal)" : ""));
     if (!bitonic_sort_supported(bucket) || bucket > max_bucket)
       user_error("bucket must be a power of two in [2, " + std::to_string(max_bucket) + "]");
     if (n < 0 || n % bucket) user_error("n must be a non-negative multiple of the bucket size");
@@ -522,13 +528,13 @@ static int network_sort(NetworkLaunch launch, int max_bucket, int max_threads, i
 
 int darm_gpu_bitonic_sort_ex(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
                              void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
-  return network_sort(launch_bitonic_sort, 4096, 256, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
+  return network_sort(launch_bitonic_sort, 4096, 256, DARM_MELDED_LITERAL, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
                       errlen);
 }
 
 int darm_gpu_oddeven_sort(int variant, int32_t *keys, int64_t n, int bucket, int keys_per_thread, int mem,
                           void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
-  return network_sort(launch_oddeven_sort, 1024, 32, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
+  return network_sort(launch_oddeven_sort, 1024, 32, DARM_PREDICATED, variant, keys, n, bucket, keys_per_thread, mem, stream, stats, err,
                       errlen);
 }
 
@@ -731,6 +737,12 @@ int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream, darm_g
   });
 }
 
+static uint32_t float_bits(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return u;
+}
+
 static void check_srad_args(int64_t rows, int64_t cols, const int *roi, float lambda) {
   if (rows < 1 || cols < 2 || rows > (1 << 20) || cols > (1 << 20) || rows * cols > (int64_t(1) << 34))
     user_error("image must be rows x cols with rows >= 1, cols >= 2");
@@ -776,9 +788,7 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
                                                                          : cudaMemcpyDeviceToDevice, s));
     tl.mark(1);
     const int it = iters;
-    GraphEntry &g = cached_graph(st, 16 + variant, it, b0, rows * 1000003 + cols * 7 + roi[0] * 131 + roi[1] * 17 +
-                                                           roi[2] * 3 + roi[3] + int64_t(lambda * 1e6) * 97,
-                                 [&](cudaStream_t cs, int *launches) {
+    GraphEntry &g = cached_graph(st, 16, variant, b0, it, [&](cudaStream_t cs, int *launches) {
       cudaError_t e = launch_srad_roi(b0, int(cols), 0, int(rows), R, roiA, cs);
       ++*launches;
       float *in = b0, *out = b1;
@@ -792,7 +802,7 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
         std::swap(ri, ro);
       }
       return e;
-    });
+    }, {rows, cols, roi[0], roi[1], roi[2], roi[3], int64_t(float_bits(lambda))});
     DARM_CUDA(cudaGraphLaunch(g.exec, s));
     tl.mark(2);
     float *res = (iters % 2 == 0) ? b0 : b1;

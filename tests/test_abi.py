@@ -157,32 +157,101 @@ def _sass(pattern):
     return [ins for _, ins in hits[0][1]]
 
 
+def _ops(ins):
+    """Opcode of each SASS instruction (predicate guard stripped)."""
+    return [i.split()[1] if i.startswith("@") else i.split()[0] for i in ins]
+
+
+def _load_classes(ins):
+    return sorted({op for op in _ops(ins) if op.startswith("LDG")})
+
+
+# IR branch arms per corpus kernel (sb1.ir ... nested.ir): every arm leads
+# with DARM_IPDOM in the unmelded form
+_ARMS = {"Sb1": 2, "Sb1r": 2, "Sb2T<false>": 4, "Sb2T<true>": 4, "Sb3T<false>": 6, "Sb3T<true>": 6,
+         "Sb4T<false>": 4, "Sb4T<true>": 4, "Nested": 6}
+
+
+@pytest.mark.parametrize("kernel", sorted(_ARMS))
+def test_sass_unmelded_corpus_keeps_ipdom_branches(kernel):
+    """SURVEY §7 H1 / interp.cpp:298-306: the unmelded form runs every IR arm
+    behind a real divergent branch that reconverges at the post-dominator
+    (BSSY ... @P BRA ... BSYNC), never as ptxas-predicated runs; the
+    predicated column (variant 2) is the same source with the if-conversion
+    left to ptxas; all three forms load the read-only inputs with the same
+    class (LDG.E.CONSTANT)."""
+    un = _sass(f"corpus_lanes<darm_gpu::{kernel}, 0, 32, 0>")
+    me = _sass(f"corpus_lanes<darm_gpu::{kernel}, 1, 32, 0>")
+    pr = _sass(f"corpus_lanes<darm_gpu::{kernel}, 2, 32, 0>")
+    ou, op = _ops(un), _ops(pr)
+    assert ou.count("PMTRIG") == _ARMS[kernel]
+    assert sum(o.startswith("BSSY") for o in ou) >= 1 and sum(o.startswith("BSYNC") for o in ou) >= 1
+    # a conditional branch per divergent condbr (plus the grid-stride loop)
+    assert sum(bool(re.match(r"@!?P\d+ BRA", i)) for i in un) >= 2
+    # no arm instruction is predicated in the unmelded form (the one guard
+    # left is the loop's exit test)
+    assert sum(i.startswith("@") and "BRA" not in i and "EXIT" not in i for i in un) <= 1
+    assert "PMTRIG" not in op and "PMTRIG" not in _ops(me)
+    assert _load_classes(un) == _load_classes(me) == _load_classes(pr) == ["LDG.E.CONSTANT"]
+
+
 def test_sass_unmelded_keeps_both_arms():
-    un = _sass("corpus_lanes<darm_gpu::Sb1, false, 32, 0>")
-    me = _sass("corpus_lanes<darm_gpu::Sb1, true, 32, 0>")
-    # unmelded: both arms load `in` and store `out` (two STG, four LDG);
-    # melded: one hoisted load of `in`, two guarded aux loads, one store.
-    assert sum(i.split()[-1].startswith("STG") or " STG" in i or i.startswith("STG") for i in un) == 2
-    assert sum(" STG" in i or i.startswith("STG") for i in me) == 1
-    assert sum("LDG" in i for i in un) == 4
-    assert sum("LDG" in i for i in me) == 3
+    un = _sass("corpus_lanes<darm_gpu::Sb1, 0, 32, 0>")
+    me = _sass("corpus_lanes<darm_gpu::Sb1, 1, 32, 0>")
+    pr = _sass("corpus_lanes<darm_gpu::Sb1, 2, 32, 0>")
+    # unmelded / predicated: both arms load `in` and store `out` (two STG, four
+    # LDG); melded: one hoisted load of `in`, two guarded aux loads, one store.
+    for form in (un, pr):
+        assert sum(o.startswith("STG") for o in _ops(form)) == 2
+        assert sum(o.startswith("LDG") for o in _ops(form)) == 4
+    assert sum(o.startswith("STG") for o in _ops(me)) == 1
+    assert sum(o.startswith("LDG") for o in _ops(me)) == 3
+    # ptxas if-converts the predicated column: its arms are guarded runs
+    assert sum(i.startswith("@") and "LDG" in i for i in pr) == 4
+
+
+@pytest.mark.parametrize("kern,steps", [("bitonic_sort_kernel<{}, 64, 256, 2>", 21),
+                                        ("oddeven_sort_kernel<{}, 64, 256>", 21)])
+def test_sass_one_key_sorts_keep_ipdom_branches(kern, steps):
+    """One key per thread: the unmelded network branches on the lane's role in
+    every step (both arms fenced), the predicated column is ptxas's
+    if-converted min/max pairs (no branch in the network)."""
+    un = _sass(kern.format(0))
+    pr = _sass(kern.format(2))
+    ou = _ops(un)
+    assert ou.count("PMTRIG") >= steps
+    assert sum(o.startswith("BSSY") for o in ou) >= steps
+    assert sum(o.startswith("BSYNC") for o in ou) >= steps
+    assert "PMTRIG" not in _ops(pr)
+    assert sum(o.startswith("BSSY") for o in _ops(pr)) <= 2
+    me = _sass(kern.format(1))
+    assert _load_classes(un) == _load_classes(me) == _load_classes(pr)
 
 
 def test_sass_bitonic_sort_forms():
-    un = _sass("bitonic_sort_kernel<false, 64, 256, 2>")
-    me = _sass("bitonic_sort_kernel<true, 64, 256, 2>")
-    # Same partner reads in both forms (20 shuffles + 1 shared exchange for
-    # B=64); the unmelded network issues both arms of every `up` branch
-    # (ptxas if-converts them into complementary predicated min/max), the
-    # melded one a single keep-predicated min/max per step.
+    un = _sass("bitonic_sort_kernel<2, 64, 256, 2>")
+    me = _sass("bitonic_sort_kernel<1, 64, 256, 2>")
+    li = _sass("bitonic_sort_kernel<3, 64, 256, 2>")
+    # Same partner reads in every form (20 shuffles + 1 shared exchange for
+    # B=64); the predicated unmelded network issues both arms of every `up`
+    # branch (complementary predicated min/max), the melded one a single
+    # keep-predicated min/max per step.
     # (two tiles per iteration, U = 2)
-    assert sum("SHFL.BFLY" in i for i in un) == sum("SHFL.BFLY" in i for i in me) == 2 * 20
-    assert sum("BAR.SYNC" in i for i in un) == sum("BAR.SYNC" in i for i in me) == 1
+    for form in (un, me, li, _sass("bitonic_sort_kernel<0, 64, 256, 2>")):
+        assert sum("SHFL.BFLY" in i for i in form) == 2 * 20
+        assert sum("BAR.SYNC" in i for i in form) == 1
     assert len(un) > 1.4 * len(me)
     assert sum("IMNMX" in i for i in un) >= 2 * 60
     assert sum("IMNMX" in i for i in me) < 0.75 * sum("IMNMX" in i for i in un)
     # melded order flips run on the FMA pipe (IMAD), not as LOP3
     assert sum(i.startswith("IMAD") and "MOV" not in i for i in me) >= 2 * 5
+    # the literal App. A.2 form: the same single predicated min/max per step
+    # as the melded form, chosen by keep == up computed per lane (no order
+    # flips: fewer IMADs), and no branch in the network either
+    imnmx = lambda ins: sum("IMNMX" in i for i in ins)  # noqa: E731
+    assert abs(imnmx(li) - imnmx(me)) <= 4
+    assert sum(o.startswith("IMAD") for o in _ops(li)) < sum(o.startswith("IMAD") for o in _ops(me))
+    assert sum(o.startswith("BSSY") for o in _ops(li)) <= 2
 
 
 def test_sass_register_blocked_forms():
@@ -190,8 +259,9 @@ def test_sass_register_blocked_forms():
     around the arms of every thread-dependent step; the melded form has none
     in the network (its few are the tile loop and the bounds checks)."""
     for kern in ("bitonic_sort_reg_kernel<{}, 64, 16, true>", "oddeven_sort_reg_kernel<{}, 64, 16>"):
-        un = _sass(kern.format("false"))
-        me = _sass(kern.format("true"))
+        un = _sass(kern.format(0))
+        me = _sass(kern.format(1))
         assert sum("SHFL" in i for i in un) > 0 and sum("SHFL" in i for i in me) > 0
         condbra = lambda ins: sum(bool(re.match(r"@!?U?P\d+ BRA", i)) and "DIV" not in i for i in ins)  # noqa: E731
         assert condbra(un) > condbra(me), kern
+        assert _ops(un).count("PMTRIG") > 0

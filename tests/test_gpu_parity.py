@@ -48,7 +48,7 @@ def _golden_batch(kernel):
         yield W, nw, args, g_in, g_out, shared, faults
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("kernel", CORPUS)
 def test_golden_vectors(kernel, variant):
     for W, nw, args, g_in, g_out, shared, faults in _golden_batch(kernel):
@@ -85,7 +85,7 @@ def test_random_batches_vs_restatement(kernel, mode, restatement):
         want = np.concatenate([g[n] for n in names])
         wf = restatement.execute_warps(kernel, warp, nw, args, want, warp,
                                        None if shared is None else shared["buf"])
-        for variant in (0, 1):
+        for variant in (0, 1, 2):
             gg = {n: v.copy() for n, v in g.items()}
             res = darm.execute_warps(kernel, variant, warp, args, gg, shared, n_warps=nw)
             got = np.concatenate([res.globals[n] for n in names])
@@ -93,7 +93,7 @@ def test_random_batches_vs_restatement(kernel, mode, restatement):
             assert (res.faults == wf).all(), (kernel, variant, warp, mode)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 def test_sb1_config1_million_lanes_vs_reference(variant, restatement, reference):
     """BASELINE config 1: 2^20 int32 lanes = 32,768 warps of makeRandomInput
     fixtures with the half-warp split n=16, checked against the reference's
@@ -102,7 +102,7 @@ def test_sb1_config1_million_lanes_vs_reference(variant, restatement, reference)
     batch = darm.make_random_input("sb1", 32, nw, 1000)
     names = ["in", "aux2", "aux3", "out"]
     g0 = np.concatenate([batch.globals[n] for n in names])
-    mod = reference.load("sb1", variant)
+    mod = reference.load("sb1", int(variant == 1))
     ref = g0.copy()
     fr, _ = mod.execute_warps(32, nw, np.array([[16]], np.int32), ref, 32, None, threads=8, want_stats=False)
     g = {n: batch.globals[n].copy() for n in names}
@@ -123,7 +123,7 @@ def test_device_mode_matches_host_mode(kernel):
     import torch
 
     names, g, args, shared = _random_batch(kernel, 32, 2048, 7, "warp")
-    for variant in (0, 1):
+    for variant in (0, 1, 2):
         host = {n: v.copy() for n, v in g.items()}
         rh = darm.execute_warps(kernel, variant, 32, args, host, shared, n_warps=2048)
         dev = {n: torch.from_numpy(v.copy()).cuda() for n, v in g.items()}
@@ -142,7 +142,7 @@ def test_bitonic_sort_golden(kpt):
         B = case["bucket"]
         if kpt > 1 and (kpt > B or B // kpt > 32):
             continue
-        for variant in (0, 1):
+        for variant in (0, 1, 2, 3):
             keys = np.array(case["keys"], dtype=np.int32)
             st = darm.bitonic_sort(keys, B, variant, keys_per_thread=kpt)
             assert keys.tolist() == case["sorted"], (B, variant, kpt)
@@ -167,7 +167,7 @@ def test_bitonic_sort_register_blocked(bucket, kpt):
             lo, hi = (-128, 129) if dup else (-(2 ** 31), 2 ** 31)
             keys = rng.integers(lo, hi, size=n, dtype=np.int64).astype(np.int32)
             want = np.sort(keys.reshape(-1, bucket), axis=1).reshape(-1)
-            for variant in (0, 1):
+            for variant in (0, 1, 2, 3):
                 k = torch.from_numpy(keys.copy()).cuda()
                 st = darm.bitonic_sort(k, bucket, variant, keys_per_thread=kpt)
                 assert st["keys_per_thread"] == kpt
@@ -189,7 +189,7 @@ def test_register_sorts_16_byte_aligned_keys(sort, kpt):
         n = bucket * 1031
         keys = rng.integers(-(2 ** 31), 2 ** 31, size=n, dtype=np.int64).astype(np.int32)
         want = np.sort(keys.reshape(-1, bucket), axis=1).reshape(-1)
-        for variant in (0, 1):
+        for variant in ((0, 1, 2, 3) if sort == "bitonic" else (0, 1, 2)):
             buf = torch.zeros(n + 4, dtype=torch.int32, device="cuda")
             k = buf[4:]
             assert k.data_ptr() % 32 == 16
@@ -238,7 +238,7 @@ def test_bitonic_sort_buckets(bucket, restatement):
         chain = keys.copy()
         restatement.bitonic_sort(chain, bucket)
         assert (chain == want).all()
-        for variant in (0, 1):
+        for variant in (0, 1, 2, 3):
             k = keys.copy()
             darm.bitonic_sort(k, bucket, variant)
             assert (k == want).all(), (bucket, dup, variant)
@@ -257,7 +257,7 @@ def test_bitonic_sort_host_pipeline(bucket):
     rng = np.random.default_rng(bucket)
     keys = rng.integers(-(2 ** 31), 2 ** 31, size=1 << 22, dtype=np.int64).astype(np.int32)
     want = np.sort(keys.reshape(-1, bucket), axis=1).reshape(-1)
-    for variant in (0, 1):
+    for variant in (0, 1, 2, 3):
         k = keys.copy()
         st = darm.bitonic_sort(k, bucket, variant)
         assert st["launches"] == 2 and st["keys_per_thread"] == 16
@@ -273,7 +273,7 @@ def test_bitonic_sort_config2_full_size():
     gen = torch.Generator(device="cuda").manual_seed(1)
     keys = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=gen)
     orig = keys.clone()
-    for variant in (0, 1):
+    for variant in (0, 1, 2, 3):
         k = orig.clone()
         darm.bitonic_sort(k, 64, variant)
         torch.cuda.synchronize()

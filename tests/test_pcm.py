@@ -51,7 +51,7 @@ def test_oddeven_gpu_golden():
         for kpt in (0, 1, 4, 8, 16):
             if kpt > 1 and (kpt > B or B // kpt > 32):
                 continue
-            for variant in (0, 1):
+            for variant in (0, 1, 2):
                 keys = np.array(case["keys"], dtype=np.int32)
                 darm.oddeven_sort(keys, B, variant, keys_per_thread=kpt)
                 assert keys.tolist() == case["sorted"], (B, kpt, variant)
@@ -69,7 +69,7 @@ def test_oddeven_gpu_vs_restatement(restatement, bucket, kpt):
             keys = rng.integers(lo, hi, size=n, dtype=np.int64).astype(np.int32)
             want = keys.copy()
             restatement.oddeven_sort(want, bucket)
-            for variant in (0, 1):
+            for variant in (0, 1, 2):
                 k = torch.from_numpy(keys.copy()).cuda()
                 st = darm.oddeven_sort(k, bucket, variant, keys_per_thread=kpt)
                 assert st["keys_per_thread"] == kpt
@@ -83,7 +83,7 @@ def test_oddeven_gpu_full_size_host_pipeline():
     rng = np.random.default_rng(7)
     keys = rng.integers(-(2 ** 31), 2 ** 31, size=1 << 24, dtype=np.int64).astype(np.int32)
     want = np.sort(keys.reshape(-1, 64), axis=1).reshape(-1)
-    for variant in (0, 1):
+    for variant in (0, 1, 2):
         k = keys.copy()
         st = darm.oddeven_sort(k, 64, variant)
         assert st["launches"] == 8

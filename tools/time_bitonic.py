@@ -1,5 +1,6 @@
-"""Time the bitonic (or, with --oddeven, the PCM odd-even) bucket sort, both
-forms and every keys-per-thread shape, on cuda:0.
+"""Time the bitonic (or, with --oddeven, the PCM odd-even) bucket sort, every
+form (unmelded IPDOM, melded, predicated, bitonic: literal App. A.2) and every
+keys-per-thread shape, on cuda:0.
 
     python tools/time_bitonic.py [--oddeven] [bucket ...]      (run under gpurun)
 L2 is flushed (256 MiB write) before every timed launch; min and mean of 10.
@@ -31,9 +32,10 @@ def main(*buckets, sort=None):
             if kpt > 1 and (kpt > B or B // kpt > wide):
                 continue
             res = {}
-            for v in (darm.UNMELDED, darm.MELDED):
+            forms = (0, 1, 2, 3) if sort is darm.bitonic_sort else (0, 1, 2)
+            for v in forms:
                 call = sort(work, B, v, stream=s.cuda_stream, want_stats=False, prepare_only=True,
-                                         keys_per_thread=kpt)
+                            keys_per_thread=kpt)
                 ts = []
                 for i in range(13):
                     work.copy_(pristine)
@@ -49,8 +51,10 @@ def main(*buckets, sort=None):
                 assert torch.equal(work, want), (B, kpt, v)
                 res[v] = (min(ts), sum(ts) / len(ts))
             gbs = 8 * n / (res[1][1] * 1e-6) / 1e9
-            print(f"{sort.__name__} B={B} kpt={kpt:2d} unmelded {res[0][1]:7.1f} us (min {res[0][0]:6.1f}) melded {res[1][1]:7.1f} us "
-                  f"(min {res[1][0]:6.1f}) speedup {res[0][1] / res[1][1]:.3f} melded {gbs:6.0f} GB/s", flush=True)
+            names = {0: "unmelded", 1: "melded", 2: "predicated", 3: "literal"}
+            cols = "  ".join(f"{names[v]} {res[v][1]:7.1f} us (min {res[v][0]:6.1f})" for v in forms)
+            print(f"{sort.__name__} B={B} kpt={kpt:2d} {cols}  melded/unmelded {res[0][1] / res[1][1]:.3f}"
+                  f"  melded {gbs:6.0f} GB/s", flush=True)
 
 
 if __name__ == "__main__":
