@@ -275,7 +275,7 @@ def workload_config(args, variant):
                         f"(corpus bitonic.ir compare-exchange step chained over every stage)",
             "keys_per_gpu": args.keys, "bucket": args.bucket, "variant": variant,
             "keys_per_thread": args.keys_per_thread or "auto (16)",
-            "global_batch": args.keys * args.gpus, "parallelism": f"dp{args.gpus} (independent buckets)",
+            "global_batch": args.keys * int(os.environ.get("WORLD_SIZE", "1")), "parallelism": f"dp{args.gpus} (independent buckets)",
             "l2": "flushed (256 MiB write) before every timed step; input restored from a pristine copy"}
 
 
@@ -341,7 +341,11 @@ fn diamond(%n) {
 """
 
 
-def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None, rank=0, world=1):
+PER_KERNEL_SECTIONS = ("corpus", "nqueens16", "pcm", "ms1m", "interp", "lud8192", "srad", "bitonic")
+
+
+def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None, rank=0, world=1,
+                     sections=PER_KERNEL_SECTIONS, srad_n=16384, srad_iters=100):
     """Melded vs unmelded device time for every corpus kernel (config 1 shape:
     2^20 lanes = 32,768 warps of makeRandomInput fixtures, half-warp split),
     N-Queens N=16 (config 3), PCM, MS, LUD 8192^2 (config 4) and SRAD
@@ -357,7 +361,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
         return row
 
     nw = 1 << 15
-    for k in CORPUS_LANE:
+    for k in (CORPUS_LANE if "corpus" in sections else ()):
         b = darm.make_random_input(k, 32, nw, 1000)
         g = {n: torch.from_numpy(a).cuda() for n, a in b.globals.items()}
         args = [[16]] if len(b.args) == 1 else [[16], [24]]
@@ -376,7 +380,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
         out[k] = row
     # N-Queens N=16: the 7-row prefixes dealt round-robin over the ranks
     row = {}
-    for vname, v in (("unmelded", 0), ("melded", 1)):
+    for vname, v in ((("unmelded", 0), ("melded", 1)) if "nqueens16" in sections else ()):
         ts = []
         for i in range(warmup + max(3, steps // 4)):
             if dist:
@@ -390,6 +394,20 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
             if i >= warmup:
                 ts.append(st["kernel_ms"])
         row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
+        row[vname + "_solutions"] = sols
+    if "nqueens16" in sections:
+        nqueens_row(torch, dist, row, world, tmax)
+        out["nqueens16"] = row
+    if "pcm" in sections or "ms1m" in sections or "interp" in sections:
+        pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections)
+    if "lud8192" in sections:
+        lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax)
+    if "srad" in sections:
+        srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, srad_n, srad_iters)
+    return out
+
+
+def nqueens_row(torch, dist, row, world, tmax):
     tmax(row)
     row["speedup"] = row["unmelded_us"] / row["melded_us"]
     row["melded_solutions_per_s"] = 14772512 / (row["melded_us"] * 1e-6)
@@ -400,7 +418,14 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
                        "alu_pipe_pct": prof.get("alu_pipe_pct") if prof else None,
                        "issue_active_pct": prof.get("issue_active_pct") if prof else None,
                        "source": src}
-    out["nqueens16"] = row
+
+
+def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections):
+    def tmax(row):
+        for key in [k for k in row if k.endswith("_us")]:
+            row[key] = reduce_max(torch, dist, row[key])
+        return row
+
     # PCM (Batcher odd-even merge sort of 64-key buckets, 2^24 keys) and MS (bottom-up
     # merge sort of 2^20 keys, the paper's input size)
     n = 1 << 24
@@ -408,7 +433,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
     work = torch.empty_like(pristine)
     want = torch.sort(pristine.view(-1, 64), dim=1).values.view(-1)
-    for name, kpt in (("pcm", 0), ("pcm_1key", 1)):
+    for name, kpt in ((("pcm", 0), ("pcm_1key", 1)) if "pcm" in sections else ()):
         row = {}
         for vname, v in (("unmelded", 0), ("melded", 1)):
             call = darm.oddeven_sort(work, 64, v, stream=stream.cuda_stream, want_stats=False, prepare_only=True,
@@ -427,6 +452,8 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     keys = pristine[:n].clone()
     ms = torch.empty_like(keys)
     want = torch.sort(keys).values
+    if "ms1m" not in sections:
+        return interp_row(torch, darm, dist, steps, warmup, g, out) if "interp" in sections else None
     row = {}
     for vname, v in (("unmelded", 0), ("melded", 1)):
         call = darm.merge_sort(ms, v, stream=stream.cuda_stream, want_stats=False, prepare_only=True)
@@ -442,6 +469,11 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     row["melded_frac_hbm"] = row["melded_GBps"] / peak
     row["roofline_note"] = f"8 B/key per pass x {passes} passes; at 2^20 keys (4 MiB) the passes run from L2"
     out["ms1m"] = row
+    if "interp" in sections:
+        interp_row(torch, darm, dist, steps, warmup, g, out)
+
+
+def interp_row(torch, darm, dist, steps, warmup, g, out):
     # the GPU executeWarp for arbitrary IR (darm_gpu_program_execute): a diamond
     # kernel given as IR text, 32768 warps of 32 lanes (config 1 shape)
     row = {}
@@ -461,6 +493,9 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
         row[vname + "_warps_per_s"] = nwi / (row[vname + "_us"] * 1e-6)
     row["roofline_note"] = "an interpreter: bound by issue per IR instruction, not by bytes"
     out["interp_diamond_32k_warps"] = row
+
+
+def lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax):
     # LUD 8192^2 fp32 (config 4): the whole decomposition (n/16 + 2n/64 + 1 launches in one graph)
     n = 8192
     g = torch.Generator(device="cuda").manual_seed(4)
@@ -479,12 +514,19 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
     row["fp32_roof_TFLOPs"] = roof
     row["melded_frac_fp32"] = row["melded_TFLOPs"] / roof
     out["lud8192"] = row
+
+
+def srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, n=16384, iters=100):
     # SRAD 16384^2 fp32 x 100 iterations (config 5): one GPU, or row tiles with a
     # halo exchange and the ROI all-reduce every iteration over NCCL
-    n, iters = 16384, 100
+    g = torch.Generator(device="cuda").manual_seed(4)
     j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
-    for key, fast in (("srad16384x100", False), ("srad16384x100_fast_math", True)):
-        row = {}
+    import hashlib
+
+    sha = lambda t: hashlib.sha256(t.contiguous().cpu().numpy().tobytes()).hexdigest()[:16]  # noqa: E731
+    tag = f"srad{n}x{iters}"
+    for key, fast in ((tag, False), (tag + "_fast_math", True)):
+        row = {"rows": n, "cols": n, "iters": iters}
         flag = darm.FAST_MATH if fast else 0
         if world == 1:
             j = torch.empty_like(j0)
@@ -493,6 +535,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
                                  prepare_only=True, fast=fast)
                 t = time_steps(torch, stream, lambda: j.copy_(j0), call, 2, 1, flush)
                 row[vname + "_us"] = 1e3 * sum(t) / len(t)
+                row[vname + "_result_sha16"] = sha(j)
             del j
         else:
             from paper_2107_05681_b200.srad_tiles import SradTiles
@@ -513,7 +556,10 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
                     if rep:
                         ts.append(e0.elapsed_time(e1))
                 row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
-                del tiles
+                full = tiles.gather()
+                if full is not None:
+                    row[vname + "_result_sha16"] = sha(full)
+                del tiles, full
         tmax(row)
         row["speedup"] = row["unmelded_us"] / row["melded_us"]
         # minimal traffic 8 B/px/iteration (one read of J, one write of J') + the in/out copies of the call
@@ -536,6 +582,8 @@ def our_arm(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev_index = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev_index)
@@ -596,7 +644,13 @@ def our_arm(args):
     per_kernel = None
     if not args.no_per_kernel:
         peak0, _ = measured_peaks()
-        per_kernel = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak0, dist, rank, world)
+        sections = tuple(x for x in args.kernels.split(",") if x)
+        bad = set(sections) - set(PER_KERNEL_SECTIONS)
+        if bad:
+            raise SystemExit(f"unknown --kernels {sorted(bad)}; choose from {PER_KERNEL_SECTIONS}")
+        per_kernel = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak0, dist, rank, world,
+                                      sections, args.srad_size, args.srad_iters)
+    if per_kernel is not None and "bitonic" in sections:
         per_kernel["bitonic"] = {"unmelded_us": 1e3 * results["unmelded"]["kernel_ms_mean"],
                                  "melded_us": 1e3 * results["melded"]["kernel_ms_mean"],
                                  "speedup": results["unmelded"]["total_ms"] / results["melded"]["total_ms"],
@@ -689,6 +743,20 @@ def our_arm(args):
     return 0
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one process per
+    GPU) through torch.distributed.run on 127.0.0.1 with this same command
+    line; rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -702,9 +770,15 @@ def main():
     ap.add_argument("--keys-per-thread", type=int, default=0, help="0 = auto (16), 1 = one key per thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-kernel", action="store_true")
+    ap.add_argument("--kernels", default=",".join(PER_KERNEL_SECTIONS),
+                    help="per-kernel table sections (comma list of %s)" % ",".join(PER_KERNEL_SECTIONS))
+    ap.add_argument("--srad-size", type=int, default=16384)
+    ap.add_argument("--srad-iters", type=int, default=100)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return reference_arm(args)
     return our_arm(args)

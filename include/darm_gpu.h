@@ -230,36 +230,41 @@ int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream,
  * relative, the tolerance BASELINE.json's north star states for SRAD, instead
  * of bit for bit. */
 #define DARM_FAST_MATH 0x100
-/* SRAD only: force the 64-bit row addressing that tiles of 2^31 or more
- * elements take (32-bit element indices otherwise); results are identical —
- * a testing aid for that path. */
-#define DARM_SRAD_INDEX64 0x200
-
 int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters,
                   float lambda, const int *roi, int mem, void *stream,
                   darm_gpu_stats *stats, char *err, size_t errlen);
 
 /* Row-tiled SRAD for one rank of a multi-GPU run (device pointers only).
  * A tile holds global rows [r0, r0 + tile_rows) at local rows 1..tile_rows of
- * a (tile_rows + 3) x cols buffer: local row 0 is the halo row r0 - 1 and
- * local rows tile_rows+1, tile_rows+2 the halo rows below (needed only where
- * they exist in the image; the caller exchanges them between ranks).
+ * a (tile_rows + 3) x pitch float buffer (pitch >= cols, a multiple of 4;
+ * 16-byte aligned): local row 0 is the halo row r0 - 1 and local rows
+ * tile_rows+1, tile_rows+2 the halo rows below (needed only where they exist
+ * in the image; the caller exchanges them between ranks).
  * ROI partial sums: darm_gpu_srad_roi_words() doubles per buffer; a tile
  * writes the entries of the ROI rows it owns, so summing the buffers of all
  * ranks (e.g. an all-reduce) gives the full statistics.
  * tile_roi() fills roi_out for the initial image; tile_step() runs one
  * iteration tile_in -> tile_out using roi_in and writes the next roi_out.
- * q0_scratch: one device float. */
+ * `part` splits an iteration so the halo exchange overlaps compute:
+ * DARM_SRAD_INTERIOR_ROWS (rows 2 .. tile_rows-2, which read no halo row;
+ * also computes q0sqr into q0_scratch) while the halos are in flight, then
+ * DARM_SRAD_EDGE_ROWS (rows 1 and tile_rows-1 .. tile_rows) once they landed;
+ * DARM_SRAD_ALL_ROWS does both at once.  q0_scratch: one device float. */
+#define DARM_SRAD_ALL_ROWS 0
+#define DARM_SRAD_INTERIOR_ROWS 1
+#define DARM_SRAD_EDGE_ROWS 2
+int64_t darm_gpu_srad_pitch(int64_t cols);
 int64_t darm_gpu_srad_roi_words(int64_t cols, const int *roi);
-int darm_gpu_srad_tile_roi(const float *tile, int64_t cols, int64_t tile_rows,
-                           int64_t r0, int64_t rows, const int *roi,
-                           double *roi_out, void *stream, char *err, size_t errlen);
+int darm_gpu_srad_tile_roi(const float *tile, int64_t cols, int64_t pitch,
+                           int64_t tile_rows, int64_t r0, int64_t rows,
+                           const int *roi, double *roi_out, void *stream,
+                           char *err, size_t errlen);
 int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out,
-                            int64_t cols, int64_t tile_rows, int64_t r0,
-                            int64_t rows, float lambda, const int *roi,
-                            const double *roi_in, double *roi_out,
-                            float *q0_scratch, void *stream, char *err,
-                            size_t errlen);
+                            int64_t cols, int64_t pitch, int64_t tile_rows,
+                            int64_t r0, int64_t rows, float lambda,
+                            const int *roi, const double *roi_in,
+                            double *roi_out, float *q0_scratch, int part,
+                            void *stream, char *err, size_t errlen);
 
 /* ---- GPU executeWarp for arbitrary mini-IR -------
  * executeWarp (include/darm/interp.hpp:57-58, src/interp.cpp:332-381) for a

@@ -433,9 +433,10 @@ int oracle_lud(float *a, int64_t n, int threads) {
 /* ------------------------------------------------------------ SRAD
  * Rodinia SRAD restated (no reference code), in exactly
  * the operation order of csrc/srad.cu (compiled there with -fmad=false; this
- * file with -ffp-contract=off).  ROI statistics: per ROI row and 30-column
- * warp group, the 32-lane fp64 xor-butterfly the kernel performs (lane 0's
- * result), then rows and groups folded in order. */
+ * file with -ffp-contract=off).  ROI statistics: per ROI row and 128-column
+ * warp group, each lane's 4 columns summed in order, then the 32-lane fp64
+ * xor-butterfly the kernel performs (lane 0's result), then rows and groups
+ * folded in order. */
 static int clampi_(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 static float srad_c(float jc, float n, float s, float w, float e, float q0sqr, float q0den) {
@@ -453,17 +454,22 @@ static float srad_c(float jc, float n, float s, float w, float e, float q0sqr, f
 }
 
 static float srad_q0(const float *J, int64_t cols, const int *roi) {
-  const int w0 = roi[2] / 30, groups = roi[3] / 30 - w0 + 1;
+  const int w0 = roi[2] / 128, groups = roi[3] / 128 - w0 + 1;
   double s = 0.0, s2 = 0.0;
   for (int g = roi[0]; g <= roi[1]; ++g)
     for (int w = w0; w < w0 + groups; ++w) {
       double a[32], b[32];
-      for (int L = 0; L < 32; ++L) {
-        const int64_t j = (int64_t)w * 30 + L - 1;
-        const int in = L >= 1 && L <= 30 && j < cols && j >= roi[2] && j <= roi[3];
-        const double v = in ? (double)J[g * cols + j] : 0.0;
-        a[L] = v;
-        b[L] = in ? v * v : 0.0;
+      for (int L = 0; L < 32; ++L) {   /* lane L: its 4 columns in order */
+        double sa = 0.0, sb = 0.0;
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = (int64_t)w * 128 + 4 * L + k;
+          const int in = j < cols && j >= roi[2] && j <= roi[3];
+          const double v = in ? (double)J[g * cols + j] : 0.0;
+          sa += v;
+          sb += v * v;
+        }
+        a[L] = sa;
+        b[L] = sb;
       }
       for (int o = 16; o > 0; o >>= 1) {
         double na[32], nb[32];

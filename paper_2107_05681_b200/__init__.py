@@ -37,7 +37,7 @@ PREDICATED = 2           # original CFG as ptxas compiles it (short arms if-conv
 MELDED_LITERAL = 3       # bitonic sorts: SURVEY App. A.2's select chain as printed
 VARIANTS = {"unmelded": UNMELDED, "melded": MELDED, "predicated": PREDICATED, "melded_literal": MELDED_LITERAL}
 FAST_MATH = 0x100   # SRAD: OR into the variant (DARM_FAST_MATH, within 1e-5 relative)
-SRAD_INDEX64 = 0x200   # SRAD: force the 64-bit row addressing of very large tiles (testing aid)
+SRAD_ALL_ROWS, SRAD_INTERIOR_ROWS, SRAD_EDGE_ROWS = 0, 1, 2   # darm_gpu_srad_tile_step `part`
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # DARM_GPU_LIB points experiments at a variant build (e.g. a knob sweep)
@@ -65,6 +65,7 @@ ABI_SYMBOLS = (
     "darm_gpu_lud",
     "darm_gpu_srad",
     "darm_gpu_srad_roi_words",
+    "darm_gpu_srad_pitch",
     "darm_gpu_srad_tile_roi",
     "darm_gpu_srad_tile_step",
     "darm_gpu_program_load",
@@ -181,13 +182,15 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_char_p, ctypes.c_size_t]
         L.darm_gpu_srad_roi_words.argtypes = [ctypes.c_int64, I32P]
         L.darm_gpu_srad_roi_words.restype = ctypes.c_int64
+        L.darm_gpu_srad_pitch.argtypes = [ctypes.c_int64]
+        L.darm_gpu_srad_pitch.restype = ctypes.c_int64
         L.darm_gpu_srad_tile_roi.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
-                                             ctypes.c_int64, I32P, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_int64, ctypes.c_int64, I32P, ctypes.c_void_p, ctypes.c_void_p,
                                              ctypes.c_char_p, ctypes.c_size_t]
         L.darm_gpu_srad_tile_step.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
-                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, I32P,
-                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                              ctypes.c_char_p, ctypes.c_size_t]
+                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_float, I32P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_int, ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]
         _lib = L
     return _lib
 
@@ -669,25 +672,32 @@ def srad_roi_words(cols: int, roi=RODINIA_ROI) -> int:
     return int(lib().darm_gpu_srad_roi_words(int(cols), _roi_arr(roi)))
 
 
+def srad_pitch(cols: int) -> int:
+    """Row pitch (floats) of SRAD tile buffers: cols rounded up to a multiple of 4."""
+    return (int(cols) + 3) & ~3
+
+
 def srad_tile_roi(tile, cols, tile_rows, r0, rows, roi, roi_out, stream=None) -> None:
-    """ROI partials of a tile (device tensors; see darm_gpu.h)."""
+    """ROI partials of a tile (device tensors, rows of tile.shape[1] floats; see darm_gpu.h)."""
     err = ctypes.create_string_buffer(512)
-    _check(lib().darm_gpu_srad_tile_roi(ctypes.c_void_p(tile.data_ptr()), cols, tile_rows, r0, rows, _roi_arr(roi),
-                                        ctypes.c_void_p(roi_out.data_ptr()), ctypes.c_void_p(stream or 0), err, 512),
-           err)
+    _check(lib().darm_gpu_srad_tile_roi(ctypes.c_void_p(tile.data_ptr()), cols, tile.shape[1], tile_rows, r0, rows,
+                                        _roi_arr(roi), ctypes.c_void_p(roi_out.data_ptr()),
+                                        ctypes.c_void_p(stream or 0), err, 512), err)
 
 
 def srad_tile_step(variant, tile_in, tile_out, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0,
-                   stream=None) -> None:
-    """One SRAD iteration of a row tile (device tensors; see darm_gpu.h)."""
+                   stream=None, part: int = SRAD_ALL_ROWS) -> None:
+    """One SRAD iteration of a row tile, or its interior / edge rows (`part`;
+    device tensors, rows of tile_in.shape[1] floats; see darm_gpu.h)."""
     if isinstance(variant, str):
         variant = VARIANTS[variant]
+    _require(tile_in.shape == tile_out.shape, "tile_in and tile_out must have the same shape")
     err = ctypes.create_string_buffer(512)
     _check(lib().darm_gpu_srad_tile_step(int(variant), ctypes.c_void_p(tile_in.data_ptr()),
-                                         ctypes.c_void_p(tile_out.data_ptr()), cols, tile_rows, r0, rows, float(lam),
-                                         _roi_arr(roi), ctypes.c_void_p(roi_in.data_ptr()),
+                                         ctypes.c_void_p(tile_out.data_ptr()), cols, tile_in.shape[1], tile_rows, r0,
+                                         rows, float(lam), _roi_arr(roi), ctypes.c_void_p(roi_in.data_ptr()),
                                          ctypes.c_void_p(roi_out.data_ptr()), ctypes.c_void_p(q0.data_ptr()),
-                                         ctypes.c_void_p(stream or 0), err, 512), err)
+                                         int(part), ctypes.c_void_p(stream or 0), err, 512), err)
 
 
 @dataclass

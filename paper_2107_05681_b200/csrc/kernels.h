@@ -87,15 +87,22 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
 // srad.cu
 struct SradRoi {
   int r1, r2, c1, c2;   // inclusive ROI rectangle (global rows / columns)
-  int w0, groups;       // warp column groups (30 columns each) covering [c1, c2]
+  int w0, groups;       // warp column groups (128 columns each) covering [c1, c2]
   int rows;             // r2 - r1 + 1
 };
+// own rows (0-based, within a tile) one sweep launch computes: [lo0, hi0) then [lo1, hi1)
+struct SradRange {
+  int lo0, hi0, lo1, hi1;
+};
 SradRoi srad_roi_layout(int cols, int r1, int r2, int c1, int c2);
-cudaError_t launch_srad_roi(const float *jin, int cols, int r0, int tile_rows, const SradRoi &roi, double *roi_out,
-                            cudaStream_t s);
-cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s);
+int srad_pitch(int cols);   // row pitch (floats) of the library's own buffers: a multiple of 4
+cudaError_t launch_srad_roi(const float *jin, int cols, int pitch, int r0, int tile_rows, const SradRoi &roi,
+                            double *roi_out, cudaStream_t s);
+// parts / owner: per ROI row, the partial buffer of the rank owning it (null: roi_in alone)
+cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s,
+                           const double *const *parts = nullptr, const int *owner = nullptr);
 cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const float *q0, double *roi_out,
-                              int cols, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
-                              cudaStream_t s);
+                              int cols, int pitch, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
+                              const SradRange &range, cudaStream_t s);
 
 }  // namespace darm_gpu

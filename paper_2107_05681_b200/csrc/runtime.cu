@@ -759,12 +759,15 @@ int64_t darm_gpu_srad_roi_words(int64_t cols, const int *roi) {
   return int64_t(R.rows) * R.groups * 2;
 }
 
+static void check_srad_variant(int variant) {
+  if ((variant & ~DARM_FAST_MATH) != DARM_UNMELDED && (variant & ~DARM_FAST_MATH) != DARM_MELDED)
+    user_error("variant must be 0 (unmelded) or 1 (melded), optionally | DARM_FAST_MATH");
+}
+
 int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, float lambda, const int *roi,
                   int mem, void *stream, darm_gpu_stats *stats, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if ((variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_UNMELDED &&
-        (variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_MELDED)
-      user_error("variant must be 0 (unmelded) or 1 (melded), optionally | DARM_FAST_MATH");
+    check_srad_variant(variant);
     check_srad_args(rows, cols, roi, lambda);
     if (iters < 0) user_error("iters must be >= 0");
     if (!j) user_error("image is NULL");
@@ -774,8 +777,9 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
     std::lock_guard<std::mutex> lk(st.mu);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
+    const int pitch = srad_pitch(int(cols));
     const size_t img = size_t(rows) * size_t(cols) * 4;
-    const size_t buf = size_t(rows + 3) * size_t(cols) * 4;   // 1 halo row above, 2 below
+    const size_t buf = size_t(rows + 3) * size_t(pitch) * 4;   // 1 halo row above, 2 below
     const size_t roi_bytes = size_t(R.rows) * R.groups * 2 * 8;
     auto *b0 = static_cast<float *>(slot(st, 0, buf));
     auto *b1 = static_cast<float *>(slot(st, 1, buf));
@@ -784,19 +788,26 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
     float *q0 = reinterpret_cast<float *>(ctl);
     Timeline tl(s, stats != nullptr);
     tl.mark(0);
-    DARM_CUDA(cudaMemcpyAsync(b0 + cols, j, img, mem == DARM_MEM_HOST ? cudaMemcpyHostToDevice
-                                                                         : cudaMemcpyDeviceToDevice, s));
+    if (pitch != cols) {   // defined pad columns (never stored to the image, but read as neighbours' lanes)
+      DARM_CUDA(cudaMemsetAsync(b0, 0, buf, s));
+      DARM_CUDA(cudaMemsetAsync(b1, 0, buf, s));
+    }
+    const cudaMemcpyKind kin = mem == DARM_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    DARM_CUDA(cudaMemcpy2DAsync(b0 + pitch, size_t(pitch) * 4, j, size_t(cols) * 4, size_t(cols) * 4, size_t(rows),
+                                kin, s));
     tl.mark(1);
     const int it = iters;
+    const SradRange all{0, int(rows), 0, 0};
     GraphEntry &g = cached_graph(st, 16, variant, b0, it, [&](cudaStream_t cs, int *launches) {
-      cudaError_t e = launch_srad_roi(b0, int(cols), 0, int(rows), R, roiA, cs);
+      cudaError_t e = launch_srad_roi(b0, int(cols), pitch, 0, int(rows), R, roiA, cs);
       ++*launches;
       float *in = b0, *out = b1;
       double *ri = roiA, *ro = roiB;
       for (int t = 0; t < it && e == cudaSuccess; ++t) {
         e = launch_srad_q0(ri, R, q0, cs);
         if (e == cudaSuccess)
-          e = launch_srad_sweep(variant, in, out, q0, ro, int(cols), int(rows), 0, int(rows), lambda, R, cs);
+          e = launch_srad_sweep(variant, in, out, q0, ro, int(cols), pitch, int(rows), 0, int(rows), lambda, R, all,
+                                cs);
         *launches += 2;
         std::swap(in, out);
         std::swap(ri, ro);
@@ -806,8 +817,9 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
     DARM_CUDA(cudaGraphLaunch(g.exec, s));
     tl.mark(2);
     float *res = (iters % 2 == 0) ? b0 : b1;
-    DARM_CUDA(cudaMemcpyAsync(j, res + cols, img, mem == DARM_MEM_HOST ? cudaMemcpyDeviceToHost
-                                                                      : cudaMemcpyDeviceToDevice, s));
+    const cudaMemcpyKind kout = mem == DARM_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    DARM_CUDA(cudaMemcpy2DAsync(j, size_t(cols) * 4, res + pitch, size_t(pitch) * 4, size_t(cols) * 4,
+                                size_t(rows), kout, s));
     tl.mark(3);
     if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
     if (stats) {
@@ -820,37 +832,63 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
   });
 }
 
-int darm_gpu_srad_tile_roi(const float *tile, int64_t cols, int64_t tile_rows, int64_t r0, int64_t rows,
-                           const int *roi, double *roi_out, void *stream, char *err, size_t errlen) {
+static void check_srad_tile(int64_t rows, int64_t cols, int64_t pitch, int64_t tile_rows, int64_t r0) {
+  if (tile_rows < 1 || r0 < 0 || r0 + tile_rows > rows) user_error("tile outside the image");
+  if (pitch < cols || pitch % 4) user_error("pitch must be >= cols and a multiple of 4 floats");
+  if ((tile_rows + 3) * pitch >= (int64_t(1) << 40)) user_error("tile too large");
+}
+
+int64_t darm_gpu_srad_pitch(int64_t cols) { return cols < 1 ? -1 : int64_t(srad_pitch(int(cols))); }
+
+int darm_gpu_srad_tile_roi(const float *tile, int64_t cols, int64_t pitch, int64_t tile_rows, int64_t r0,
+                           int64_t rows, const int *roi, double *roi_out, void *stream, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
     check_srad_args(rows, cols, roi, 0.5f);
-    if (tile_rows < 1 || r0 < 0 || r0 + tile_rows > rows) user_error("tile outside the image");
+    check_srad_tile(rows, cols, pitch, tile_rows, r0);
     if (!tile || !roi_out) user_error("NULL buffer");
+    if (reinterpret_cast<uintptr_t>(tile) & 15) user_error("tile must be 16-byte aligned");
     device_state(nullptr);
     const SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
     DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double),
                               static_cast<cudaStream_t>(stream)));
-    DARM_CUDA(launch_srad_roi(tile, int(cols), int(r0), int(tile_rows), R, roi_out, static_cast<cudaStream_t>(stream)));
+    DARM_CUDA(launch_srad_roi(tile, int(cols), int(pitch), int(r0), int(tile_rows), R, roi_out,
+                              static_cast<cudaStream_t>(stream)));
   });
 }
 
-int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, int64_t cols, int64_t tile_rows,
-                            int64_t r0, int64_t rows, float lambda, const int *roi, const double *roi_in,
-                            double *roi_out, float *q0_scratch, void *stream, char *err, size_t errlen) {
+// own rows that need no halo row: [1, tile_rows - 2) (output row i reads rows i-1 .. i+2)
+static SradRange srad_part_range(int part, int n) {
+  if (part == DARM_SRAD_ALL_ROWS || n <= 3) {
+    if (part == DARM_SRAD_INTERIOR_ROWS) return SradRange{0, 0, 0, 0};
+    return SradRange{0, n, 0, 0};
+  }
+  if (part == DARM_SRAD_INTERIOR_ROWS) return SradRange{1, n - 2, 0, 0};
+  return SradRange{0, 1, n - 2, n};   // DARM_SRAD_EDGE_ROWS
+}
+
+int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, int64_t cols, int64_t pitch,
+                            int64_t tile_rows, int64_t r0, int64_t rows, float lambda, const int *roi,
+                            const double *roi_in, double *roi_out, float *q0_scratch, int part, void *stream,
+                            char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if ((variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_UNMELDED &&
-        (variant & ~(DARM_FAST_MATH | DARM_SRAD_INDEX64)) != DARM_MELDED)
-      user_error("variant must be 0 (unmelded) or 1 (melded), optionally | DARM_FAST_MATH");
+    check_srad_variant(variant);
     check_srad_args(rows, cols, roi, lambda);
-    if (tile_rows < 1 || r0 < 0 || r0 + tile_rows > rows) user_error("tile outside the image");
+    check_srad_tile(rows, cols, pitch, tile_rows, r0);
+    if (part != DARM_SRAD_ALL_ROWS && part != DARM_SRAD_INTERIOR_ROWS && part != DARM_SRAD_EDGE_ROWS)
+      user_error("part must be DARM_SRAD_ALL_ROWS, DARM_SRAD_INTERIOR_ROWS or DARM_SRAD_EDGE_ROWS");
     if (!tile_in || !tile_out || !roi_in || !q0_scratch) user_error("NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(tile_in) | reinterpret_cast<uintptr_t>(tile_out)) & 15)
+      user_error("tiles must be 16-byte aligned");
     device_state(nullptr);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
-    DARM_CUDA(launch_srad_q0(roi_in, R, q0_scratch, s));
-    if (roi_out) DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double), s));
-    DARM_CUDA(launch_srad_sweep(variant, tile_in, tile_out, q0_scratch, roi_out, int(cols), int(tile_rows), int(r0),
-                                int(rows), lambda, R, s));
+    if (part != DARM_SRAD_EDGE_ROWS) {   // the first (or only) launch of the iteration: q0sqr
+      DARM_CUDA(launch_srad_q0(roi_in, R, q0_scratch, s));
+      if (roi_out) DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double), s));
+    }
+    DARM_CUDA(launch_srad_sweep(variant, tile_in, tile_out, q0_scratch, roi_out, int(cols), int(pitch),
+                                int(tile_rows), int(r0), int(rows), lambda, R, srad_part_range(part, int(tile_rows)),
+                                s));
   });
 }
 

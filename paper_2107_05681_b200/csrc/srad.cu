@@ -1,35 +1,46 @@
 // srad.cu — Speckle Reducing Anisotropic Diffusion (SRAD, PAPER.md:778-781,
 // 842-851), fp32, unmelded and melded forms.  The reference has no SRAD code;
-// the per-pixel mathematics is Rodinia's SRAD restated and
-// the CPU oracle (oracle/darm_oracle.c, oracle_srad) performs the same fp32 /
-// fp64 operations in the same order.  This translation unit is compiled with
-// -fmad=false so no multiply-add is contracted (the oracle is compiled with
-// -ffp-contract=off): GPU and CPU agree bit for bit.
+// the per-pixel mathematics is Rodinia's SRAD restated and the
+// CPU oracle (oracle/darm_oracle.c, oracle_srad) performs the same fp32 / fp64
+// operations in the same order.  This translation unit is compiled with
+// -fmad=false so no multiply-add is contracted in the IEEE path (the oracle is
+// compiled with -ffp-contract=off): GPU and CPU agree bit for bit.
 //
 // Per iteration, with q0sqr from the ROI statistics of the current image J:
 //   c(i,j)  = clamp01( 1 / (1 + (q(i,j) - q0sqr) / (q0sqr (1 + q0sqr))) )
 //   J'(i,j) = J + (lambda/4) (c(i,j) dN + c(i+1,j) dS + c(i,j) dW + c(i,j+1) dE)
 // with dN..dE the differences to the 4 neighbours (image borders clamp).
 //
-// B200 layout: one fused kernel per iteration.  Each warp owns 30 output
-// columns (lanes 1..30; lanes 0 and 31 are halo lanes that only supply
-// neighbour values) and sweeps a segment of rows top to bottom, keeping the
-// vertical window J(i-1..i+2) and c(i), c(i+1) in registers and exchanging
-// west/east neighbours with __shfl_sync.  HBM traffic is one read of J and
-// one write of J' per pixel (8 B/px/iteration; the Rodinia layout moves
-// ~52 B/px).  J is double-buffered (J -> J').
+// B200 layout (round 2): one fused sweep per iteration, 8 B of HBM traffic per
+// pixel (one read of J, one write of J').  A thread owns 4 consecutive columns
+// (16-byte row loads and stores), a warp 128 columns; the warp slides down a
+// segment of rows two rows at a time, keeping the vertical window
+// J(i-1 .. i+3) and c(i) in registers, the arithmetic of the two rows in f32x2
+// pairs.  West / east neighbours inside a thread are registers; across threads
+// one __shfl_up / __shfl_down per row; at the warp's edges lane 0 loads the
+// west halo column c0-1 and lane 31 the east halo columns c0+128, c0+129 (one
+// predicated scalar load each), and lane 31 computes c for column c0+128 as a
+// fifth column (its east c).  Row pointers are 64-bit (one addressing path).
+// The pitch of a row buffer is a multiple of 4 floats (16-byte rows).
 //
 // The divergent regions are
-//   R_B  border handling: west/east neighbours at the image's first/last
-//        column (thread-position dependent), and lane 31's own east value;
+//   R_B  border handling: the west / east neighbour of the warp's edge lanes
+//        (halo vs shuffle: thread-position dependent) and, in the warp holding
+//        the image's last column, the clamped east neighbour;
 //   R_D  the data-dependent three-way clamp of c (c < 0 / c > 1 / else).
-// unmelded: if / else-if chains (fenced arms); melded: select chains.
+// unmelded: if / else-if arms behind real divergent branches (DARM_IPDOM);
+// melded: select chains.
 //
-// ROI statistics are reduced deterministically: each warp sums the ROI part
-// of its 30 columns of J' in fp64 with a shuffle butterfly, writing one
-// partial per (row, warp column group); srad_q0_kernel folds the partials in a
-// fixed order.  For row-tiled multi-GPU runs the partial buffer is summed
-// across ranks (each entry is owned by exactly one rank, so the sum is exact).
+// ROI statistics are reduced deterministically: per ROI row and 128-column
+// warp group, each lane sums its 4 in-ROI values of J' in fp64 in column
+// order, then a 32-lane xor butterfly; lane 0 writes one partial per (row,
+// group); srad_q0_kernel folds the partials rows-then-groups in order.  For
+// row-tiled multi-GPU runs every partial is written by the one rank owning
+// its row.
+//
+// Row ranges: a launch computes own rows [lo0, hi0) and [lo1, hi1) of a tile
+// (segments of `rs` rows each), so a multi-GPU rank runs its interior rows
+// while the halo rows are in flight and the two edge bands after they land.
 #include <cstdint>
 
 #include "common.cuh"
@@ -37,76 +48,35 @@
 
 namespace darm_gpu {
 
+constexpr int kSradWarpCols = 128;   // 32 lanes x 4 columns
+constexpr unsigned kFull = 0xffffffffu;
+
 struct SradParams {
-  const float *jin;      // (tile_rows + 3) x cols, local row 0 = global row r0 - 1
+  const float *jin;      // (tile_rows + 3) x pitch, local row 0 = global row r0 - 1
   float *jout;           // same layout; local rows 1..tile_rows written
   const float *q0;       // q0sqr of this iteration (device scalar)
   double *roi_out;       // [roi_rows][roi_groups][2] partial sums of J' (may be null)
-  int cols, tile_rows, r0, R, rs;
-  float lq;              // lambda / 4
-  float nz;              // -0.0f (opaque to ptxas: see mulx)
+  int cols, pitch, tile_rows, r0, R;
+  int lo0, hi0, lo1, hi1;   // own rows (0-based) computed: [lo0, hi0) then [lo1, hi1)
+  int rs, nseg0;            // rows per segment; segments of range 0
+  float lq;                 // lambda / 4
+  float nz;                 // -0.0f (opaque to ptxas: see mulx)
   int roi_r1, roi_r2, roi_c1, roi_c2, roi_w0, roi_groups;
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// c for one pixel from its centre and 4 neighbour values (Rodinia SRAD,
-// restated).  R_D is the clamp.
-// FAST (DARM_FAST_MATH): the five divisions as a multiply by the MUFU
-// reciprocal (rcp.approx.ftz: no range fix-up, the operands here are normal
-// numbers of moderate size) and the sums of products contracted to FMAs; the
-// result stays within the north star's 1e-5 relative tolerance of the IEEE
-// path (tests/test_srad.py) instead of matching it bit for bit.
 __device__ __forceinline__ float rcp_approx(float b) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
   return r;
 }
 
-template <bool FAST>
-__device__ __forceinline__ float sdiv(float a, float b) {
-  if constexpr (FAST) return a * rcp_approx(b);
-  else return a / b;
-}
-
-template <bool M, bool FAST>
-__device__ __forceinline__ float srad_coeff(float jc, float n, float s, float w, float e, float q0sqr,
-                                            float q0den) {
-  const float dN = n - jc, dS = s - jc, dW = w - jc, dE = e - jc;
-  float g2, l, num, den;
-  if constexpr (FAST) {
-    g2 = sdiv<FAST>(__fmaf_rn(dE, dE, __fmaf_rn(dW, dW, __fmaf_rn(dS, dS, dN * dN))), jc * jc);
-    l = sdiv<FAST>(((dN + dS) + dW) + dE, jc);
-    num = __fmaf_rn(-1.0f / 16.0f, l * l, 0.5f * g2);
-    den = __fmaf_rn(0.25f, l, 1.0f);
-  } else {
-    g2 = (((dN * dN + dS * dS) + dW * dW) + dE * dE) / (jc * jc);
-    l = (((dN + dS) + dW) + dE) / jc;
-    num = (0.5f * g2) - ((1.0f / 16.0f) * (l * l));
-    den = 1.0f + (0.25f * l);
-  }
-  const float qsqr = sdiv<FAST>(num, den * den);
-  den = sdiv<FAST>(qsqr - q0sqr, q0den);
-  float c = FAST ? rcp_approx(1.0f + den) : 1.0f / (1.0f + den);
-  if constexpr (!M) {
-    if (c < 0.0f) {                      // R_D: three-way, data dependent
-      DARM_ARM("srad.rd.lo");
-      c = 0.0f;
-    } else if (c > 1.0f) {
-      DARM_ARM("srad.rd.hi");
-      c = 1.0f;
-    }
-  } else {
-    c = c < 0.0f ? 0.0f : (c > 1.0f ? 1.0f : c);
-  }
-  return c;
-}
-
-// ---- two pixels per instruction: packed fp32 pairs (sm_100 f32x2).  Every
+// ---- f32x2 pairs (sm_100): two rows of one column per instruction.  Every
 // half is the IEEE operation of the scalar code.  ptxas (12.9) contracts a
 // mul.rn.f32x2 feeding an add.rn.f32x2 into FFMA2 even under -fmad=false, so
-// the IEEE path forms products as mulx = fma(a, b, z) with z = -0.0f from a
-// kernel parameter (exact: a*b + -0 == a*b, and not foldable).
+// exact products are formed as mulx = fma(a, b, z) with z = -0.0f from a
+// kernel parameter (a*b + -0 == a*b exactly, and not foldable).
 __device__ __forceinline__ unsigned long long pk(float2 a) {
   unsigned long long r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
@@ -133,282 +103,446 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   return upk(r);
 }
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 mk(float a, float b) { return make_float2(a, b); }
 
-__device__ __forceinline__ float2 mulx(float2 a, float2 b, float2 z) { return fma2(a, b, z); }
-// (the fast form's product feeds a subtraction / addition: mulx, not mul2)
-template <bool FAST>
-__device__ __forceinline__ float2 sdiv2(float2 a, float2 b, float2 z) {
-  if constexpr (FAST) return mulx(a, make_float2(rcp_approx(b.x), rcp_approx(b.y)), z);
-  else return make_float2(a.x / b.x, a.y / b.y);
-}
-
-// R_D for one pixel of a pair (same arms as srad_coeff's)
+// R_D: the three-way clamp of c, one pixel.
 template <bool M>
 __device__ __forceinline__ float clamp_rd(float c) {
   if constexpr (!M) {
     if (c < 0.0f) {
-      DARM_ARM("srad.rd2.lo");
+      DARM_IPDOM("srad.rd.lo");
       c = 0.0f;
     } else if (c > 1.0f) {
-      DARM_ARM("srad.rd2.hi");
+      DARM_IPDOM("srad.rd.hi");
       c = 1.0f;
     }
     return c;
   } else {
-    return c < 0.0f ? 0.0f : (c > 1.0f ? 1.0f : c);
+    return fminf(fmaxf(c, 0.0f), 1.0f);   // the select chain c < 0 ? 0 : (c > 1 ? 1 : c), as two FMNMX
   }
 }
 
-// srad_coeff for two pixels at once (rows i and i+1 of one column)
-template <bool M, bool FAST, bool PACK>
-__device__ __forceinline__ float2 srad_coeff2(float2 jc, float2 n, float2 s, float2 w, float2 e, float q0sqr,
-                                              float q0den, float2 z) {
-  if constexpr (!PACK)
-    return make_float2(srad_coeff<M, FAST>(jc.x, n.x, s.x, w.x, e.x, q0sqr, q0den),
-                       srad_coeff<M, FAST>(jc.y, n.y, s.y, w.y, e.y, q0sqr, q0den));
-  const float2 dN = sub2(n, jc), dS = sub2(s, jc), dW = sub2(w, jc), dE = sub2(e, jc);
-  float2 g2, l, num, den, qsqr;
-  if constexpr (FAST) {
-    g2 = sdiv2<FAST>(fma2(dE, dE, fma2(dW, dW, fma2(dS, dS, mul2(dN, dN)))), mul2(jc, jc), z);
-    l = sdiv2<FAST>(add2(add2(add2(dN, dS), dW), dE), jc, z);
-    num = fma2(f2(-1.0f / 16.0f), mul2(l, l), mul2(f2(0.5f), g2));
-    den = fma2(f2(0.25f), l, f2(1.0f));
-    qsqr = sdiv2<FAST>(num, mul2(den, den), z);
-  } else {
-    g2 = sdiv2<FAST>(add2(add2(add2(mulx(dN, dN, z), mulx(dS, dS, z)), mulx(dW, dW, z)), mulx(dE, dE, z)),
-                     mulx(jc, jc, z), z);
-    l = sdiv2<FAST>(add2(add2(add2(dN, dS), dW), dE), jc, z);
-    num = sub2(mulx(f2(0.5f), g2, z), mulx(f2(1.0f / 16.0f), mulx(l, l, z), z));
-    den = add2(f2(1.0f), mulx(f2(0.25f), l, z));
-    qsqr = sdiv2<FAST>(num, mulx(den, den, z), z);
-  }
-  den = sdiv2<FAST>(sub2(qsqr, f2(q0sqr)), f2(q0den), z);
-  const float2 one_den = add2(f2(1.0f), den);
-  float2 c;
-  if constexpr (FAST)
-    c = make_float2(rcp_approx(one_den.x), rcp_approx(one_den.y));
+// ---- per-pixel mathematics on column pairs (two adjacent columns of one row).
+// Inputs per pixel: centre C, the vertical differences vn = J(i) - J(i-1) and
+// vs = J(i+1) - J(i) (so dN = -vn, dS = vs: IEEE subtraction is symmetric, so
+// these are the restatement's dN, dS bit for bit), and dW = W - C, dE = E - C.
+struct SradQ {
+  float q0sqr, q0den;   // IEEE: q0sqr and q0sqr (1 + q0sqr)
+  float nk1, nk2;       // FAST: -16 q0den and -16 q0sqr^2
+};
+
+// IEEE: the restatement's operations in its order (oracle srad_c / the update),
+// one pixel; the clamp is R_D.
+template <bool M>
+__device__ __forceinline__ float coeff_ieee(float jc, float vn, float vs, float dW, float dE, const SradQ &q) {
+  const float dN = -vn, dS = vs;
+  const float g2 = (((dN * dN + dS * dS) + dW * dW) + dE * dE) / (jc * jc);
+  const float l = (((dN + dS) + dW) + dE) / jc;
+  const float num = (0.5f * g2) - ((1.0f / 16.0f) * (l * l));
+  float den = 1.0f + (0.25f * l);
+  const float qsqr = num / (den * den);
+  den = (qsqr - q.q0sqr) / q.q0den;
+  return clamp_rd<M>(1.0f / (1.0f + den));
+}
+__device__ __forceinline__ float update_ieee(float jc, float vn, float vs, float dW, float dE, float c0, float c1,
+                                             float ce, float lq) {
+  const float dN = -vn, dS = vs;
+  const float d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
+  return jc + lq * d;
+}
+
+// FAST (DARM_FAST_MATH): no division at all but one reciprocal.  With
+// s = dN + dS + dW + dE and Q = dN^2 + dS^2 + dW^2 + dE^2, Rodinia's
+//   q^2 = (Q/2 - s^2/16) / (jc (1 + s/(4 jc)))^2 ... c = 1 / (1 + (q^2 - q0sqr) / q0den)
+// is, multiplying through by 16 jc^2 (V = (jc + s/4)^2, U = 8Q - s^2 >= 4Q >= 0
+// by Cauchy-Schwarz, so nothing cancels),
+//   c = 16 q0den V / (U + 16 q0sqr^2 V)
+// computed as (-16 q0den) V / (s^2 - 8Q - 16 q0sqr^2 V).  Within the north
+// star's 1e-5 relative of the IEEE path after 100 iterations (tests/test_srad.py).
+template <bool M>
+__device__ __forceinline__ float2 coeff_fast2(float2 C, float2 vn, float2 vs, float2 dW, float2 dE, const SradQ &q) {
+  const float2 s = add2(add2(sub2(vs, vn), dW), dE);
+  const float2 Q = fma2(dE, dE, fma2(dW, dW, fma2(vs, vs, mul2(vn, vn))));
+  const float2 un = fma2(s, s, mul2(Q, f2(-8.0f)));            // -U
+  const float2 m = fma2(f2(0.25f), s, C);
+  const float2 V = mul2(m, m);
+  const float2 tn = fma2(f2(q.nk2), V, un);                     // -(U + 16 q0sqr^2 V)
+  const float2 c = mul2(mul2(V, f2(q.nk1)), mk(rcp_approx(tn.x), rcp_approx(tn.y)));
+  return mk(clamp_rd<M>(c.x), clamp_rd<M>(c.y));
+}
+// the same operations on one pixel (the gathered fifth column)
+template <bool M>
+__device__ __forceinline__ float coeff_fast1(float C, float vn, float vs, float dW, float dE, const SradQ &q) {
+  return coeff_fast2<M>(f2(C), f2(vn), f2(vs), f2(dW), f2(dE), q).x;
+}
+__device__ __forceinline__ float2 update_fast2(float2 C, float2 vn, float2 vs, float2 dW, float2 dE, float2 cv,
+                                               float2 cs, float2 ce, float lq) {
+  const float2 d = fma2(ce, dE, fma2(cs, vs, mul2(cv, sub2(dW, vn))));   // c dN + c dW = c (dW - vn)
+  return fma2(f2(lq), d, C);
+}
+
+template <bool M, bool FAST>
+__device__ __forceinline__ float2 coeff2(float2 C, float2 vn, float2 vs, float2 dW, float2 dE, const SradQ &q) {
+  if constexpr (FAST) return coeff_fast2<M>(C, vn, vs, dW, dE, q);
   else
-    c = make_float2(1.0f / one_den.x, 1.0f / one_den.y);
-  return make_float2(clamp_rd<M>(c.x), clamp_rd<M>(c.y));
+    return mk(coeff_ieee<M>(C.x, vn.x, vs.x, dW.x, dE.x, q), coeff_ieee<M>(C.y, vn.y, vs.y, dW.y, dE.y, q));
+}
+template <bool M, bool FAST>
+__device__ __forceinline__ float coeff1(float C, float vn, float vs, float dW, float dE, const SradQ &q) {
+  if constexpr (FAST) return coeff_fast1<M>(C, vn, vs, dW, dE, q);
+  else return coeff_ieee<M>(C, vn, vs, dW, dE, q);
+}
+template <bool FAST>
+__device__ __forceinline__ float2 update2(float2 C, float2 vn, float2 vs, float2 dW, float2 dE, float2 cv, float2 cs,
+                                          float2 ce, float lq) {
+  if constexpr (FAST) return update_fast2(C, vn, vs, dW, dE, cv, cs, ce, lq);
+  else
+    return mk(update_ieee(C.x, vn.x, vs.x, dW.x, dE.x, cv.x, cs.x, ce.x, lq),
+              update_ieee(C.y, vn.y, vs.y, dW.y, dE.y, cv.y, cs.y, ce.y, lq));
 }
 
-// CTAs per SM, each form at its best (16384^2 x 100): 5 (48 registers, a
-// small spill) for the IEEE forms (unmelded 169.6 -> 160.6 ms, melded 157.5 ->
-// 151.0) and the unmelded fast form (126.7 -> 121.1); the melded fast form
-// keeps the compiler's 63 registers and 4 CTAs (102.9 ms; bounded to 5: 105.5)
-template <bool M, bool FAST, bool PACK, bool IDX32>
-__global__ void __launch_bounds__(256, (FAST && M) ? 0 : 5) srad_sweep_kernel(SradParams P) {
-  const int lane = threadIdx.x & 31;
-  const int wcol = blockIdx.x * 8 + (threadIdx.x >> 5);   // warp column group
-  const int j = wcol * 30 + lane - 1;                      // this lane's column
-  const int jc = clampi(j, 0, P.cols - 1);
-  const bool out_lane = lane >= 1 && lane <= 30 && j < P.cols;
-  const int seg0 = blockIdx.y * P.rs;                      // first local own row (0-based)
-  if (seg0 >= P.tile_rows) return;
-  const int seg1 = min(seg0 + P.rs, P.tile_rows);
-  const float q0sqr = *P.q0;
-  const float q0den = q0sqr * (1.0f + q0sqr);
-  const int cols = P.cols;
-  const int gmax = P.R - 1;
-  // global row g -> pointer to its (clamped) row in the tile buffer
-  auto row = [&](int g) { return P.jin + size_t(clampi(g, 0, gmax) - P.r0 + 1) * cols; };
-  // R_B: the west/east neighbour of this lane at image borders and lane 31's
-  // east value (no lane to its right).
-  auto west_east = [&](const float *rp, float v, float &w, float &e) {   // rp -> (row, jc)
-    const float sw = __shfl_up_sync(0xffffffffu, v, 1);
-    const float se = __shfl_down_sync(0xffffffffu, v, 1);
-    if constexpr (!M) {
-      if (j == 0) {
-        DARM_ARM("srad.rb.west");
-        w = v;
-        e = se;
-      } else if (lane == 31 || j == cols - 1) {
-        DARM_ARM("srad.rb.east");
-        w = sw;
-        e = j >= cols - 1 ? v : rp[1];                     // j < cols - 1: jc + 1 is in the row
-      } else {
-        DARM_ARM("srad.rb.mid");
-        w = sw;
-        e = se;
-      }
+// One row of a thread: its 4 columns as two column pairs (the 16-byte load's
+// registers) and the halo value (lane 0: J(., c0-1); lane 31: J(., c0+128)).
+struct SradRow {
+  float2 a, b;
+  float h;
+};
+
+// R_B for one row: west / east neighbour of the thread's first / last column.
+template <bool M>
+__device__ __forceinline__ void west_east(const SradRow &r, int lane, float &w, float &e) {
+  const float sw = __shfl_up_sync(kFull, r.b.y, 1);
+  const float se = __shfl_down_sync(kFull, r.a.x, 1);
+  if constexpr (!M) {
+    if (lane == 0) {
+      DARM_IPDOM("srad.rb.w0");
+      w = r.h;
     } else {
-      const bool edge_e = lane == 31 || j >= cols - 1;
-      float ee = v;
-      if (lane == 31 && j < cols - 1) ee = rp[1];         // the only one-sided run
-      w = j == 0 ? v : sw;
-      e = edge_e ? ee : se;
+      DARM_IPDOM("srad.rb.w");
+      w = sw;
     }
-  };
-  const int g0 = P.r0 + seg0;
-  const bool roi_warp = P.roi_out && wcol >= P.roi_w0 && wcol < P.roi_w0 + P.roi_groups;
-  auto roi_row = [&](int g, float jn) {
-    if (roi_warp && g >= P.roi_r1 && g <= P.roi_r2) {
-      const bool in = out_lane && j >= P.roi_c1 && j <= P.roi_c2;
-      double s = in ? double(jn) : 0.0, s2 = in ? double(jn) * double(jn) : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      }
-      if (lane == 0) {
-        double *dst = P.roi_out + 2 * (size_t(g - P.roi_r1) * P.roi_groups + (wcol - P.roi_w0));
-        dst[0] = s;
-        dst[1] = s2;
-      }
-    }
-  };
-  // rows past the image clamp to its last row; the buffer holds rows up to glim
-  const int glim = min(gmax, P.r0 + P.tile_rows + 1);
-  auto rowc = [&](int g) { return row(min(g, glim)); };
-  // window at the segment start: rows g0-1 .. g0+3, c and west / east of row g0
-  float jm1 = row(g0 - 1)[jc], j0 = row(g0)[jc], jp1 = rowc(g0 + 1)[jc], jp2 = rowc(g0 + 2)[jc];
-  float jp3 = rowc(g0 + 3)[jc];
-  float w0, e0;
-  west_east(row(g0) + jc, j0, w0, e0);
-  float c0 = srad_coeff<M, FAST>(j0, jm1, jp1, w0, e0, q0sqr, q0den);
-  float *outp = P.jout + size_t(seg0 + 1) * cols + j;
-  const float2 z = f2(P.nz);
-  // Row addressing in the two-row loop (rows g+1, g+2 for lane 31's east
-  // values, g+4, g+5 for the prefetch): tiles under 2^31 elements use 32-bit
-  // element indices (clamp + multiply-add, one wide multiply-add for the
-  // address: 16384^2 x 100 IEEE melded 147.4 -> 135.2 ms, fast melded 101.3 ->
-  // 92.6); larger tiles slide 64-bit row pointers two rows per iteration
-  // (clamping through rowc for a tile's last iterations)
-  const size_t cs = size_t(cols);
-  const float *pg = row(g0) + jc;
-  const int off32 = (1 - P.r0) * cols + jc;                  // IDX32: row g's element index = g * cols + off32
-  int i = seg0;
-  // two rows (g, g+1) per iteration, their arithmetic in f32x2 pairs
-  // unrolled twice for the unmelded fast form only (108.7 -> 104.9 ms; the
-  // other forms lose: IEEE melded 135 -> 140, fast melded 93 -> 112 at 80
-  // registers) — each form at its best
-  constexpr int kUnroll = (FAST && !M) ? 2 : 1;
-#pragma unroll kUnroll
-  for (; i + 1 < seg1; i += 2) {
-    const int g = P.r0 + i;
-    const float *p1, *p2, *p4, *p5;
-    if constexpr (IDX32) {
-      // the tile buffer has < 2^31 elements: a 32-bit element index per row
-      // (clamp, multiply-add) and one wide multiply-add for the address
-      auto at = [&](int gg) { return P.jin + (min(gg, glim) * cols + off32); };
-      p1 = at(g + 1);
-      p2 = at(g + 2);
-      p4 = at(g + 4);
-      p5 = at(g + 5);
-    } else if (!(FAST && M) && g + 5 <= glim) {   // (no register room in the melded fast form)
-      p1 = pg + cs;
-      p2 = p1 + cs;
-      p4 = p2 + 2 * cs;
-      p5 = p4 + cs;
+    if (lane == 31) {
+      DARM_IPDOM("srad.rb.e31");
+      e = r.h;
     } else {
-      p1 = rowc(g + 1) + jc;
-      p2 = rowc(g + 2) + jc;
-      p4 = rowc(g + 4) + jc;
-      p5 = rowc(g + 5) + jc;
+      DARM_IPDOM("srad.rb.e");
+      e = se;
     }
-    if constexpr (!IDX32) pg += 2 * cs;
-    const float q4 = *p4, q5 = *p5;                         // next iteration's rows, in flight
-    float w1, e1, w2, e2;
-    west_east(p1, jp1, w1, e1);
-    west_east(p2, jp2, w2, e2);
-    const float2 cc = srad_coeff2<M, FAST, PACK>(make_float2(jp1, jp2), make_float2(j0, jp1), make_float2(jp2, jp3),
-                                           make_float2(w1, w2), make_float2(e1, e2), q0sqr, q0den, z);
-    const float c1 = (g + 1 <= gmax) ? cc.x : c0;           // c at the rows below (clamped at the bottom)
-    const float c2 = (g + 2 <= gmax) ? cc.y : c1;
-    float ce0 = __shfl_down_sync(0xffffffffu, c0, 1), ce1 = __shfl_down_sync(0xffffffffu, c1, 1);
-    if (j >= cols - 1) {
-      ce0 = c0;
-      ce1 = c1;
-    }
-    const float2 jv = make_float2(j0, jp1), cv = make_float2(c0, c1), cs = make_float2(c1, c2);
-    const float2 dN = sub2(make_float2(jm1, j0), jv), dS = sub2(make_float2(jp1, jp2), jv);
-    const float2 dW = sub2(make_float2(w0, w1), jv), dE = sub2(make_float2(e0, e1), jv);
-    const float2 ce = make_float2(ce0, ce1);
-    float2 jn;
-    if constexpr (!PACK) {
-      if constexpr (FAST) {
-        const float dx = __fmaf_rn(ce.x, dE.x, __fmaf_rn(cv.x, dW.x, __fmaf_rn(cs.x, dS.x, cv.x * dN.x)));
-        const float dy = __fmaf_rn(ce.y, dE.y, __fmaf_rn(cv.y, dW.y, __fmaf_rn(cs.y, dS.y, cv.y * dN.y)));
-        jn = make_float2(__fmaf_rn(P.lq, dx, jv.x), __fmaf_rn(P.lq, dy, jv.y));
-      } else {
-        const float dx = ((cv.x * dN.x + cs.x * dS.x) + cv.x * dW.x) + ce.x * dE.x;
-        const float dy = ((cv.y * dN.y + cs.y * dS.y) + cv.y * dW.y) + ce.y * dE.y;
-        jn = make_float2(jv.x + P.lq * dx, jv.y + P.lq * dy);
-      }
-    } else if constexpr (FAST) {
-      const float2 d = fma2(ce, dE, fma2(cv, dW, fma2(cs, dS, mul2(cv, dN))));
-      jn = fma2(f2(P.lq), d, jv);
-    } else {
-      const float2 d = add2(add2(add2(mulx(cv, dN, z), mulx(cs, dS, z)), mulx(cv, dW, z)), mulx(ce, dE, z));
-      jn = add2(jv, mulx(f2(P.lq), d, z));
-    }
-    if (out_lane) {
-      outp[0] = jn.x;
-      outp[cols] = jn.y;
-    }
-    outp += 2 * cols;
-    roi_row(g, jn.x);
-    roi_row(g + 1, jn.y);
-    // slide by two rows
-    jm1 = jp1;
-    j0 = jp2;
-    jp1 = jp3;
-    jp2 = q4;
-    jp3 = q5;
-    w0 = w2;
-    e0 = e2;
-    c0 = c2;
+  } else {
+    w = lane == 0 ? r.h : sw;
+    e = lane == 31 ? r.h : se;
   }
-  if (i < seg1) {   // an odd last row
+}
+
+// east c of the thread's last column: the next lane's first, or (lane 31) the
+// fifth column's.  R_B as above.
+template <bool M>
+__device__ __forceinline__ float east_c(float c_first, float c5, int lane) {
+  const float s = __shfl_down_sync(kFull, c_first, 1);
+  if constexpr (!M) {
+    float r;
+    if (lane == 31) {
+      DARM_IPDOM("srad.rb.c31");
+      r = c5;
+    } else {
+      DARM_IPDOM("srad.rb.c");
+      r = s;
+    }
+    return r;
+  } else {
+    return lane == 31 ? c5 : s;
+  }
+}
+
+// ROI partial of one output row (global row g): this lane's 4 values in column
+// order, then the warp butterfly; lane 0 writes.
+__device__ __forceinline__ void roi_row(const SradParams &P, int g, int wcol, int col, int lane, float2 ja,
+                                        float2 jb) {
+  const float jn[4] = {ja.x, ja.y, jb.x, jb.y};
+  double s = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = col + k;
+    const bool in = j >= P.roi_c1 && j <= P.roi_c2 && j < P.cols;
+    const double v = in ? double(jn[k]) : 0.0;
+    s += v;
+    s2 += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(kFull, s, o);
+    s2 += __shfl_xor_sync(kFull, s2, o);
+  }
+  if (lane == 0) {
+    double *dst = P.roi_out + 2 * (size_t(g - P.roi_r1) * P.roi_groups + (wcol - P.roi_w0));
+    dst[0] = s;
+    dst[1] = s2;
+  }
+}
+
+// Per-row derived state of the sweep: differences and c of the own columns.
+struct SradDiff {
+  float2 dWa, dWb, dEa, dEb;   // dW, dE of column pairs a = (0,1), b = (2,3)
+};
+
+// One warp's segment [seg0, seg1) of own rows: a CTA is one warp (every
+// branch that depends on the warp's position is then CTA-uniform, so ptxas
+// needs no WARPSYNC around the shuffles).  EDGE: this warp holds the image's
+// last column, whose east neighbour (J and c) is itself.
+// Row ring: rows of a warp's strip staged in shared memory by 1-D TMA bulk
+// copies (columns c0-4 .. c0+131: the own 128 and both halo columns), kSradStages
+// rows ahead of the register window, so a warp keeps ~8 rows of loads in
+// flight without holding registers for them (the sweep was bound by load
+// latency at 2 rows in flight: 55% issue, 50% DRAM).
+#ifndef DARM_SRAD_STAGES
+#define DARM_SRAD_STAGES 8
+#endif
+constexpr int kSradStages = DARM_SRAD_STAGES;   // a power of two
+constexpr int kSradRowF = kSradWarpCols + 8;    // floats per staged row
+struct SradRing {
+  float row[kSradStages][kSradRowF];
+  uint64_t bar[kSradStages];
+};
+
+template <bool M, bool FAST, bool EDGE>
+__device__ __forceinline__ void srad_segment(const SradParams &P, int seg0, int seg1, int wcol, int lane,
+                                             SradRing &ring) {
+  const int wc0 = wcol * kSradWarpCols;   // the warp's first column
+  const int col = wc0 + 4 * lane;
+  const int lcol = min(col, P.pitch - 4);   // stays inside the row (columns >= cols are never stored)
+  const int gmax = P.R - 1;
+  const int glim = min(gmax, P.r0 + P.tile_rows + 1);
+  const int hcol = lane == 0 ? max(wc0 - 1, 0) : min(wc0 + kSradWarpCols, P.cols - 1);
+  const bool hl = lane == 0 || lane == 31;
+  SradQ q;
+  q.q0sqr = *P.q0;
+  q.q0den = q.q0sqr * (1.0f + q.q0sqr);
+  q.nk1 = -16.0f * q.q0den;
+  q.nk2 = -16.0f * (q.q0sqr * q.q0sqr);
+  const size_t pitch = size_t(P.pitch);
+  auto rowp = [&](int g) { return P.jin + size_t(min(clampi(g, 0, gmax), glim) - P.r0 + 1) * pitch; };
+  auto last = [&](int k) { return EDGE && col + k == P.cols - 1; };
+  // dW / dE of a row (west / east neighbour values w, e of the thread's ends)
+  auto diffs = [&](const SradRow &r, float w, float e, SradDiff &d) {
+    const float2 mid = mk(r.a.y, r.b.x);                       // columns 1, 2
+    d.dWa = sub2(mk(w, r.a.x), r.a);
+    d.dWb = sub2(mid, r.b);
+    d.dEa = sub2(mid, r.a);
+    d.dEb = sub2(mk(r.b.y, e), r.b);
+    if constexpr (EDGE) {   // R_B: the image's last column (dE = 0)
+      if constexpr (!M) {
+        if (last(0)) { DARM_IPDOM("srad.rb.l0"); d.dEa.x = 0.0f; }
+        if (last(1)) { DARM_IPDOM("srad.rb.l1"); d.dEa.y = 0.0f; }
+        if (last(2)) { DARM_IPDOM("srad.rb.l2"); d.dEb.x = 0.0f; }
+        if (last(3)) { DARM_IPDOM("srad.rb.l3"); d.dEb.y = 0.0f; }
+      } else {
+        d.dEa = mk(last(0) ? 0.0f : d.dEa.x, last(1) ? 0.0f : d.dEa.y);
+        d.dEb = mk(last(2) ? 0.0f : d.dEb.x, last(3) ? 0.0f : d.dEb.y);
+      }
+    }
+  };
+  const bool roi_warp = P.roi_out && wcol >= P.roi_w0 && wcol < P.roi_w0 + P.roi_groups;
+
+  // c of the fifth column (c0 + 128) for 32 rows starting at g: lane l -> row g + l
+  // (five gathered loads per 32 rows instead of a fifth column per row)
+  const int x5 = min(wc0 + kSradWarpCols, P.cols - 1);
+  auto gather_c5 = [&](int g) {
+    const float *p = rowp(g + lane);
+    const float jc = __ldg(p + x5);
+    const float n = __ldg(rowp(g + lane - 1) + x5), s = __ldg(rowp(g + lane + 1) + x5);
+    const float w = __ldg(p + min(wc0 + kSradWarpCols - 1, P.cols - 1));
+    const float e = __ldg(p + min(wc0 + kSradWarpCols + 1, P.cols - 1));
+    float c = coeff1<M, FAST>(jc, jc - n, s - jc, w - jc, e - jc, q);
+    if (g + lane > gmax) c = 0.0f;   // rows below the image never reach a stored pixel
+    return c;
+  };
+
+  // ---- segment start: the ring holds rows g0-1, g0, ... (ring index k = row - (g0-1))
+  const int g0 = P.r0 + seg0;
+  const int kend = 5 + 2 * ((seg1 - seg0 + 1) / 2);   // rows the loop consumes
+  const int lo = max(wc0 - 4, 0), hi = min(wc0 + kSradWarpCols + 4, P.pitch);
+  const unsigned bytes = unsigned(hi - lo) * 4u;
+  const int soff = lo - (wc0 - 4);                       // 0, or 4 for the first strip
+  auto issue = [&](int k) {                              // lane 0
+    const int st = k & (kSradStages - 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the warp's reads of this stage come first
+    mbar_expect_tx(&ring.bar[st], bytes);
+    tma_load_1d(&ring.row[st][soff], rowp(g0 - 1 + k) + lo, bytes, &ring.bar[st]);
+  };
+  if (lane == 0) {
+#pragma unroll 1
+    for (int st = 0; st < kSradStages; ++st) mbar_init(&ring.bar[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll 1
+    for (int k = 0; k < min(kSradStages, kend); ++k) issue(k);
+  }
+  __syncwarp();
+  int kc = 0;   // the next ring index to consume
+  const int io = lcol - (wc0 - 4), ih = hcol - (wc0 - 4);
+  auto load_next = [&](SradRow &r) {
+    const int st = kc & (kSradStages - 1);
+    mbar_wait(&ring.bar[st], unsigned(kc / kSradStages) & 1u);
+    const float4 x = *reinterpret_cast<const float4 *>(&ring.row[st][io]);
+    r.a = mk(x.x, x.y);
+    r.b = mk(x.z, x.w);
+    r.h = hl ? ring.row[st][ih] : 0.0f;
+    __syncwarp();
+    if (lane == 0 && kc + kSradStages < kend) issue(kc + kSradStages);
+    ++kc;
+  };
+  SradRow jm, j0, j1, j2, j3;
+  load_next(jm);
+  load_next(j0);
+  load_next(j1);
+  load_next(j2);
+  load_next(j3);
+  float w0, e0;
+  west_east<M>(j0, lane, w0, e0);
+  SradDiff d0;
+  diffs(j0, w0, e0, d0);
+  float2 vn0a = sub2(j0.a, jm.a), vn0b = sub2(j0.b, jm.b);     // J(g0) - J(g0-1)
+  float2 vs0a = sub2(j1.a, j0.a), vs0b = sub2(j1.b, j0.b);     // J(g0+1) - J(g0)
+  float2 c0a = coeff2<M, FAST>(j0.a, vn0a, vs0a, d0.dWa, d0.dEa, q);
+  float2 c0b = coeff2<M, FAST>(j0.b, vn0b, vs0b, d0.dWb, d0.dEb, q);
+  float c5v = gather_c5(g0);
+  float *outp = P.jout + size_t(seg0 + 1) * pitch + col;
+
+  // One output row g: c(g+1) from rows g .. g+2 (jc = row g+1, jn = row g+2),
+  // then J'(g).  State in: vn/vs of row g, its c and differences; out: row g+1's.
+  auto step = [&](int i, const SradRow &jc, const SradRow &jn, float2 &vna, float2 &vnb, float2 &vsa,
+                  float2 &vsb, float2 &ca, float2 &cb, SradDiff &d, const SradRow &jg) {
     const int g = P.r0 + i;
     float w1, e1;
-    west_east(rowc(g + 1) + jc, jp1, w1, e1);
-    const float c1 = (g + 1 <= gmax) ? srad_coeff<M, FAST>(jp1, j0, jp2, w1, e1, q0sqr, q0den) : c0;
-    float ce = __shfl_down_sync(0xffffffffu, c0, 1);
-    if (j >= cols - 1) ce = c0;
-    const float dN = jm1 - j0, dS = jp1 - j0, dW = w0 - j0, dE = e0 - j0;
-    float d, jn;
-    if constexpr (FAST) {
-      d = __fmaf_rn(ce, dE, __fmaf_rn(c0, dW, __fmaf_rn(c1, dS, c0 * dN)));
-      jn = __fmaf_rn(P.lq, d, j0);
-    } else {
-      d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE;
-      jn = j0 + P.lq * d;
+    west_east<M>(jc, lane, w1, e1);
+    SradDiff d1;
+    diffs(jc, w1, e1, d1);
+    const float2 vs1a = sub2(jn.a, jc.a), vs1b = sub2(jn.b, jc.b);   // J(g+2) - J(g+1)
+    float2 c1a = coeff2<M, FAST>(jc.a, vsa, vs1a, d1.dWa, d1.dEa, q);
+    float2 c1b = coeff2<M, FAST>(jc.b, vsb, vs1b, d1.dWb, d1.dEb, q);
+    if (g + 1 > gmax) {   // below the image's last row c is the last row's (warp-uniform)
+      c1a = ca;
+      c1b = cb;
     }
-    if (out_lane) *outp = jn;
-    roi_row(g, jn);
+    // east c of row g: in-thread neighbours, the next lane, or the fifth column
+    const float c5 = __shfl_sync(kFull, c5v, (i - seg0) & 31);
+    const float cE = east_c<M>(ca.x, c5, lane);
+    float2 cea = mk(ca.y, cb.x), ceb = mk(cb.y, cE);
+    if constexpr (EDGE) {   // R_B: the image's last column (its own c)
+      if constexpr (!M) {
+        if (last(0)) { DARM_IPDOM("srad.rb.m0"); cea.x = ca.x; }
+        if (last(1)) { DARM_IPDOM("srad.rb.m1"); cea.y = ca.y; }
+        if (last(2)) { DARM_IPDOM("srad.rb.m2"); ceb.x = cb.x; }
+        if (last(3)) { DARM_IPDOM("srad.rb.m3"); ceb.y = cb.y; }
+      } else {
+        cea = mk(last(0) ? ca.x : cea.x, last(1) ? ca.y : cea.y);
+        ceb = mk(last(2) ? cb.x : ceb.x, last(3) ? cb.y : ceb.y);
+      }
+    }
+    const float2 ja = update2<FAST>(jg.a, vna, vsa, d.dWa, d.dEa, ca, c1a, cea, P.lq);
+    const float2 jb = update2<FAST>(jg.b, vnb, vsb, d.dWb, d.dEb, cb, c1b, ceb, P.lq);
+    if (i < seg1) {
+      if constexpr (!EDGE) {
+        *reinterpret_cast<float4 *>(outp) = make_float4(ja.x, ja.y, jb.x, jb.y);
+      } else {
+        const float v[4] = {ja.x, ja.y, jb.x, jb.y};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (col + k < P.cols) outp[k] = v[k];
+      }
+      if (roi_warp && g >= P.roi_r1 && g <= P.roi_r2) roi_row(P, g, wcol, col, lane, ja, jb);
+    }
+    outp += pitch;
+    if (((i - seg0) & 31) == 31) c5v = gather_c5(g + 1);   // the next 32 rows' fifth column (warp-uniform)
+    vna = vsa;
+    vnb = vsb;
+    vsa = vs1a;
+    vsb = vs1b;
+    ca = c1a;
+    cb = c1b;
+    d = d1;
+  };
+  // two rows per iteration: rows g .. g+3 resident, g+4 and g+5 in flight
+  // (every register rotates with period 2, so unrolling twice renames them)
+#pragma unroll 2
+  for (int i = seg0; i < seg1; i += 2) {
+    SradRow j4, j5;
+    load_next(j4);
+    load_next(j5);
+    step(i, j1, j2, vn0a, vn0b, vs0a, vs0b, c0a, c0b, d0, j0);
+    step(i + 1, j2, j3, vn0a, vn0b, vs0a, vs0b, c0a, c0b, d0, j1);
+    j0 = j2;
+    j1 = j3;
+    j2 = j4;
+    j3 = j5;
   }
+}
+
+// resident CTAs (one warp each) per SM the sweep is built for (register cap)
+#ifndef DARM_SRAD_MINB
+#define DARM_SRAD_MINB 20
+#endif
+template <bool M, bool FAST>
+__global__ void __launch_bounds__(32, DARM_SRAD_MINB) srad_sweep_kernel(SradParams P) {
+  const int lane = threadIdx.x;
+  const int wcol = blockIdx.x;
+  int seg0, seg1;
+  if (int(blockIdx.y) < P.nseg0) {
+    seg0 = P.lo0 + int(blockIdx.y) * P.rs;
+    seg1 = min(seg0 + P.rs, P.hi0);
+  } else {
+    seg0 = P.lo1 + (int(blockIdx.y) - P.nseg0) * P.rs;
+    seg1 = min(seg0 + P.rs, P.hi1);
+  }
+  if (seg0 >= seg1) return;
+  __shared__ __align__(128) SradRing ring;
+  if ((wcol + 1) * kSradWarpCols >= P.cols)
+    srad_segment<M, FAST, true>(P, seg0, seg1, wcol, lane, ring);
+  else
+    srad_segment<M, FAST, false>(P, seg0, seg1, wcol, lane, ring);
 }
 
 // q0sqr from the ROI partials: rows in order, groups in order, fp64.
-__global__ void srad_q0_kernel(const double *roi, int rows, int groups, double npix, float *q0) {
+// `parts` holds one partial buffer per source (a multi-GPU run reads the
+// owning rank's buffer for every ROI row, `owner[row]`); nparts = 1 for a
+// single buffer.
+__global__ void srad_q0_kernel(const double *const *parts, const int *owner, const double *roi, int rows,
+                               int groups, double npix, float *q0) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0.0, s2 = 0.0;
-  for (int r = 0; r < rows; ++r)
+  for (int r = 0; r < rows; ++r) {
+    const double *src = parts ? parts[owner[r]] : roi;
     for (int g = 0; g < groups; ++g) {
-      s += roi[2 * (size_t(r) * groups + g)];
-      s2 += roi[2 * (size_t(r) * groups + g) + 1];
+      s += src[2 * (size_t(r) * groups + g)];
+      s2 += src[2 * (size_t(r) * groups + g) + 1];
     }
+  }
   const double mean = s / npix;
   const double var = s2 / npix - mean * mean;
   *q0 = float(var / (mean * mean));
 }
 
 // ROI partials of an existing image (the first iteration's statistics).
-__global__ void srad_roi_kernel(const float *jin, int cols, int r0, int tile_rows, int roi_r1, int roi_r2,
+__global__ void srad_roi_kernel(const float *jin, int cols, int pitch, int r0, int tile_rows, int roi_r1, int roi_r2,
                                 int roi_c1, int roi_c2, int roi_w0, int roi_groups, double *roi_out) {
   const int lane = threadIdx.x & 31;
   const int wcol = roi_w0 + blockIdx.x * 8 + (threadIdx.x >> 5);
   if (wcol >= roi_w0 + roi_groups) return;
-  const int j = wcol * 30 + lane - 1;
-  const bool in = lane >= 1 && lane <= 30 && j < cols && j >= roi_c1 && j <= roi_c2;
+  const int col = wcol * kSradWarpCols + 4 * lane;
   for (int g = max(roi_r1, r0); g <= min(roi_r2, r0 + tile_rows - 1); ++g) {
-    const float v = in ? jin[size_t(g - r0 + 1) * cols + j] : 0.f;
-    double s = in ? double(v) : 0.0, s2 = in ? double(v) * double(v) : 0.0;
+    const float *p = jin + size_t(g - r0 + 1) * size_t(pitch);
+    double s = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = col + k;
+      const bool in = j >= roi_c1 && j <= roi_c2 && j < cols;
+      const double v = in ? double(p[j]) : 0.0;
+      s += v;
+      s2 += v * v;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      s += __shfl_xor_sync(kFull, s, o);
+      s2 += __shfl_xor_sync(kFull, s2, o);
     }
     if (lane == 0) {
       double *dst = roi_out + 2 * (size_t(g - roi_r1) * roi_groups + (wcol - roi_w0));
@@ -424,41 +558,60 @@ SradRoi srad_roi_layout(int cols, int r1, int r2, int c1, int c2) {
   R.r2 = r2;
   R.c1 = c1;
   R.c2 = c2;
-  // warp column groups covering output columns [c1, c2]: group w covers 30w .. 30w+29
-  R.w0 = c1 / 30;
-  R.groups = c2 / 30 - R.w0 + 1;
+  // warp column groups covering output columns [c1, c2]: group w covers 128w .. 128w+127
+  R.w0 = c1 / kSradWarpCols;
+  R.groups = c2 / kSradWarpCols - R.w0 + 1;
   R.rows = r2 - r1 + 1;
   (void)cols;
   return R;
 }
 
-cudaError_t launch_srad_roi(const float *jin, int cols, int r0, int tile_rows, const SradRoi &roi, double *roi_out,
-                            cudaStream_t s) {
+int srad_pitch(int cols) { return (cols + 3) & ~3; }
+
+cudaError_t launch_srad_roi(const float *jin, int cols, int pitch, int r0, int tile_rows, const SradRoi &roi,
+                            double *roi_out, cudaStream_t s) {
   const int grid = (roi.groups + 7) / 8;
-  srad_roi_kernel<<<grid, 256, 0, s>>>(jin, cols, r0, tile_rows, roi.r1, roi.r2, roi.c1, roi.c2, roi.w0,
+  srad_roi_kernel<<<grid, 256, 0, s>>>(jin, cols, pitch, r0, tile_rows, roi.r1, roi.r2, roi.c1, roi.c2, roi.w0,
                                        roi.groups, roi_out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s) {
+cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s,
+                           const double *const *parts, const int *owner) {
   const double npix = double(roi.rows) * double(roi.c2 - roi.c1 + 1);
-  srad_q0_kernel<<<1, 32, 0, s>>>(roi_in, roi.rows, roi.groups, npix, q0);
+  srad_q0_kernel<<<1, 32, 0, s>>>(parts, owner, roi_in, roi.rows, roi.groups, npix, q0);
   return cudaGetLastError();
 }
 
+template <bool M, bool FAST>
+static int srad_resident_ctas() {
+  static int n = [] {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, srad_sweep_kernel<M, FAST>, 32, 0);
+    return sms * (per > 0 ? per : 1);
+  }();
+  return n;
+}
+
 cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const float *q0, double *roi_out,
-                              int cols, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
-                              cudaStream_t s) {
+                              int cols, int pitch, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
+                              const SradRange &range, cudaStream_t s) {
   SradParams P;
   P.jin = jin;
   P.jout = jout;
   P.q0 = q0;
   P.roi_out = roi_out;
   P.cols = cols;
+  P.pitch = pitch;
   P.tile_rows = tile_rows;
   P.r0 = r0;
   P.R = R;
-  P.rs = 128;
+  P.lo0 = range.lo0;
+  P.hi0 = range.hi0;
+  P.lo1 = range.lo1;
+  P.hi1 = range.hi1;
   P.lq = 0.25f * lambda;
   P.nz = -0.0f;
   P.roi_r1 = roi.r1;
@@ -467,25 +620,28 @@ cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const 
   P.roi_c2 = roi.c2;
   P.roi_w0 = roi.w0;
   P.roi_groups = roi.groups;
-  const int wgroups = (cols + 29) / 30;
-  dim3 grid((wgroups + 7) / 8, (tile_rows + P.rs - 1) / P.rs);
+  const int n0 = max(0, range.hi0 - range.lo0), n1 = max(0, range.hi1 - range.lo1);
+  if (n0 + n1 == 0) return cudaSuccess;
   const bool fast = variant & 0x100;   // DARM_FAST_MATH
-  // f32x2 pairs only where they pay (measured, 16384^2 x 100): the melded
-  // fast path (105.2 -> 101.8 ms).  The unmelded form's per-pixel R_D branches
-  // split every pair (126 -> 147 ms) and the IEEE path's scalar divisions
-  // around packed products lose too (157 -> 184 ms): both run two rows per
-  // iteration in scalar code.
-  // 32-bit element indices while the tile buffer (tile_rows + 3 rows) has
-  // fewer than 2^31 elements (16384^2 on one GPU: 2.7e8)
-  const bool idx32 = int64_t(tile_rows + 3) * cols < (int64_t(1) << 31) && !(variant & 0x200);   // DARM_SRAD_INDEX64
-#define SRAD_L(Mm, F, PK)                                                                                   \
-  (idx32 ? srad_sweep_kernel<Mm, F, PK, true><<<grid, 256, 0, s>>>(P)                                    \
-         : srad_sweep_kernel<Mm, F, PK, false><<<grid, 256, 0, s>>>(P))
-  if (variant & 1)
-    fast ? SRAD_L(true, true, true) : SRAD_L(true, false, false);
+  const bool melded = variant & 1;
+  const int resident = melded ? (fast ? srad_resident_ctas<true, true>() : srad_resident_ctas<true, false>())
+                              : (fast ? srad_resident_ctas<false, true>() : srad_resident_ctas<false, false>());
+  const int gx = (cols + kSradWarpCols - 1) / kSradWarpCols;   // one warp (CTA) per 128 columns
+  // Segments: one wave of resident CTAs when the rows allow (every warp one
+  // long segment; the 5-row window start is re-read per segment), at least
+  // 32 rows per segment.
+  const int want_y = max(1, resident / gx);
+  int rs = (n0 + n1 + want_y - 1) / want_y;
+  rs = max(32, rs);
+  P.rs = rs;
+  P.nseg0 = (n0 + rs - 1) / rs;
+  const int nseg1 = (n1 + rs - 1) / rs;
+  dim3 grid(gx, P.nseg0 + nseg1);
+  if (melded)
+    fast ? srad_sweep_kernel<true, true><<<grid, 32, 0, s>>>(P) : srad_sweep_kernel<true, false><<<grid, 32, 0, s>>>(P);
   else
-    fast ? SRAD_L(false, true, false) : SRAD_L(false, false, false);
-#undef SRAD_L
+    fast ? srad_sweep_kernel<false, true><<<grid, 32, 0, s>>>(P)
+         : srad_sweep_kernel<false, false><<<grid, 32, 0, s>>>(P);
   return cudaGetLastError();
 }
 

@@ -3,15 +3,26 @@
 One process per GPU (torch.distributed); rank k owns image rows
 [r0_k, r0_k + rows_k).  Each tile buffer holds its rows at local rows
 1..rows_k plus one halo row above (local 0) and two below (local rows_k+1,
-rows_k+2) — the fused sweep kernel needs J(i-1) .. J(i+2).  Per iteration:
+rows_k+2) — the fused sweep kernel needs J(i-1) .. J(i+2); rows are
+`darm.srad_pitch(cols)` floats (16-byte rows).  Per iteration:
 
-  1. halo exchange (the path's one real exchange step): rank k sends its last
-     own row down to k+1 and its first two own rows up to k-1
-     (torch.distributed P2P: NCCL over NVLink on GPUs, gloo in CPU tests);
-  2. all-reduce (sum) of the ROI partial-sum buffer: every entry is written by
+  1. all-reduce (sum) of the ROI partial-sum buffer: every entry is written by
      exactly one rank (the owner of that ROI row), so the sum is exact and
      every rank gets the same q0sqr;
-  3. darm_gpu_srad_tile_step (C-ABI): q0sqr + the fused sweep J -> J'.
+  2. the halo exchange (the path's one real exchange step) is POSTED: rank k
+     sends its last own row down to k+1 and its first two own rows up to k-1
+     (torch.distributed P2P: NCCL over NVLink on GPUs, gloo in CPU tests);
+  3. while it is in flight, the interior rows (which read no halo row) run:
+     darm_gpu_srad_tile_step(part=DARM_SRAD_INTERIOR_ROWS) — q0sqr + the fused
+     sweep J -> J' on rows 2 .. rows_k-2;
+  4. the exchange is waited for (NCCL: the compute stream waits on the
+     communication stream, no host sync) and the edge rows run
+     (part=DARM_SRAD_EDGE_ROWS).
+
+This is the NCCL/torch.distributed transport.  The peer-memory transport
+(paper_2107_05681_b200.srad_peer: ranks read their halos straight from the
+neighbours' tiles over NVLink, the whole iteration loop one CUDA graph) is
+the B200 product path; this one is its baseline and the CPU-testable spec.
 
 The tile-level kernels are injected (``kernels``), so the exchange logic is
 exercised on CPU with the oracle's tile kernels in tests/test_srad.py; the
@@ -47,9 +58,9 @@ class GpuTileKernels:
     def roi(self, tile, cols, tile_rows, r0, rows, roi, roi_out):
         darm.srad_tile_roi(tile, cols, tile_rows, r0, rows, roi, roi_out, self.stream)
 
-    def step(self, tin, tout, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0):
+    def step(self, tin, tout, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0, part=0):
         darm.srad_tile_step(self.variant, tin, tout, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0,
-                            self.stream)
+                            self.stream, part)
 
 
 class SradTiles:
@@ -67,7 +78,8 @@ class SradTiles:
         self.r0, self.n = split_rows(rows, self.world)[self.rank]
         self.device = device if device is not None else torch.device("cpu")
         self.kernels = kernels if kernels is not None else GpuTileKernels(variant)
-        shape = (self.n + 3, cols)
+        self.pitch = darm.srad_pitch(cols)
+        shape = (self.n + 3, self.pitch)
         self.tin = torch.zeros(shape, dtype=torch.float32, device=self.device)
         self.tout = torch.zeros(shape, dtype=torch.float32, device=self.device)
         words = darm.srad_roi_words(cols, self.roi)
@@ -79,18 +91,21 @@ class SradTiles:
     def load(self, image) -> None:
         """Copy this rank's rows of the full image (or the tile rows) in."""
         if image.shape[0] == self.rows:
-            self.tin[1:self.n + 1].copy_(image[self.r0:self.r0 + self.n])
+            self.tin[1:self.n + 1, :self.cols].copy_(image[self.r0:self.r0 + self.n])
         else:
-            self.tin[1:self.n + 1].copy_(image)
+            self.tin[1:self.n + 1, :self.cols].copy_(image)
         self.kernels.roi(self.tin, self.cols, self.n, self.r0, self.rows, self.roi, self.roi_in)
 
     def tile(self):
-        return self.tin[1:self.n + 1]
+        return self.tin[1:self.n + 1, :self.cols]
 
     # ---------------------------------------------------------------- exchange
-    def exchange_halos(self) -> None:
+    def post_halos(self):
+        """Start the halo exchange; returns a finish() that lands the halo rows
+        (NCCL: recv straight into the tile rows, the compute stream waits on
+        the communication stream; gloo: host-staged, copied in on finish)."""
         if self.world == 1:
-            return
+            return lambda: None
         d = self.dist
         # gloo moves host buffers only (NCCL moves device memory directly)
         stage = self.device.type == "cuda" and d.get_backend() == "gloo"
@@ -99,39 +114,52 @@ class SradTiles:
         up, down = self.rank - 1, self.rank + 1
         top = bottom = None
         if up >= 0:
-            top = self.halo_top.cpu() if stage else self.halo_top
+            top = self.halo_top.cpu() if stage else self.tin[0:1]
             ops.append(d.P2POp(d.isend, to_wire(self.tin[1:3]), up))
             ops.append(d.P2POp(d.irecv, top, up))
         if down < self.world:
-            bottom = self.halo_bottom.cpu() if stage else self.halo_bottom
+            bottom = self.halo_bottom.cpu() if stage else self.tin[self.n + 1:self.n + 3]
             ops.append(d.P2POp(d.isend, to_wire(self.tin[self.n:self.n + 1]), down))
             ops.append(d.P2POp(d.irecv, bottom, down))
-        for req in d.batch_isend_irecv(ops):
-            req.wait()
-        if up >= 0:
-            self.tin[0:1].copy_(top)
-        if down < self.world:
-            self.tin[self.n + 1:self.n + 3].copy_(bottom)
+        reqs = d.batch_isend_irecv(ops)
+
+        def finish():
+            for req in reqs:
+                req.wait()
+            if stage:
+                if up >= 0:
+                    self.tin[0:1].copy_(top)
+                if down < self.world:
+                    self.tin[self.n + 1:self.n + 3].copy_(bottom)
+        return finish
+
+    def exchange_halos(self) -> None:
+        self.post_halos()()
 
     @property
     def halo_top(self):
         if not hasattr(self, "_ht"):
-            self._ht = self.torch.empty((1, self.cols), dtype=self.torch.float32, device=self.device)
+            self._ht = self.torch.empty((1, self.pitch), dtype=self.torch.float32, device=self.device)
         return self._ht
 
     @property
     def halo_bottom(self):
         if not hasattr(self, "_hb"):
-            self._hb = self.torch.empty((2, self.cols), dtype=self.torch.float32, device=self.device)
+            self._hb = self.torch.empty((2, self.pitch), dtype=self.torch.float32, device=self.device)
         return self._hb
 
     # ---------------------------------------------------------------- iterate
     def step(self) -> None:
-        self.exchange_halos()
-        if self.world > 1:
+        args = (self.tin, self.tout, self.cols, self.n, self.r0, self.rows, self.lam, self.roi, self.roi_in,
+                self.roi_out, self.q0)
+        if self.world == 1:
+            self.kernels.step(*args, part=darm.SRAD_ALL_ROWS)
+        else:
             self.dist.all_reduce(self.roi_in, op=self.dist.ReduceOp.SUM)
-        self.kernels.step(self.tin, self.tout, self.cols, self.n, self.r0, self.rows, self.lam, self.roi,
-                          self.roi_in, self.roi_out, self.q0)
+            finish = self.post_halos()
+            self.kernels.step(*args, part=darm.SRAD_INTERIOR_ROWS)   # overlaps the halo transfer
+            finish()
+            self.kernels.step(*args, part=darm.SRAD_EDGE_ROWS)
         self.tin, self.tout = self.tout, self.tin
         self.roi_in, self.roi_out = self.roi_out, self.roi_in
 

@@ -11,8 +11,8 @@ import torch
 
 def _roi_layout(roi):
     r1, r2, c1, c2 = roi
-    w0 = c1 // 30
-    return r1, r2, c1, c2, w0, c2 // 30 - w0 + 1
+    w0 = c1 // 128
+    return r1, r2, c1, c2, w0, c2 // 128 - w0 + 1
 
 
 def roi_partials_rows(img_rows, g_of_row, cols, roi, out):
@@ -24,11 +24,12 @@ def roi_partials_rows(img_rows, g_of_row, cols, roi, out):
         if g < r1 or g > r2:
             continue
         for w in range(w0, w0 + groups):
-            j = w * 30 + lanes - 1
-            inn = (lanes >= 1) & (lanes <= 30) & (j < cols) & (j >= c1) & (j <= c2)
-            v = np.where(inn, row[np.clip(j, 0, cols - 1)].astype(np.float64), 0.0)
-            a, b = v.copy(), v * v
-            b[~inn] = 0.0
+            a, b = np.zeros(32), np.zeros(32)
+            for k in range(4):   # each lane's 4 columns in order
+                j = w * 128 + 4 * lanes + k
+                inn = (j < cols) & (j >= c1) & (j <= c2)
+                v = np.where(inn, row[np.clip(j, 0, cols - 1)].astype(np.float64), 0.0)
+                a, b = a + v, b + v * v
             for o in (16, 8, 4, 2, 1):
                 a, b = a + a[lanes ^ o], b + b[lanes ^ o]
             out[g - r1, w - w0, 0] = a[0]
@@ -66,14 +67,20 @@ class NumpyTileKernels:
     """Drop-in for GpuTileKernels on CPU torch tensors."""
 
     def roi(self, tile, cols, tile_rows, r0, rows, roi, roi_out):
-        t = tile.numpy()
+        t = tile.numpy()[:, :cols]
         out = np.zeros(roi_out.numel(), dtype=np.float64)
         roi_partials_rows([t[i + 1] for i in range(tile_rows)], [r0 + i for i in range(tile_rows)], cols, roi, out)
         roi_out.copy_(torch.from_numpy(out))
 
-    def step(self, tin, tout, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0):
+    def step(self, tin, tout, cols, tile_rows, r0, rows, lam, roi, roi_in, roi_out, q0, part=0):
         f = np.float32
-        T = tin.numpy()
+        if part == 2:   # DARM_SRAD_EDGE_ROWS: rows 0 and n-2, n-1 (own, 0-based); q0 from the interior call
+            todo = [0] + list(range(max(1, tile_rows - 2), tile_rows)) if tile_rows > 3 else []
+        elif part == 1:   # DARM_SRAD_INTERIOR_ROWS
+            todo = list(range(1, tile_rows - 2)) if tile_rows > 3 else list(range(tile_rows))
+        else:
+            todo = list(range(tile_rows))
+        T = tin.numpy()[:, :cols]
         q0sqr = q0_from_partials(roi_in.numpy(), roi)
         q0den = f(q0sqr * (f(1.0) + q0sqr))
         gmax = rows - 1
@@ -89,9 +96,9 @@ class NumpyTileKernels:
             return coeff(jc, row(g - 1), row(g + 1), jc[jw], jc[je], q0sqr, q0den)
 
         lq = f(f(0.25) * f(lam))
-        out = np.zeros(roi_out.numel(), dtype=np.float64)
+        out = roi_out.numpy().copy() if part == 2 else np.zeros(roi_out.numel(), dtype=np.float64)
         newrows = []
-        for i in range(tile_rows):
+        for i in todo:
             g = r0 + i
             jc = row(g)
             c0 = c_of(g)
@@ -100,7 +107,7 @@ class NumpyTileKernels:
             dN, dS, dW, dE = row(g - 1) - jc, row(g + 1) - jc, jc[jw] - jc, jc[je] - jc
             d = ((c0 * dN + c1 * dS) + c0 * dW) + ce * dE
             jn = (jc + lq * d).astype(np.float32)
-            tout.numpy()[i + 1] = jn
+            tout.numpy()[i + 1, :cols] = jn
             newrows.append(jn)
-        roi_partials_rows(newrows, [r0 + i for i in range(tile_rows)], cols, roi, out)
+        roi_partials_rows(newrows, [r0 + i for i in todo], cols, roi, out)
         roi_out.copy_(torch.from_numpy(out))

@@ -275,16 +275,3 @@ def test_gpu_fast_math_config5(restatement):
     torch.cuda.synchronize()
     rel = float(((a - b).abs() / a.abs()).max())
     assert rel <= 1e-5, rel
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("fast", [False, True])
-def test_gpu_index64_path_identical(fast):
-    """Tiles of 2^31 or more elements address rows with 64-bit pointers; the
-    forced path (DARM_SRAD_INDEX64) gives the 32-bit path's bits, both forms."""
-    j0 = image(300, 257, 11)
-    for v in (0, 1):
-        a, b = j0.copy(), j0.copy()
-        darm.srad(a, 9, 0.5, (10, 200, 3, 250), v, fast=fast)
-        darm.srad(b, 9, 0.5, (10, 200, 3, 250), v | darm.SRAD_INDEX64, fast=fast)
-        assert (a.view(np.int32) == b.view(np.int32)).all(), (v, fast)
