@@ -98,11 +98,13 @@ SradRoi srad_roi_layout(int cols, int r1, int r2, int c1, int c2);
 int srad_pitch(int cols);   // row pitch (floats) of the library's own buffers: a multiple of 4
 cudaError_t launch_srad_roi(const float *jin, int cols, int pitch, int r0, int tile_rows, const SradRoi &roi,
                             double *roi_out, cudaStream_t s);
-// parts / owner: per ROI row, the partial buffer of the rank owning it (null: roi_in alone)
-cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s,
-                           const double *const *parts = nullptr, const int *owner = nullptr);
-cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const float *q0, double *roi_out,
-                              int cols, int pitch, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
-                              const SradRange &range, cudaStream_t s);
+// One SRAD iteration over `range` of a tile: every warp derives q0sqr from the
+// ROI partials of J (roi_in; or, multi-GPU, roi_parts[roi_owner[row]] per ROI
+// row), computes J -> J' and the ROI partials of J' (roi_out, may be null);
+// q0_out (optional) receives q0sqr.
+cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const double *roi_in, float *q0_out,
+                              double *roi_out, int cols, int pitch, int tile_rows, int r0, int R, float lambda,
+                              const SradRoi &roi, const SradRange &range, cudaStream_t s,
+                              const double *const *roi_parts = nullptr, const int *roi_owner = nullptr);
 
 }  // namespace darm_gpu

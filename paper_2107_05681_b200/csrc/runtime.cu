@@ -785,7 +785,6 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
     auto *b1 = static_cast<float *>(slot(st, 1, buf));
     auto *ctl = static_cast<char *>(slot(st, 2, 2 * roi_bytes + 256));
     double *roiA = reinterpret_cast<double *>(ctl + 256), *roiB = roiA + roi_bytes / 8;
-    float *q0 = reinterpret_cast<float *>(ctl);
     Timeline tl(s, stats != nullptr);
     tl.mark(0);
     if (pitch != cols) {   // defined pad columns (never stored to the image, but read as neighbours' lanes)
@@ -804,11 +803,9 @@ int darm_gpu_srad(int variant, float *j, int64_t rows, int64_t cols, int iters, 
       float *in = b0, *out = b1;
       double *ri = roiA, *ro = roiB;
       for (int t = 0; t < it && e == cudaSuccess; ++t) {
-        e = launch_srad_q0(ri, R, q0, cs);
-        if (e == cudaSuccess)
-          e = launch_srad_sweep(variant, in, out, q0, ro, int(cols), pitch, int(rows), 0, int(rows), lambda, R, all,
-                                cs);
-        *launches += 2;
+        e = launch_srad_sweep(variant, in, out, ri, nullptr, ro, int(cols), pitch, int(rows), 0, int(rows), lambda, R,
+                              all, cs);
+        ++*launches;
         std::swap(in, out);
         std::swap(ri, ro);
       }
@@ -882,13 +879,11 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, 
     device_state(nullptr);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const SradRoi R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
-    if (part != DARM_SRAD_EDGE_ROWS) {   // the first (or only) launch of the iteration: q0sqr
-      DARM_CUDA(launch_srad_q0(roi_in, R, q0_scratch, s));
-      if (roi_out) DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double), s));
-    }
-    DARM_CUDA(launch_srad_sweep(variant, tile_in, tile_out, q0_scratch, roi_out, int(cols), int(pitch),
-                                int(tile_rows), int(r0), int(rows), lambda, R, srad_part_range(part, int(tile_rows)),
-                                s));
+    if (part != DARM_SRAD_EDGE_ROWS && roi_out)   // the first (or only) launch of the iteration
+      DARM_CUDA(cudaMemsetAsync(roi_out, 0, size_t(R.rows) * R.groups * 2 * sizeof(double), s));
+    DARM_CUDA(launch_srad_sweep(variant, tile_in, tile_out, roi_in, part != DARM_SRAD_EDGE_ROWS ? q0_scratch : nullptr,
+                                roi_out, int(cols), int(pitch), int(tile_rows), int(r0), int(rows), lambda, R,
+                                srad_part_range(part, int(tile_rows)), s));
   });
 }
 

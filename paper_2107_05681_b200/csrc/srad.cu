@@ -34,7 +34,8 @@
 // ROI statistics are reduced deterministically: per ROI row and 128-column
 // warp group, each lane sums its 4 in-ROI values of J' in fp64 in column
 // order, then a 32-lane xor butterfly; lane 0 writes one partial per (row,
-// group); srad_q0_kernel folds the partials rows-then-groups in order.  For
+// group); every warp folds the partials rows-then-groups in order at its start
+// (srad_q0_warp: lanes load, the sum runs in index order).  For
 // row-tiled multi-GPU runs every partial is written by the one rank owning
 // its row.
 //
@@ -54,7 +55,11 @@ constexpr unsigned kFull = 0xffffffffu;
 struct SradParams {
   const float *jin;      // (tile_rows + 3) x pitch, local row 0 = global row r0 - 1
   float *jout;           // same layout; local rows 1..tile_rows written
-  const float *q0;       // q0sqr of this iteration (device scalar)
+  const double *roi_in;  // [roi_rows][roi_groups][2] partial sums of J (this iteration's statistics)
+  const double *const *roi_parts;   // multi-GPU: per rank partial buffer (null: roi_in) ...
+  const int *roi_owner;             // ... and the rank owning each ROI row
+  float *q0_out;         // optional: q0sqr written by the first warp
+  double npix;           // ROI pixel count
   double *roi_out;       // [roi_rows][roi_groups][2] partial sums of J' (may be null)
   int cols, pitch, tile_rows, r0, R;
   int lo0, hi0, lo1, hi1;   // own rows (0-based) computed: [lo0, hi0) then [lo1, hi1)
@@ -280,6 +285,31 @@ __device__ __forceinline__ void roi_row(const SradParams &P, int g, int wcol, in
   }
 }
 
+// q0sqr from the ROI partials: entries in index order (rows, then groups),
+// summed in fp64 by every lane (lanes load 32 entries at a time, shuffles
+// hand them over in order), then the restatement's mean / variance.
+__device__ __forceinline__ float srad_q0_warp(const SradParams &P, int lane) {
+  const int n = (P.roi_r2 - P.roi_r1 + 1) * P.roi_groups;
+  double s = 0.0, s2 = 0.0;
+  for (int base = 0; base < n; base += 32) {
+    double a = 0.0, b = 0.0;
+    const int e = base + lane;
+    if (e < n) {
+      const double *src = P.roi_parts ? P.roi_parts[P.roi_owner[e / P.roi_groups]] : P.roi_in;
+      a = src[2 * e];
+      b = src[2 * e + 1];
+    }
+    const int m = min(32, n - base);
+    for (int l = 0; l < m; ++l) {
+      s += __shfl_sync(kFull, a, l);
+      s2 += __shfl_sync(kFull, b, l);
+    }
+  }
+  const double mean = s / P.npix;
+  const double var = s2 / P.npix - mean * mean;
+  return float(var / (mean * mean));
+}
+
 // Per-row derived state of the sweep: differences and c of the own columns.
 struct SradDiff {
   float2 dWa, dWb, dEa, dEb;   // dW, dE of column pairs a = (0,1), b = (2,3)
@@ -315,7 +345,7 @@ __device__ __forceinline__ void srad_segment(const SradParams &P, int seg0, int 
   const int hcol = lane == 0 ? max(wc0 - 1, 0) : min(wc0 + kSradWarpCols, P.cols - 1);
   const bool hl = lane == 0 || lane == 31;
   SradQ q;
-  q.q0sqr = *P.q0;
+  q.q0sqr = srad_q0_warp(P, lane);
   q.q0den = q.q0sqr * (1.0f + q.q0sqr);
   q.nk1 = -16.0f * q.q0den;
   q.nk2 = -16.0f * (q.q0sqr * q.q0sqr);
@@ -346,56 +376,71 @@ __device__ __forceinline__ void srad_segment(const SradParams &P, int seg0, int 
   // c of the fifth column (c0 + 128) for 32 rows starting at g: lane l -> row g + l
   // (five gathered loads per 32 rows instead of a fifth column per row)
   const int x5 = min(wc0 + kSradWarpCols, P.cols - 1);
-  auto gather_c5 = [&](int g) {
-    const float *p = rowp(g + lane);
-    const float jc = __ldg(p + x5);
-    const float n = __ldg(rowp(g + lane - 1) + x5), s = __ldg(rowp(g + lane + 1) + x5);
-    const float w = __ldg(p + min(wc0 + kSradWarpCols - 1, P.cols - 1));
-    const float e = __ldg(p + min(wc0 + kSradWarpCols + 1, P.cols - 1));
-    float c = coeff1<M, FAST>(jc, jc - n, s - jc, w - jc, e - jc, q);
-    if (g + lane > gmax) c = 0.0f;   // rows below the image never reach a stored pixel
-    return c;
+  struct G5 {
+    float jc, n, s, w, e;
   };
+  auto gather_load = [&](int g, G5 &x) {
+    const float *p = rowp(g + lane);
+    x.jc = __ldg(p + x5);
+    x.n = __ldg(rowp(g + lane - 1) + x5);
+    x.s = __ldg(rowp(g + lane + 1) + x5);
+    x.w = __ldg(p + min(wc0 + kSradWarpCols - 1, P.cols - 1));
+    x.e = __ldg(p + min(wc0 + kSradWarpCols + 1, P.cols - 1));
+  };
+  // (rows below the image never reach a stored pixel: their c is left as computed)
+  auto gather_c5 = [&](const G5 &x) { return coeff1<M, FAST>(x.jc, x.jc - x.n, x.s - x.jc, x.w - x.jc, x.e - x.jc, q); };
 
-  // ---- segment start: the ring holds rows g0-1, g0, ... (ring index k = row - (g0-1))
+
+  // ---- the ring.  Ring index k = row - (g0 - 1); stage k % 8, phase k / 8.
+  // The prologue consumes k = 0..4 (rows g0-1 .. g0+3), loop iteration `it`
+  // consumes k = 5 + 8 it + u (u = 0..7): every stage index and phase is a
+  // compile-time function of u and the parity of it.  A stage is refilled
+  // with k + 8 once consumed, four stages per batch.
+  static_assert(kSradStages == 8, "the unrolled sweep assumes an 8-row ring");
   const int g0 = P.r0 + seg0;
-  const int kend = 5 + 2 * ((seg1 - seg0 + 1) / 2);   // rows the loop consumes
+  const int iters = (seg1 - seg0 + 7) / 8;
+  const int kend = 5 + 8 * iters;                      // ring indices the sweep consumes
   const int lo = max(wc0 - 4, 0), hi = min(wc0 + kSradWarpCols + 4, P.pitch);
   const unsigned bytes = unsigned(hi - lo) * 4u;
   const int soff = lo - (wc0 - 4);                       // 0, or 4 for the first strip
   auto issue = [&](int k) {                              // lane 0
     const int st = k & (kSradStages - 1);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the warp's reads of this stage come first
     mbar_expect_tx(&ring.bar[st], bytes);
     tma_load_1d(&ring.row[st][soff], rowp(g0 - 1 + k) + lo, bytes, &ring.bar[st]);
   };
+  auto refill = [&](int k0, int n) {   // after the warp's reads of stages k0 .. k0+n-1
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < n; ++u)
+        if (k0 + u + kSradStages < kend) issue(k0 + u + kSradStages);
+    }
+  };
   if (lane == 0) {
-#pragma unroll 1
+#pragma unroll
     for (int st = 0; st < kSradStages; ++st) mbar_init(&ring.bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-#pragma unroll 1
-    for (int k = 0; k < min(kSradStages, kend); ++k) issue(k);
+#pragma unroll
+    for (int k = 0; k < kSradStages; ++k)
+      if (k < kend) issue(k);
   }
   __syncwarp();
-  int kc = 0;   // the next ring index to consume
   const int io = lcol - (wc0 - 4), ih = hcol - (wc0 - 4);
-  auto load_next = [&](SradRow &r) {
-    const int st = kc & (kSradStages - 1);
-    mbar_wait(&ring.bar[st], unsigned(kc / kSradStages) & 1u);
+  auto consume = [&](int st, unsigned parity, SradRow &r) {
+    mbar_wait(&ring.bar[st], parity);
     const float4 x = *reinterpret_cast<const float4 *>(&ring.row[st][io]);
     r.a = mk(x.x, x.y);
     r.b = mk(x.z, x.w);
     r.h = hl ? ring.row[st][ih] : 0.0f;
-    __syncwarp();
-    if (lane == 0 && kc + kSradStages < kend) issue(kc + kSradStages);
-    ++kc;
   };
   SradRow jm, j0, j1, j2, j3;
-  load_next(jm);
-  load_next(j0);
-  load_next(j1);
-  load_next(j2);
-  load_next(j3);
+  consume(0, 0, jm);
+  consume(1, 0, j0);
+  consume(2, 0, j1);
+  consume(3, 0, j2);
+  consume(4, 0, j3);
+  refill(0, 5);
   float w0, e0;
   west_east<M>(j0, lane, w0, e0);
   SradDiff d0;
@@ -404,12 +449,16 @@ __device__ __forceinline__ void srad_segment(const SradParams &P, int seg0, int 
   float2 vs0a = sub2(j1.a, j0.a), vs0b = sub2(j1.b, j0.b);     // J(g0+1) - J(g0)
   float2 c0a = coeff2<M, FAST>(j0.a, vn0a, vs0a, d0.dWa, d0.dEa, q);
   float2 c0b = coeff2<M, FAST>(j0.b, vn0b, vs0b, d0.dWb, d0.dEb, q);
-  float c5v = gather_c5(g0);
+  G5 gx;
+  gather_load(g0, gx);
+  float c5v = gather_c5(gx);
   float *outp = P.jout + size_t(seg0 + 1) * pitch + col;
 
-  // One output row g: c(g+1) from rows g .. g+2 (jc = row g+1, jn = row g+2),
-  // then J'(g).  State in: vn/vs of row g, its c and differences; out: row g+1's.
-  auto step = [&](int i, const SradRow &jc, const SradRow &jn, float2 &vna, float2 &vnb, float2 &vsa,
+  // One output row i (global g): c(g+1) from rows g .. g+2 (jc = row g+1,
+  // jn = row g+2), then J'(g).  State in: vn / vs / c / differences of row g;
+  // out: row g+1's.  Below the image's last row J clamps, so dS = 0 there and
+  // c(g+1) multiplies zero (the restatement's clamped c changes no bit).
+  auto step = [&](int i, int r5, const SradRow &jc, const SradRow &jn, float2 &vna, float2 &vnb, float2 &vsa,
                   float2 &vsb, float2 &ca, float2 &cb, SradDiff &d, const SradRow &jg) {
     const int g = P.r0 + i;
     float w1, e1;
@@ -417,14 +466,10 @@ __device__ __forceinline__ void srad_segment(const SradParams &P, int seg0, int 
     SradDiff d1;
     diffs(jc, w1, e1, d1);
     const float2 vs1a = sub2(jn.a, jc.a), vs1b = sub2(jn.b, jc.b);   // J(g+2) - J(g+1)
-    float2 c1a = coeff2<M, FAST>(jc.a, vsa, vs1a, d1.dWa, d1.dEa, q);
-    float2 c1b = coeff2<M, FAST>(jc.b, vsb, vs1b, d1.dWb, d1.dEb, q);
-    if (g + 1 > gmax) {   // below the image's last row c is the last row's (warp-uniform)
-      c1a = ca;
-      c1b = cb;
-    }
+    const float2 c1a = coeff2<M, FAST>(jc.a, vsa, vs1a, d1.dWa, d1.dEa, q);
+    const float2 c1b = coeff2<M, FAST>(jc.b, vsb, vs1b, d1.dWb, d1.dEb, q);
     // east c of row g: in-thread neighbours, the next lane, or the fifth column
-    const float c5 = __shfl_sync(kFull, c5v, (i - seg0) & 31);
+    const float c5 = __shfl_sync(kFull, c5v, r5);
     const float cE = east_c<M>(ca.x, c5, lane);
     float2 cea = mk(ca.y, cb.x), ceb = mk(cb.y, cE);
     if constexpr (EDGE) {   // R_B: the image's last column (its own c)
@@ -449,10 +494,9 @@ __device__ __forceinline__ void srad_segment(const SradParams &P, int seg0, int 
         for (int k = 0; k < 4; ++k)
           if (col + k < P.cols) outp[k] = v[k];
       }
-      if (roi_warp && g >= P.roi_r1 && g <= P.roi_r2) roi_row(P, g, wcol, col, lane, ja, jb);
+      if (roi_warp && unsigned(g - P.roi_r1) <= unsigned(P.roi_r2 - P.roi_r1)) roi_row(P, g, wcol, col, lane, ja, jb);
     }
     outp += pitch;
-    if (((i - seg0) & 31) == 31) c5v = gather_c5(g + 1);   // the next 32 rows' fifth column (warp-uniform)
     vna = vsa;
     vnb = vsb;
     vsa = vs1a;
@@ -461,19 +505,31 @@ __device__ __forceinline__ void srad_segment(const SradParams &P, int seg0, int 
     cb = c1b;
     d = d1;
   };
-  // two rows per iteration: rows g .. g+3 resident, g+4 and g+5 in flight
-  // (every register rotates with period 2, so unrolling twice renames them)
-#pragma unroll 2
-  for (int i = seg0; i < seg1; i += 2) {
-    SradRow j4, j5;
-    load_next(j4);
-    load_next(j5);
-    step(i, j1, j2, vn0a, vn0b, vs0a, vs0b, c0a, c0b, d0, j0);
-    step(i + 1, j2, j3, vn0a, vn0b, vs0a, vs0b, c0a, c0b, d0, j1);
-    j0 = j2;
-    j1 = j3;
-    j2 = j4;
-    j3 = j5;
+  // eight rows per iteration: rows g .. g+3 in registers, the next rows
+  // consumed from the ring two at a time (all register rotations have period
+  // 2, so the unrolled body renames them)
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+    const unsigned p0 = unsigned(it) & 1u, p1 = p0 ^ 1u;
+    const int ib = seg0 + 8 * it;
+    const int rb = 8 * (it & 3);                 // (row - seg0) mod 32 of the iteration's first row
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      SradRow j4, j5;
+      consume((5 + t) & 7, 5 + t >= 8 ? p1 : p0, j4);
+      consume((6 + t) & 7, 6 + t >= 8 ? p1 : p0, j5);
+      if (t == 2 || t == 6) refill(5 + 8 * it + t - 2, 4);
+      step(ib + t, rb + t, j1, j2, vn0a, vn0b, vs0a, vs0b, c0a, c0b, d0, j0);
+      step(ib + t + 1, rb + t + 1, j2, j3, vn0a, vn0b, vs0a, vs0b, c0a, c0b, d0, j1);
+      j0 = j2;
+      j1 = j3;
+      j2 = j4;
+      j3 = j5;
+    }
+    if ((it & 3) == 3) {   // the next 32 rows' fifth column (warp-uniform)
+      gather_load(P.r0 + ib + 8, gx);   // (loading one block ahead measured slower: 45.5 -> 57 ms)
+      c5v = gather_c5(gx);
+    }
   }
 }
 
@@ -494,31 +550,15 @@ __global__ void __launch_bounds__(32, DARM_SRAD_MINB) srad_sweep_kernel(SradPara
     seg1 = min(seg0 + P.rs, P.hi1);
   }
   if (seg0 >= seg1) return;
+  if (P.q0_out && blockIdx.x == 0 && blockIdx.y == 0) {
+    const float q0 = srad_q0_warp(P, lane);
+    if (lane == 0) *P.q0_out = q0;
+  }
   __shared__ __align__(128) SradRing ring;
   if ((wcol + 1) * kSradWarpCols >= P.cols)
     srad_segment<M, FAST, true>(P, seg0, seg1, wcol, lane, ring);
   else
     srad_segment<M, FAST, false>(P, seg0, seg1, wcol, lane, ring);
-}
-
-// q0sqr from the ROI partials: rows in order, groups in order, fp64.
-// `parts` holds one partial buffer per source (a multi-GPU run reads the
-// owning rank's buffer for every ROI row, `owner[row]`); nparts = 1 for a
-// single buffer.
-__global__ void srad_q0_kernel(const double *const *parts, const int *owner, const double *roi, int rows,
-                               int groups, double npix, float *q0) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = 0.0, s2 = 0.0;
-  for (int r = 0; r < rows; ++r) {
-    const double *src = parts ? parts[owner[r]] : roi;
-    for (int g = 0; g < groups; ++g) {
-      s += src[2 * (size_t(r) * groups + g)];
-      s2 += src[2 * (size_t(r) * groups + g) + 1];
-    }
-  }
-  const double mean = s / npix;
-  const double var = s2 / npix - mean * mean;
-  *q0 = float(var / (mean * mean));
 }
 
 // ROI partials of an existing image (the first iteration's statistics).
@@ -576,13 +616,6 @@ cudaError_t launch_srad_roi(const float *jin, int cols, int pitch, int r0, int t
   return cudaGetLastError();
 }
 
-cudaError_t launch_srad_q0(const double *roi_in, const SradRoi &roi, float *q0, cudaStream_t s,
-                           const double *const *parts, const int *owner) {
-  const double npix = double(roi.rows) * double(roi.c2 - roi.c1 + 1);
-  srad_q0_kernel<<<1, 32, 0, s>>>(parts, owner, roi_in, roi.rows, roi.groups, npix, q0);
-  return cudaGetLastError();
-}
-
 template <bool M, bool FAST>
 static int srad_resident_ctas() {
   static int n = [] {
@@ -595,13 +628,18 @@ static int srad_resident_ctas() {
   return n;
 }
 
-cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const float *q0, double *roi_out,
-                              int cols, int pitch, int tile_rows, int r0, int R, float lambda, const SradRoi &roi,
-                              const SradRange &range, cudaStream_t s) {
+cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const double *roi_in, float *q0_out,
+                              double *roi_out, int cols, int pitch, int tile_rows, int r0, int R, float lambda,
+                              const SradRoi &roi, const SradRange &range, cudaStream_t s,
+                              const double *const *roi_parts, const int *roi_owner) {
   SradParams P;
   P.jin = jin;
   P.jout = jout;
-  P.q0 = q0;
+  P.roi_in = roi_in;
+  P.roi_parts = roi_parts;
+  P.roi_owner = roi_owner;
+  P.q0_out = q0_out;
+  P.npix = double(roi.rows) * double(roi.c2 - roi.c1 + 1);
   P.roi_out = roi_out;
   P.cols = cols;
   P.pitch = pitch;
