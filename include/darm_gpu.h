@@ -266,6 +266,45 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out,
                             double *roi_out, float *q0_scratch, int part,
                             void *stream, char *err, size_t errlen);
 
+/* Peer-memory row-tiled SRAD: the multi-GPU product path (one process per
+ * GPU, one group per rank).  Instead of a collective library, a rank reads its
+ * halo rows and the ROI partial sums straight out of its neighbours' memory
+ * (CUDA IPC mappings over NVLink / NVSwitch) and the ranks keep phase with
+ * flags in device memory: after the load and after every iteration a rank
+ * publishes its phase count into every rank's flag array; before a phase it
+ * waits on the GPU until all peers reached its own count.  An iteration is:
+ * wait, halo pull (side stream) beside the interior rows, edge rows, signal —
+ * all `iters` iterations one cached CUDA graph.  Results are bit-identical to
+ * darm_gpu_srad() on the whole image.
+ *   create:  allocate this rank's tile (global rows split as evenly as in
+ *            paper_2107_05681_b200.srad_tiles.split_rows) and write its
+ *            DARM_SRAD_HANDLE_BYTES-byte handle;
+ *   connect: give every rank's handle (rank order); peers in another process
+ *            are opened by CUDA IPC, in this process used directly;
+ *   load:    this rank's rows (tile_rows x cols, row-major) -> the tile;
+ *   run:     `iters` iterations (asynchronous on `stream`);
+ *   read:    the tile's rows out; returns 3 if a peer never arrived (a device
+ *            wait gives up after DARM_PEER_TIMEOUT_S seconds, default 60).
+ * Every rank must call load / run with the same sequence of arguments. */
+#define DARM_SRAD_HANDLE_BYTES 128
+typedef struct darm_gpu_srad_group darm_gpu_srad_group;
+int darm_gpu_srad_group_create(int variant, int64_t rows, int64_t cols, float lambda,
+                               const int *roi, int rank, int world,
+                               darm_gpu_srad_group **out, void *handle_out,
+                               char *err, size_t errlen);
+int darm_gpu_srad_group_connect(darm_gpu_srad_group *group, const void *handles,
+                                char *err, size_t errlen);
+int darm_gpu_srad_group_load(darm_gpu_srad_group *group, const float *tile, int mem,
+                             void *stream, char *err, size_t errlen);
+int darm_gpu_srad_group_run(darm_gpu_srad_group *group, int iters, void *stream,
+                            darm_gpu_stats *stats, char *err, size_t errlen);
+int darm_gpu_srad_group_read(darm_gpu_srad_group *group, float *tile, int mem,
+                             void *stream, char *err, size_t errlen);
+/* this rank's first global row and row count */
+int darm_gpu_srad_group_rows(const darm_gpu_srad_group *group, int64_t *r0,
+                             int64_t *tile_rows);
+void darm_gpu_srad_group_free(darm_gpu_srad_group *group);
+
 /* ---- GPU executeWarp for arbitrary mini-IR -------
  * executeWarp (include/darm/interp.hpp:57-58, src/interp.cpp:332-381) for a
  * batch of warps of ANY function in the reference's textual IR (SPEC.md:

@@ -68,6 +68,13 @@ ABI_SYMBOLS = (
     "darm_gpu_srad_pitch",
     "darm_gpu_srad_tile_roi",
     "darm_gpu_srad_tile_step",
+    "darm_gpu_srad_group_create",
+    "darm_gpu_srad_group_connect",
+    "darm_gpu_srad_group_load",
+    "darm_gpu_srad_group_run",
+    "darm_gpu_srad_group_read",
+    "darm_gpu_srad_group_rows",
+    "darm_gpu_srad_group_free",
     "darm_gpu_program_load",
     "darm_gpu_program_free",
     "darm_gpu_program_shape",
@@ -191,6 +198,16 @@ def lib() -> ctypes.CDLL:
                                               ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_float, I32P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                               ctypes.c_int, ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]
+        VP, E = ctypes.c_void_p, [ctypes.c_char_p, ctypes.c_size_t]
+        L.darm_gpu_srad_group_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, I32P,
+                                                 ctypes.c_int, ctypes.c_int, ctypes.POINTER(VP), VP] + E
+        L.darm_gpu_srad_group_connect.argtypes = [VP, VP] + E
+        L.darm_gpu_srad_group_load.argtypes = [VP, VP, ctypes.c_int, VP] + E
+        L.darm_gpu_srad_group_run.argtypes = [VP, ctypes.c_int, VP, ctypes.POINTER(Stats)] + E
+        L.darm_gpu_srad_group_read.argtypes = [VP, VP, ctypes.c_int, VP] + E
+        L.darm_gpu_srad_group_rows.argtypes = [VP, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        L.darm_gpu_srad_group_free.argtypes = [VP]
+        L.darm_gpu_srad_group_free.restype = None
         _lib = L
     return _lib
 

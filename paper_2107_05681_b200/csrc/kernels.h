@@ -106,5 +106,11 @@ cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const 
                               double *roi_out, int cols, int pitch, int tile_rows, int r0, int R, float lambda,
                               const SradRoi &roi, const SradRange &range, cudaStream_t s,
                               const double *const *roi_parts = nullptr, const int *roi_owner = nullptr);
+// peer-memory row tiles (darm_gpu_srad_group_*): phase barrier, phase signal, halo pull
+cudaError_t launch_srad_peer_wait(const unsigned *flags, const unsigned *seq, int rank, int world,
+                                  unsigned long long timeout_ns, int *status, cudaStream_t s);
+cudaError_t launch_srad_peer_signal(unsigned *const *peer_flags, unsigned *seq, int rank, int world, cudaStream_t s);
+cudaError_t launch_srad_peer_halo(float *dst, const float *up, int up_rows, const float *down, int n, int pitch,
+                                  cudaStream_t s);
 
 }  // namespace darm_gpu

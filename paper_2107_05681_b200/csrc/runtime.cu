@@ -7,13 +7,17 @@
 // D2H copy.  Errors follow the CLI's exit codes (darm_cli.cpp:25-27).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
+
+#include <unistd.h>
 
 #include "../../include/darm_gpu.h"
 #include "corpus.cuh"
@@ -887,6 +891,322 @@ int darm_gpu_srad_tile_step(int variant, const float *tile_in, float *tile_out, 
   });
 }
 
+
+// ---------------------------------------------------------------- peer-memory SRAD tiles
+namespace darm_gpu {
+namespace {
+struct SradHandle {   // DARM_SRAD_HANDLE_BYTES bytes on the wire
+  uint32_t magic;
+  int32_t pid, dev, world;
+  uint64_t ptr;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(SradHandle) <= DARM_SRAD_HANDLE_BYTES, "handle size");
+constexpr uint32_t kSradMagic = 0x53524144u;   // "SRAD"
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// every rank's allocation: flags[world] | ROI partials x2 | tile x2
+struct SradLayout {
+  size_t roi, tile[2], tile_bytes, roi_bytes, total;
+};
+SradLayout srad_layout(int world, const SradRoi &R, int n, int pitch) {
+  SradLayout L;
+  L.roi_bytes = align256(size_t(R.rows) * R.groups * 2 * sizeof(double));
+  L.tile_bytes = align256(size_t(n + 3) * size_t(pitch) * sizeof(float));
+  L.roi = align256(size_t(world) * sizeof(unsigned));
+  L.tile[0] = L.roi + 2 * L.roi_bytes;
+  L.tile[1] = L.tile[0] + L.tile_bytes;
+  L.total = L.tile[1] + L.tile_bytes;
+  return L;
+}
+}  // namespace
+}  // namespace darm_gpu
+
+struct darm_gpu_srad_group {
+  int variant = 0, rank = 0, world = 1, dev = 0, pitch = 0, cur = 0;
+  int64_t rows = 0, cols = 0;
+  float lambda = 0.5f;
+  int roi[4] = {0, 0, 0, 0};
+  darm_gpu::SradRoi R{};
+  std::vector<std::pair<int, int>> split;   // (r0, n) per rank
+  std::vector<char *> base;                 // every rank's allocation as mapped here
+  std::vector<bool> opened;                 // opened through CUDA IPC (closed on free)
+  char *own = nullptr;
+  // device control block: seq, status, peer flag pointers, ROI partial pointers x2, ROI row owners
+  char *ctl = nullptr;
+  unsigned *seq = nullptr;
+  int *status = nullptr;
+  unsigned **peer_flags = nullptr;
+  const double **parts[2] = {nullptr, nullptr};
+  int *owner = nullptr;
+  cudaStream_t capture = nullptr, side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  struct G {
+    int iters, cur;
+    cudaGraphExec_t exec;
+  };
+  std::vector<G> graphs;
+  unsigned long long timeout_ns = 60ull * 1000000000ull;
+  bool connected = false;
+
+  darm_gpu::SradLayout layout(int k) const { return darm_gpu::srad_layout(world, R, split[k].second, pitch); }
+  float *tile(int k, int which) const { return reinterpret_cast<float *>(base[k] + layout(k).tile[which]); }
+  double *roi_buf(int k, int which) const {
+    const auto L = layout(k);
+    return reinterpret_cast<double *>(base[k] + L.roi + size_t(which) * L.roi_bytes);
+  }
+  unsigned *flags(int k) const { return reinterpret_cast<unsigned *>(base[k]); }
+};
+
+using darm_gpu::srad_layout;
+
+int darm_gpu_srad_group_create(int variant, int64_t rows, int64_t cols, float lambda, const int *roi, int rank,
+                               int world, darm_gpu_srad_group **out, void *handle_out, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    check_srad_variant(variant);
+    check_srad_args(rows, cols, roi, lambda);
+    if (!out || !handle_out) user_error("out / handle_out is NULL");
+    if (world < 1 || world > 64 || rank < 0 || rank >= world) user_error("need 0 <= rank < world <= 64");
+    auto g = std::make_unique<darm_gpu_srad_group>();
+    g->variant = variant;
+    g->rank = rank;
+    g->world = world;
+    g->rows = rows;
+    g->cols = cols;
+    g->lambda = lambda;
+    std::memcpy(g->roi, roi, sizeof(g->roi));
+    g->R = srad_roi_layout(int(cols), roi[0], roi[1], roi[2], roi[3]);
+    g->pitch = srad_pitch(int(cols));
+    int64_t r0 = 0;
+    for (int k = 0; k < world; ++k) {   // as srad_tiles.split_rows
+      const int64_t n = rows / world + (k < rows % world ? 1 : 0);
+      if (n < 2) user_error("every rank needs at least 2 image rows");
+      g->split.emplace_back(int(r0), int(n));
+      r0 += n;
+    }
+    if (const char *t = std::getenv("DARM_PEER_TIMEOUT_S")) g->timeout_ns = (unsigned long long)(std::atof(t) * 1e9);
+    device_state(&g->dev);
+    DARM_CUDA(cudaGetDevice(&g->dev));
+    const auto L = g->layout(rank);
+    DARM_CUDA(cudaMalloc(&g->own, L.total));
+    DARM_CUDA(cudaMemset(g->own, 0, L.total));   // flags, partials, halo and pad columns defined
+    const size_t ctl_bytes = 256 + size_t(world) * sizeof(void *) * 3 + size_t(g->R.rows) * sizeof(int);
+    DARM_CUDA(cudaMalloc(&g->ctl, ctl_bytes));
+    DARM_CUDA(cudaMemset(g->ctl, 0, ctl_bytes));
+    g->seq = reinterpret_cast<unsigned *>(g->ctl);
+    g->status = reinterpret_cast<int *>(g->ctl + 16);
+    g->peer_flags = reinterpret_cast<unsigned **>(g->ctl + 256);
+    g->parts[0] = reinterpret_cast<const double **>(g->ctl + 256 + size_t(world) * sizeof(void *));
+    g->parts[1] = g->parts[0] + world;
+    g->owner = reinterpret_cast<int *>(g->ctl + 256 + size_t(world) * sizeof(void *) * 3);
+    SradHandle h{};
+    h.magic = kSradMagic;
+    h.pid = int32_t(getpid());
+    h.dev = g->dev;
+    h.world = world;
+    h.ptr = reinterpret_cast<uint64_t>(g->own);
+    DARM_CUDA(cudaIpcGetMemHandle(&h.ipc, g->own));
+    std::memset(handle_out, 0, DARM_SRAD_HANDLE_BYTES);
+    std::memcpy(handle_out, &h, sizeof(h));
+    *out = g.release();
+  });
+}
+
+int darm_gpu_srad_group_connect(darm_gpu_srad_group *g, const void *handles, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!g || !handles) user_error("group / handles is NULL");
+    if (g->connected) user_error("group already connected");
+    DARM_CUDA(cudaSetDevice(g->dev));
+    g->base.assign(size_t(g->world), nullptr);
+    g->opened.assign(size_t(g->world), false);
+    const char *hb = static_cast<const char *>(handles);
+    for (int k = 0; k < g->world; ++k) {
+      SradHandle h;
+      std::memcpy(&h, hb + size_t(k) * DARM_SRAD_HANDLE_BYTES, sizeof(h));
+      if (h.magic != kSradMagic || h.world != g->world) user_error("handle " + std::to_string(k) + " is not a SRAD group handle of this world");
+      if (k == g->rank) {
+        g->base[k] = g->own;
+      } else if (h.pid == int32_t(getpid())) {   // a rank in this process: its pointer as is
+        if (h.dev != g->dev) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(h.dev, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) DARM_CUDA(e);
+          cudaGetLastError();
+        }
+        g->base[k] = reinterpret_cast<char *>(h.ptr);
+      } else {
+        void *p = nullptr;
+        DARM_CUDA(cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+        g->base[k] = static_cast<char *>(p);
+        g->opened[k] = true;
+      }
+    }
+    std::vector<unsigned *> pf(size_t(g->world));
+    std::vector<const double *> parts(2 * size_t(g->world));
+    for (int k = 0; k < g->world; ++k) {
+      pf[k] = g->flags(k);
+      parts[k] = g->roi_buf(k, 0);
+      parts[g->world + k] = g->roi_buf(k, 1);
+    }
+    std::vector<int> owner(size_t(g->R.rows));
+    for (int r = 0; r < g->R.rows; ++r) {
+      const int row = g->R.r1 + r;
+      for (int k = 0; k < g->world; ++k)
+        if (row >= g->split[k].first && row < g->split[k].first + g->split[k].second) owner[r] = k;
+    }
+    DARM_CUDA(cudaMemcpy(g->peer_flags, pf.data(), pf.size() * sizeof(void *), cudaMemcpyHostToDevice));
+    DARM_CUDA(cudaMemcpy(g->parts[0], parts.data(), parts.size() * sizeof(void *), cudaMemcpyHostToDevice));
+    DARM_CUDA(cudaMemcpy(g->owner, owner.data(), owner.size() * sizeof(int), cudaMemcpyHostToDevice));
+    DARM_CUDA(cudaStreamCreateWithFlags(&g->capture, cudaStreamNonBlocking));
+    DARM_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+    DARM_CUDA(cudaEventCreateWithFlags(&g->fork, cudaEventDisableTiming));
+    DARM_CUDA(cudaEventCreateWithFlags(&g->join, cudaEventDisableTiming));
+    g->connected = true;
+  });
+}
+
+static void srad_group_ready(const darm_gpu_srad_group *g) {
+  if (!g) user_error("group is NULL");
+  if (!g->connected) user_error("group not connected");
+  DARM_CUDA(cudaSetDevice(g->dev));
+}
+
+int darm_gpu_srad_group_load(darm_gpu_srad_group *g, const float *tile, int mem, void *stream, char *err,
+                             size_t errlen) {
+  return guarded(err, errlen, [&] {
+    srad_group_ready(g);
+    if (!tile) user_error("tile is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int r0 = g->split[g->rank].first, n = g->split[g->rank].second;
+    DARM_CUDA(launch_srad_peer_wait(g->flags(g->rank), g->seq, g->rank, g->world, g->timeout_ns, g->status, s));
+    float *t = g->tile(g->rank, 0);
+    DARM_CUDA(cudaMemcpy2DAsync(t + g->pitch, size_t(g->pitch) * 4, tile, size_t(g->cols) * 4, size_t(g->cols) * 4,
+                                size_t(n), mem == DARM_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                s));
+    DARM_CUDA(cudaMemsetAsync(g->roi_buf(g->rank, 0), 0, g->layout(g->rank).roi_bytes, s));
+    DARM_CUDA(launch_srad_roi(t, int(g->cols), g->pitch, r0, n, g->R, g->roi_buf(g->rank, 0), s));
+    DARM_CUDA(launch_srad_peer_signal(g->peer_flags, g->seq, g->rank, g->world, s));
+    g->cur = 0;
+    if (mem == DARM_MEM_HOST) DARM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// one iteration from tile buffer `cur` into 1 - cur, recorded on g->capture
+static cudaError_t record_srad_group_iteration(darm_gpu_srad_group *g, int cur, int *launches) {
+  using namespace darm_gpu;
+  cudaStream_t s = g->capture;
+  const int r0 = g->split[g->rank].first, n = g->split[g->rank].second;
+  const int k = g->rank;
+  cudaError_t e = launch_srad_peer_wait(g->flags(k), g->seq, k, g->world, g->timeout_ns, g->status, s);
+  if (e != cudaSuccess) return e;
+  const bool halo = g->world > 1;
+  if (halo) {   // the halo rows come over NVLink while the interior rows run
+    if ((e = cudaEventRecord(g->fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(g->side, g->fork, 0)) != cudaSuccess) return e;
+    const float *up = k > 0 ? g->tile(k - 1, cur) : nullptr;
+    const float *down = k + 1 < g->world ? g->tile(k + 1, cur) : nullptr;
+    const int up_rows = k > 0 ? g->split[k - 1].second : 0;
+    if ((e = launch_srad_peer_halo(g->tile(k, cur), up, up_rows, down, n, g->pitch, g->side)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(g->join, g->side)) != cudaSuccess) return e;
+  }
+  auto sweep = [&](SradRange range) {
+    return launch_srad_sweep(g->variant, g->tile(k, cur), g->tile(k, 1 - cur), nullptr, nullptr,
+                             g->roi_buf(k, 1 - cur), int(g->cols), g->pitch, n, r0, int(g->rows), g->lambda, g->R,
+                             range, s, g->parts[cur], g->owner);
+  };
+  const bool split = halo && n > 3;
+  if ((e = sweep(split ? SradRange{1, n - 2, 0, 0} : SradRange{0, 0, 0, 0})) != cudaSuccess) return e;
+  if (halo && (e = cudaStreamWaitEvent(s, g->join, 0)) != cudaSuccess) return e;
+  if ((e = sweep(split ? SradRange{0, 1, n - 2, n} : SradRange{0, n, 0, 0})) != cudaSuccess) return e;
+  e = launch_srad_peer_signal(g->peer_flags, g->seq, k, g->world, s);
+  *launches += halo ? 5 : 4;
+  return e;
+}
+
+int darm_gpu_srad_group_run(darm_gpu_srad_group *g, int iters, void *stream, darm_gpu_stats *stats, char *err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    srad_group_ready(g);
+    if (iters < 0) user_error("iters must be >= 0");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    darm_gpu_srad_group::G *gr = nullptr;
+    for (auto &x : g->graphs)
+      if (x.iters == iters && x.cur == g->cur) gr = &x;
+    int launches = 0;
+    if (!gr) {
+      cudaGraph_t graph = nullptr;
+      DARM_CUDA(cudaStreamBeginCapture(g->capture, cudaStreamCaptureModeThreadLocal));
+      cudaError_t rec = cudaSuccess;
+      for (int t = 0, cur = g->cur; t < iters && rec == cudaSuccess; ++t, cur = 1 - cur)
+        rec = record_srad_group_iteration(g, cur, &launches);
+      cudaError_t end = cudaStreamEndCapture(g->capture, &graph);
+      DARM_CUDA(rec);
+      DARM_CUDA(end);
+      cudaGraphExec_t exec = nullptr;
+      cudaError_t inst = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      DARM_CUDA(inst);
+      g->graphs.push_back({iters, g->cur, exec});
+      gr = &g->graphs.back();
+    } else {
+      launches = iters * (g->world > 1 ? 5 : 4);
+    }
+    Timeline tl(s, stats != nullptr);
+    tl.mark(0);
+    tl.mark(1);
+    DARM_CUDA(cudaGraphLaunch(gr->exec, s));
+    tl.mark(2);
+    tl.mark(3);
+    g->cur = (g->cur + iters) & 1;
+    if (stats) {
+      tl.fill(stats);
+      stats->launches = launches;
+      stats->algorithmic_bytes = uint64_t(iters) * uint64_t(g->split[g->rank].second) * uint64_t(g->cols) * 8;
+    }
+  });
+}
+
+int darm_gpu_srad_group_read(darm_gpu_srad_group *g, float *tile, int mem, void *stream, char *err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    srad_group_ready(g);
+    if (!tile) user_error("tile is NULL");
+    if (mem != DARM_MEM_HOST && mem != DARM_MEM_DEVICE) user_error("mem must be HOST or DEVICE");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int n = g->split[g->rank].second;
+    DARM_CUDA(cudaMemcpy2DAsync(tile, size_t(g->cols) * 4, g->tile(g->rank, g->cur) + g->pitch, size_t(g->pitch) * 4,
+                                size_t(g->cols) * 4, size_t(n),
+                                mem == DARM_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    int status = 0;
+    DARM_CUDA(cudaMemcpyAsync(&status, g->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DARM_CUDA(cudaStreamSynchronize(s));
+    if (status) throw Error{DARM_INTERNAL_ERROR, "a peer rank never reached this phase (device wait timed out)"};
+  });
+}
+
+int darm_gpu_srad_group_rows(const darm_gpu_srad_group *g, int64_t *r0, int64_t *tile_rows) {
+  if (!g || !r0 || !tile_rows) return DARM_USER_ERROR;
+  *r0 = g->split[g->rank].first;
+  *tile_rows = g->split[g->rank].second;
+  return DARM_OK;
+}
+
+void darm_gpu_srad_group_free(darm_gpu_srad_group *g) {
+  if (!g) return;
+  cudaSetDevice(g->dev);
+  cudaDeviceSynchronize();
+  for (auto &x : g->graphs) cudaGraphExecDestroy(x.exec);
+  for (size_t k = 0; k < g->base.size(); ++k)
+    if (g->opened[k]) cudaIpcCloseMemHandle(g->base[k]);
+  if (g->capture) cudaStreamDestroy(g->capture);
+  if (g->side) cudaStreamDestroy(g->side);
+  if (g->fork) cudaEventDestroy(g->fork);
+  if (g->join) cudaEventDestroy(g->join);
+  cudaFree(g->ctl);
+  cudaFree(g->own);
+  delete g;
+}
 
 // ---------------------------------------------------------------- mini-IR programs
 struct darm_gpu_program {

@@ -295,9 +295,14 @@ __device__ __forceinline__ float srad_q0_warp(const SradParams &P, int lane) {
     double a = 0.0, b = 0.0;
     const int e = base + lane;
     if (e < n) {
-      const double *src = P.roi_parts ? P.roi_parts[P.roi_owner[e / P.roi_groups]] : P.roi_in;
-      a = src[2 * e];
-      b = src[2 * e + 1];
+      if (P.roi_parts) {   // a peer's buffer over NVLink: never a stale cached line
+        const double *src = P.roi_parts[P.roi_owner[e / P.roi_groups]];
+        a = __ldcv(src + 2 * e);
+        b = __ldcv(src + 2 * e + 1);
+      } else {
+        a = P.roi_in[2 * e];
+        b = P.roi_in[2 * e + 1];
+      }
     }
     const int m = min(32, n - base);
     for (int l = 0; l < m; ++l) {
@@ -680,6 +685,92 @@ cudaError_t launch_srad_sweep(int variant, const float *jin, float *jout, const 
   else
     fast ? srad_sweep_kernel<false, true><<<grid, 32, 0, s>>>(P)
          : srad_sweep_kernel<false, false><<<grid, 32, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+// ---- peer-memory row tiles (multi-GPU SRAD without a collective library).
+// Every rank's flags[world] live in its own memory; after a phase (the load,
+// or one iteration) rank r stores its phase count into flags[r] of every rank.
+// Before a phase a rank waits until every peer's flag has reached its own
+// count: all peers finished the previous phase (so their J / ROI partials of
+// it are complete, and they are done reading this rank's buffers of the phase
+// before).  The counts live in device memory, so a captured graph of N
+// iterations is reusable across runs.
+
+// one warp: lane k spins on flags[k] (k != rank) until >= *seq; gives up after
+// `timeout_ns` and records the failure in *status (never hangs the GPU)
+__global__ void srad_peer_wait_kernel(const unsigned *flags, const unsigned *seq, int rank, int world,
+                                      unsigned long long timeout_ns, int *status) {
+  const int k = threadIdx.x;
+  if (k >= world || k == rank) return;
+  const unsigned want = *seq;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + k) : "memory");
+    if (int(v - want) >= 0) break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      atomicExch(status, 1);
+      break;
+    }
+    __nanosleep(200);
+  }
+}
+
+// one warp: ++*seq, then lane k stores it into peer k's flags[rank] (release,
+// system scope: every write of this rank's earlier kernels is visible first)
+__global__ void srad_peer_signal_kernel(unsigned *const *peer_flags, unsigned *seq, int rank, int world) {
+  __shared__ unsigned v;
+  if (threadIdx.x == 0) {
+    v = *seq + 1;
+    *seq = v;
+  }
+  __syncwarp();
+  __threadfence_system();
+  const int k = threadIdx.x;
+  if (k < world) {
+    unsigned *dst = peer_flags[k] + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst), "r"(v) : "memory");
+  }
+}
+
+// halo rows: dst local row 0 <- the upper neighbour's last own row, dst local
+// rows n+1, n+2 <- the lower neighbour's first two own rows (peer loads over
+// NVLink, 16 bytes per thread, volatile: the neighbour wrote them this phase)
+__global__ void srad_peer_halo_kernel(float *dst, const float *up, int up_rows, const float *down, int n,
+                                      int pitch) {
+  const int v4 = pitch / 4;
+  const int r = blockIdx.y;   // 0: top halo, 1, 2: bottom halos
+  const float4 *src = nullptr;
+  float4 *out = nullptr;
+  if (r == 0 && up) {
+    src = reinterpret_cast<const float4 *>(up + size_t(up_rows) * pitch);
+    out = reinterpret_cast<float4 *>(dst);
+  } else if (r > 0 && down) {
+    src = reinterpret_cast<const float4 *>(down + size_t(r) * pitch);
+    out = reinterpret_cast<float4 *>(dst + size_t(n + r) * pitch);
+  }
+  if (!src) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < v4; i += gridDim.x * blockDim.x) out[i] = __ldcv(src + i);
+}
+
+cudaError_t launch_srad_peer_wait(const unsigned *flags, const unsigned *seq, int rank, int world,
+                                  unsigned long long timeout_ns, int *status, cudaStream_t s) {
+  srad_peer_wait_kernel<<<1, 32, 0, s>>>(flags, seq, rank, world, timeout_ns, status);
+  return cudaGetLastError();
+}
+cudaError_t launch_srad_peer_signal(unsigned *const *peer_flags, unsigned *seq, int rank, int world, cudaStream_t s) {
+  srad_peer_signal_kernel<<<1, 32, 0, s>>>(peer_flags, seq, rank, world);
+  return cudaGetLastError();
+}
+cudaError_t launch_srad_peer_halo(float *dst, const float *up, int up_rows, const float *down, int n, int pitch,
+                                  cudaStream_t s) {
+  const int v4 = pitch / 4;
+  dim3 grid((v4 + 255) / 256 < 16 ? (v4 + 255) / 256 : 16, 3);
+  srad_peer_halo_kernel<<<grid, 256, 0, s>>>(dst, up, up_rows, down, n, pitch);
   return cudaGetLastError();
 }
 

@@ -4,6 +4,10 @@ import sys
 
 import pytest
 
+# several streams per test process (peer-memory SRAD ranks as threads): give
+# them their own hardware queues (must be set before CUDA initialises)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))

@@ -1,5 +1,2 @@
-nvidia-smi --query-gpu=name,clocks.sm,clocks.mem,power.draw --format=csv
-for v in default ahead minb16 default; do
-  if [ $v = default ]; then L=""; else L="DARM_GPU_LIB=variants/$v/libdarm_gpu.so"; fi
-  env $L timeout 300 python tools/time_srad.py $v 2>&1 | tail -2
-done
+export DARM_PEER_TIMEOUT_S=20
+timeout 900 python -m pytest tests/test_srad_peer.py -q -m gpu -k thin > gpurun_out/pytest_peer.log 2>&1; echo "peer tests rc=$?"; grep -E "passed|failed|Error|assert" gpurun_out/pytest_peer.log | tail -20
