@@ -538,11 +538,12 @@ def srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, n=16384,
                 row[vname + "_result_sha16"] = sha(j)
             del j
         else:
+            from paper_2107_05681_b200.srad_peer import SradPeerTiles
             from paper_2107_05681_b200.srad_tiles import SradTiles
 
+            # the product path: peer-memory tiles, the whole run one CUDA graph per rank
             for vname, v in (("unmelded", 0), ("melded", 1)):
-                tiles = SradTiles(n, n, 0.5, darm.RODINIA_ROI, dist=dist, device=torch.device("cuda"),
-                                  variant=v | flag)
+                tiles = SradPeerTiles(n, n, 0.5, darm.RODINIA_ROI, dist=dist, variant=v, fast=fast)
                 ts = []
                 for rep in range(2):
                     tiles.load(j0)
@@ -559,14 +560,33 @@ def srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, n=16384,
                 full = tiles.gather()
                 if full is not None:
                     row[vname + "_result_sha16"] = sha(full)
+                dist.barrier()
+                tiles.close()
                 del tiles, full
+            row["transport"] = "peer memory (CUDA IPC over NVLink), device-flag phases, one CUDA graph"
+            # the baseline transport: torch.distributed P2P halos + ROI all-reduce per iteration (melded)
+            tiles = SradTiles(n, n, 0.5, darm.RODINIA_ROI, dist=dist, device=torch.device("cuda"),
+                              variant=1 | flag)
+            tiles.load(j0)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tiles.run(iters)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            row["melded_torch_dist_transport_us"] = reduce_max(torch, dist, 1e3 * e0.elapsed_time(e1))
+            full = tiles.gather()
+            if full is not None:
+                row["melded_torch_dist_result_sha16"] = sha(full)
+            del tiles, full
         tmax(row)
         row["speedup"] = row["unmelded_us"] / row["melded_us"]
         # minimal traffic 8 B/px/iteration (one read of J, one write of J') + the in/out copies of the call
         alg = 8.0 * n * n * iters + 8.0 * n * n
         row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
         row["melded_frac_hbm"] = row["melded_GBps"] / (peak * world)
-        row["n_gpus"], row["scaling"] = world, ("strong (row tiles, NCCL halo exchange)" if world > 1 else
+        row["n_gpus"], row["scaling"] = world, ("strong (row tiles, peer-memory halos)" if world > 1 else
                                                 "single GPU")
         row["arithmetic"] = ("reciprocal-multiply divisions + FMA, within 1e-5 relative (DARM_FAST_MATH)" if fast
                              else "IEEE, bit-exact vs the restatement")

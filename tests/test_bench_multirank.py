@@ -10,8 +10,9 @@ exchange steps are the ones an 8-GPU NCCL run executes.
 Bit-exactness against one GPU:
   * bitonic: every rank checks its sorted keys against torch.sort inside bench.py;
   * N-Queens: the prefix shards of both ranks sum to Q(16) = 14,772,512 (asserted in bench.py);
-  * SRAD: the row-tiled image (halo exchange + ROI all-reduce every iteration)
-    gathered on rank 0 hashes to the same bytes as the single-GPU run.
+  * SRAD: the row-tiled image gathered on rank 0 hashes to the same bytes as
+    the single-GPU run, through both transports (peer-memory tiles over CUDA
+    IPC, and torch.distributed halos + ROI all-reduce).
 """
 import json
 import os
@@ -50,6 +51,8 @@ def test_bench_two_ranks_match_one_gpu():
         assert r2["n_gpus"] == 2
         for form in ("unmelded", "melded"):
             assert r1[form + "_result_sha16"] == r2[form + "_result_sha16"], (key, form)
+        # the torch.distributed transport (P2P halos + ROI all-reduce) gives the same bits
+        assert r2["melded_torch_dist_result_sha16"] == r1["melded_result_sha16"], key
 
 
 def test_bench_rejects_world_mismatch():
