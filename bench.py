@@ -84,7 +84,7 @@ def attach_lane_efficiency(per_kernel):
             row["lane_efficiency"] = {
                 form: {"thread_inst_per_inst_div32": round(e[form]["lane_efficiency"], 4),
                        "pred_on_div32": round(e[form]["lane_efficiency_pred_on"], 4)}
-                for form in ("unmelded", "melded") if form in e}
+                for form in ("unmelded", "predicated", "melded", "melded_literal") if form in e}
             row["lane_efficiency"]["source"] = le_src
         sk = "bitonic_step" if key == "bitonic_step" else key
         if sim and sk in sim["utilization"]:
@@ -105,6 +105,31 @@ def ncu_kernel_summary(stem, pattern):
         if pattern in k.get("kernel", ""):
             return k, os.path.relpath(paths[-1], ROOT)
     return None, os.path.relpath(paths[-1], ROOT)
+
+
+def roof(bound, achieved, peak, unit, **extra):
+    """A per-kernel roofline object: achieved / peak of the binding roof."""
+    d = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+         "frac": (achieved / peak) if (achieved is not None and peak) else None}
+    d.update(extra)
+    return d
+
+
+def issue_roof(stem, pattern, seconds, sms, mhz, **extra):
+    """Instruction-issue roof: warp instructions of one launch (the committed
+    ncu summary of the same launch shape) / the live device time, against
+    4 warp instructions per clock per SM (one per scheduler)."""
+    prof, src = ncu_kernel_summary(stem, pattern)
+    if not prof or not prof.get("warp_inst_executed") or not seconds:
+        return roof("issue", None, None, "warp-inst/s", source=src, note="no ncu summary for this kernel")
+    peak = 4.0 * sms * mhz * 1e6
+    return roof("issue", prof["warp_inst_executed"] / seconds, peak, "warp-inst/s",
+                warp_inst_per_launch=prof["warp_inst_executed"], source=src,
+                issue_active_pct_ncu=prof.get("issue_active_pct"), **extra)
+
+
+def cpu_threads():
+    return os.cpu_count() or 1
 
 
 # ------------------------------------------------------------------ clocks
@@ -275,6 +300,8 @@ def workload_config(args, variant):
                         f"(corpus bitonic.ir compare-exchange step chained over every stage)",
             "keys_per_gpu": args.keys, "bucket": args.bucket, "variant": variant,
             "keys_per_thread": args.keys_per_thread or "auto (16)",
+            "form": "melded = the order-flip form (`up` folded into the keys); per_kernel.*.melded_literal_us is "
+                    "App. A.2's select chain",
             "global_batch": args.keys * int(os.environ.get("WORLD_SIZE", "1")), "parallelism": f"dp{args.gpus} (independent buckets)",
             "l2": "flushed (256 MiB write) before every timed step; input restored from a pristine copy"}
 
@@ -311,6 +338,9 @@ def cpu_baseline(args):
 # ------------------------------------------------------------------ per-kernel table
 CORPUS_LANE = ["sb1", "sb1r", "sb2", "sb2r", "sb3", "sb3r", "sb4", "sb4r", "nested"]
 NQ_NODES_16 = 1141190303
+# nodes below the 7-row prefixes of the mirror-symmetric search (row-0 queen in
+# columns 0..7) — the GPU's work per N=16 solve (oracle restatement count)
+NQ_MIRROR_NODES = 568094534
 # A divergent diamond written for this row (not a corpus file): the GPU
 # interpreter runs it from IR text like any reference module.
 DIAMOND_IR = """global x[64]
@@ -341,11 +371,98 @@ fn diamond(%n) {
 """
 
 
+# ------------------------------------------------------------------ CPU baselines (rank 0, N=1)
+def _oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    return oracle
+
+
+def cpu_corpus(kernel, nw):
+    """Config 1 CPU path: the reference's executeWarp (oracle/_ref, unmodified
+    interp.cpp) over all nw makeRandomInput warps of the original and of the
+    runDarm-melded module on all host threads, plus its compareRuns per warp
+    (darm_cli.cpp:250-263's benchOne loop)."""
+    o = _oracle()
+    if not o.reference_available():
+        return None
+    import paper_2107_05681_b200 as darm
+
+    ref = o.Reference()
+    b = darm.make_random_input(kernel, 32, nw, 1000)
+    names = [n for n, _ in ref.load(kernel, 0).globals]
+    g0 = np.concatenate([b.globals[n] for n in names])
+    args = np.array([[16]] if len(b.args) == 1 else [[16, 24]], np.int32)
+    th = cpu_threads()
+    res, out = {}, {}
+    for form, meld in (("unmelded", 0), ("melded", 1)):
+        mod = ref.load(kernel, meld)
+        g = g0.copy()
+        t0 = time.perf_counter()
+        f, _ = mod.execute_warps(32, nw, args, g, 32, None, threads=th, want_stats=False)
+        res[form] = time.perf_counter() - t0
+        out[form] = (g, f)
+    mod = ref.load(kernel, 0)
+    w, _ = ref.compare_warps(mod, 32, nw, 32, out["unmelded"][0], out["unmelded"][1], out["melded"][0],
+                             out["melded"][1])
+    lanes = nw * 32
+    return {"value": lanes / res["melded"], "unit": "lanes/s", "cores": th, "kind": "reference",
+            "unmelded_lanes_per_s": lanes / res["unmelded"], "compare_runs_equal": w == -1,
+            "sample": f"all {nw} warps x 32 lanes (the full config), oracle/_ref executeWarp of the original and "
+                      f"the runDarm-melded module, {th} threads"}
+
+
+def cpu_nqueens(mirror_prefixes):
+    """Config 3 CPU path: the restatement's bitmask DFS (oracle/darm_oracle.c)
+    below the same mirror-symmetric 7-row prefixes the GPU searches, all host threads."""
+    o = _oracle()
+    r = o.Restatement()
+    th = cpu_threads()
+    t0 = time.perf_counter()
+    sols, nodes = r.nqueens_count_threads(16, 7, mirror_prefixes, th)
+    sec = time.perf_counter() - t0
+    assert 2 * sols == 14772512, sols
+    return {"value": nodes / sec, "unit": "nodes/s", "cores": th, "kind": "port", "seconds": sec,
+            "solutions_per_s": 2 * sols / sec,
+            "sample": f"the full N=16 count by mirror symmetry ({len(mirror_prefixes)} prefixes, {nodes} nodes), "
+                      f"{th} threads"}
+
+
+def cpu_lud(n=4096):
+    """Config 4 CPU path: the blocked-LU restatement on all host threads, on a
+    stated subsample (n^2 instead of 8192^2; flops scale as n^3)."""
+    o = _oracle()
+    r = o.Restatement()
+    th = cpu_threads()
+    a = np.random.default_rng(4).random((n, n), dtype=np.float32) + n * np.eye(n, dtype=np.float32)
+    t0 = time.perf_counter()
+    r.lud(a, threads=th)
+    sec = time.perf_counter() - t0
+    flop = (2.0 / 3.0) * n ** 3
+    return {"value": flop / sec / 1e12, "unit": "TFLOP/s", "cores": th, "kind": "port", "seconds": sec,
+            "sample": f"{n}^2 blocked LU ({flop / ((2.0 / 3.0) * 8192 ** 3):.3f} of the 8192^2 flops), {th} threads"}
+
+
+def cpu_srad(n=16384, iters=3):
+    """Config 5 CPU path: the SRAD restatement on all host threads, on the full
+    16384^2 image for a stated subsample of the iterations."""
+    o = _oracle()
+    r = o.Restatement()
+    th = cpu_threads()
+    j = np.exp(np.random.default_rng(5).random((n, n), dtype=np.float32)).astype(np.float32)
+    t0 = time.perf_counter()
+    r.srad(j, iters, 0.5, (0, 127, 0, 127), threads=th)
+    sec = time.perf_counter() - t0
+    return {"value": n * n * iters / sec, "unit": "pixel-iterations/s", "cores": th, "kind": "port",
+            "seconds": sec, "sample": f"{n}^2 image, {iters} of the 100 iterations, {th} threads"}
+
+
 PER_KERNEL_SECTIONS = ("corpus", "nqueens16", "pcm", "ms1m", "interp", "lud8192", "srad", "bitonic")
 
 
 def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None, rank=0, world=1,
-                     sections=PER_KERNEL_SECTIONS, srad_n=16384, srad_iters=100):
+                     sections=PER_KERNEL_SECTIONS, srad_n=16384, srad_iters=100, with_cpu=True):
     """Melded vs unmelded device time for every corpus kernel (config 1 shape:
     2^20 lanes = 32,768 warps of makeRandomInput fixtures, half-warp split),
     N-Queens N=16 (config 3), PCM, MS, LUD 8192^2 (config 4) and SRAD
@@ -361,23 +478,28 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
         return row
 
     nw = 1 << 15
-    for k in (CORPUS_LANE if "corpus" in sections else ()):
-        b = darm.make_random_input(k, 32, nw, 1000)
-        g = {n: torch.from_numpy(a).cuda() for n, a in b.globals.items()}
-        args = [[16]] if len(b.args) == 1 else [[16], [24]]
-        info = darm.kernel_info(k)
-        row = {}
-        for vname, v in (("unmelded", 0), ("melded", 1)):
-            step = darm.execute_warps(k, v, 32, args, g, want_stats=False, stream=stream.cuda_stream,
-                                      prepare_only=True)
-            t = time_steps(torch, stream, lambda: None, step, steps, warmup, flush)
-            row[vname + "_us"] = 1e3 * sum(t) / len(t)
-        alg = info["lane_bytes"] * nw * 32
-        tmax(row)
-        row["speedup"] = row["unmelded_us"] / row["melded_us"]
-        row["melded_GBps"] = alg / (row["melded_us"] * 1e-6) / 1e9
-        row["melded_frac_hbm"] = row["melded_GBps"] / peak
-        out[k] = row
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = sm_max_mhz()
+    cpu = rank == 0 and world == 1 and with_cpu
+    if "corpus" in sections:
+        # graph replay of 100 launches, each on its own 2^20-lane batch (inputs from HBM)
+        from tools.time_corpus import time_corpus
+
+        times = time_corpus(CORPUS_LANE, launches=100, reps=max(3, steps // 4), n_warps=nw)
+        for k in CORPUS_LANE:
+            info = darm.kernel_info(k)
+            row = {f + "_us": times[k][f] for f in ("unmelded", "predicated", "melded")}
+            tmax(row)
+            row["speedup"] = row["unmelded_us"] / row["melded_us"]
+            row["speedup_vs_predicated"] = row["predicated_us"] / row["melded_us"]
+            row["timing"] = "CUDA graph of 100 launches on 100 distinct 2^20-lane batches, per-launch mean, best of reps"
+            alg = info["lane_bytes"] * nw * 32
+            row["roofline"] = roof("hbm", alg / (row["melded_us"] * 1e-6) / 1e9, peak, "GB/s",
+                                   algorithmic_bytes_per_launch=alg,
+                                   bytes_per_lane=info["lane_bytes"], form="melded")
+            if cpu:
+                row["cpu_baseline"] = cpu_corpus(k, nw)
+            out[k] = row
     # N-Queens N=16: the 7-row prefixes dealt round-robin over the ranks
     row = {}
     for vname, v in ((("unmelded", 0), ("melded", 1)) if "nqueens16" in sections else ()):
@@ -397,13 +519,22 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
         row[vname + "_solutions"] = sols
     if "nqueens16" in sections:
         nqueens_row(torch, dist, row, world, tmax)
+        nodes = NQ_MIRROR_NODES
+        row["nodes_searched"] = nodes
+        row["melded_nodes_per_s"] = nodes / (row["melded_us"] * 1e-6)
+        row["roofline"] = issue_roof("nqueens", "nqueens_kernel<1", row["melded_us"] * 1e-6 * world, sms, mhz,
+                                     note="integer-issue bound; nodes below the mirror-symmetric 7-row prefixes")
+        if cpu:
+            o = _oracle()
+            pre = o.Restatement().nqueens_prefixes(16, 7, mirror=True)
+            row["cpu_baseline"] = cpu_nqueens(pre)
         out["nqueens16"] = row
     if "pcm" in sections or "ms1m" in sections or "interp" in sections:
         pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections)
     if "lud8192" in sections:
-        lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax)
+        lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax, cpu)
     if "srad" in sections:
-        srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, srad_n, srad_iters)
+        srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, srad_n, srad_iters, cpu)
     return out
 
 
@@ -413,11 +544,7 @@ def nqueens_row(torch, dist, row, world, tmax):
     row["melded_solutions_per_s"] = 14772512 / (row["melded_us"] * 1e-6)
     row["prefix_rows"], row["mirror_symmetry"] = 7, True
     row["n_gpus"], row["scaling"] = world, "strong (prefixes sharded over the ranks)"
-    prof, src = ncu_kernel_summary("nqueens", "nqueens_kernel<1")
-    row["roofline"] = {"bound": "ALU pipe (integer issue)", "nodes": 1141190303,
-                       "alu_pipe_pct": prof.get("alu_pipe_pct") if prof else None,
-                       "issue_active_pct": prof.get("issue_active_pct") if prof else None,
-                       "source": src}
+    row["full_tree_nodes"] = NQ_NODES_16
 
 
 def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections):
@@ -447,6 +574,7 @@ def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, ou
         row["keys_per_thread"] = kpt or 16
         row["melded_GBps"] = 8.0 * n / (row["melded_us"] * 1e-6) / 1e9
         row["melded_frac_hbm"] = row["melded_GBps"] / peak
+        row["roofline"] = roof("hbm", row["melded_GBps"], peak, "GB/s", algorithmic_bytes_per_launch=8 * n)
         out[name] = row
     n = 1 << 20
     keys = pristine[:n].clone()
@@ -467,7 +595,8 @@ def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, ou
     passes = 1 + max(0, (n // 4096).bit_length() - 1)        # tile pass + one per width >= 4096
     row["melded_GBps"] = 8.0 * n * passes / (row["melded_us"] * 1e-6) / 1e9
     row["melded_frac_hbm"] = row["melded_GBps"] / peak
-    row["roofline_note"] = f"8 B/key per pass x {passes} passes; at 2^20 keys (4 MiB) the passes run from L2"
+    row["roofline"] = roof("hbm", row["melded_GBps"], peak, "GB/s", algorithmic_bytes_per_launch=8 * n * passes,
+                           note=f"8 B/key per pass x {passes} passes; at 2^20 keys (4 MiB) the passes run from L2")
     out["ms1m"] = row
     if "interp" in sections:
         interp_row(torch, darm, dist, steps, warmup, g, out)
@@ -491,11 +620,12 @@ def interp_row(torch, darm, dist, steps, warmup, g, out):
                 ts.append(res.call_stats["kernel_ms"])
         row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(ts) / len(ts))
         row[vname + "_warps_per_s"] = nwi / (row[vname + "_us"] * 1e-6)
-    row["roofline_note"] = "an interpreter: bound by issue per IR instruction, not by bytes"
+    row["roofline"] = roof("issue", None, None, "warp-inst/s",
+                           note="an interpreter: bound by issue per IR instruction, not by bytes; no byte roof")
     out["interp_diamond_32k_warps"] = row
 
 
-def lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax):
+def lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax, cpu=False):
     # LUD 8192^2 fp32 (config 4): the whole decomposition (n/16 + 2n/64 + 1 launches in one graph)
     n = 8192
     g = torch.Generator(device="cuda").manual_seed(4)
@@ -513,10 +643,15 @@ def lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax):
     roof = sms * 256 * sm_max_mhz() * 1e6 / 1e12             # fp32 FMA: 128 lanes x 2 flop per SM per clock
     row["fp32_roof_TFLOPs"] = roof
     row["melded_frac_fp32"] = row["melded_TFLOPs"] / roof
+    row["roofline"] = {"bound": "fp32 FMA (CUDA cores)", "achieved": row["melded_TFLOPs"], "peak": roof,
+                       "unit": "TFLOP/s", "frac": row["melded_frac_fp32"],
+                       "algorithmic_flop": (2.0 / 3.0) * n ** 3, "peak_source": "SMs x 128 FMA x 2 x sm_max_mhz"}
+    if cpu:
+        row["cpu_baseline"] = cpu_lud()
     out["lud8192"] = row
 
 
-def srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, n=16384, iters=100):
+def srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, n=16384, iters=100, cpu=False):
     # SRAD 16384^2 fp32 x 100 iterations (config 5): one GPU, or row tiles with a
     # halo exchange and the ROI all-reduce every iteration over NCCL
     g = torch.Generator(device="cuda").manual_seed(4)
@@ -588,8 +723,15 @@ def srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, n=16384,
         row["melded_frac_hbm"] = row["melded_GBps"] / (peak * world)
         row["n_gpus"], row["scaling"] = world, ("strong (row tiles, peer-memory halos)" if world > 1 else
                                                 "single GPU")
-        row["arithmetic"] = ("reciprocal-multiply divisions + FMA, within 1e-5 relative (DARM_FAST_MATH)" if fast
+        row["arithmetic"] = ("one reciprocal per pixel, f32x2 FMA (DARM_FAST_MATH), within 1e-5 relative" if fast
                              else "IEEE, bit-exact vs the restatement")
+        row["roofline"] = roof("hbm", row["melded_GBps"], peak * world, "GB/s", algorithmic_bytes=alg,
+                               bytes_per_px_iter=8, note="one read of J and one write of J' per pixel and iteration")
+        row["melded_pixel_iters_per_s"] = n * n * iters / (row["melded_us"] * 1e-6)
+        if cpu and fast:
+            row["cpu_baseline"] = out[tag]["cpu_baseline"]
+        elif cpu:
+            row["cpu_baseline"] = cpu_srad()
         out[key] = row
     return out
 
@@ -669,43 +811,41 @@ def our_arm(args):
         if bad:
             raise SystemExit(f"unknown --kernels {sorted(bad)}; choose from {PER_KERNEL_SECTIONS}")
         per_kernel = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak0, dist, rank, world,
-                                      sections, args.srad_size, args.srad_iters)
+                                      sections, args.srad_size, args.srad_iters, with_cpu=not args.no_cpu_baseline)
     if per_kernel is not None and "bitonic" in sections:
-        per_kernel["bitonic"] = {"unmelded_us": 1e3 * results["unmelded"]["kernel_ms_mean"],
-                                 "melded_us": 1e3 * results["melded"]["kernel_ms_mean"],
-                                 "speedup": results["unmelded"]["total_ms"] / results["melded"]["total_ms"],
-                                 "keys_per_thread": kpt,
-                                 "melded_frac_hbm": 8 * n / results["melded"]["kernel_ms_mean"] / 1e6 / peak0}
-        # the IR warp shape: one key (one IR lane) per hardware thread
-        row = {}
-        for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
-            step = darm.bitonic_sort(work, B, variant, stream=stream.cuda_stream, want_stats=False,
-                                     prepare_only=True, keys_per_thread=1)
-            t = time_steps(torch, stream, lambda: work.copy_(pristine), step, args.steps, args.warmup, flush)
-            if not torch.equal(work, want):
-                raise SystemExit(f"bitonic one-key {vname}: result is not the bucket-sorted input")
-            row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(t) / len(t))
-        row["speedup"] = row["unmelded_us"] / row["melded_us"]
-        row["keys_per_thread"] = 1
-        row["melded_frac_hbm"] = 8 * n / (row["melded_us"] * 1e-6) / 1e9 / peak0
-        per_kernel["bitonic_1key"] = row
-        # bucket sweep (B = 256 .. 4096; 16 keys per
-        # thread, buckets over 512 keys span warps and exchange through shared memory)
-        for Bs in (256, 1024, 4096):
-            want_s = torch.sort(pristine.view(-1, Bs), dim=1).values.view(-1)
+        # every shape in four forms: unmelded (IPDOM branches), predicated
+        # (ptxas if-conversion of the same CFG), melded (the order-flip form the
+        # headline reports: `up` folded into the data) and melded_literal (App.
+        # A.2's select chain on `up` as runDarm prints it) — the literal form
+        # isolates the melding gain, the order-flip form adds the data rewrite
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        forms = (("unmelded", darm.UNMELDED), ("predicated", darm.PREDICATED), ("melded", darm.MELDED),
+                 ("melded_literal", darm.MELDED_LITERAL))
+        shapes = [("bitonic", B, 0), ("bitonic_1key", B, 1)] + [(f"bitonic_B{b}", b, 0) for b in (256, 1024, 4096)] + \
+                 [(f"bitonic_B{b}_1key", b, 1) for b in (256, 1024)]
+        for key, Bs, kp in shapes:
+            want_s = want if Bs == B else torch.sort(pristine.view(-1, Bs), dim=1).values.view(-1)
             row = {}
-            for vname, variant in (("unmelded", darm.UNMELDED), ("melded", darm.MELDED)):
+            for vname, variant in forms:
+                if key == "bitonic" and vname in ("unmelded", "melded") and kp == (args.keys_per_thread or 0):
+                    row[vname + "_us"] = 1e3 * results[vname]["kernel_ms_mean"]
+                    continue
                 step = darm.bitonic_sort(work, Bs, variant, stream=stream.cuda_stream, want_stats=False,
-                                         prepare_only=True)
+                                         prepare_only=True, keys_per_thread=kp)
                 t = time_steps(torch, stream, lambda: work.copy_(pristine), step, args.steps, args.warmup, flush)
                 if not torch.equal(work, want_s):
-                    raise SystemExit(f"bitonic B={Bs} {vname}: result is not the bucket-sorted input")
+                    raise SystemExit(f"{key} {vname}: result is not the bucket-sorted input")
                 row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(t) / len(t))
             row["speedup"] = row["unmelded_us"] / row["melded_us"]
-            row["keys_per_thread"] = 16
-            row["melded_hbm_gbs"] = 8 * n / (row["melded_us"] * 1e-6) / 1e9
-            row["melded_frac_hbm"] = row["melded_hbm_gbs"] / peak0
-            per_kernel[f"bitonic_B{Bs}"] = row
+            row["speedup_literal"] = row["unmelded_us"] / row["melded_literal_us"]
+            row["speedup_vs_predicated"] = row["predicated_us"] / row["melded_us"]
+            row["keys_per_thread"] = kp or 16
+            row["bucket"] = Bs
+            gbs = 8 * n / (row["melded_us"] * 1e-6) / 1e9
+            kpt_name = f"bitonic_sort_reg_kernel<1, {Bs}, 16" if kp != 1 else f"bitonic_sort_kernel<1, {Bs},"
+            row["roofline"] = roof("hbm", gbs, peak0, "GB/s", algorithmic_bytes_per_launch=8 * n, form="melded",
+                                   issue=issue_roof("bitonic", kpt_name, row["melded_us"] * 1e-6, sms, sm_max_mhz()))
+            per_kernel[key] = row
 
     if rank != 0:
         if dist:
@@ -743,9 +883,12 @@ def our_arm(args):
                      "kernel": kname.format("true"),
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "alu_pipe_pct": (prof_m or {}).get("alu_pipe_pct"),
-                     "note": "instruction-issue-bound (83% issue-active in ncu: VIMNMX compare-exchanges on the "
-                             "ALU pipe, half the in-register maxima as IMADs on the FMA pipe, 21 steps per key); "
-                             "see DESIGN.md §5"},
+                     "issue": issue_roof("bitonic", kname.format(1), mel["kernel_ms_mean"] / 1e3,
+                                         torch.cuda.get_device_properties(torch.cuda.current_device())
+                                         .multi_processor_count, sm_max_mhz()),
+                     "note": "instruction-issue-bound (VIMNMX compare-exchanges on the ALU pipe, half the "
+                             "in-register maxima as IMADs on the FMA pipe, 21 steps per key): the `issue` object is "
+                             "the binding roof; see DESIGN.md §5"},
         "e2e": {"value": n * world / (e2e_total / args.steps / 1e3), "unit": "keys/s",
                 "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                 "how": "darm_gpu_bitonic_sort(mem=HOST) on pinned numpy buffers; library CUDA events t0..t3"},

@@ -271,7 +271,7 @@ int oracle_merge_sort(int32_t *keys, int64_t n) {
  * rows 0..base-1, lowest free column first; prefix i belongs to rank i % world. */
 typedef struct {
   int n, base, rank, world;
-  uint32_t mask;
+  uint32_t mask, row0;   /* row0: the columns row 0 may take */
   uint32_t *out;
   int64_t cap, idx, kept;
 } nq_enum;
@@ -289,7 +289,7 @@ static void nq_prefix_rec(nq_enum *e, int row, uint32_t cols, uint32_t d1, uint3
     e->idx++;
     return;
   }
-  uint32_t av = ~(cols | d1 | d2) & e->mask;
+  uint32_t av = ~(cols | d1 | d2) & (row == 0 ? e->row0 : e->mask);
   while (av) {
     uint32_t bit = av & (0u - av);
     av ^= bit;
@@ -298,7 +298,14 @@ static void nq_prefix_rec(nq_enum *e, int row, uint32_t cols, uint32_t d1, uint3
 }
 
 int64_t oracle_nqueens_prefixes(int n, int base, int rank, int world, uint32_t *out, int64_t cap) {
-  nq_enum e = {n, base, rank, world, n >= 32 ? 0xffffffffu : ((1u << n) - 1u), out, cap, 0, 0};
+  return oracle_nqueens_prefixes_ex(n, base, rank, world, 0, out, cap);
+}
+
+/* mirror: row 0 only in the columns < ceil(n/2) (the GPU's DARM_NQ_MIRROR
+ * prefix set; for even n every kept placement counts twice) */
+int64_t oracle_nqueens_prefixes_ex(int n, int base, int rank, int world, int mirror, uint32_t *out, int64_t cap) {
+  const uint32_t mask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+  nq_enum e = {n, base, rank, world, mask, mirror ? ((1u << ((n + 1) / 2)) - 1u) : mask, out, cap, 0, 0};
   nq_prefix_rec(&e, 0, 0, 0, 0);
   return e.kept;
 }

@@ -61,6 +61,7 @@ int oracle_merge_sort(int32_t *keys, int64_t n);
  * number kept.  oracle_nqueens_count returns the total solutions below the
  * prefixes, per-prefix counts, and the placements made below them (`nodes`). */
 int64_t oracle_nqueens_prefixes(int n, int base, int rank, int world, uint32_t *out, int64_t cap);
+int64_t oracle_nqueens_prefixes_ex(int n, int base, int rank, int world, int mirror, uint32_t *out, int64_t cap);
 uint64_t oracle_nqueens_count(int n, int base, const uint32_t *states, int64_t count, uint32_t *per_prefix,
                               uint64_t *nodes);
 

@@ -67,6 +67,8 @@ class Restatement:
         L.oracle_nqueens_prefixes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, U32P,
                                               ctypes.c_int64]
         L.oracle_nqueens_prefixes.restype = ctypes.c_int64
+        L.oracle_nqueens_prefixes_ex.argtypes = [ctypes.c_int] * 5 + [U32P, ctypes.c_int64]
+        L.oracle_nqueens_prefixes_ex.restype = ctypes.c_int64
         L.oracle_nqueens_count.argtypes = [ctypes.c_int, ctypes.c_int, U32P, ctypes.c_int64, U32P,
                                            ctypes.POINTER(ctypes.c_uint64)]
         L.oracle_nqueens_count.restype = ctypes.c_uint64
@@ -131,11 +133,24 @@ class Restatement:
         if rc:
             raise ValueError(f"oracle_srad -> {rc}")
 
-    def nqueens_prefixes(self, n: int, base: int, rank: int = 0, world: int = 1) -> np.ndarray:
-        cnt = self.lib.oracle_nqueens_prefixes(n, base, rank, world, None, 0)
+    def nqueens_prefixes(self, n: int, base: int, rank: int = 0, world: int = 1, mirror: bool = False) -> np.ndarray:
+        cnt = self.lib.oracle_nqueens_prefixes_ex(n, base, rank, world, int(mirror), None, 0)
         out = np.zeros(3 * max(1, cnt), dtype=np.uint32)
-        self.lib.oracle_nqueens_prefixes(n, base, rank, world, _p(out, ctypes.POINTER(ctypes.c_uint32)), cnt)
+        self.lib.oracle_nqueens_prefixes_ex(n, base, rank, world, int(mirror),
+                                            _p(out, ctypes.POINTER(ctypes.c_uint32)), cnt)
         return out[: 3 * cnt].reshape(-1, 3)
+
+    def nqueens_count_threads(self, n: int, base: int, states: np.ndarray, threads: int = 0):
+        """nqueens_count over contiguous chunks of `states` on `threads` host
+        threads (ctypes releases the GIL) -> (solutions, nodes below the prefixes)."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        threads = threads or (os.cpu_count() or 1)
+        chunks = np.array_split(np.arange(len(states)), threads * 8)
+        with ThreadPoolExecutor(threads) as ex:
+            res = list(ex.map(lambda ix: self.nqueens_count(n, base, states[ix])[::2] if len(ix) else (0, 0),
+                              chunks))
+        return sum(r[0] for r in res), sum(r[1] for r in res)
 
     def nqueens_count(self, n: int, base: int, states: np.ndarray):
         """-> (total solutions, per-prefix counts, placements below the prefixes)."""

@@ -24,7 +24,7 @@ def label(name):
     fam, _, targs = base.partition("<")
     args = [a.strip() for a in targs.rstrip(">").split(",")] if targs else []
     def form(x):
-        return "melded" if x in ("1", "true") else "unmelded"
+        return {"1": "melded", "true": "melded", "2": "predicated", "3": "melded_literal"}.get(x, "unmelded")
     if fam == "corpus_lanes":
         k = args[0].lower()
         k = {"sb2t<0>": "sb2", "sb2t<1>": "sb2r", "sb3t<0>": "sb3", "sb3t<1>": "sb3r", "sb4t<0>": "sb4",

@@ -19,21 +19,21 @@ def main():
     for k in CORPUS:
         b = darm.make_random_input(k, 32, nw, 1000)
         args = b.args if k == "bitonic" else ([[16]] if len(b.args) == 1 else [[16], [24]])
-        for v in (0, 1):
+        for v in ((0, 1) if k == "bitonic" else (0, 1, 2)):   # + the predicated form of the corpus lanes
             g = {n: torch.from_numpy(a.copy()).cuda() for n, a in b.globals.items()}
             sh = {n: torch.from_numpy(a).cuda() for n, a in b.shared.items()} or None
             darm.execute_warps(k, v, 32, args, g, sh, want_stats=False)
     n = 1 << 22
     gen = torch.Generator(device="cuda").manual_seed(3)
     keys = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=gen)
-    for sort in (darm.bitonic_sort, darm.oddeven_sort):
+    for sort, forms in ((darm.bitonic_sort, (0, 1, 2, 3)), (darm.oddeven_sort, (0, 1, 2))):
         for kpt in (16, 1):
-            for v in (0, 1):
+            for v in forms:
                 sort(keys.clone(), 64, v, want_stats=False, keys_per_thread=kpt)
     for v in (0, 1):
         darm.merge_sort(keys[: 1 << 20].clone(), v, want_stats=False)
     for v in (0, 1):
-        darm.nqueens(14, 5, v, want_stats=False)
+        darm.nqueens(14, 5, v, want_stats=False, mirror=True)
     a0 = torch.rand((2048, 2048), generator=gen, device="cuda") + 2048 * torch.eye(2048, device="cuda")
     for v in (0, 1):
         darm.lud(a0.clone(), v, want_stats=False)

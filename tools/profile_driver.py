@@ -29,15 +29,15 @@ def main(which, bucket=64):
         n = 16384
         g = torch.Generator(device="cuda").manual_seed(5)
         j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
-        for fast in (False, True):
+        for fast in (False, True):       # one sweep per form: IEEE unmelded, melded, then fast
             for v in (darm.UNMELDED, darm.MELDED):
                 j = j0.clone()
-                darm.srad(j, 2, 0.5, darm.RODINIA_ROI, v, want_stats=False, fast=fast)
+                darm.srad(j, 1, 0.5, darm.RODINIA_ROI, v, want_stats=False, fast=fast)
         torch.cuda.synchronize()
         return
     if which == "nqueens":
-        for v in (darm.UNMELDED, darm.MELDED):
-            assert darm.nqueens(16, 6, v, want_stats=False)[0] == 14772512
+        for v in (darm.UNMELDED, darm.MELDED):   # the bench's launch: 7-row prefixes, mirror symmetry
+            assert darm.nqueens(16, 7, v, want_stats=False, mirror=True)[0] == 14772512
         return
     if which == "merge":
         n = bucket if bucket > 64 else 1 << 24
@@ -62,8 +62,9 @@ def main(which, bucket=64):
         n = 1 << 24
         g = torch.Generator(device="cuda").manual_seed(1234)
         pristine = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
-        for kpt in (0, 1):       # register-blocked (auto: 16 keys per thread), then one key per thread
-            for v in (darm.UNMELDED, darm.MELDED):
+        kpts = (0, 1) if bucket <= 1024 else (0,)
+        for kpt in kpts:       # register-blocked (auto: 16 keys per thread), then one key per thread
+            for v in (darm.UNMELDED, darm.MELDED, darm.PREDICATED, darm.MELDED_LITERAL):
                 k = pristine.clone()
                 darm.bitonic_sort(k, bucket, v, want_stats=False, keys_per_thread=kpt)
         torch.cuda.synchronize()
@@ -71,7 +72,7 @@ def main(which, bucket=64):
         nw = 1 << 15
         b = darm.make_random_input(which, 32, nw, 1000)
         args = [[16]] if len(darm.kernel_info(which)["params"]) == 1 else [[16], [24]]
-        for v in (darm.UNMELDED, darm.MELDED):
+        for v in (darm.UNMELDED, darm.MELDED, darm.PREDICATED):
             g = {n: torch.from_numpy(a.copy()).cuda() for n, a in b.globals.items()}
             sh = {n: torch.from_numpy(a).cuda() for n, a in b.shared.items()} or None
             darm.execute_warps(which, v, 32, args if which != "bitonic" else b.args, g, sh, want_stats=False)
