@@ -132,7 +132,9 @@ OE_IR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def oddeven_sort_fixtures(ref: Reference) -> dict:
     """PCM: the reference interpreter chains ir/oddeven_step.ir (original and
     as melded by runDarm) over every Batcher odd-even merge step of B-key
-    buckets: sorted outputs and unit-latency simulator statistics."""
+    buckets: sorted outputs and the simulator statistics (unit and default
+    latencies: issued, threadCycles, usefulThreadCycles, serializedCycles,
+    divergentBranchCount, sharedMemIssues, globalMemIssues)."""
     from oracle import oddeven_schedule
 
     text = open(OE_IR).read()
@@ -151,8 +153,13 @@ def oddeven_sort_fixtures(ref: Reference) -> dict:
             st_m = meld.chain_sort(b, B, oddeven_schedule(B), unit_latency=True)
             assert (a == b).all()
             assert (a.reshape(-1, B) == np.sort(keys.reshape(-1, B), axis=1)).all()
+            c, d = keys.copy(), keys.copy()
+            dl_u = mod.chain_sort(c, B, oddeven_schedule(B))
+            dl_m = meld.chain_sort(d, B, oddeven_schedule(B))
+            assert (c == a).all() and (d == a).all()
             out["cases"].append({"bucket": B, "keys": keys.tolist(), "sorted": a.tolist(),
-                                 "stats_unit_latency": {"unmelded": st_u.tolist(), "melded": st_m.tolist()}})
+                                 "stats_unit_latency": {"unmelded": st_u.tolist(), "melded": st_m.tolist()},
+                                 "stats_default_latency": {"unmelded": dl_u.tolist(), "melded": dl_m.tolist()}})
     return out
 
 

@@ -1,25 +1,41 @@
 // oddeven_sort.cu — PCM: Batcher odd-even merge sort of
 // independent buckets, built from the step of paper_2107_05681_b200/ir/
-// oddeven_step.ir in its unmelded and melded forms.  The reference has no PCM
-// code; the step is written in the reference's mini-IR and the melded form is
-// what runDarm emits for it (one region-region meld, as for bitonic.ir: the
-// partner compare is melded and one select picks gt / lt by the role).
+// oddeven_step.ir in three forms.  The reference has no PCM code; the step is
+// written in the reference's mini-IR and the melded form is what runDarm emits
+// for it: a block-region meld of the upper comparator
+// region with the idle block (region replication), then a region-region meld
+// of the lower region with the result.
 //
 // Step (p, k) over a B-key bucket: comparators (x, x + k) for every x with
 // x >= k % p, (x - k % p) mod 2k < k, x + k < B and x, x + k in the same 2p
 // block; the lower end keeps the smaller key, the upper end the larger, other
-// lanes are idle (their own partner).  Steps: p = 1, 2, .., B/2; k = p, .., 1.
+// lanes are idle.  Steps: p = 1, 2, .., B/2; k = p, .., 1.
 //
+// The IR's step reads the bucket from shared memory inside the divergent
+// region — three-way, lower / upper / idle — and each comparator arm holds a
+// nested data-dependent if-then ("loops with nested data-dependent branches",
+// PAPER.md:753; "complex control-flow regions with shared memory
+// instructions", :835-836):
+//   lower: x0 = buf[t+k]; cv = buf[t]; res[t] = cv; if (cv > x0) res[t] = x0
+//   upper: x1 = buf[t-k]; dv = buf[t]; res[t] = dv; if (dv < x1) res[t] = x1
+//   idle:  res[t] = buf[t]
+// Forms:
+//   unmelded   that CFG with its IPDOM reconvergence: the role branch and the
+//              nested data-dependent branches are real divergent branches
+//              (DARM_IPDOM), the shared loads inside the arms;
+//   predicated the same CFG as ptxas compiles it (short arms if-converted);
+//   melded     runDarm's output: the partner and own loads hoisted and melded
+//              (one load at a selected address), the comparison direction and
+//              the stored value as selects, one store.
 // Two shapes, as for the bitonic sort (bitonic_sort.cu):
-//   one key per thread (the IR warp shape): partner by __shfl_sync inside a
-//     warp, through shared memory when it may sit in another warp; the
-//     divergent branch is the lower / not-lower role of every lane;
+//   one key per thread (the IR warp shape): the bucket staged in shared
+//     memory every step (double-buffered), the roles per lane;
 //   R keys per thread: strides below R pair registers of one thread
-//     (compile-time roles) or the top k registers of a thread with the bottom
-//     k of the next (one shuffle each way), strides k >= R pair whole threads
-//     (role per thread, the divergent branch).
-// Unmelded: `if (lower) keep min else keep max`, both arms fenced (DARM_ARM).
-// Melded:   the select of SURVEY App. A.2's shape: v = lower ? min : max.
+//     (compile-time roles, no divergence in any form) or the top k registers
+//     of a thread with the bottom k of the next; strides k >= R pair whole
+//     threads: the R keys are staged in shared memory ([R/4][thread] int4s,
+//     conflict-free) and the role is per thread — the divergent region, with
+//     one nested data-dependent branch per key.
 #include <climits>
 
 #include "common.cuh"
@@ -45,28 +61,31 @@ __device__ __forceinline__ bool oe_is_upper(int x) {
   else return !(x & k) && (x & (2 * p - 1)) >= k;
 }
 
-// lower ? min(v, b) : max(v, b) issued as a complementary predicated pair:
-// for the plain select ptxas emits min; @!P max, whose write-after-write on
-// one register stalls every serial step.
-__device__ __forceinline__ int32_t oe_select_minmax(int32_t v, int32_t b, bool lower) {
-  asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p min.s32 %0, %0, %2;\n @!p max.s32 %0, %0, %2;\n}"
-      : "+r"(v)
-      : "r"(int(lower)), "r"(b));
-  return v;
-}
-
+// One comparator region of the IR for one key: own key cv, partner key xp
+// (read inside the arm by the caller), role lower / upper / idle.
+//   F == kUnmelded: res = cv; if (out of order) res = xp — behind a real branch.
 template <int F>
-__device__ __forceinline__ int32_t oe_exchange_unmelded(int32_t v, int32_t b0, bool lower) {
-  if (lower) {                                             // condbr %lower ^lo ^up
-    DARM_ARM_F(F, "oddeven.lo");
-    v = min(v, b0);                                        // ^lo: cv > b0 -> store b0
-    DARM_ARM("oddeven.lo.end");
-  } else {
-    DARM_ARM_F(F, "oddeven.up");
-    v = max(v, b0);                                        // ^up: cv < b0 -> store b0
-    DARM_ARM("oddeven.up.end");
+__device__ __forceinline__ int32_t oe_arm_lower(int32_t cv, int32_t xp) {
+  int32_t r = cv;                                          // store.global res %t %cv
+  if (cv > xp) {                                           // condbr %g1 ^ls ^lx
+    DARM_ARM_F(F, "oddeven.ls");
+    r = xp;                                                // ^ls: store.global res %t %x0
   }
-  return v;
+  return r;
+}
+template <int F>
+__device__ __forceinline__ int32_t oe_arm_upper(int32_t dv, int32_t xp) {
+  int32_t r = dv;                                          // store.global res %t %dv
+  if (dv < xp) {                                           // condbr %g2 ^us ^ux
+    DARM_ARM_F(F, "oddeven.us");
+    r = xp;                                                // ^us: store.global res %t %x1
+  }
+  return r;
+}
+// melded: out of order = lower ? cv > xp : upper ? cv < xp : false; one store
+__device__ __forceinline__ int32_t oe_melded(int32_t cv, int32_t xp, bool lower, bool upper) {
+  const bool swap = lower ? (cv > xp) : (upper && cv < xp);
+  return swap ? xp : cv;
 }
 
 }  // namespace
@@ -86,38 +105,46 @@ __device__ __forceinline__ void oe_roles(int t, uint64_t &lo, uint64_t &up) {
   }
 }
 
-template <int F, int CTA, int p, int k, int s>
-__device__ __forceinline__ int32_t oe_one_step(int32_t v, int lane, uint64_t lo, uint64_t up, int32_t (*xch)[CTA],
-                                               int &par) {
+template <int F, int B, int CTA, int p, int k, int s>
+__device__ __forceinline__ int32_t oe_one_step(int32_t v, uint64_t lo, uint64_t up, int32_t (*buf)[CTA], int &par) {
   const bool lower = (lo >> s) & 1u;
   const bool upper = (up >> s) & 1u;
-  int32_t b0;                                              // load.shared buf %j (partner, or own slot)
-  // x + k stays in x's warp unless k >= 32 or (k < p) the add carries across
-  // a 32-key boundary inside a 2p > 32 block
-  if constexpr (k < 32 && (k == p || 2 * p <= 32)) {
-    const int src = lower ? lane + k : (upper ? lane - k : lane);
-    b0 = __shfl_sync(0xffffffffu, v, src);
+  const int t = int(threadIdx.x);
+  int32_t *b = buf[par];
+  b[t] = v;                                                // the bucket in shared buf
+  if constexpr (B <= 32) __syncwarp();                     // a bucket never spans warps
+  else __syncthreads();
+  par ^= 1;                                                // double buffer: no barrier before the next write
+  if constexpr (F == kMelded) {
+    // the hoisted, melded loads: partner at a selected address, own key
+    const int32_t xp = b[lower ? t + k : (upper ? t - k : t)];
+    const int32_t cv = b[t];
+    return oe_melded(cv, xp, lower, upper);
   } else {
-    xch[par][threadIdx.x] = v;
-    __syncthreads();
-    b0 = xch[par][lower ? threadIdx.x + k : (upper ? threadIdx.x - k : threadIdx.x)];
-    par ^= 1;
+    int32_t r;
+    if (lower) {                                           // condbr %lower ^lo ^nl
+      DARM_ARM_F(F, "oddeven.lo");
+      r = oe_arm_lower<F>(b[t], b[t + k]);                 // ^lo: load.shared buf %t, buf %tk
+    } else if (upper) {                                    // ^nl: condbr %upper ^up ^id
+      DARM_ARM_F(F, "oddeven.up");
+      r = oe_arm_upper<F>(b[t], b[t - k]);                 // ^up: load.shared buf %t, buf %s
+    } else {
+      DARM_ARM_F(F, "oddeven.id");
+      r = b[t];                                            // ^id: load.shared buf %t
+    }
+    return r;
   }
-  if constexpr (F == kMelded)
-    return oe_select_minmax(v, b0, lower);   // %sel = select %lower %g1 %g2; one store
-  else
-    return oe_exchange_unmelded<F>(v, b0, lower);
 }
 
 template <int F, int B, int CTA, int p, int k, int s>
-__device__ __forceinline__ int32_t oe_one_network(int32_t v, int lane, uint64_t lo, uint64_t up,
-                                                  int32_t (*xch)[CTA], int &par) {
+__device__ __forceinline__ int32_t oe_one_network(int32_t v, uint64_t lo, uint64_t up, int32_t (*buf)[CTA],
+                                                  int &par) {
   if constexpr (p < B) {
-    v = oe_one_step<F, CTA, p, k, s>(v, lane, lo, up, xch, par);
+    v = oe_one_step<F, B, CTA, p, k, s>(v, lo, up, buf, par);
     if constexpr (k > 1)
-      return oe_one_network<F, B, CTA, p, k / 2, s + 1>(v, lane, lo, up, xch, par);
+      return oe_one_network<F, B, CTA, p, k / 2, s + 1>(v, lo, up, buf, par);
     else
-      return oe_one_network<F, B, CTA, 2 * p, 2 * p, s + 1>(v, lane, lo, up, xch, par);
+      return oe_one_network<F, B, CTA, 2 * p, 2 * p, s + 1>(v, lo, up, buf, par);
   }
   return v;
 }
@@ -125,9 +152,8 @@ __device__ __forceinline__ int32_t oe_one_network(int32_t v, int lane, uint64_t 
 template <int F, int B, int CTA>
 __global__ void __launch_bounds__(CTA) oddeven_sort_kernel(int32_t *__restrict__ keys, uint32_t n) {
   static_assert(__builtin_ctz(B) * (__builtin_ctz(B) + 1) / 2 <= 64, "step masks are 64-bit");
-  __shared__ int32_t xch[2][CTA];
+  __shared__ int32_t buf[2][CTA];
   const int t = int(threadIdx.x) & (B - 1);
-  const int lane = int(threadIdx.x) & 31;
   uint64_t lo = 0, up = 0;
   oe_roles<B, 1, 1, 0>(t, lo, up);
   const uint32_t tiles = (n + CTA - 1) / CTA;
@@ -135,7 +161,7 @@ __global__ void __launch_bounds__(CTA) oddeven_sort_kernel(int32_t *__restrict__
     const uint32_t id = tile * CTA + threadIdx.x;
     int32_t v = id < n ? keys[id] : INT_MAX;
     int par = 0;
-    v = oe_one_network<F, B, CTA, 1, 1, 0>(v, lane, lo, up, xch, par);
+    v = oe_one_network<F, B, CTA, 1, 1, 0>(v, lo, up, buf, par);
     if (id < n) keys[id] = v;
   }
 }
@@ -144,35 +170,52 @@ __global__ void __launch_bounds__(CTA) oddeven_sort_kernel(int32_t *__restrict__
 // One step (p, k) on the R registers of a thread; p and k are template
 // parameters so every register index and role test is resolved at compile time.
 template <int F, int B, int R, int p, int k>
-__device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, int x0) {
+__device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, int x0, int4 (*xs)[256]) {
   constexpr int P = B / R;
   if constexpr (k >= R) {
-    // whole threads pair up: partner lane +- k/R, same register; role per thread
+    // whole threads pair up: partner thread +- k/R, same register; role per
+    // thread.  The R keys go through shared memory (the IR's buf): written by
+    // every thread, read by its partner inside the divergent region.
     const bool lower = oe_is_lower<p, k>(x0);
     const bool upper = oe_is_upper<p, k>(x0);
-    const int src = lower ? lane + k / R : (upper ? lane - k / R : lane);
-    int32_t b0[R];
+    const int t = int(threadIdx.x);
+    __syncwarp();                                          // the previous step's reads are done
 #pragma unroll
-    for (int j = 0; j < R; ++j) b0[j] = __shfl_sync(0xffffffffu, v[j], src);
+    for (int q = 0; q < R / 4; ++q) xs[q][t] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    __syncwarp();
+    auto partner = [&](int src, int32_t (&xp)[R]) {       // load.shared buf %tk / %s
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        const int4 x = xs[q][src];
+        xp[4 * q] = x.x;
+        xp[4 * q + 1] = x.y;
+        xp[4 * q + 2] = x.z;
+        xp[4 * q + 3] = x.w;
+      }
+    };
     if constexpr (F == kMelded) {
-      // the select as a complementary predicated pair (see oe_one_step) from 8
-      // keys per thread up; at 4 the plain select schedules better (57 vs 63 µs)
+      int32_t xp[R];
+      partner(lower ? t + k / R : (upper ? t - k / R : t), xp);   // one load, selected address
 #pragma unroll
-      for (int j = 0; j < R; ++j)
-        v[j] = R >= 8 ? oe_select_minmax(v[j], b0[j], lower) : (lower ? min(v[j], b0[j]) : max(v[j], b0[j]));
+      for (int j = 0; j < R; ++j) v[j] = oe_melded(v[j], xp[j], lower, upper);
     } else {
-      if (lower) {                                         // condbr %lower ^lo ^up
+      if (lower) {                                         // condbr %lower ^lo ^nl
         DARM_ARM_F(F, "oddeven.reg.lo");
+        int32_t xp[R];
+        partner(t + k / R, xp);
 #pragma unroll
-        for (int j = 0; j < R; ++j) v[j] = min(v[j], b0[j]);
-        DARM_ARM("oddeven.reg.lo.end");
-      } else {
+        for (int j = 0; j < R; ++j) v[j] = oe_arm_lower<F>(v[j], xp[j]);
+      } else if (upper) {                                  // ^nl: condbr %upper ^up ^id
         DARM_ARM_F(F, "oddeven.reg.up");
+        int32_t xp[R];
+        partner(t - k / R, xp);
 #pragma unroll
-        for (int j = 0; j < R; ++j) v[j] = max(v[j], b0[j]);
-        DARM_ARM("oddeven.reg.up.end");
+        for (int j = 0; j < R; ++j) v[j] = oe_arm_upper<F>(v[j], xp[j]);
+      } else {
+        DARM_ARM_F(F, "oddeven.reg.id");                   // ^id: the own keys stay
       }
     }
+    (void)lane;
   } else if constexpr (2 * p <= R) {
     // the whole 2p block sits in this thread: compile-time comparators
 #pragma unroll
@@ -215,13 +258,13 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
 
 // steps k = K, K/2, .., 1 of stage p, then the next stage
 template <int F, int B, int R, int p, int k>
-__device__ __forceinline__ void oe_reg_network(int32_t (&v)[R], int lane, int tib, int x0) {
+__device__ __forceinline__ void oe_reg_network(int32_t (&v)[R], int lane, int tib, int x0, int4 (*xs)[256]) {
   if constexpr (p < B) {
-    oe_reg_step<F, B, R, p, k>(v, lane, tib, x0);
+    oe_reg_step<F, B, R, p, k>(v, lane, tib, x0, xs);
     if constexpr (k > 1)
-      oe_reg_network<F, B, R, p, k / 2>(v, lane, tib, x0);
+      oe_reg_network<F, B, R, p, k / 2>(v, lane, tib, x0, xs);
     else
-      oe_reg_network<F, B, R, 2 * p, 2 * p>(v, lane, tib, x0);
+      oe_reg_network<F, B, R, 2 * p, 2 * p>(v, lane, tib, x0, xs);
   }
 }
 
@@ -253,6 +296,7 @@ __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__res
   static_assert(R >= 4 && R <= B && P <= 32, "R keys per thread, at most 32 threads per bucket");
   // CTA-uniform walk over 256 R-key tiles: ptxas sees every shuffle converged
   constexpr uint32_t kTile = 256u * R;
+  __shared__ int4 xs[R / 4][256];                          // the cross-thread steps' buf
   const int lane = int(threadIdx.x) & 31;
   const int tib = lane & (P - 1);
   const int x0 = tib * R;                                  // bucket index of register 0
@@ -266,7 +310,7 @@ __global__ void __launch_bounds__(256, 4) oddeven_sort_reg_kernel(int32_t *__res
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = nxt[j];
     if (tile + gridDim.x < tiles) oe_load_keys<R>(nxt, keys, base + gridDim.x * kTile, n);
-    oe_reg_network<F, B, R, 1, 1>(v, lane, tib, x0);
+    oe_reg_network<F, B, R, 1, 1>(v, lane, tib, x0, xs);
     if (base < n && R % 8 == 0 && aligned32(keys)) {
 #pragma unroll
       for (int q = 0; q < R / 8; ++q) st_v8(keys + base + 8 * q, &v[8 * q]);

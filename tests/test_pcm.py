@@ -19,15 +19,21 @@ def test_oddeven_restatement_matches_reference_golden(restatement):
 
 
 def test_oddeven_melded_spec_is_the_reference_pass_output():
-    """The melded forms mirror runDarm's output for ir/oddeven_step.ir: one
-    region-region meld with one select (the role picks gt / lt), and the
-    reference simulator sees fewer serialized cycles after it."""
+    """The melded forms mirror runDarm's output for ir/oddeven_step.ir: a
+    block-region meld (the upper region with the idle block, by region
+    replication) and a region-region meld (the lower region with the result),
+    PAPER.md:947-948.  The reference simulator sees higher lane utilisation
+    after it and, with its default latencies (where the melded shared / global
+    memory instructions count), fewer serialized cycles from 4-key buckets up."""
     gold = load_golden("oddeven_sort.json")
-    assert [(m["kind"], m["selectsInserted"]) for m in gold["melds"]] == [("region-region", 1)]
+    assert [m["kind"] for m in gold["melds"]] == ["block-region", "region-region"]
     for case in gold["cases"]:
         u, m = case["stats_unit_latency"]["unmelded"], case["stats_unit_latency"]["melded"]
-        assert m[3] < u[3]                      # serialized cycles
         assert m[2] / m[1] > u[2] / u[1]        # utilisation
+        du, dm = case["stats_default_latency"]["unmelded"], case["stats_default_latency"]["melded"]
+        assert dm[5] < du[5] and dm[6] <= du[6]  # shared / global memory issues
+        if case["bucket"] >= 4:
+            assert dm[3] < du[3]                 # serialized cycles
 
 
 @pytest.mark.parametrize("B", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024])
