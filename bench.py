@@ -393,7 +393,9 @@ def cpu_corpus(kernel, nw):
     b = darm.make_random_input(kernel, 32, nw, 1000)
     names = [n for n, _ in ref.load(kernel, 0).globals]
     g0 = np.concatenate([b.globals[n] for n in names])
-    args = np.array([[16]] if len(b.args) == 1 else [[16, 24]], np.int32)
+    from tools.time_corpus import corpus_args
+
+    args = np.array(corpus_args(kernel), np.int32)                 # [param][set]: the GPU rows' split
     th = cpu_threads()
     res, out = {}, {}
     for form, meld in (("unmelded", 0), ("melded", 1)):

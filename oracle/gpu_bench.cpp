@@ -12,8 +12,9 @@
 //   gpuOracleOk      compareRuns(reference before, GPU unmelded / melded) on the
 //                    same fixtures (acceptance criterion 1's check)
 //   gpuLanes         lanes of the timed batch (warp x warps, config 1 shape)
-//   gpuUnmeldedUs / gpuMeldedUs / gpuSpeedup   kernel time (library events,
-//                    best of `reps`) for makeRandomInput batches
+//   gpuUnmeldedUs / gpuMeldedUs / gpuSpeedup   kernel time per launch: mean
+//                    of `launches` back-to-back DEVICE-mode launches over 8
+//                    device copies of the batch (CUDA events), best of `reps`
 //   gpuSimEqual      the simulator run on the GPU interpreter
 //                    (darm::gpu::executeWarpsIR, before and after the pass)
 //                    produced exactly the CPU interpreter's WarpResults,
@@ -23,7 +24,7 @@
 // prints the reference's columns followed by the GPU ones.
 //
 //   darm_gpu_bench [--fixtures N] [--warp W] [--threshold T] [--gpu-warps G]
-//                  [--reps R] [--seed S] [--json PATH] [--no-gpu]
+//                  [--reps R] [--launches L] [--seed S] [--json PATH] [--no-gpu]
 // Exit codes as the reference CLI (darm_cli.cpp:25-27): 0 ok, 2 usage,
 // 3 oracle failure or internal error.
 #include <algorithm>
@@ -34,6 +35,8 @@
 #include <fstream>
 #include <string>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "darm/fixtures.hpp"
 #include "darm/interp.hpp"
@@ -69,9 +72,22 @@ struct Row {
 
 double reduction(double b, double a) { return b <= 0 ? 0.0 : 100.0 * (b - a) / b; }
 
-// kernel time of one batch through the C-ABI (HOST buffers; stats.kernel_ms
-// brackets the launch only), best of reps
-double gpu_kernel_us(const Module &m, const Function &f, const std::vector<WarpInput> &ins, int form, int reps) {
+// Kernel time of one batch through the C-ABI, DEVICE-resident buffers: the
+// batch is uploaded once into kCopies device copies (together larger than the
+// 126 MB L2 at the config 1 shape, so consecutive launches read from HBM),
+// then `launches` launches rotate over the copies between two CUDA events on
+// the stream they run on; the figure is the per-launch mean, best of `reps`
+// such batches after one untimed batch.  (Round 1 timed single HOST-mode
+// launches, whose launch overhead and first-touch effects swamped the
+// 7-16 us kernels.)
+constexpr int kCopies = 8;
+
+void cuda_ok(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+double gpu_kernel_us(const Module &m, const Function &f, const std::vector<WarpInput> &ins, int form, int reps,
+                     int launches) {
   const int W = ins[0].warpSize;
   const int64_t n = int64_t(ins.size());
   const size_t np = f.params.size();
@@ -99,26 +115,58 @@ double gpu_kernel_us(const Module &m, const Function &f, const std::vector<WarpI
         std::copy_n(it->second.begin(), std::min(size, it->second.size()), sh[s].begin() + size_t(w) * size);
     }
   }
-  std::vector<const int32_t *> sp;
-  for (auto &v : sh) sp.push_back(v.data());
-  double best = 1e30;
-  for (int r = 0; r < reps; ++r) {
-    auto g2 = gl;   // every rep starts from the initial globals
-    std::vector<int32_t *> gp;
-    for (auto &v : g2) gp.push_back(v.data());
-    darm_gpu_stats st{};
-    char err[512] = {0};
-    int rc = darm_gpu_execute_warps(f.name.c_str(), form, W, n, args.data(), n * W, gp.data(), int(gp.size()),
-                                    sp.empty() ? nullptr : sp.data(), int(sp.size()), nullptr, DARM_MEM_HOST,
-                                    nullptr, &st, err, sizeof err);
-    if (rc != DARM_OK) throw std::runtime_error(std::string("darm_gpu: ") + err);
-    best = std::min(best, st.kernel_ms * 1e3);
+  // device copies: args, globals and shared initialisers per copy
+  std::vector<void *> owned;
+  auto upload = [&](const std::vector<int32_t> &v) {
+    void *d = nullptr;
+    cuda_ok(cudaMalloc(&d, std::max<size_t>(4, v.size() * 4)), "cudaMalloc");
+    owned.push_back(d);
+    if (!v.empty()) cuda_ok(cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    return static_cast<int32_t *>(d);
+  };
+  struct Copy {
+    int32_t *args;
+    std::vector<int32_t *> g;
+    std::vector<const int32_t *> s;
+  };
+  std::vector<Copy> copies(kCopies);
+  for (auto &c : copies) {
+    c.args = upload(args);
+    for (auto &v : gl) c.g.push_back(upload(v));
+    for (auto &v : sh) c.s.push_back(upload(v));
   }
+  cudaStream_t stream;
+  cudaEvent_t e0, e1;
+  cuda_ok(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_ok(cudaEventCreate(&e0), "cudaEventCreate");
+  cuda_ok(cudaEventCreate(&e1), "cudaEventCreate");
+  auto launch = [&](const Copy &c) {
+    char err[512] = {0};
+    int rc = darm_gpu_execute_warps(f.name.c_str(), form, W, n, c.args, n * W,
+                                    c.g.data(), int(c.g.size()), c.s.empty() ? nullptr : c.s.data(), int(c.s.size()),
+                                    nullptr, DARM_MEM_DEVICE, stream, nullptr, err, sizeof err);
+    if (rc != DARM_OK) throw std::runtime_error(std::string("darm_gpu: ") + err);
+  };
+  double best = 1e30;
+  for (int r = 0; r <= reps; ++r) {
+    cuda_ok(cudaStreamSynchronize(stream), "sync");
+    cuda_ok(cudaEventRecord(e0, stream), "record");
+    for (int i = 0; i < launches; ++i) launch(copies[size_t(i % kCopies)]);
+    cuda_ok(cudaEventRecord(e1, stream), "record");
+    cuda_ok(cudaEventSynchronize(e1), "sync");
+    float ms = 0;
+    cuda_ok(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    if (r > 0) best = std::min(best, 1e3 * double(ms) / launches);   // batch 0 is the warm-up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(stream);
+  for (void *d : owned) cudaFree(d);
   return best;
 }
 
 Row bench_one(const std::string &kernel, const char *text, const Row &opts, int fixtures, int warp,
-              uint64_t seed, bool use_gpu, int gpu_warps, int reps) {
+              uint64_t seed, bool use_gpu, int gpu_warps, int reps, int launches) {
   Row row = opts;
   row.kernel = kernel;
   Module m = parseModule(text);
@@ -219,8 +267,8 @@ Row bench_one(const std::string &kernel, const char *text, const Row &opts, int 
     }
     row.gpu = true;
     row.gpuLanes = 32LL * gpu_warps;
-    row.gpuUnmeldedUs = gpu_kernel_us(m, f0, big, DARM_UNMELDED, reps);
-    row.gpuMeldedUs = gpu_kernel_us(m, f0, big, DARM_MELDED, reps);
+    row.gpuUnmeldedUs = gpu_kernel_us(m, f0, big, DARM_UNMELDED, reps, launches);
+    row.gpuMeldedUs = gpu_kernel_us(m, f0, big, DARM_MELDED, reps, launches);
   }
   return row;
 }
@@ -262,7 +310,7 @@ json to_json(const Row &r) {
 }  // namespace
 
 int main(int argc, char **argv) {
-  int fixtures = 10, warp = 32, gpu_warps = 1 << 15, reps = 5;
+  int fixtures = 10, warp = 32, gpu_warps = 1 << 15, reps = 5, launches = 50;
   uint64_t seed = 3000;
   Row opts;
   std::string json_path;
@@ -281,16 +329,17 @@ int main(int argc, char **argv) {
     else if (a == "--threshold") opts.threshold = std::atof(next());
     else if (a == "--gpu-warps") gpu_warps = std::atoi(next());
     else if (a == "--reps") reps = std::atoi(next());
+    else if (a == "--launches") launches = std::atoi(next());
     else if (a == "--seed") seed = std::strtoull(next(), nullptr, 10);
     else if (a == "--json") json_path = next();
     else if (a == "--no-gpu") use_gpu = false;
     else {
       std::fprintf(stderr, "usage: darm_gpu_bench [--fixtures N] [--warp W] [--threshold T] [--gpu-warps G] "
-                           "[--reps R] [--seed S] [--json PATH] [--no-gpu]\n");
+                           "[--reps R] [--launches L] [--seed S] [--json PATH] [--no-gpu]\n");
       return 2;
     }
   }
-  if (fixtures < 1 || warp < 1 || warp > 64 || gpu_warps < 1 || reps < 1) {
+  if (fixtures < 1 || warp < 1 || warp > 64 || gpu_warps < 1 || reps < 1 || launches < 1) {
     std::fprintf(stderr, "bad arguments\n");
     return 2;
   }
@@ -314,7 +363,7 @@ int main(int argc, char **argv) {
       for (int i = 0; ref_corpus_names[i]; ++i)
         if (std::string(ref_corpus_names[i]) == k) text = ref_corpus_texts[i];
       if (!text) throw std::runtime_error(std::string("corpus kernel not embedded: ") + k);
-      Row r = bench_one(k, text, opts, fixtures, warp, seed, use_gpu, gpu_warps, reps);
+      Row r = bench_one(k, text, opts, fixtures, warp, seed, use_gpu, gpu_warps, reps, launches);
       std::string status = r.rejected ? "rejected" : (r.melds > 0 ? "melded" : "no-meld");
       if (!r.oracleOk) status = "ORACLE-FAIL";
       const char *gst = !r.gpu ? "-" : (r.gpuOracleOk && r.gpuSimEqual ? "ok" : "FAIL");

@@ -64,6 +64,11 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
   // shuffle -> compare -> select chains interleave and hide each other's latency.
   const uint32_t G = gridDim.x;
   uint32_t tile = blockIdx.x;
+  // exchange-buffer parity runs on across tiles: a write goes to the buffer
+  // the previous exchange did not read, whose last reads precede that
+  // exchange's barrier (an odd exchange count per tile otherwise lets a fast
+  // warp overwrite a slot a slow warp still reads)
+  int par = 0;
   int32_t next[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -80,7 +85,6 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
       const uint32_t tn = tile + (U + u) * G, id = tn * CTA + threadIdx.x;
       if (tn < tiles) next[u] = id < n ? keys[id] : INT_MAX;   // prefetch
     }
-    int par = 0;
     int32_t neg = 0;   // melded: lanes of a descending half work on ~v (order reversal)
 #pragma unroll
     for (int d = 1; d <= LB; ++d) {

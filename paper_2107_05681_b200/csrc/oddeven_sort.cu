@@ -157,10 +157,12 @@ __global__ void __launch_bounds__(CTA) oddeven_sort_kernel(int32_t *__restrict__
   uint64_t lo = 0, up = 0;
   oe_roles<B, 1, 1, 0>(t, lo, up);
   const uint32_t tiles = (n + CTA - 1) / CTA;
+  // buffer parity runs on across tiles (21 steps at B = 64: reset per tile,
+  // the next tile's first write would hit the buffer the last step reads)
+  int par = 0;
   for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint32_t id = tile * CTA + threadIdx.x;
     int32_t v = id < n ? keys[id] : INT_MAX;
-    int par = 0;
     v = oe_one_network<F, B, CTA, 1, 1, 0>(v, lo, up, buf, par);
     if (id < n) keys[id] = v;
   }

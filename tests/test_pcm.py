@@ -94,3 +94,25 @@ def test_oddeven_gpu_full_size_host_pipeline():
         st = darm.oddeven_sort(k, 64, variant)
         assert st["launches"] == 8
         assert (k == want).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sort", ["oddeven", "bitonic"])
+@pytest.mark.parametrize("bucket", [64, 128, 256])
+def test_one_key_shape_many_tiles_per_cta(sort, bucket):
+    """One key per thread at 2^22 keys: every CTA walks many 256-key tiles, so
+    the shared exchange buffers are reused across tiles (round-2 bench found a
+    cross-tile hazard at 2^24 keys that 1-tile-per-CTA sizes never exercised)."""
+    import torch
+
+    n = 1 << 22
+    g = torch.Generator(device="cuda").manual_seed(bucket)
+    keys = torch.randint(-(2 ** 31), 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+    want = torch.sort(keys.view(-1, bucket), dim=1).values.view(-1)
+    fn = darm.oddeven_sort if sort == "oddeven" else darm.bitonic_sort
+    for variant in ((0, 1, 2) if sort == "oddeven" else (0, 1, 2, 3)):
+        for _ in range(3):
+            k = keys.clone()
+            fn(k, bucket, variant, keys_per_thread=1, want_stats=False)
+            torch.cuda.synchronize()
+            assert torch.equal(k, want), (sort, bucket, variant)

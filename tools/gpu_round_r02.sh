@@ -34,6 +34,7 @@ timeout 600 python tools/time_bitonic.py 64 256 1024 4096 > gpurun_out/time_bito
 timeout 600 python tools/time_bitonic.py --oddeven 64 256 > gpurun_out/time_oddeven.log 2>&1
 timeout 300 python tools/time_corpus.py > gpurun_out/time_corpus.log 2>&1
 for k in bitonic bitonic_b256 bitonic_b1024 bitonic_b4096 sb1 srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens; do
-  python tools/ncu_summary.py gpurun_out/prof_$k.ncu-rep > gpurun_out/ncusum_$k.json && rm -f gpurun_out/prof_$k.ncu-rep
+  python tools/ncu_summary.py gpurun_out/prof_$k.ncu-rep > gpurun_out/ncusum_$k.json
+  case " ${KEEP_REPS:-lud_far srad_fast} " in *" $k "*) ;; *) rm -f gpurun_out/prof_$k.ncu-rep ;; esac
 done
 ls -la gpurun_out

@@ -52,6 +52,19 @@ def summarise(path):
             if key == "duration_us":
                 v = v * UNIT_SCALE.get(u, 1) / 1e3
             k[key] = v
+        # warp-state breakdown: cycles stalled per issued instruction, by reason
+        stalls = {}
+        for i, h in enumerate(hdr):
+            m = h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")
+            if m:
+                try:
+                    v = float(r[i].replace(",", ""))
+                except ValueError:
+                    continue
+                if v >= 0.05:
+                    stalls[h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = round(v, 3)
+        if stalls:
+            k["stall_cycles_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
         if "thread_inst_per_inst" in k:
             k["lane_efficiency"] = k["thread_inst_per_inst"] / 32.0
         if "thread_inst_pred_on_per_inst" in k:

@@ -56,6 +56,17 @@ def main():
                     k = keys.copy()
                     darm.oddeven_sort(k, B, v, keys_per_thread=kpt)
                     assert (k.reshape(-1, B) == np.sort(keys.reshape(-1, B), axis=1)).all()
+    # one key per thread with several 256-key tiles per CTA (the exchange
+    # buffers reused across tiles): 2^19 keys = 2048 tiles over <= 1184 CTAs
+    keys = rng.integers(-(2 ** 31), 2 ** 31, size=1 << 19, dtype=np.int64).astype(np.int32)
+    for B in (64, 128):
+        for v in (0, 1):
+            k = keys.copy()
+            darm.oddeven_sort(k, B, v, keys_per_thread=1)
+            assert (k.reshape(-1, B) == np.sort(keys.reshape(-1, B), axis=1)).all()
+            k = keys.copy()
+            darm.bitonic_sort(k, B, v, keys_per_thread=1)
+            assert (k.reshape(-1, B) == np.sort(keys.reshape(-1, B), axis=1)).all()
     keys = rng.integers(-(2 ** 31), 2 ** 31, size=3 * 8192 + 5, dtype=np.int64).astype(np.int32)
     for v in (0, 1):
         k = keys.copy()
