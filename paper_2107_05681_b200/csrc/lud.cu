@@ -385,7 +385,8 @@ constexpr int kFarThreads = 256;               // thread = 8 rows x 8 columns of
 // Per 4 k's a thread reads 8 float4 of L and 8 of U for 128 FFMA2 (the L
 // operand broadcast to both halves); the accumulators and the tile take 128
 // registers.  Band tiles (64 rows or 64 columns) run a half-size variant.
-// Per element the operation sequence above.
+// Per element the operation sequence above; the step's subtraction as FADD2
+// (sub.rn.f32x2: both halves IEEE subtractions, half the FMA-pipe issues).
 constexpr int kPipeK = kLook * BS;                 // 64
 // dense tiles as the tensor memory accelerator writes them (no padding)
 constexpr int kLdL = kPipeK;                       // lp[r][k] row pitch
@@ -402,6 +403,16 @@ __device__ __forceinline__ void tma_load_2d(float *dst, const CUtensorMap *map, 
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
+}
+
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {   // sub.rn.f32x2: two IEEE subtractions (FADD2)
+  unsigned long long ra, rb, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+  return d;
 }
 
 // T steps on one tile: NI row groups (of 16 rows: 8 = all, 4 = a 64-row band)
@@ -443,10 +454,9 @@ __device__ __forceinline__ void far_tile(const float *__restrict__ lp, const flo
     for (int i = 0; i < NI; ++i)
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        v[i][h].x -= acc[i][2 * h].x;
-        v[i][h].y -= acc[i][2 * h].y;
-        v[i][h].z -= acc[i][2 * h + 1].x;
-        v[i][h].w -= acc[i][2 * h + 1].y;
+        const float2 lo = sub2(make_float2(v[i][h].x, v[i][h].y), acc[i][2 * h]);
+        const float2 hi = sub2(make_float2(v[i][h].z, v[i][h].w), acc[i][2 * h + 1]);
+        v[i][h] = make_float4(lo.x, lo.y, hi.x, hi.y);
       }
   }
 }
