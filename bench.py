@@ -431,6 +431,95 @@ def cpu_nqueens(mirror_prefixes):
                       f"{th} threads"}
 
 
+def _timed_sample(run, seconds):
+    """Repeat run() (one bounded batch -> units done) until about `seconds` of
+    CPU work; returns (units, seconds)."""
+    done, sec = 0, 0.0
+    while sec < seconds:
+        t0 = time.perf_counter()
+        done += run()
+        sec += time.perf_counter() - t0
+    return done, sec
+
+
+def cpu_bucket_sort(net, bucket, seconds=2.0):
+    """The CPU path of a bucket-sort row.  Buckets of <= 64 keys: the reference
+    itself (oracle/_ref executeWarp chained over the IR step: bitonic.ir, or
+    this repo's ir/oddeven_step.ir for PCM) on all host threads.  Larger
+    buckets exceed the interpreter's 64-lane warp, so the restatement's
+    network (oracle/darm_oracle.c, one thread) is timed instead."""
+    o = _oracle()
+    rng = np.random.default_rng(11)
+    th = cpu_threads()
+    if bucket <= 64 and o.reference_available():
+        ref = o.Reference()
+        if net == "bitonic":
+            mod = ref.load("bitonic", 0)
+            sort = lambda k: mod.bitonic_sort(k, bucket, threads=th)  # noqa: E731
+        else:
+            with open(os.path.join(ROOT, "paper_2107_05681_b200", "ir", "oddeven_step.ir")) as f:
+                mod = ref.load_text(f.read(), 0)
+            sched = o.oddeven_schedule(bucket)
+            sort = lambda k: mod.chain_sort(k, bucket, sched, threads=th)  # noqa: E731
+        kind, cores, nb = "reference", th, 1024
+        what = f"oracle/_ref executeWarp chained over {'bitonic.ir' if net == 'bitonic' else 'ir/oddeven_step.ir'}"
+    else:
+        r = o.Restatement()
+        sort = (lambda k: r.bitonic_sort(k, bucket)) if net == "bitonic" else (lambda k: r.oddeven_sort(k, bucket))
+        kind, cores, nb = "port", 1, max(64, (1 << 20) // bucket)
+        what = "the C restatement's network (oracle/darm_oracle.c), one thread"
+
+    def batch():
+        keys = rng.integers(-(2 ** 31), 2 ** 31, size=nb * bucket, dtype=np.int64).astype(np.int32)
+        sort(keys)
+        assert (keys.reshape(-1, bucket)[:, 1:] >= keys.reshape(-1, bucket)[:, :-1]).all()
+        return nb * bucket
+
+    keys_done, sec = _timed_sample(batch, seconds)
+    return {"value": keys_done / sec, "unit": "keys/s", "cores": cores, "kind": kind,
+            "sample": f"{keys_done // bucket} buckets x {bucket} keys, {what}, {sec:.1f} s"}
+
+
+def cpu_merge_sort(n=1 << 20, seconds=2.0):
+    """MS CPU path: the restatement's bottom-up merge sort (oracle/darm_oracle.c,
+    the same passes as ir/merge_step.ir) of 2^20 keys, one thread."""
+    r = _oracle().Restatement()
+    rng = np.random.default_rng(12)
+
+    def batch():
+        keys = rng.integers(-(2 ** 31), 2 ** 31, size=n, dtype=np.int64).astype(np.int32)
+        r.merge_sort(keys)
+        return n
+
+    keys_done, sec = _timed_sample(batch, seconds)
+    return {"value": keys_done / sec, "unit": "keys/s", "cores": 1, "kind": "port",
+            "sample": f"{keys_done // n} sorts of {n} keys, the C restatement, {sec:.1f} s"}
+
+
+def cpu_interp(ir_text, n_warps, seconds=2.0):
+    """Interpreter row CPU path: the reference's executeWarp (oracle/_ref) over
+    the same 32-lane warps of the IR function, all host threads."""
+    o = _oracle()
+    if not o.reference_available():
+        return None
+    mod = o.Reference().load_text(ir_text, 0)
+    sizes = {sz for _, sz in mod.globals}
+    assert len(sizes) == 1, "equal global sizes (one per-warp stride)"
+    gw = sizes.pop()
+    rng = np.random.default_rng(13)
+    th = cpu_threads()
+    args = np.full((1, 1), 16, np.int32)
+
+    def batch():
+        g = rng.integers(-128, 129, size=len(mod.globals) * n_warps * gw, dtype=np.int64).astype(np.int32)
+        mod.execute_warps(32, n_warps, args, g, gw, None, threads=th, want_stats=False)
+        return n_warps
+
+    warps, sec = _timed_sample(batch, seconds)
+    return {"value": warps / sec, "unit": "warps/s", "cores": th, "kind": "reference",
+            "sample": f"{warps} warps x 32 lanes, oracle/_ref executeWarp, {sec:.1f} s"}
+
+
 def cpu_lud(n=4096):
     """Config 4 CPU path: the blocked-LU restatement on all host threads, on a
     stated subsample (n^2 instead of 8192^2; flops scale as n^3)."""
@@ -532,7 +621,7 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
             row["cpu_baseline"] = cpu_nqueens(pre)
         out["nqueens16"] = row
     if "pcm" in sections or "ms1m" in sections or "interp" in sections:
-        pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections)
+        pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections, cpu=cpu)
     if "lud8192" in sections:
         lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax, cpu)
     if "srad" in sections:
@@ -549,7 +638,7 @@ def nqueens_row(torch, dist, row, world, tmax):
     row["full_tree_nodes"] = NQ_NODES_16
 
 
-def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections):
+def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections, cpu=False):
     def tmax(row):
         for key in [k for k in row if k.endswith("_us")]:
             row[key] = reduce_max(torch, dist, row[key])
@@ -576,14 +665,19 @@ def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, ou
         row["keys_per_thread"] = kpt or 16
         row["melded_GBps"] = 8.0 * n / (row["melded_us"] * 1e-6) / 1e9
         row["melded_frac_hbm"] = row["melded_GBps"] / peak
-        row["roofline"] = roof("hbm", row["melded_GBps"], peak, "GB/s", algorithmic_bytes_per_launch=8 * n)
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        pat = "oddeven_sort_reg_kernel<1, 64, 16" if kpt == 0 else "oddeven_sort_kernel<1, 64,"
+        row["roofline"] = roof("hbm", row["melded_GBps"], peak, "GB/s", algorithmic_bytes_per_launch=8 * n,
+                               issue=issue_roof("oddeven", pat, row["melded_us"] * 1e-6, sms, sm_max_mhz()))
+        if cpu:
+            row["cpu_baseline"] = out["pcm"]["cpu_baseline"] if name == "pcm_1key" else cpu_bucket_sort("oddeven", 64)
         out[name] = row
     n = 1 << 20
     keys = pristine[:n].clone()
     ms = torch.empty_like(keys)
     want = torch.sort(keys).values
     if "ms1m" not in sections:
-        return interp_row(torch, darm, dist, steps, warmup, g, out) if "interp" in sections else None
+        return interp_row(torch, darm, dist, steps, warmup, g, out, cpu=cpu) if "interp" in sections else None
     row = {}
     for vname, v in (("unmelded", 0), ("melded", 1)):
         call = darm.merge_sort(ms, v, stream=stream.cuda_stream, want_stats=False, prepare_only=True)
@@ -599,12 +693,14 @@ def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, ou
     row["melded_frac_hbm"] = row["melded_GBps"] / peak
     row["roofline"] = roof("hbm", row["melded_GBps"], peak, "GB/s", algorithmic_bytes_per_launch=8 * n * passes,
                            note=f"8 B/key per pass x {passes} passes; at 2^20 keys (4 MiB) the passes run from L2")
+    if cpu:
+        row["cpu_baseline"] = cpu_merge_sort(n)
     out["ms1m"] = row
     if "interp" in sections:
-        interp_row(torch, darm, dist, steps, warmup, g, out)
+        interp_row(torch, darm, dist, steps, warmup, g, out, cpu=cpu)
 
 
-def interp_row(torch, darm, dist, steps, warmup, g, out):
+def interp_row(torch, darm, dist, steps, warmup, g, out, cpu=False):
     # the GPU executeWarp for arbitrary IR (darm_gpu_program_execute): a diamond
     # kernel given as IR text, 32768 warps of 32 lanes (config 1 shape)
     row = {}
@@ -622,8 +718,11 @@ def interp_row(torch, darm, dist, steps, warmup, g, out):
                 ts.append(res.call_stats["kernel_ms"])
         row[vname + "_us"] = reduce_max(torch, dist, 1e3 * sum(ts) / len(ts))
         row[vname + "_warps_per_s"] = nwi / (row[vname + "_us"] * 1e-6)
-    row["roofline"] = roof("issue", None, None, "warp-inst/s",
-                           note="an interpreter: bound by issue per IR instruction, not by bytes; no byte roof")
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    row["roofline"] = issue_roof("interp", "ir_interp_kernel", row["diamond_us"] * 1e-6, sms, sm_max_mhz(),
+                                 note="an interpreter: bound by issue per IR instruction, not by bytes")
+    if cpu:
+        row["cpu_baseline"] = cpu_interp(DIAMOND_IR, 1 << 15)
     out["interp_diamond_32k_warps"] = row
 
 
@@ -825,6 +924,7 @@ def our_arm(args):
                  ("melded_literal", darm.MELDED_LITERAL))
         shapes = [("bitonic", B, 0), ("bitonic_1key", B, 1)] + [(f"bitonic_B{b}", b, 0) for b in (256, 1024, 4096)] + \
                  [(f"bitonic_B{b}_1key", b, 1) for b in (256, 1024)]
+        cpu_rows = {}
         for key, Bs, kp in shapes:
             want_s = want if Bs == B else torch.sort(pristine.view(-1, Bs), dim=1).values.view(-1)
             row = {}
@@ -845,8 +945,13 @@ def our_arm(args):
             row["bucket"] = Bs
             gbs = 8 * n / (row["melded_us"] * 1e-6) / 1e9
             kpt_name = f"bitonic_sort_reg_kernel<1, {Bs}, 16" if kp != 1 else f"bitonic_sort_kernel<1, {Bs},"
+            stem = "bitonic" if Bs == 64 else f"bitonic_b{Bs}"
             row["roofline"] = roof("hbm", gbs, peak0, "GB/s", algorithmic_bytes_per_launch=8 * n, form="melded",
-                                   issue=issue_roof("bitonic", kpt_name, row["melded_us"] * 1e-6, sms, sm_max_mhz()))
+                                   issue=issue_roof(stem, kpt_name, row["melded_us"] * 1e-6, sms, sm_max_mhz()))
+            if world == 1 and not args.no_cpu_baseline:
+                # the CPU path does not depend on the GPU shape: one sample per bucket size
+                cpu_rows.setdefault(Bs, cpu_bucket_sort("bitonic", Bs))
+                row["cpu_baseline"] = cpu_rows[Bs]
             per_kernel[key] = row
 
     if rank != 0:

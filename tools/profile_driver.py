@@ -35,6 +35,17 @@ def main(which, bucket=64):
                 darm.srad(j, 1, 0.5, darm.RODINIA_ROI, v, want_stats=False, fast=fast)
         torch.cuda.synchronize()
         return
+    if which == "interp":   # bench.py's interpreter row: the diamond IR, 32,768 warps of 32 lanes
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from bench import DIAMOND_IR
+
+        prog = darm.Program(DIAMOND_IR)
+        nwi = 1 << 15
+        g = torch.Generator(device="cuda").manual_seed(3)
+        gi = torch.randint(-128, 129, (nwi, prog.global_words), dtype=torch.int32, device="cuda", generator=g)
+        prog.execute_warps(32, np.full((1, 1), 16, np.int32), gi, n_warps=nwi)
+        torch.cuda.synchronize()
+        return
     if which == "nqueens":
         for v in (darm.UNMELDED, darm.MELDED):   # the bench's launch: 7-row prefixes, mirror symmetry
             assert darm.nqueens(16, 7, v, want_stats=False, mirror=True)[0] == 14772512
