@@ -1,6 +1,6 @@
 """Markdown tables for DESIGN.md §8 from the committed profiles:
-bench per-kernel rows (profiles/r01_bench.json) and the ncu lane-efficiency
-sweep (profiles/r01_lane_efficiency.json, r01_simulator_util.json).
+bench per-kernel rows (profiles/rNN_bench.json) and the ncu lane-efficiency
+sweep (profiles/rNN_lane_efficiency.json, the latest *_simulator_util.json).
 
     python tools/design_tables.py [rNN]
 """
@@ -44,7 +44,7 @@ def main(r="r01"):
             unm = " / ".join(t(c["unmelded_us"]) for c in cells)
             mel = " / ".join(t(c["melded_us"]) for c in cells)
             sps = " / ".join(f"{c['speedup']:.2f}×" for c in cells)
-            fr = " / ".join(f"{c['melded_frac_hbm']:.2f}" for c in cells)
+            fr = " / ".join(f"{c['roofline']['frac']:.2f}" for c in cells)
             print(f"| {label} | {unm} | {mel} | {sps} | {fr} HBM |")
             continue
         if key is None:
@@ -53,28 +53,34 @@ def main(r="r01"):
             print(f"| {label} | {min(c['unmelded_us'] for c in cs):.1f}–{max(c['unmelded_us'] for c in cs):.1f} µs | "
                   f"{min(c['melded_us'] for c in cs):.1f}–{max(c['melded_us'] for c in cs):.1f} µs | "
                   f"{min(c['speedup'] for c in cs):.2f}–{max(c['speedup'] for c in cs):.2f}× | "
-                  f"{min(c['melded_frac_hbm'] for c in cs):.2f}–{max(c['melded_frac_hbm'] for c in cs):.2f} HBM (latency-bound) |")
+                  f"{min(c['roofline']['frac'] for c in cs):.2f}–{max(c['roofline']['frac'] for c in cs):.2f} HBM (latency-bound) |")
             continue
         c = pk[key]
         if key == "nqueens16":
-            frac = f"ALU pipe {c['roofline']['alu_pipe_pct']:.0f}% (ncu)"
+            frac = f"{c['roofline']['frac']:.2f} issue"
         else:
-            frac = f"{c[fk]:.2f} {roof}"
+            frac = f"{c['roofline']['frac']:.2f} {roof}"
         sp = c["speedup"]
         print(f"| {label} | {t(c['unmelded_us'])} | **{t(c['melded_us'])}** | {sp:.2f}× | {frac} |")
     print()
     le = json.load(open(os.path.join(ROOT, "profiles", f"{r}_lane_efficiency.json")))["kernels"]
-    sim = json.load(open(os.path.join(ROOT, "profiles", f"{r}_simulator_util.json")))["utilization"]
+    import glob
+
+    sim_path = sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9][0-9]_simulator_util.json")))[-1]
+    sim = json.load(open(sim_path))["utilization"]
     print("| kernel | reference simulator utilisation (unit latency) unmelded → melded | ncu thread_inst/(32·inst) | "
-          "ncu pred_on/(32·inst) | branch uniformity % | warp instructions melded / unmelded |")
-    print("|---|---|---|---|---|---|")
-    for k, e in le.items():
+          "ncu pred_on/(32·inst) | branch uniformity % | warp instructions melded / unmelded | "
+          "predicated compile: pred_on/(32·inst), branch uniformity % |")
+    print("|---|---|---|---|---|---|---|")
+    for k, e in sorted(le.items()):
         u, m = e["unmelded"], e["melded"]
+        p = e.get("predicated")
         s = sim.get(k)
         ss = f"{s['unmelded']:.3f} → {s['melded']:.3f}" if s else "—"
+        ps = f"{p['lane_efficiency_pred_on']:.3f}, {p['branch_uniform_pct']:.0f}" if p else "—"
         print(f"| {k} | {ss} | {u['lane_efficiency']:.3f} → {m['lane_efficiency']:.3f} | "
               f"{u['lane_efficiency_pred_on']:.3f} → {m['lane_efficiency_pred_on']:.3f} | "
-              f"{u['branch_uniform_pct']:.0f} → {m['branch_uniform_pct']:.0f} | {m['warp_inst'] / u['warp_inst']:.2f} |")
+              f"{u['branch_uniform_pct']:.0f} → {m['branch_uniform_pct']:.0f} | {m['warp_inst'] / u['warp_inst']:.2f} | {ps} |")
 
 
 if __name__ == "__main__":
