@@ -82,7 +82,8 @@ cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefi
 
 // lud.cu: records the launches of one decomposition on `s`; dscr: 256-float
 // device scratch for the factored diagonal block
-cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches);
+cudaError_t record_lud(int variant, float *a, int n, float *dscr, int *counters, cudaStream_t s, int *launches);
+int lud_counter_words(int n);   // ints of `counters` record_lud uses
 
 // srad.cu
 struct SradRoi {

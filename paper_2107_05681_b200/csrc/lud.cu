@@ -492,9 +492,11 @@ struct FarMaps {                 // tensor maps of A (n x n fp32, row-major): th
 
 template <int T>   // steps in the super-step (kLook but for the last one)
 __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__restrict__ a, int n, int o, FarRects R,
-                                                                      const __grid_constant__ FarMaps maps) {
+                                                                      const __grid_constant__ FarMaps maps,
+                                                                      int *__restrict__ next_tile) {
   extern __shared__ __align__(128) float psm[];
   __shared__ __align__(8) uint64_t bar[3];   // stage 0 / stage 1 (L, U) landed; the A tile landed
+  __shared__ int s_tile[2];                  // tiles handed out by the launch's counter (double-buffered)
   const int tiles = R.tiles;
   // tile -> its origin (r0, c0) and extent (nr, nc)
   auto place = [&](int tile, int &r0, int &c0, int &nr, int &nc) {
@@ -526,16 +528,20 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
     mbar_expect_tx(&bar[2], kTileABytes);
     tma_load_2d(ap, &maps.t, c0, r0, &bar[2]);
   };
+  // Tiles are handed out dynamically (one atomic per tile on the launch's
+  // zeroed counter): a CTA that starts late — the band kernel beside this one
+  // holds SMs for its first microseconds — simply takes fewer tiles.
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_tile[0] = atomicAdd(next_tile, 1);
   }
   __syncthreads();
-  int tile = blockIdx.x;
+  int tile = s_tile[0];
   if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
-  for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
+  for (int it = 0; tile < tiles; ++it) {
     const int st = it & 1;
     int r0, c0, nr, nc;
     place(tile, r0, c0, nr, nc);
@@ -547,8 +553,9 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int h = 0; h < 2; ++h) v[i][h] = *reinterpret_cast<const float4 *>(ap + (ty + 16 * i) * kLdA + c1 + 64 * h);
+    if (threadIdx.x == 0) s_tile[(it + 1) & 1] = atomicAdd(next_tile, 1);
     __syncthreads();
-    const int next = tile + gridDim.x;
+    const int next = s_tile[(it + 1) & 1];
     if (threadIdx.x == 0 && next < tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
       issue(next, st ^ 1);
@@ -569,6 +576,7 @@ __global__ void __launch_bounds__(kFarThreads, 1) lud_far_pipe_kernel(float *__r
         const int r = ty + 16 * i, c = c1 + 64 * h;
         if (r < nr && c < nc) *reinterpret_cast<float4 *>(a + size_t(r0 + r) * n + c0 + c) = v[i][h];
       }
+    tile = next;
   }
 }
 
@@ -646,15 +654,15 @@ cudaError_t far_maps(float *a, int n, FarMaps &m) {
 }
 
 cudaError_t launch_far(float *a, int n, int O, int T, const FarRects &R, const FarMaps &maps, int grid,
-                       cudaStream_t s) {
+                       int *counter, cudaStream_t s) {
   if (R.tiles == 0) return cudaSuccess;
   const size_t shm = size_t(kFarSmemWords) * sizeof(float);
   grid = max(1, min(grid, R.tiles));
   switch (T) {
-    case 1: lud_far_pipe_kernel<1><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
-    case 2: lud_far_pipe_kernel<2><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
-    case 3: lud_far_pipe_kernel<3><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
-    default: lud_far_pipe_kernel<4><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps); break;
+    case 1: lud_far_pipe_kernel<1><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps, counter); break;
+    case 2: lud_far_pipe_kernel<2><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps, counter); break;
+    case 3: lud_far_pipe_kernel<3><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps, counter); break;
+    default: lud_far_pipe_kernel<4><<<grid, kFarThreads, shm, s>>>(a, n, O, R, maps, counter); break;
   }
   return cudaGetLastError();
 }
@@ -666,19 +674,28 @@ struct LudSide {       // per device: the panel stream of the look-ahead and its
 
 }  // namespace
 
+// Tile counters record_lud needs (two trailing-update launches per super-step).
+int lud_counter_words(int n) { return 2 * (n / (kLook * BS) + 2); }
+
 // Look-ahead across super-steps (two streams inside the captured graph):
-//   main   ... far strips(g) -> far block(g) -> [join] -> far strips(g+1) ...
-//   panel       [fork] -> panels(g+1) (4 launches) -> join
-// The strips are the rows and columns the next super-step's panels read
-// (the 64-wide L-shaped band at E = end of super-step g); once they hold
-// super-step g's updates the next panels run on the side stream while the
-// far block [E+64, n)^2 takes them on all but kPanelSMs SMs.  Disjoint
-// regions, and every element still receives its updates in step order.
+//   main   ... far block(g-1) -> [fork] -> far block(g) -> [join] -> ...
+//   panel       [fork] -> band(g) -> panels(g+1) (4 launches) -> join
+// The band is the 64-wide L-shaped strip at E = end of super-step g — the
+// rows and columns the next super-step's panels read; it needs super-step
+// g's panels and the far block of g-1, exactly like the far block of g, and
+// the two regions are disjoint, so the band runs beside the far block on the
+// high-priority panel stream (its CTAs are dispatched first; the far block's
+// tiles are handed out dynamically, so its late-starting CTAs take fewer)
+// and the next panels follow it there while the far block [E+64, n)^2 takes
+// super-step g's update on all but kPanelSMs SMs.  Every element still
+// receives its updates in step order.  The critical path per super-step is
+// max(far block, band + panel chain) instead of band + max(far block, panel
+// chain).
 // SMs the far block leaves to the concurrent panels (measured at 8192:
 // 0 -> 15.65 ms, 4 -> 14.98, 8 -> 14.72, 16 -> 14.89, 32 -> 16.13)
 constexpr int kPanelSMs = 8;
 
-cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s, int *launches) {
+cudaError_t record_lud(int variant, float *a, int n, float *dscr, int *counters, cudaStream_t s, int *launches) {
   // per device: kernel attributes, SM count, the panel stream (callers hold
   // the device's lock)
   struct LudDevice {
@@ -717,6 +734,12 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
     cudaError_t e = far_maps(a, n, maps);
     if (e != cudaSuccess) return e;
   }
+  // one tile counter per trailing-update launch, zeroed at the graph's start
+  if (n > G) {
+    cudaError_t e = cudaMemsetAsync(counters, 0, size_t(lud_counter_words(n)) * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
+  int *ctr = counters;
   launch_panels(variant, a, n, 0, dscr, s, launches);   // super-step 0: nothing to overlap with
   for (int O = 0; O < n; O += G) {
     const int T = min(kLook, (n - O) / BS);
@@ -726,24 +749,28 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, cudaStream_t s
     const int F = E + Tn * BS;                  // end of its band
     // the band the next panels read: rows [E, F) x cols [E, n), rows [F, n) x cols [E, F)
     const int band[2][4] = {{E, F, E, n}, {F, n, E, F}};
-    cudaError_t e = launch_far(a, n, O, T, far_rects(2, band), maps, sms, s);
-    if (e != cudaSuccess) return e;
-    ++*launches;
+    cudaError_t e;
     if (F < n) {
       e = cudaEventRecord(sd.fork, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(sd.s, sd.fork, 0);
+      if (e == cudaSuccess) e = launch_far(a, n, O, T, far_rects(2, band), maps, sms, ctr++, sd.s);
       if (e != cudaSuccess) return e;
+      ++*launches;
       launch_panels(variant, a, n, E, dscr, sd.s, launches);
       e = cudaEventRecord(sd.join, sd.s);
       if (e != cudaSuccess) return e;
       const int far[1][4] = {{F, n, F, n}};
-      e = launch_far(a, n, O, T, far_rects(1, far), maps, sms - kPanelSMs, s);
+      e = launch_far(a, n, O, T, far_rects(1, far), maps, sms - kPanelSMs, ctr++, s);
       if (e != cudaSuccess) return e;
       ++*launches;
       e = cudaStreamWaitEvent(s, sd.join, 0);
       if (e != cudaSuccess) return e;
     } else {
-      launch_panels(variant, a, n, E, dscr, s, launches);   // the last super-step: no far block left
+      // the last super-step: no far block left
+      e = launch_far(a, n, O, T, far_rects(2, band), maps, sms, ctr++, s);
+      if (e != cudaSuccess) return e;
+      ++*launches;
+      launch_panels(variant, a, n, E, dscr, s, launches);
     }
   }
   if (nb > 1) {

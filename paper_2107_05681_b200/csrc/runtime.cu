@@ -718,9 +718,13 @@ int darm_gpu_lud(int variant, float *a, int64_t n, int mem, void *stream, darm_g
       d = static_cast<float *>(slot(st, 0, bytes));
       DARM_CUDA(cudaMemcpyAsync(d, a, bytes, cudaMemcpyHostToDevice, s));
     }
-    auto *dscr = static_cast<float *>(slot(st, 7, size_t(n / 16) * 256 * sizeof(float)));   // factored diagonals
+    // factored diagonals, then the trailing-update launches' tile counters
+    const size_t diag_words = size_t(n / 16) * 256;
+    auto *dscr = static_cast<float *>(
+        slot(st, 7, (diag_words + size_t(darm_gpu::lud_counter_words(int(n)))) * sizeof(float)));
+    int *counters = reinterpret_cast<int *>(dscr + diag_words);
     GraphEntry &g = cached_graph(st, 1, variant, d, n, [&](cudaStream_t cs, int *launches) {
-      return record_lud(variant, d, int(n), dscr, cs, launches);
+      return record_lud(variant, d, int(n), dscr, counters, cs, launches);
     });
     tl.mark(1);
     DARM_CUDA(cudaGraphLaunch(g.exec, s));

@@ -59,5 +59,29 @@ def main(n=8192, variant=1, out="gpurun_out/trace_lud.json"):
     print(f"  idle gaps (no kernel running): {gaps / 1e3:.3f} ms")
 
 
+def super_steps(path="gpurun_out/trace_lud.json"):
+    """Per super-step timeline from a trace: the band (trailing-update kernel
+    on the panel stream), the four panels, the far block (on the main stream)."""
+    ev = [e for e in json.load(open(path))["traceEvents"] if e.get("cat") == "kernel"]
+    ev.sort(key=lambda e: e["ts"])
+    t0 = ev[0]["ts"]
+    panel_stream = next(e["args"].get("stream") for e in ev if "panel" in e["name"] and e["ts"] > ev[5]["ts"])
+    bands = [e for e in ev if "far" in e["name"] and e["args"].get("stream") == panel_stream]
+    fars = [e for e in ev if "far" in e["name"] and e["args"].get("stream") != panel_stream]
+    panels = [e for e in ev if "panel" in e["name"]][4:]          # super-step 0's panels run first
+    print(f"panel stream {panel_stream}: {len(bands)} bands, {len(fars)} far blocks, {len(panels)} panels")
+    for g in (0, 10, 30, 50, 70, 90, 110, 120):
+        if g >= len(bands):
+            continue
+        b = bands[g]
+        ps = panels[4 * g:4 * g + 4]
+        f = fars[g] if g < len(fars) else None
+        r = lambda e: f"[{(e['ts'] - t0):9.1f}, {(e['ts'] + e['dur'] - t0):9.1f}]"  # noqa: E731
+        print(f"  g={g:3d} band {r(b)} panels {r(ps[0])[:11]}..{r(ps[-1])[11:]} far {r(f) if f else '-'}")
+
+
 if __name__ == "__main__":
-    main(*[int(x) for x in sys.argv[1:]])
+    if len(sys.argv) > 1 and sys.argv[1] == "steps":
+        super_steps(*sys.argv[2:])
+    else:
+        main(*[int(x) for x in sys.argv[1:]])
