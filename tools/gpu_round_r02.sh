@@ -33,6 +33,8 @@ timeout 300 python tools/time_srad.py > gpurun_out/time_srad.log 2>&1
 timeout 600 python tools/time_bitonic.py 64 256 1024 4096 > gpurun_out/time_bitonic.log 2>&1
 timeout 600 python tools/time_bitonic.py --oddeven 64 256 > gpurun_out/time_oddeven.log 2>&1
 timeout 300 python tools/time_corpus.py > gpurun_out/time_corpus.log 2>&1
+timeout 300 python tools/time_lud.py 2048 4096 8192 > gpurun_out/time_lud.log 2>&1
+timeout 300 python tools/trace_lud.py > gpurun_out/trace_lud.log 2>&1; python tools/trace_lud.py steps >> gpurun_out/trace_lud.log 2>&1
 for k in bitonic bitonic_b256 bitonic_b1024 bitonic_b4096 sb1 srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens interp; do
   python tools/ncu_summary.py gpurun_out/prof_$k.ncu-rep > gpurun_out/ncusum_$k.json
   case " ${KEEP_REPS:-lud_far srad_fast} " in *" $k "*) ;; *) rm -f gpurun_out/prof_$k.ncu-rep ;; esac
