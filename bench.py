@@ -653,7 +653,7 @@ def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, ou
     want = torch.sort(pristine.view(-1, 64), dim=1).values.view(-1)
     for name, kpt in ((("pcm", 0), ("pcm_1key", 1)) if "pcm" in sections else ()):
         row = {}
-        for vname, v in (("unmelded", 0), ("melded", 1)):
+        for vname, v in (("unmelded", 0), ("predicated", 2), ("melded", 1)):
             call = darm.oddeven_sort(work, 64, v, stream=stream.cuda_stream, want_stats=False, prepare_only=True,
                                      keys_per_thread=kpt)
             t = time_steps(torch, stream, lambda: work.copy_(pristine), call, steps, warmup, flush)
@@ -662,6 +662,7 @@ def pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, ou
             row[vname + "_us"] = 1e3 * sum(t) / len(t)
         tmax(row)
         row["speedup"] = row["unmelded_us"] / row["melded_us"]
+        row["speedup_vs_predicated"] = row["predicated_us"] / row["melded_us"]
         row["keys_per_thread"] = kpt or 16
         row["melded_GBps"] = 8.0 * n / (row["melded_us"] * 1e-6) / 1e9
         row["melded_frac_hbm"] = row["melded_GBps"] / peak

@@ -82,10 +82,13 @@ __device__ __forceinline__ int32_t oe_arm_upper(int32_t dv, int32_t xp) {
   }
   return r;
 }
-// melded: out of order = lower ? cv > xp : upper ? cv < xp : false; one store
-__device__ __forceinline__ int32_t oe_melded(int32_t cv, int32_t xp, bool lower, bool upper) {
-  const bool swap = lower ? (cv > xp) : (upper && cv < xp);
-  return swap ? xp : cv;
+// melded: out of order = lower ? cv > xp : upper ? cv < xp : false, one
+// store.  The melded load gives an idle lane its own key as the partner
+// (xp == cv), so the stored value is `lower ? min(cv, xp) : max(cv, xp)` for
+// every role: one predicated VIMNMX (min or max by the role predicate), as
+// the bitonic melded exchange.
+__device__ __forceinline__ int32_t oe_melded(int32_t cv, int32_t xp, bool lower) {
+  return lower ? min(cv, xp) : max(cv, xp);
 }
 
 }  // namespace
@@ -119,7 +122,7 @@ __device__ __forceinline__ int32_t oe_one_step(int32_t v, uint64_t lo, uint64_t 
     // the hoisted, melded loads: partner at a selected address, own key
     const int32_t xp = b[lower ? t + k : (upper ? t - k : t)];
     const int32_t cv = b[t];
-    return oe_melded(cv, xp, lower, upper);
+    return oe_melded(cv, xp, lower);
   } else {
     int32_t r;
     if (lower) {                                           // condbr %lower ^lo ^nl
@@ -199,7 +202,7 @@ __device__ __forceinline__ void oe_reg_step(int32_t (&v)[R], int lane, int tib, 
       int32_t xp[R];
       partner(lower ? t + k / R : (upper ? t - k / R : t), xp);   // one load, selected address
 #pragma unroll
-      for (int j = 0; j < R; ++j) v[j] = oe_melded(v[j], xp[j], lower, upper);
+      for (int j = 0; j < R; ++j) v[j] = oe_melded(v[j], xp[j], lower);
     } else {
       if (lower) {                                         // condbr %lower ^lo ^nl
         DARM_ARM_F(F, "oddeven.reg.lo");
