@@ -17,6 +17,12 @@
  *     data pointer is device memory on the current device; nothing is copied.
  *   - stream: a cudaStream_t (NULL = legacy default stream).  HOST calls return
  *     after the D2H copy completed; DEVICE calls are asynchronous on `stream`.
+ *   - Thread safety: calls from several host threads are serialised per device
+ *     (one lock per device guards the cached buffers and graphs).  The cached
+ *     device work areas (HOST staging buffers, LUD's diagonal scratch and
+ *     tile counters, SRAD's ping-pong image) are per device, not per stream:
+ *     two asynchronous calls of the same entry point on different streams must
+ *     be ordered by the caller (an event), or run on one stream.
  *   - There is no CPU fallback: without a usable sm_100 device every compute
  *     entry point fails with DARM_INTERNAL_ERROR.
  */
