@@ -11,8 +11,8 @@
 // L21 = A21 U11^-1 for every block below it (the melded kernel).  Four steps
 // form a super-step; the trailing matrix takes their four updates in one
 // pass (A22 -= L21 U12 as 16-term fp32 FMA chains, same per-element operation
-// order), first the 64-wide band the next super-step's panels read, then the
-// far block while those panels run beside it (record_lud).
+// order): the 64-wide band the next super-step's panels read, followed by
+// those panels on a side stream, beside the far block (record_lud).
 // The perimeter kernel is the paper's melding target: each warp owns one
 // block pair, lanes 0-15 the row block and lanes 16-31 the column block, so
 // the thread-ID test `lane < 16` splits every warp in half (divergent on a
