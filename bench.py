@@ -748,9 +748,35 @@ def lud_row(torch, darm, stream, flush, steps, warmup, dist, out, tmax, cpu=Fals
     row["roofline"] = {"bound": "fp32 FMA (CUDA cores)", "achieved": row["melded_TFLOPs"], "peak": roof,
                        "unit": "TFLOP/s", "frac": row["melded_frac_fp32"],
                        "algorithmic_flop": (2.0 / 3.0) * n ** 3, "peak_source": "SMs x 128 FMA x 2 x sm_max_mhz"}
+    pattern = ffma2_outer_product_roof()
+    if pattern:
+        # the trailing update's instruction pattern (8 x 8 register outer product of
+        # FFMA2 with both operands in registers) measured alone on this GPU, no memory
+        row["roofline"]["pattern_roof"] = pattern
+        row["roofline"]["frac_of_pattern_roof"] = row["melded_TFLOPs"] / pattern["TFLOPs"]
     if cpu:
         row["cpu_baseline"] = cpu_lud()
     out["lud8192"] = row
+
+
+def ffma2_outer_product_roof():
+    """FFMA2 throughput of the LUD far update's register outer product (8 rows
+    x 4 column pairs per thread, L broadcast, U and the accumulators in
+    registers, no memory traffic) measured now by tools/micro/ffma2_outer; None
+    when the binary was not built."""
+    exe = os.path.join(ROOT, "tools", "micro", "ffma2_outer")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60, check=True).stdout
+    except (subprocess.SubprocessError, OSError):
+        return None
+    vals = [float(line.rsplit(":", 1)[1].split()[0]) for line in out.splitlines() if "TFLOP/s" in line]
+    if not vals:
+        return None
+    return {"TFLOPs": max(vals), "source": "tools/micro/ffma2_outer (best of 8 / 16 warps per SM, both operand orders)",
+            "note": "an FFMA2 with two register-pair sources issues at about two thirds of the pipe's rate; "
+                    "with a uniform-register operand the same pipe reaches ~69 TFLOP/s (tools/micro/ffma2_peak)"}
 
 
 def srad_rows(torch, darm, stream, flush, peak, dist, world, out, tmax, n=16384, iters=100, cpu=False):
