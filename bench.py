@@ -56,7 +56,7 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-LANE_KEYS = {"nqueens16": "nqueens", "pcm": "pcm_16kpt", "pcm_1key": "pcm_1kpt", "ms1m": "ms",
+LANE_KEYS = {"nqueens16": "nqueens", "nqueens16_paper_shape": "nqueens_paper_shape", "pcm": "pcm_16kpt", "pcm_1key": "pcm_1kpt", "ms1m": "ms",
              "lud8192": "lud_panel", "srad16384x100": "srad", "srad16384x100_fast_math": "srad_fast",
              "bitonic": "bitonic_sort_16kpt", "bitonic_1key": "bitonic_sort_1kpt"}
 
@@ -620,6 +620,34 @@ def per_kernel_table(torch, darm, stream, flush, steps, warmup, peak, dist=None,
             pre = o.Restatement().nqueens_prefixes(16, 7, mirror=True)
             row["cpu_baseline"] = cpu_nqueens(pre)
         out["nqueens16"] = row
+        # the same search in the paper's shape (ir/nqueens_step.ir: pop / leaf /
+        # push, melded by region replication), beside the symmetric encoding
+        row = {}
+        for vname, v in (("unmelded", 0), ("melded", 1)):
+            ts = []
+            for i in range(warmup + max(3, steps // 4)):
+                if dist:
+                    dist.barrier()
+                sols, _, st = darm.nqueens(16, 7, v, rank=rank, world=world, stream=stream.cuda_stream, mirror=True,
+                                           paper_shape=True)
+                if dist:
+                    t = torch.tensor([sols], dtype=torch.int64, device="cuda")
+                    dist.all_reduce(t)
+                    sols = int(t.item())
+                assert sols == 14772512, sols
+                if i >= warmup:
+                    ts.append(st["kernel_ms"])
+            row[vname + "_us"] = 1e3 * sum(ts) / len(ts)
+        tmax(row)
+        row["speedup"] = row["unmelded_us"] / row["melded_us"]
+        row["ir"] = "paper_2107_05681_b200/ir/nqueens_step.ir (runDarm: two block-region melds, region replication)"
+        row["nodes_searched"] = NQ_MIRROR_NODES
+        row["melded_nodes_per_s"] = NQ_MIRROR_NODES / (row["melded_us"] * 1e-6)
+        row["roofline"] = issue_roof("nqueens_step", "nqueens_step_kernel<1", row["melded_us"] * 1e-6 * world, sms,
+                                     mhz, note="integer-issue bound; the paper-shaped encoding")
+        if cpu:
+            row["cpu_baseline"] = out["nqueens16"]["cpu_baseline"]
+        out["nqueens16_paper_shape"] = row
     if "pcm" in sections or "ms1m" in sections or "interp" in sections:
         pcm_ms_interp_rows(torch, darm, stream, flush, steps, warmup, peak, dist, out, sections, cpu=cpu)
     if "lud8192" in sections:

@@ -205,6 +205,12 @@ int darm_gpu_nqueens(int variant, int n, int prefix_rows, int rank, int world,
  * only in columns < ceil(n/2), those left of the middle counted twice — which
  * halves the search; the prefix set (and per_prefix) is then the reduced one. */
 #define DARM_NQ_MIRROR 1
+/* DARM_NQ_PAPER_SHAPE runs the search loop in the shape the paper names
+ * (ir/nqueens_step.ir: pop / count a leaf / push, an if-then-elseif-then
+ * section that runDarm melds by region replication — two block-region melds)
+ * instead of the symmetric push/pop encoding (ir/nqueens_sym.ir); n <= 16.
+ * Same counts, per prefix and in total. */
+#define DARM_NQ_PAPER_SHAPE 2
 int darm_gpu_nqueens_ex(int variant, int n, int prefix_rows, int rank, int world,
                         int flags, uint64_t *solutions, uint32_t *per_prefix,
                         int64_t per_prefix_len, int64_t *n_prefixes, void *stream,

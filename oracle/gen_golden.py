@@ -296,6 +296,51 @@ def nqueens_chain_fixtures(ref: Reference) -> dict:
     return out
 
 
+NQ_STEP_IR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                          "paper_2107_05681_b200", "ir", "nqueens_step.ir")
+
+
+def nqueens_step_chain_fixtures(ref: Reference) -> dict:
+    """The paper-shaped encoding, ir/nqueens_step.ir (pop / count a leaf / push,
+    an if-then-elseif-then that runDarm melds by region replication), run by
+    the reference interpreter to a fixpoint per warp of prefixes, original and
+    melded: per-prefix solution counts and unit-latency statistics.  Row-
+    relative diagonals, as the host enumerates them."""
+    text = open(NQ_STEP_IR).read()
+    orig = ref.load_text(text, 0)
+    meld = ref.load_text(text, 1)
+    out = {"ir": "paper_2107_05681_b200/ir/nqueens_step.ir", "melds": meld.layout["melds"], "cases": []}
+    W = 32
+    for n, base in ((4, 1), (5, 1), (6, 2), (7, 2), (8, 2), (9, 2), (10, 3)):
+        pre = nq_prefixes(n, base)
+        mask = (1 << n) - 1
+        case = {"n": n, "base": base, "per_prefix": [],
+                "stats_unit_latency": {"unmelded": [0] * 7, "melded": [0] * 7}, "rounds": {"unmelded": 0, "melded": 0}}
+        for w0 in range(0, len(pre), W):
+            chunk = pre[w0:w0 + W]
+            res = {}
+            for tag, mod in (("unmelded", orig), ("melded", meld)):
+                g = np.zeros(6 * 64, np.int32)
+                for t in range(W):
+                    if t < len(chunk):
+                        c, d1, d2 = chunk[t]
+                        g[t], g[64 + t] = base, c
+                        g[128 + t], g[192 + t] = np.int64(d1).astype(np.int32), np.int64(d2).astype(np.int32)
+                        g[256 + t] = ~(c | d1 | d2) & mask
+                    else:
+                        g[t] = base - 1
+                sh = np.zeros(4 * 1024, np.int32)
+                rounds, st = mod.run_to_fixpoint(W, np.array([n, mask, base], np.int32), g, sh, unit_latency=True)
+                res[tag] = g[320:320 + len(chunk)].tolist()
+                case["rounds"][tag] += rounds
+                case["stats_unit_latency"][tag] = [a + int(b) for a, b in zip(case["stats_unit_latency"][tag], st)]
+            assert res["unmelded"] == res["melded"], (n, base, w0)
+            case["per_prefix"] += res["unmelded"]
+        case["solutions"] = sum(case["per_prefix"])
+        out["cases"].append(case)
+    return out
+
+
 def main():
     ref = Reference()
     os.makedirs(OUT, exist_ok=True)
@@ -310,6 +355,8 @@ def main():
         json.dump(oddeven_sort_fixtures(ref), f, separators=(",", ":"))
     with open(os.path.join(OUT, "nqueens_chain.json"), "w") as f:
         json.dump(nqueens_chain_fixtures(ref), f, separators=(",", ":"))
+    with open(os.path.join(OUT, "nqueens_step_chain.json"), "w") as f:
+        json.dump(nqueens_step_chain_fixtures(ref), f, separators=(",", ":"))
     with open(os.path.join(OUT, "mt19937_64.json"), "w") as f:
         json.dump(std_mt19937_64_kat(), f)
     print("wrote", sorted(os.listdir(OUT)))

@@ -595,14 +595,21 @@ class Program:
         return ProgramResult(rets, valid, globals_, shared, faults, stats, st.as_dict() if want_stats else {})
 
 
+NQ_MIRROR, NQ_PAPER_SHAPE = 1, 2     # darm_gpu.h DARM_NQ_*
+
+
 def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int = 1,
-            per_prefix: bool = False, stream=None, want_stats: bool = True, mirror: bool = False):
+            per_prefix: bool = False, stream=None, want_stats: bool = True, mirror: bool = False,
+            paper_shape: bool = False):
     """Count n-queens solutions below the prefixes i % world == rank.
 
     ``mirror``: count by mirror symmetry (half the search, DARM_NQ_MIRROR).
+    ``paper_shape``: run ir/nqueens_step.ir (pop / leaf / push, the paper's
+    if-then-elseif-then melded by region replication) instead of the
+    symmetric encoding (DARM_NQ_PAPER_SHAPE, n <= 16).
     Returns ``(solutions, per_prefix_counts or None, stats)``.
     """
-    flags = 1 if mirror else 0
+    flags = (NQ_MIRROR if mirror else 0) | (NQ_PAPER_SHAPE if paper_shape else 0)
     if isinstance(variant, str):
         variant = VARIANTS[variant]
     sols = ctypes.c_uint64(0)
@@ -610,7 +617,7 @@ def nqueens(n: int, prefix_rows: int, variant=MELDED, rank: int = 0, world: int 
     err = ctypes.create_string_buffer(512)
     per = None
     if per_prefix:
-        cnt = lib().darm_gpu_nqueens_prefix_count_ex(n, prefix_rows, rank, world, flags)
+        cnt = lib().darm_gpu_nqueens_prefix_count_ex(n, prefix_rows, rank, world, flags & NQ_MIRROR)
         if cnt < 0:
             raise DarmUserError("bad n-queens arguments")
         per = np.zeros(max(1, cnt), dtype=np.uint32)

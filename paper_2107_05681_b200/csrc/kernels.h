@@ -78,7 +78,7 @@ int ir_interp_max_phis();
 // nqueens.cu
 cudaError_t launch_nqueens(int variant, const uint32_t *prefix, uint32_t n_prefix, uint32_t n_double, int n, int base,
                            uint32_t *per_prefix, unsigned long long *total, unsigned int *counter,
-                           int sms, cudaStream_t s);
+                           int sms, cudaStream_t s, bool paper_shape = false);
 
 // lud.cu: records the launches of one decomposition on `s`; dscr: 256-float
 // device scratch for the factored diagonal block

@@ -636,7 +636,7 @@ int64_t darm_gpu_nqueens_prefix_count(int n, int prefix_rows, int rank, int worl
 
 int64_t darm_gpu_nqueens_prefix_count_ex(int n, int prefix_rows, int rank, int world, int flags) {
   if (n < 2 || n > 31 || prefix_rows < 1 || prefix_rows > n - 1 || world < 1 || rank < 0 || rank >= world ||
-      (flags & ~DARM_NQ_MIRROR))
+      (flags & ~(DARM_NQ_MIRROR | DARM_NQ_PAPER_SHAPE)))
     return -1;
   std::vector<uint32_t> pre;
   nqueens_prefixes(n, prefix_rows, rank, world, pre, (flags & DARM_NQ_MIRROR) != 0);
@@ -654,7 +654,9 @@ int darm_gpu_nqueens_ex(int variant, int n, int prefix_rows, int rank, int world
                         uint32_t *per_prefix, int64_t per_prefix_len, int64_t *n_prefixes, void *stream,
                         darm_gpu_stats *stats, char *err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (flags & ~DARM_NQ_MIRROR) user_error("unknown n-queens flags");
+    if (flags & ~(DARM_NQ_MIRROR | DARM_NQ_PAPER_SHAPE)) user_error("unknown n-queens flags");
+    const bool paper_shape = (flags & DARM_NQ_PAPER_SHAPE) != 0;
+    if (paper_shape && n > 16) user_error("the paper-shaped encoding (DARM_NQ_PAPER_SHAPE) takes n <= 16");
     if (variant != DARM_UNMELDED && variant != DARM_MELDED) user_error("variant must be 0 (unmelded) or 1 (melded)");
     if (n < 2 || n > 31) user_error("n must be in [2, 31]");
     if (prefix_rows < 1 || prefix_rows > n - 1) user_error("prefix_rows must be in [1, n-1]");
@@ -680,7 +682,7 @@ int darm_gpu_nqueens_ex(int variant, int n, int prefix_rows, int rank, int world
     DARM_CUDA(cudaMemsetAsync(dctl, 0, 16, s));
     tl.mark(1);
     if (np) DARM_CUDA(launch_nqueens(variant, dpre, uint32_t(np), uint32_t(n_double), n, prefix_rows, dper, dctl,
-                                     reinterpret_cast<unsigned int *>(dctl + 1), st.sms, s));
+                                     reinterpret_cast<unsigned int *>(dctl + 1), st.sms, s, paper_shape));
     tl.mark(2);
     unsigned long long total = 0;
     DARM_CUDA(cudaMemcpyAsync(&total, dctl, 8, cudaMemcpyDeviceToHost, s));

@@ -77,3 +77,35 @@ def test_nqueens_mirror_symmetry(variant):
     _, per, _ = darm.nqueens(9, 3, variant, per_prefix=True, mirror=True)
     _, per_full, _ = darm.nqueens(9, 3, variant, per_prefix=True)
     assert len(per) < len(per_full)
+
+
+# ---- the paper's shape: ir/nqueens_step.ir (DARM_NQ_PAPER_SHAPE)
+@pytest.mark.parametrize("variant", [0, 1])
+def test_nqueens_paper_shape_reference_chain_golden(variant):
+    """Both forms of the paper-shaped encoding against the reference
+    interpreter running ir/nqueens_step.ir to a fixpoint."""
+    gold = load_golden("nqueens_step_chain.json")
+    for case in gold["cases"]:
+        sols, per, _ = darm.nqueens(case["n"], case["base"], variant, per_prefix=True, paper_shape=True)
+        assert per.tolist() == case["per_prefix"], (case["n"], variant)
+        assert sols == case["solutions"]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("n,base,mirror", [(10, 3, False), (12, 4, True), (14, 4, False), (14, 5, True)])
+def test_nqueens_paper_shape_equals_symmetric(variant, n, base, mirror):
+    """Same search, two encodings: per-prefix counts equal, totals = OEIS."""
+    a = darm.nqueens(n, base, variant, per_prefix=True, mirror=mirror, paper_shape=True)
+    b = darm.nqueens(n, base, variant, per_prefix=True, mirror=mirror)
+    assert (a[1] == b[1]).all()
+    assert a[0] == b[0] == NQUEENS[n]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_nqueens_paper_shape_n16(variant):
+    assert darm.nqueens(16, 7, variant, mirror=True, paper_shape=True, want_stats=False)[0] == 14772512
+
+
+def test_nqueens_paper_shape_limits():
+    with pytest.raises(darm.DarmUserError):
+        darm.nqueens(17, 5, 1, paper_shape=True)

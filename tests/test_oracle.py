@@ -138,6 +138,25 @@ def test_nqueens_melded_spec_is_the_reference_pass_output():
     assert big["melded"][2] / big["melded"][1] > big["unmelded"][2] / big["unmelded"][1]
 
 
+def test_nqueens_paper_shape_chain_and_melds(restatement):
+    """ir/nqueens_step.ir, the paper's shape (pop / count a leaf / push, an
+    if-then-elseif-then): runDarm melds it by region
+    replication — two block-region melds — and the reference
+    interpreter running it (original and melded) to a fixpoint gives the
+    restatement's per-prefix counts.  Its simulator sees higher utilisation
+    after the meld but more issued instructions (the replicated region)."""
+    gold = load_golden("nqueens_step_chain.json")
+    assert [m["kind"] for m in gold["melds"]] == ["block-region", "block-region"]
+    for case in gold["cases"]:
+        states = restatement.nqueens_prefixes(case["n"], case["base"])
+        tot, per, _ = restatement.nqueens_count(case["n"], case["base"], states)
+        assert per.tolist() == case["per_prefix"]
+        assert tot == case["solutions"] == NQUEENS[case["n"]]
+    big = gold["cases"][-1]["stats_unit_latency"]
+    assert big["melded"][2] / big["melded"][1] > big["unmelded"][2] / big["unmelded"][1]
+    assert big["melded"][0] > big["unmelded"][0]
+
+
 @pytest.mark.parametrize("n", range(4, 13))
 def test_nqueens_restatement_known_answers(restatement, n):
     for base in (1, 2, n - 1):

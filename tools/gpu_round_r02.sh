@@ -22,7 +22,8 @@ timeout 600 $N -k regex:corpus_lanes -c 3 -o gpurun_out/prof_sb1 python tools/pr
 timeout 600 $N -k regex:srad_sweep -c 4 -o gpurun_out/prof_srad python tools/profile_driver.py srad > gpurun_out/ncu_srad.log 2>&1
 timeout 600 $N -k regex:oddeven_sort -c 4 -o gpurun_out/prof_oddeven python tools/profile_driver.py oddeven > gpurun_out/ncu_oddeven.log 2>&1
 timeout 600 $N -k regex:merge_sort -c 4 -o gpurun_out/prof_merge python tools/profile_driver.py merge 1048576 > gpurun_out/ncu_merge.log 2>&1
-timeout 600 $N -k regex:nqueens -c 2 -o gpurun_out/prof_nqueens python tools/profile_driver.py nqueens > gpurun_out/ncu_nqueens.log 2>&1
+timeout 600 $N -k regex:"nqueens_kernel" -c 2 -o gpurun_out/prof_nqueens python tools/profile_driver.py nqueens > gpurun_out/ncu_nqueens.log 2>&1
+timeout 600 $N -k regex:nqueens_step -c 2 -o gpurun_out/prof_nqueens_step python tools/profile_driver.py nqueens_step > gpurun_out/ncu_nqueens_step.log 2>&1
 timeout 600 $N -k regex:ir_interp -c 1 -o gpurun_out/prof_interp python tools/profile_driver.py interp > gpurun_out/ncu_interp.log 2>&1
 timeout 600 $N -k regex:lud_far -s 21 -c 1 -o gpurun_out/prof_lud_far python tools/profile_driver.py lud > gpurun_out/ncu_lud_far.log 2>&1
 timeout 600 $N -k regex:lud_panel -s 100 -c 1 -o gpurun_out/prof_lud_unmelded python tools/profile_driver.py lud > gpurun_out/ncu_lud_u.log 2>&1
@@ -35,7 +36,7 @@ timeout 600 python tools/time_bitonic.py --oddeven 64 256 > gpurun_out/time_odde
 timeout 300 python tools/time_corpus.py > gpurun_out/time_corpus.log 2>&1
 timeout 300 python tools/time_lud.py 2048 4096 8192 > gpurun_out/time_lud.log 2>&1
 timeout 300 python tools/trace_lud.py > gpurun_out/trace_lud.log 2>&1; python tools/trace_lud.py steps >> gpurun_out/trace_lud.log 2>&1
-for k in bitonic bitonic_b256 bitonic_b1024 bitonic_b4096 sb1 srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens interp; do
+for k in bitonic bitonic_b256 bitonic_b1024 bitonic_b4096 sb1 srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens nqueens_step interp; do
   python tools/ncu_summary.py gpurun_out/prof_$k.ncu-rep > gpurun_out/ncusum_$k.json
   case " ${KEEP_REPS:-lud_far srad_fast} " in *" $k "*) ;; *) rm -f gpurun_out/prof_$k.ncu-rep ;; esac
 done

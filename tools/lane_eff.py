@@ -45,6 +45,8 @@ def label(name):
         return "ms", form(args[0])
     if fam == "nqueens_kernel":
         return "nqueens", form(args[0])
+    if fam == "nqueens_step_kernel":
+        return "nqueens_paper_shape", form(args[0])
     if fam == "lud_panel_kernel":
         return "lud_panel", form(args[0])
     if fam == "srad_sweep_kernel":

@@ -34,6 +34,7 @@ def main():
         darm.merge_sort(keys[: 1 << 20].clone(), v, want_stats=False)
     for v in (0, 1):
         darm.nqueens(14, 5, v, want_stats=False, mirror=True)
+        darm.nqueens(14, 5, v, want_stats=False, mirror=True, paper_shape=True)
     a0 = torch.rand((2048, 2048), generator=gen, device="cuda") + 2048 * torch.eye(2048, device="cuda")
     for v in (0, 1):
         darm.lud(a0.clone(), v, want_stats=False)

@@ -46,6 +46,10 @@ def main(which, bucket=64):
         prog.execute_warps(32, np.full((1, 1), 16, np.int32), gi, n_warps=nwi)
         torch.cuda.synchronize()
         return
+    if which == "nqueens_step":   # the paper-shaped encoding, the bench's launch
+        for v in (darm.UNMELDED, darm.MELDED):
+            assert darm.nqueens(16, 7, v, want_stats=False, mirror=True, paper_shape=True)[0] == 14772512
+        return
     if which == "nqueens":
         for v in (darm.UNMELDED, darm.MELDED):   # the bench's launch: 7-row prefixes, mirror symmetry
             assert darm.nqueens(16, 7, v, want_stats=False, mirror=True)[0] == 14772512

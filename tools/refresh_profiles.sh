@@ -16,7 +16,7 @@ if [ -f $O/launches_lud8192.csv ]; then
   cp $O/launches_lud8192.csv $P/${R}_launches_lud8192.csv
   python tools/launch_share.py $O/launches_lud8192.csv > $P/${R}_launches_lud8192_summary.txt
 fi
-for k in bitonic bitonic_b256 bitonic_b1024 bitonic_b4096 sb1 srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens interp; do
+for k in bitonic bitonic_b256 bitonic_b1024 bitonic_b4096 sb1 srad srad_fast lud_far lud_melded lud_unmelded oddeven merge nqueens nqueens_step interp; do
   if [ -s $O/ncusum_$k.json ]; then cp $O/ncusum_$k.json $P/${R}_ncu_$k.json
   elif [ -f $O/prof_$k.ncu-rep ]; then python tools/ncu_summary.py $O/prof_$k.ncu-rep > $P/${R}_ncu_$k.json; fi
 done

@@ -75,6 +75,7 @@ def main():
     for v in (0, 1):
         assert darm.nqueens(8, 3, v, want_stats=False)[0] == 92
         assert darm.nqueens(10, 4, v, want_stats=False, mirror=True)[0] == 724
+        assert darm.nqueens(10, 4, v, want_stats=False, mirror=True, paper_shape=True)[0] == 724
     n = 256
     a0 = (rng.random((n, n), dtype=np.float32) + n * np.eye(n, dtype=np.float32)).astype(np.float32)
     for v in (0, 1):
