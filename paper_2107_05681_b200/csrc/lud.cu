@@ -694,6 +694,9 @@ int lud_counter_words(int n) { return 2 * (n / (kLook * BS) + 2); }
 // SMs the far block leaves to the concurrent panels (measured at 8192:
 // 0 -> 15.65 ms, 4 -> 14.98, 8 -> 14.72, 16 -> 14.89, 32 -> 16.13)
 constexpr int kPanelSMs = 8;
+#ifndef DARM_LUD_PANEL_ADAPT_M
+#define DARM_LUD_PANEL_ADAPT_M 6144   // swept at 8192^2: 0 -> 10.49 ms, 3072 -> 10.49, 5120 -> 10.42, 6144 -> 10.40, 7168 -> 10.52, 8192 -> 10.74
+#endif
 
 cudaError_t record_lud(int variant, float *a, int n, float *dscr, int *counters, cudaStream_t s, int *launches) {
   // per device: kernel attributes, SM count, the panel stream (callers hold
@@ -760,7 +763,13 @@ cudaError_t record_lud(int variant, float *a, int n, float *dscr, int *counters,
       e = cudaEventRecord(sd.join, sd.s);
       if (e != cudaSuccess) return e;
       const int far[1][4] = {{F, n, F, n}};
-      e = launch_far(a, n, O, T, far_rects(1, far), maps, sms - kPanelSMs, ctr++, s);
+      // SMs left to the panels beside the far block: kPanelSMs while the far
+      // block dominates; once it is small (m <= DARM_LUD_PANEL_ADAPT_M) enough
+      // for the next panels' CTAs to run in one wave (six per SM)
+      int reserve = kPanelSMs;
+      const int m_far = n - F, pairs = (n - E) / BS - 1;
+      if (m_far <= DARM_LUD_PANEL_ADAPT_M) reserve = max(kPanelSMs, min(32, ((pairs + kPairs - 1) / kPairs + 5) / 6));
+      e = launch_far(a, n, O, T, far_rects(1, far), maps, sms - reserve, ctr++, s);
       if (e != cudaSuccess) return e;
       ++*launches;
       e = cudaStreamWaitEvent(s, sd.join, 0);
