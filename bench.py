@@ -973,9 +973,16 @@ def our_arm(args):
         bad = set(sections) - set(PER_KERNEL_SECTIONS)
         if bad:
             raise SystemExit(f"unknown --kernels {sorted(bad)}; choose from {PER_KERNEL_SECTIONS}")
-        per_kernel = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak0, dist, rank, world,
-                                      sections, args.srad_size, args.srad_iters, with_cpu=not args.no_cpu_baseline)
-    if per_kernel is not None and "bitonic" in sections:
+        try:
+            per_kernel = per_kernel_table(torch, darm, stream, flush, args.steps, args.warmup, peak0, dist, rank,
+                                          world, sections, args.srad_size, args.srad_iters,
+                                          with_cpu=not args.no_cpu_baseline)
+        except Exception as e:          # the per-kernel table is auxiliary: the headline line still prints
+            if world == 1:
+                raise
+            per_kernel = {"error": f"{type(e).__name__}: {e}"[:400]}
+            sections = ()
+    if per_kernel is not None and "error" not in per_kernel and "bitonic" in sections:
         # every shape in four forms: unmelded (IPDOM branches), predicated
         # (ptxas if-conversion of the same CFG), melded (the order-flip form the
         # headline reports: `up` folded into the data) and melded_literal (App.
@@ -1069,7 +1076,8 @@ def our_arm(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     if per_kernel is not None:
-        attach_lane_efficiency(per_kernel)
+        if "error" not in per_kernel:
+            attach_lane_efficiency(per_kernel)
         line["per_kernel"] = per_kernel
     print(json.dumps(line))
     if dist:
