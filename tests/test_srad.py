@@ -243,6 +243,27 @@ def test_gpu_config5_16384(restatement):
 
 
 @pytest.mark.gpu
+def test_gpu_config5_16384_100_iterations_vs_restatement(restatement):
+    """BASELINE config 5 at full size and full length: 16384^2 x 100 on the GPU
+    (melded, IEEE) equals the CPU restatement run for all 100 iterations on
+    every host thread, bit for bit; the fast-math form stays within the north
+    star's 1e-5 relative of it."""
+    n = 16384
+    g = torch.Generator(device="cuda").manual_seed(6)
+    j0 = torch.exp(torch.rand((n, n), generator=g, device="cuda"))
+    want = j0.cpu().numpy()
+    restatement.srad(want, 100, 0.5, ROI, threads=os.cpu_count() or 1)
+    j = j0.clone()
+    darm.srad(j, 100, 0.5, ROI, 1)
+    got = j.cpu().numpy()
+    assert (got.view(np.int32) == want.view(np.int32)).all(), float(np.max(np.abs(got - want) / np.abs(want)))
+    f = j0.clone()
+    darm.srad(f, 100, 0.5, ROI, 1, fast=True)
+    rel = float(np.max(np.abs(f.cpu().numpy() - want) / np.abs(want)))
+    assert rel <= 1e-5, rel
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("rows,cols,iters,roi", [(256, 256, 100, ROI), (513, 377, 30, (10, 200, 31, 300)),
                                                   (2049, 1000, 20, ROI)])
