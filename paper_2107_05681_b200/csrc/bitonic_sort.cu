@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(CTA) bitonic_sort_kernel(int32_t *__restrict__
         } else {
 #pragma unroll
           for (int u = 0; u < U; ++u) xch[par][u][threadIdx.x] = v[u];
-          __syncthreads();
+          bucket_sync<B, CTA>();                           // the bucket's own warps only
 #pragma unroll
           for (int u = 0; u < U; ++u) b0[u] = xch[par][u][threadIdx.x ^ k];
           par ^= 1;

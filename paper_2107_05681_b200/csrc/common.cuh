@@ -99,6 +99,23 @@ __host__ __device__ constexpr bool cx_on_fma(int j, int mod = DARM_CX_FMA_MOD) {
 #define DARM_CX_FMA_MOD_MELDED DARM_CX_FMA_MOD
 #endif
 
+// Barrier over the B threads of one bucket (B a power of two, CTA a multiple
+// of B): a warp for B <= 32, a named barrier per bucket (ids 1 .. CTA/B) for
+// buckets spanning warps, the whole CTA only when the bucket is the CTA.
+// Buckets never exchange keys with each other, so a bucket waits only for
+// its own warps.
+template <int B, int CTA>
+__device__ __forceinline__ void bucket_sync() {
+  if constexpr (B >= CTA) {
+    __syncthreads();
+  } else if constexpr (B <= 32) {
+    __syncwarp();
+  } else {
+    static_assert(CTA / B <= 15, "named barriers 1..15");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + int(threadIdx.x) / B), "n"(B) : "memory");
+  }
+}
+
 // mbarrier primitives (TMA completion): init, producer arrive + expected
 // bytes, consumer wait on a phase parity.
 __device__ __forceinline__ unsigned smem_u32(const void *p) {

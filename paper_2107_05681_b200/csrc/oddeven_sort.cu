@@ -116,7 +116,8 @@ __device__ __forceinline__ int32_t oe_one_step(int32_t v, uint64_t lo, uint64_t 
   int32_t *b = buf[par];
   b[t] = v;                                                // the bucket in shared buf
   if constexpr (B <= 32) __syncwarp();                     // a bucket never spans warps
-  else __syncthreads();
+  else __syncthreads();                                    // (per-bucket named barriers measured slower here:
+                                                           //  B = 64 melded 190 -> 227 us)
   par ^= 1;                                                // double buffer: no barrier before the next write
   if constexpr (F == kMelded) {
     // the hoisted, melded loads: partner at a selected address, own key
