@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256, PF ? DARM_BITONIC_MIN_CTAS : 1) bitonic_s
             // another warp: one exchange through double-buffered shared memory
 #pragma unroll
             for (int j = 0; j < R; ++j) xch[par][j][threadIdx.x] = v[j];
-            __syncthreads();
+            bucket_sync<P, 256>();                         // the bucket's own warps only
 #pragma unroll
             for (int j = 0; j < R; ++j) b0[j] = xch[par][j][threadIdx.x ^ pk];
             par ^= 1;
