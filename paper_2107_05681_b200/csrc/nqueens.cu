@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256) nqueens_kernel(NqParams P) {
 // the host) and the stack keeps the whole row state (cols, d1, d2, av) at
 // [array][row - base + 1][thread].  32-bit words: n <= 16.  Kept beside the
 // symmetric encoding above so the two can be compared on the same search: this
-// is the shape the paper names (melded: 0.84x of unmelded on the B200), the
+// is the shape the paper names (melded: 0.83x of unmelded on the B200), the
 // symmetric one the shape where melding pays.
 template <bool M>
 __global__ void __launch_bounds__(256) nqueens_step_kernel(NqParams P) {
