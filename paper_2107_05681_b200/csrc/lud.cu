@@ -691,9 +691,14 @@ int lud_counter_words(int n) { return 2 * (n / (kLook * BS) + 2); }
 // receives its updates in step order.  The critical path per super-step is
 // max(far block, band + panel chain) instead of band + max(far block, panel
 // chain).
-// SMs the far block leaves to the concurrent panels (measured at 8192:
+// SMs the far block leaves to the concurrent panels (round 2, band beside the far
+// block, at 8192: 4 -> 10.66 ms, 6 -> 10.57, 8 -> 10.42, 10 -> 10.44, 12 -> 10.45;
+// round 1 schedule:
 // 0 -> 15.65 ms, 4 -> 14.98, 8 -> 14.72, 16 -> 14.89, 32 -> 16.13)
-constexpr int kPanelSMs = 8;
+#ifndef DARM_LUD_PANEL_SMS
+#define DARM_LUD_PANEL_SMS 8
+#endif
+constexpr int kPanelSMs = DARM_LUD_PANEL_SMS;
 #ifndef DARM_LUD_PANEL_ADAPT_M
 #define DARM_LUD_PANEL_ADAPT_M 6144   // swept at 8192^2: 0 -> 10.49 ms, 3072 -> 10.49, 5120 -> 10.42, 6144 -> 10.40, 7168 -> 10.52, 8192 -> 10.74
 #endif
